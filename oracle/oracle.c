@@ -1,0 +1,287 @@
+/*
+ * oracle.c -- plain, slow, fp64 CPU oracle for the VSA-OGM hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA
+ * product path (paper_2408_09066_b200/csrc); neither includes the other.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (arXiv 2408.09066
+ * LaTeX source), "S:n" = SPEC.md line n.  Readings of ambiguous passages are
+ * the ledger items L1..L17 of SURVEY.md section 8(c), restated in DESIGN.md.
+ *
+ * What it computes -- the plain definitions, no factorisation, no blocking:
+ *   theta      : phases of the two axis vectors, uniform on (-pi, pi]
+ *                (Eq. 3, sec. III-B-3; L2).
+ *   encode     : m_{c,k} = sum_{i : psi_i = c} exp(i (thx_k x_i + thy_k y_i) / l)
+ *                (Eq. 9 with Eq. 8 length scale P:232-235;
+ *                 bundling = addition P:216-219 Eq. 5; Alg. 1 P:260-285 with
+ *                 delta = 1 so the memory slot is the label psi; L1, L6).
+ *   decode     : n_c = ||m_c||_2 (Eq. 10); per cell centre (x, y)
+ *                H_c = sum_k Re(conj(m_{c,k}) exp(i (thx_k x + thy_k y)/l)),
+ *                q_c = H_c / (sqrt(D) n_c), 0 if n_c = 0 (Eq. 11; L5, L7, L8),
+ *                p_c = q_c^2 (Born rule; L9).
+ *   entropy    : hb(p) = -p log2 p - (1-p) log2 (1-p), 0 log 0 = 0;
+ *                S_c(r,c) = mean of hb(p_c) over the window footprint clipped
+ *                to the full grid; S = S_1 - S_0 (Alg. 2, P:330-356, P:318;
+ *                L10, L11, L12, L13).
+ *   labels     : occupied (1) if S >= rho_occ, empty (0) if S < rho_emp,
+ *                unknown (2) otherwise (Eq. 12; L14).
+ *
+ * Parallelism: pthreads split points (encode; per-thread partial sums added in
+ * thread order) or cells (decode).  Results are deterministic for a fixed
+ * thread count.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_PI 3.14159265358979323846
+
+/* ------------------------------------------------------------------ theta */
+/* splitmix64 (Steele, Lea, Flood 2014; Vigna's public-domain splitmix64.c).
+ * Draw order (L2): thx_0 .. thx_{D-1}, then thy_0 .. thy_{D-1} from one
+ * stream seeded with `seed`; u = (z >> 11) * 2^-53 in [0,1);
+ * theta = pi (1 - 2u) in (-pi, pi].                                        */
+static uint64_t orc_splitmix64(uint64_t *state)
+{
+    uint64_t z = (*state += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+uint64_t oracle_splitmix64_stream(uint64_t seed, int64_t n, uint64_t *out)
+{
+    uint64_t s = seed;
+    for (int64_t i = 0; i < n; ++i) out[i] = orc_splitmix64(&s);
+    return s;
+}
+
+int oracle_theta(uint64_t seed, int32_t D, double *theta_x, double *theta_y)
+{
+    if (D < 1) return -1;
+    uint64_t s = seed;
+    for (int32_t k = 0; k < D; ++k) {
+        double u = (double)(orc_splitmix64(&s) >> 11) * 0x1.0p-53;
+        theta_x[k] = ORC_PI * (1.0 - 2.0 * u);
+    }
+    for (int32_t k = 0; k < D; ++k) {
+        double u = (double)(orc_splitmix64(&s) >> 11) * 0x1.0p-53;
+        theta_y[k] = ORC_PI * (1.0 - 2.0 * u);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ encode */
+typedef struct {
+    int32_t D;
+    const double *tx, *ty;
+    double l;
+    const float *xy;
+    const uint8_t *lab;
+    int64_t i0, i1;
+    double *m;          /* [2][D][2] partial for this thread */
+    int64_t cnt[2];
+    int64_t bad;
+} enc_job;
+
+static void *enc_worker(void *arg)
+{
+    enc_job *j = (enc_job *)arg;
+    memset(j->m, 0, sizeof(double) * 4 * (size_t)j->D);
+    j->cnt[0] = j->cnt[1] = 0;
+    j->bad = 0;
+    for (int64_t i = j->i0; i < j->i1; ++i) {
+        double x = (double)j->xy[2 * i], y = (double)j->xy[2 * i + 1];
+        int c = j->lab[i];
+        if (c > 1 || !isfinite(x) || !isfinite(y)) { j->bad++; continue; }
+        j->cnt[c]++;
+        double *mc = j->m + (size_t)c * 2 * j->D;
+        for (int32_t k = 0; k < j->D; ++k) {
+            /* Eq. 9: phase of the bound x- and y- fractional powers, Eq. 8 scaling by l */
+            double a = (j->tx[k] * x + j->ty[k] * y) / j->l;
+            mc[2 * k] += cos(a);
+            mc[2 * k + 1] += sin(a);
+        }
+    }
+    return NULL;
+}
+
+/* m: [2][D][2] (class, k, re/im), ADDED to (bundling is addition, Eq. 5).
+ * counts[2] added to.  Returns the number of skipped invalid points. */
+int64_t oracle_encode(int32_t D, const double *tx, const double *ty, double l,
+                      int64_t n, const float *xy, const uint8_t *labels,
+                      double *m, int64_t *counts, int32_t nthreads)
+{
+    if (nthreads < 1) nthreads = 1;
+    if (n < (int64_t)nthreads) nthreads = n > 0 ? (int32_t)n : 1;
+    enc_job *jobs = (enc_job *)calloc((size_t)nthreads, sizeof(enc_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    double *parts = (double *)malloc(sizeof(double) * 4 * (size_t)D * (size_t)nthreads);
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].D = D; jobs[t].tx = tx; jobs[t].ty = ty; jobs[t].l = l;
+        jobs[t].xy = xy; jobs[t].lab = labels;
+        jobs[t].i0 = n * t / nthreads; jobs[t].i1 = n * (t + 1) / nthreads;
+        jobs[t].m = parts + (size_t)t * 4 * D;
+        pthread_create(&th[t], NULL, enc_worker, &jobs[t]);
+    }
+    int64_t bad = 0;
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    for (int t = 0; t < nthreads; ++t) {            /* fixed thread order */
+        for (int64_t e = 0; e < 4 * (int64_t)D; ++e) m[e] += jobs[t].m[e];
+        counts[0] += jobs[t].cnt[0];
+        counts[1] += jobs[t].cnt[1];
+        bad += jobs[t].bad;
+    }
+    free(parts); free(th); free(jobs);
+    return bad;
+}
+
+/* ------------------------------------------------------------------ norms */
+/* Eq. 10: n_c = ||m_c||_2 over the D complex components. */
+void oracle_norms(int32_t D, const double *m, double *norms)
+{
+    for (int c = 0; c < 2; ++c) {
+        double s = 0.0;
+        for (int32_t k = 0; k < D; ++k) {
+            double re = m[(size_t)c * 2 * D + 2 * k], im = m[(size_t)c * 2 * D + 2 * k + 1];
+            s += re * re + im * im;
+        }
+        norms[c] = sqrt(s);
+    }
+}
+
+/* ------------------------------------------------------------------ decode */
+typedef struct {
+    int32_t D;
+    const double *tx, *ty;
+    double l;
+    const double *m;
+    double norms[2];
+    double x0, y0, res;
+    const int32_t *rows, *cols;
+    int64_t c0, c1, ncell;
+    double *q;     /* [2][ncell] */
+    int64_t range_violations;
+} dec_job;
+
+static void *dec_worker(void *arg)
+{
+    dec_job *j = (dec_job *)arg;
+    j->range_violations = 0;
+    for (int64_t e = j->c0; e < j->c1; ++e) {
+        /* L7: query points are cell centres, row index grows along +y */
+        double x = j->x0 + ((double)j->cols[e] + 0.5) * j->res;
+        double y = j->y0 + ((double)j->rows[e] + 0.5) * j->res;
+        for (int c = 0; c < 2; ++c) {
+            double q = 0.0;
+            if (j->norms[c] > 0.0) {                        /* L8: empty class decodes to 0 */
+                const double *mc = j->m + (size_t)c * 2 * j->D;
+                double H = 0.0;
+                for (int32_t k = 0; k < j->D; ++k) {
+                    double a = (j->tx[k] * x + j->ty[k] * y) / j->l;
+                    /* Re(conj(m) * e^{ia}) = Re m cos a + Im m sin a   (Eq. 11) */
+                    H += mc[2 * k] * cos(a) + mc[2 * k + 1] * sin(a);
+                }
+                q = H / (sqrt((double)j->D) * j->norms[c]);
+                if (fabs(q) > 1.0 + 1e-12) j->range_violations++;   /* Cauchy-Schwarz */
+            }
+            j->q[(size_t)c * j->ncell + e] = q;
+        }
+    }
+    return NULL;
+}
+
+/* Signed similarity q for a list of cells (rows[e], cols[e]) of the grid with
+ * lower-left corner (x0, y0) and cell size res.  q: [2][ncell].
+ * Returns the number of |q| > 1 + 1e-12 violations (must be 0). */
+int64_t oracle_decode_cells(int32_t D, const double *tx, const double *ty, double l,
+                            const double *m, double x0, double y0, double res,
+                            int64_t ncell, const int32_t *rows, const int32_t *cols,
+                            double *q, int32_t nthreads)
+{
+    double norms[2];
+    oracle_norms(D, m, norms);
+    if (nthreads < 1) nthreads = 1;
+    if (ncell < (int64_t)nthreads) nthreads = ncell > 0 ? (int32_t)ncell : 1;
+    dec_job *jobs = (dec_job *)calloc((size_t)nthreads, sizeof(dec_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        dec_job *j = &jobs[t];
+        j->D = D; j->tx = tx; j->ty = ty; j->l = l; j->m = m;
+        j->norms[0] = norms[0]; j->norms[1] = norms[1];
+        j->x0 = x0; j->y0 = y0; j->res = res; j->rows = rows; j->cols = cols;
+        j->c0 = ncell * t / nthreads; j->c1 = ncell * (t + 1) / nthreads;
+        j->ncell = ncell; j->q = q;
+        pthread_create(&th[t], NULL, dec_worker, j);
+    }
+    int64_t viol = 0;
+    for (int t = 0; t < nthreads; ++t) { pthread_join(th[t], NULL); viol += jobs[t].range_violations; }
+    free(th); free(jobs);
+    return viol;
+}
+
+/* ------------------------------------------------------------------ entropy */
+/* Binary Shannon entropy in bits with 0 log 0 = 0. */
+double oracle_hb(double p)
+{
+    double h = 0.0;
+    if (p > 0.0) h -= p * log2(p);
+    if (p < 1.0) h -= (1.0 - p) * log2(1.0 - p);
+    return h;
+}
+
+/* Footprint membership (L11): box |du|,|dv| <= h, or disk du^2 + dv^2 <= h^2. */
+static int in_footprint(int du, int dv, int h, int disk)
+{
+    if (disk) return du * du + dv * dv <= h * h;
+    return abs(du) <= h && abs(dv) <= h;
+}
+
+/* Entropy maps and labels for a list of target cells.
+ * q_region: [2][rb-ra][cb-ca] signed similarities of the full-grid region
+ * rows [ra, rb) x cols [ca, cb) of an R x C grid.  For each target cell
+ * (rows[e], cols[e]) every footprint offset that lands inside the full grid
+ * must land inside the region (else returns -1).
+ * Class 1 (occupied) uses half-width h_occ, class 0 (empty) h_emp (Alg. 2 r(psi)).
+ * S: [3][n] = (S_occ, S_emp, S_occ - S_emp); labels[n] in {0 empty, 1 occupied, 2 unknown}.
+ * Returns the number of |q| > 1 + 1e-12 violations seen, or -1 on a region error. */
+int64_t oracle_entropy_cells(int32_t R, int32_t C, int32_t ra, int32_t rb, int32_t ca, int32_t cb,
+                             const double *q_region, int32_t h_occ, int32_t h_emp, int32_t disk,
+                             double rho_occ, double rho_emp, int64_t n,
+                             const int32_t *rows, const int32_t *cols,
+                             double *S, uint8_t *labels)
+{
+    int32_t W = cb - ca, Hh = rb - ra;
+    int64_t viol = 0;
+    for (int64_t e = 0; e < n; ++e) {
+        int32_t r = rows[e], c = cols[e];
+        double Sc[2];
+        for (int cls = 0; cls < 2; ++cls) {
+            int h = cls == 1 ? h_occ : h_emp;
+            double sum = 0.0;
+            int64_t cnt = 0;
+            for (int du = -h; du <= h; ++du)
+                for (int dv = -h; dv <= h; ++dv) {
+                    if (!in_footprint(du, dv, h, disk)) continue;
+                    int rr = r + du, cc = c + dv;
+                    if (rr < 0 || rr >= R || cc < 0 || cc >= C) continue;   /* L13: clip to full grid */
+                    if (rr < ra || rr >= rb || cc < ca || cc >= cb) return -1;
+                    double q = q_region[(size_t)cls * Hh * W + (size_t)(rr - ra) * W + (cc - ca)];
+                    if (fabs(q) > 1.0 + 1e-12) viol++;
+                    sum += oracle_hb(q * q);      /* Born rule p = q^2 */
+                    cnt++;
+                }
+            Sc[cls] = sum / (double)cnt;
+        }
+        double s = Sc[1] - Sc[0];          /* S(psi=1) - S(psi=0), Alg. 2 */
+        S[e] = Sc[1];
+        S[n + e] = Sc[0];
+        S[2 * n + e] = s;
+        labels[e] = s >= rho_occ ? 1 : (s < rho_emp ? 0 : 2);   /* Eq. 12 + L14 */
+    }
+    return viol;
+}
