@@ -1,0 +1,207 @@
+/*
+ * vsaogm.h -- C ABI of the B200-native VSA-OGM hot path (arXiv 2408.09066).
+ *
+ * The library computes, on an sm_100a GPU, the data-parallel hot path of
+ * VSA-OGM (Snyder et al., "Brain Inspired Probabilistic Occupancy Grid
+ * Mapping with Vector Symbolic Architectures"):
+ *
+ *   encode/bundle  m_{c,k} += sum_{i: psi_i = c} exp(i (thx_k x_i + thy_k y_i) / l)
+ *                  PAPER.md:252-258 (Eq. 9), :216-219 (Eq. 5), :260-285 (Alg. 1, delta = 1)
+ *   normalise      m_c / ||m_c||                      PAPER.md:292-295 (Eq. 10)
+ *   decode         q_c(x,y) = Re <m_c/||m_c||, phi(x,y)> / sqrt(D)
+ *                                                     PAPER.md:297-301 (Eq. 11)
+ *   Born rule      p_c = q_c^2
+ *   local entropy  S_c = window mean of H_b(p_c); S = S_1 - S_0
+ *                                                     PAPER.md:318, :330-356 (Alg. 2)
+ *   classify       occupied if S >= rho_occ, empty if S < rho_emp, else unknown
+ *                                                     PAPER.md:320-328 (Eq. 12) + DESIGN.md L14
+ *
+ * Conventions: D independent complex phasors per
+ * vector, phases uniform on (-pi, pi] drawn by splitmix64 (x axis then y
+ * axis, u = (z >> 11) 2^-53, theta = pi (1 - 2u)); class 0 = empty,
+ * class 1 = occupied; grid cell (r, c) has centre (x0 + (c + .5) res,
+ * y0 + (r + .5) res), row r grows along +y.
+ *
+ * Memory and streams.  Every pointer named *_dev is a device pointer owned by
+ * the caller (e.g. a torch CUDA tensor) that must stay valid until the work
+ * queued on the context's stream has reached it; *_host pointers are host
+ * memory (pinned memory gives asynchronous copies).  All calls enqueue work on
+ * the context's stream and return without synchronising unless they say so.
+ * A context is bound to the CUDA device current at vsaogm_create and is not
+ * thread-safe: use one context per (device, thread).
+ *
+ * Errors.  Every int-returning call returns VSAOGM_OK (0) or a negative code
+ * below; vsaogm_strerror() names it.  Argument errors are detected on the host
+ * before any work is queued (the call then has no effect).  Invalid points
+ * (label not in {0,1}, non-finite coordinate) are detected on the device,
+ * skipped, and reported by the next vsaogm_sync() (deferred error).
+ */
+#ifndef VSAOGM_H
+#define VSAOGM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VSAOGM_OK 0
+#define VSAOGM_EINVAL_DIM (-1)   /* D < 1 (SPEC.md:47 analogue for complex phasors)      */
+#define VSAOGM_EINVAL_ARG (-2)   /* bad length scale, bounds, grid, band, window or rho   */
+#define VSAOGM_EEMPTY (-3)       /* n < 1 points                      */
+#define VSAOGM_ELABEL (-4)       /* deferred: a label not in {0,1}          */
+#define VSAOGM_ENONFINITE (-5)   /* deferred: a non-finite coordinate       */
+#define VSAOGM_ENOMEM (-6)       /* device or host allocation failed                      */
+#define VSAOGM_ECUDA (-7)        /* a CUDA runtime / driver call failed                   */
+#define VSAOGM_ESTATE (-8)       /* call not valid in the current state (see each call)   */
+
+/* Opaque per-(device, rank) context: owns theta, the memories, tables, scratch. */
+typedef struct vsaogm_ctx vsaogm_ctx;
+
+/* World bounds in metres (x_max > x_min, y_max > y_min, all finite).  Their
+ * centre is the phase origin of the device tables; results do not depend on
+ * it (a common phase rotation cancels in Eq. 11), but every rank of a
+ * multi-GPU job must pass the same bounds (Alg. 3 preconditions). */
+typedef struct {
+    double x_min, y_min, x_max, y_max;
+} vsaogm_bounds;
+
+/* Query grid.  Full grid rows x cols, cell size res > 0, lower-left corner
+ * (x0, y0).  This rank owns rows [row_begin, row_end) (0 <= row_begin <
+ * row_end <= rows); the decode also evaluates `halo` extra rows on each side
+ * (clipped to [0, rows)) so that vsaogm_entropy can use window half-widths up
+ * to `halo` without communication (row-band sharding). */
+typedef struct {
+    double x0, y0, res;
+    int32_t rows, cols;
+    int32_t row_begin, row_end;
+    int32_t halo;
+} vsaogm_grid;
+
+/* Tensor-core operand precision of the decode contraction (fp32 accumulate). */
+typedef enum { VSAOGM_F16 = 0, VSAOGM_BF16 = 1 } vsaogm_precision;
+
+/* Alg. 2 window + Eq. 12 thresholds.  Class 1 (occupied) uses half-width
+ * half_occ, class 0 (empty) half_emp; window (2h+1)^2 box if disk == 0, the
+ * paper's disk u^2 + v^2 <= h^2 if disk == 1; 1 <= h <= 16.  Windows are
+ * clipped to the full grid and averaged over the clipped count. */
+typedef struct {
+    int32_t half_occ, half_emp;
+    int32_t disk;
+    float rho_occ, rho_emp;   /* rho_emp <= rho_occ; equal values give the binary Eq. 12 */
+} vsaogm_entropy_params;
+
+/* Create a context on the current CUDA device: draws theta (D phases per axis,
+ * seed as above), allocates zeroed memories.  l = length scale in metres
+ * (Eq. 8), l > 0.  *out receives the context.
+ * Errors: EINVAL_DIM (D < 1), EINVAL_ARG (l, bounds, out == NULL), ENOMEM, ECUDA. */
+int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds bounds,
+                  vsaogm_ctx **out);
+
+/* Release every resource of the context (synchronises its stream). NULL is a no-op. */
+void vsaogm_destroy(vsaogm_ctx *ctx);
+
+/* Queue all later work on `stream` (a cudaStream_t; NULL = the legacy default stream). */
+int vsaogm_set_stream(vsaogm_ctx *ctx, void *stream);
+
+/* Bundle n labelled points into the pending memories (Eq. 9 + Eq. 5, Alg. 1
+ * with delta = 1: the slot is the label).  xy_dev: float32 [n][2] metres
+ * (x, y interleaved), labels_dev: uint8 [n] in {0 empty, 1 occupied}.  Points
+ * with another label or a non-finite coordinate are skipped and raise the
+ * deferred ELABEL / ENONFINITE.  Errors: EINVAL_ARG (NULL), EEMPTY (n < 1). */
+int vsaogm_encode_bundle(vsaogm_ctx *ctx, const float *xy_dev, const uint8_t *labels_dev,
+                         int64_t n);
+
+/* As vsaogm_encode_bundle, from host arrays: the host->device copies are
+ * queued on the context's stream into context-owned staging buffers. */
+int vsaogm_encode_bundle_host(vsaogm_ctx *ctx, const float *xy_host, const uint8_t *labels_host,
+                              int64_t n);
+
+/* Expose the pending (not yet committed) memories for a multi-rank all-reduce
+ * (Alg. 3 fusion): *dev_ptr = fp64 [2][Dp][2] (class, k,
+ * re/im) in the context's centred-phase convention, Dp = D rounded up to a
+ * multiple of 32 (padding entries stay zero), *n_doubles = 4 Dp.  After
+ * this call the context is in multi-rank mode: vsaogm_decode no longer commits
+ * implicitly and returns ESTATE while pending work is uncommitted.  The
+ * pointer stays valid for the life of the context. */
+int vsaogm_pending(vsaogm_ctx *ctx, double **dev_ptr, int64_t *n_doubles);
+
+/* Same as vsaogm_pending for the per-class point counts: int64 [2] device. */
+int vsaogm_pending_counts(vsaogm_ctx *ctx, int64_t **dev_ptr);
+
+/* m += pending; pending = 0 (and the counts). */
+int vsaogm_commit(vsaogm_ctx *ctx);
+
+/* Zero the memories, pending memories and counts. */
+int vsaogm_reset(vsaogm_ctx *ctx);
+
+/* Decode every cell of this rank's band (plus halo rows) into signed
+ * similarities (Eq. 10 normalisation, Eq. 11 query) on the tensor cores, and
+ * the per-cell binary entropy H_b(q^2) kept in the context for
+ * vsaogm_entropy.  q_dev: NULL, or float32 [2][row_end-row_begin][cols]
+ * (class 0 empty, 1 occupied) receiving q for the band's own rows.  In
+ * single-rank mode pending memories are committed first.
+ * Errors: EINVAL_ARG (grid), ESTATE (multi-rank mode with uncommitted
+ * pending), ENOMEM, ECUDA. */
+int vsaogm_decode(vsaogm_ctx *ctx, const vsaogm_grid *grid, vsaogm_precision precision,
+                  float *q_dev);
+
+/* Local entropy (Alg. 2), global entropy S = S_occ - S_emp, 3-way labels
+ * (Eq. 12 + L14) over the band of the last vsaogm_decode.  s_dev: NULL or
+ * float32 [3][band][cols] = (S_occ, S_emp, S); labels_dev: NULL or uint8
+ * [band][cols] with 0 empty, 1 occupied, 2 unknown.
+ * Errors: ESTATE (no decode yet), EINVAL_ARG (params, or a half-width larger
+ * than the decode halo where the band has neighbours). */
+int vsaogm_entropy(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *s_dev,
+                   uint8_t *labels_dev);
+
+/* As vsaogm_entropy, returning to host memory: s_host NULL or float32
+ * [3][band][cols], labels_host uint8 [band][cols].  Synchronises the stream. */
+int vsaogm_entropy_host(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *s_host,
+                        uint8_t *labels_host);
+
+/* Wait for the context's stream; return a deferred device error (ELABEL or
+ * ENONFINITE, first one seen since the last sync) or ECUDA, else OK. */
+int vsaogm_sync(vsaogm_ctx *ctx);
+
+/* Test hook (synchronises): committed + pending memories as fp64 [2][D][2]
+ * in the raw-coordinate convention of Eq. 9 (the centring rotation undone on
+ * the host in fp64), and counts[2].  Either pointer may be NULL. */
+int vsaogm_get_memory(vsaogm_ctx *ctx, double *host, int64_t *counts);
+
+/* Test hook: theta as fp64 [2][D] (x axis, then y axis). */
+int vsaogm_get_phases(vsaogm_ctx *ctx, double *host);
+
+/* Kernel-level timing.  While enabled, the library brackets each of its
+ * kernel launches with CUDA events on the context's stream.  read: waits for
+ * the stream, writes the summed milliseconds and launch counts per kernel id
+ * (ms[VSAOGM_NKERNELS], launches[VSAOGM_NKERNELS]; either may be NULL) since
+ * the last read, then clears them. */
+#define VSAOGM_K_ENCODE 0
+#define VSAOGM_K_REDUCE 1
+#define VSAOGM_K_COMMIT 2
+#define VSAOGM_K_NORMS 3
+#define VSAOGM_K_TABLE_B 4
+#define VSAOGM_K_TABLE_A 5
+#define VSAOGM_K_DECODE_GEMM 6
+#define VSAOGM_K_ENTROPY 7
+#define VSAOGM_NKERNELS 8
+int vsaogm_profile_enable(vsaogm_ctx *ctx, int enable);
+int vsaogm_profile_read(vsaogm_ctx *ctx, double *ms, int64_t *launches);
+
+/* Total number of kernels this context has launched (all ids). */
+int64_t vsaogm_launch_count(const vsaogm_ctx *ctx);
+
+/* Test hook: the decode GEMM kernel alone.  C[M][N] (float32, row-major) =
+ * A[M][K] . B[N][K]^T with A, B 16-bit (precision) K-major device arrays,
+ * K a multiple of 64, 1 <= M, N.  Runs on `stream` and synchronises it. */
+int vsaogm_test_gemm(const void *A_dev, const void *B_dev, int32_t M, int32_t N, int32_t K,
+                     vsaogm_precision precision, float *C_dev, void *stream);
+
+/* Name of an error code. */
+const char *vsaogm_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSAOGM_H */

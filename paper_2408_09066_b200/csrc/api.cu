@@ -1,0 +1,424 @@
+// api.cu -- the C ABI of include/vsaogm.h: context, theta, state machine,
+// argument checks, launch sequencing, profiling and test hooks.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+
+#include "common.cuh"
+
+namespace {
+
+// splitmix64 (Steele, Lea & Flood 2014): theta draw order x axis then y axis,
+// u = (z >> 11) 2^-53 in [0,1), theta = pi (1 - 2u) in (-pi, pi]   (L2)
+uint64_t splitmix64(uint64_t &s)
+{
+    uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+constexpr double kPi = 3.14159265358979323846;
+
+template <typename T>
+int dev_alloc_zero(T **p, size_t n)
+{
+    if (cudaMalloc(p, n * sizeof(T)) != cudaSuccess) { *p = nullptr; return VSAOGM_ENOMEM; }
+    if (cudaMemset(*p, 0, n * sizeof(T)) != cudaSuccess) return VSAOGM_ECUDA;
+    return VSAOGM_OK;
+}
+
+int grow_bytes(void **p, size_t *cap, size_t need)
+{
+    if (need <= *cap) return VSAOGM_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    if (cudaMalloc(p, need) != cudaSuccess) { *p = nullptr; return VSAOGM_ENOMEM; }
+    *cap = need;
+    return VSAOGM_OK;
+}
+
+bool finite_all(double a, double b, double c, double d) { return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ profiling
+
+int vsa_prof_begin(vsaogm_ctx *c, int kid, cudaEvent_t *a)
+{
+    (void)kid;
+    *a = nullptr;
+    if (!c->prof) return 0;
+    if (c->ev_pool.empty()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return 0;
+        c->ev_pool.push_back(e);
+    }
+    *a = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    cudaEventRecord(*a, c->stream);
+    return 0;
+}
+
+void vsa_prof_end(vsaogm_ctx *c, int kid, cudaEvent_t a)
+{
+    if (!c->prof || !a) return;
+    cudaEvent_t b;
+    if (c->ev_pool.empty()) {
+        if (cudaEventCreate(&b) != cudaSuccess) return;
+    } else {
+        b = c->ev_pool.back();
+        c->ev_pool.pop_back();
+    }
+    cudaEventRecord(b, c->stream);
+    c->prof_live.push_back({kid, a, b});
+}
+
+static void prof_harvest(vsaogm_ctx *c)
+{
+    for (auto &r : c->prof_live) {
+        float ms = 0.f;
+        cudaEventSynchronize(r.b);
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            c->prof_ms[r.kid] += ms;
+            c->prof_n[r.kid] += 1;
+        }
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->prof_live.clear();
+}
+
+// ------------------------------------------------------------------ ABI
+
+extern "C" {
+
+const char *vsaogm_strerror(int code)
+{
+    switch (code) {
+    case VSAOGM_OK: return "ok";
+    case VSAOGM_EINVAL_DIM: return "invalid dimension (D < 1)";
+    case VSAOGM_EINVAL_ARG: return "invalid argument";
+    case VSAOGM_EEMPTY: return "empty point set (n < 1)";
+    case VSAOGM_ELABEL: return "a point label is not in {0, 1}";
+    case VSAOGM_ENONFINITE: return "a point coordinate is not finite";
+    case VSAOGM_ENOMEM: return "out of memory";
+    case VSAOGM_ECUDA: return "CUDA error";
+    case VSAOGM_ESTATE: return "call not valid in the current state";
+    default: return "unknown error";
+    }
+}
+
+int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b, vsaogm_ctx **out)
+{
+    if (!out) return VSAOGM_EINVAL_ARG;
+    *out = nullptr;
+    if (D < 1) return VSAOGM_EINVAL_DIM;
+    if (!(length_scale > 0.0) || !isfinite(length_scale)) return VSAOGM_EINVAL_ARG;
+    if (!finite_all(b.x_min, b.y_min, b.x_max, b.y_max) || !(b.x_max > b.x_min) || !(b.y_max > b.y_min))
+        return VSAOGM_EINVAL_ARG;
+    vsaogm_ctx *c = new (std::nothrow) vsaogm_ctx();
+    if (!c) return VSAOGM_ENOMEM;
+    int rc = VSAOGM_OK;
+    do {
+        if (cudaGetDevice(&c->device) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
+        cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+        c->D = D;
+        c->Dp = (D + 31) / 32 * 32;
+        c->Kp = 2 * c->Dp;
+        c->l = length_scale;
+        c->bounds = b;
+        c->cx = 0.5 * (b.x_min + b.x_max);
+        c->cy = 0.5 * (b.y_min + b.y_max);
+        c->thx.resize(D);
+        c->thy.resize(D);
+        uint64_t s = seed;
+        for (int k = 0; k < D; ++k) c->thx[k] = kPi * (1.0 - 2.0 * ((double)(splitmix64(s) >> 11) * 0x1.0p-53));
+        for (int k = 0; k < D; ++k) c->thy[k] = kPi * (1.0 - 2.0 * ((double)(splitmix64(s) >> 11) * 0x1.0p-53));
+        std::vector<float> wx(c->Dp, 0.f), wy(c->Dp, 0.f);
+        std::vector<double> wx64(c->Dp, 0.0), wy64(c->Dp, 0.0);
+        for (int k = 0; k < D; ++k) {
+            wx64[k] = c->thx[k] / length_scale;
+            wy64[k] = c->thy[k] / length_scale;
+            wx[k] = (float)wx64[k];
+            wy[k] = (float)wy64[k];
+        }
+        if ((rc = dev_alloc_zero(&c->d_wx, c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_wy, c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_wx64, c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_wy64, c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_m, 4 * (size_t)c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_pending, 4 * (size_t)c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_counts, 2))) break;
+        if ((rc = dev_alloc_zero(&c->d_pcounts, 2))) break;
+        if ((rc = dev_alloc_zero(&c->d_norm2, 2))) break;
+        if ((rc = dev_alloc_zero(&c->d_err, 1))) break;
+        if (cudaMemcpy(c->d_wx, wx.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->d_wy, wy.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->d_wx64, wx64.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->d_wy64, wy64.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+            rc = VSAOGM_ECUDA;
+            break;
+        }
+    } while (0);
+    if (rc) {
+        vsaogm_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return VSAOGM_OK;
+}
+
+void vsaogm_destroy(vsaogm_ctx *c)
+{
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    void *ptrs[] = {c->d_wx, c->d_wy, c->d_wx64, c->d_wy64, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
+                    c->d_norm2, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
+                    c->d_B, c->d_hb, c->d_S, c->d_lab};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+}
+
+int vsaogm_set_stream(vsaogm_ctx *c, void *stream)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    c->stream = (cudaStream_t)stream;
+    return VSAOGM_OK;
+}
+
+int vsaogm_encode_bundle(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    if (n < 1) return VSAOGM_EEMPTY;
+    if (!xy || !lab) return VSAOGM_EINVAL_ARG;
+    int rc = vsa_launch_encode(c, xy, lab, n);
+    if (rc) return rc;
+    c->dirty = true;
+    return VSAOGM_OK;
+}
+
+int vsaogm_encode_bundle_host(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    if (n < 1) return VSAOGM_EEMPTY;
+    if (!xy || !lab) return VSAOGM_EINVAL_ARG;
+    if ((size_t)n > c->stage_cap) {
+        if (c->d_stage_xy) cudaFree(c->d_stage_xy);
+        if (c->d_stage_lab) cudaFree(c->d_stage_lab);
+        c->d_stage_xy = nullptr;
+        c->d_stage_lab = nullptr;
+        c->stage_cap = 0;
+        if (cudaMalloc(&c->d_stage_xy, n * sizeof(float2)) != cudaSuccess ||
+            cudaMalloc(&c->d_stage_lab, n) != cudaSuccess)
+            return VSAOGM_ENOMEM;
+        c->stage_cap = n;
+    }
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_xy, xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_lab, lab, n, cudaMemcpyHostToDevice, c->stream));
+    return vsaogm_encode_bundle(c, (const float *)c->d_stage_xy, c->d_stage_lab, n);
+}
+
+int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
+{
+    if (!c || !p) return VSAOGM_EINVAL_ARG;
+    *p = c->d_pending;
+    if (n) *n = 4 * (int64_t)c->Dp;
+    c->pending_taken = true;
+    return VSAOGM_OK;
+}
+
+int vsaogm_pending_counts(vsaogm_ctx *c, int64_t **p)
+{
+    if (!c || !p) return VSAOGM_EINVAL_ARG;
+    *p = (int64_t *)c->d_pcounts;
+    c->pending_taken = true;
+    return VSAOGM_OK;
+}
+
+int vsaogm_commit(vsaogm_ctx *c)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    int rc = vsa_launch_commit(c);
+    if (rc) return rc;
+    c->dirty = false;
+    return VSAOGM_OK;
+}
+
+int vsaogm_reset(vsaogm_ctx *c)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_m, 0, 4 * (size_t)c->Dp * sizeof(double), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pending, 0, 4 * (size_t)c->Dp * sizeof(double), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_counts, 0, 2 * sizeof(long long), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pcounts, 0, 2 * sizeof(long long), c->stream));
+    c->dirty = false;
+    c->decoded = false;
+    return VSAOGM_OK;
+}
+
+int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, float *q)
+{
+    if (!c || !g) return VSAOGM_EINVAL_ARG;
+    if (!(g->res > 0.0) || !isfinite(g->res) || !isfinite(g->x0) || !isfinite(g->y0) || g->rows < 1 ||
+        g->cols < 1 || g->row_begin < 0 || g->row_end > g->rows || g->row_begin >= g->row_end || g->halo < 0 ||
+        (prec != VSAOGM_F16 && prec != VSAOGM_BF16))
+        return VSAOGM_EINVAL_ARG;
+    int rc;
+    if (c->dirty) {
+        if (c->pending_taken) return VSAOGM_ESTATE;
+        if ((rc = vsaogm_commit(c))) return rc;
+    }
+    const int32_t r_lo = std::max(0, g->row_begin - g->halo);
+    const int32_t r_hi = std::min(g->rows, g->row_end + g->halo);
+    const int32_t r_ext = r_hi - r_lo;
+    const int64_t M = 2 * (int64_t)r_ext;
+    if (M > (int64_t)1 << 30 || (int64_t)g->cols > (int64_t)1 << 30) return VSAOGM_EINVAL_ARG;
+    if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * g->cols * sizeof(float)))) return rc;
+    if ((rc = vsa_launch_norms(c))) return rc;
+    if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
+    if ((rc = vsa_launch_table_A(c, g->y0, g->res, r_lo, r_ext, prec))) return rc;
+    if ((rc = vsa_launch_decode_gemm(c, (int32_t)M, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,
+                                     g->row_begin - r_lo, g->row_end - g->row_begin)))
+        return rc;
+    c->decoded = true;
+    c->g_rows = g->rows;
+    c->g_cols = g->cols;
+    c->g_r0 = g->row_begin;
+    c->g_r1 = g->row_end;
+    c->g_rlo = r_lo;
+    c->g_rext = r_ext;
+    c->g_halo = g->halo;
+    return VSAOGM_OK;
+}
+
+static int check_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p)
+{
+    if (!c || !p) return VSAOGM_EINVAL_ARG;
+    if (!c->decoded) return VSAOGM_ESTATE;
+    if (p->half_occ < 1 || p->half_emp < 1 || p->half_occ > 16 || p->half_emp > 16 || (p->disk != 0 && p->disk != 1) ||
+        !isfinite(p->rho_occ) || !isfinite(p->rho_emp) || p->rho_emp > p->rho_occ)
+        return VSAOGM_EINVAL_ARG;
+    const int H = std::max(p->half_occ, p->half_emp);
+    // every window row inside the full grid must have been decoded
+    if (std::max(0, c->g_r0 - H) < c->g_rlo || std::min(c->g_rows, c->g_r1 + H) > c->g_rlo + c->g_rext)
+        return VSAOGM_EINVAL_ARG;
+    return VSAOGM_OK;
+}
+
+int vsaogm_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab)
+{
+    int rc = check_entropy(c, p);
+    if (rc) return rc;
+    return vsa_launch_entropy(c, p, S, lab);
+}
+
+int vsaogm_entropy_host(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S_host, uint8_t *lab_host)
+{
+    int rc = check_entropy(c, p);
+    if (rc) return rc;
+    const size_t cells = (size_t)(c->g_r1 - c->g_r0) * c->g_cols;
+    if (S_host && (rc = grow_bytes((void **)&c->d_S, &c->S_cap, 3 * cells * sizeof(float)))) return rc;
+    if (lab_host && (rc = grow_bytes((void **)&c->d_lab, &c->lab_cap, cells))) return rc;
+    if ((rc = vsa_launch_entropy(c, p, S_host ? c->d_S : nullptr, lab_host ? c->d_lab : nullptr))) return rc;
+    if (S_host) VSA_CUDA_TRY(cudaMemcpyAsync(S_host, c->d_S, 3 * cells * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    if (lab_host) VSA_CUDA_TRY(cudaMemcpyAsync(lab_host, c->d_lab, cells, cudaMemcpyDeviceToHost, c->stream));
+    VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return VSAOGM_OK;
+}
+
+int vsaogm_sync(vsaogm_ctx *c)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    int err = 0;
+    VSA_CUDA_TRY(cudaMemcpyAsync(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (err) {
+        VSA_CUDA_TRY(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
+        VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return (err & VSA_ERRBIT_LABEL) ? VSAOGM_ELABEL : VSAOGM_ENONFINITE;
+    }
+    return VSAOGM_OK;
+}
+
+int vsaogm_get_memory(vsaogm_ctx *c, double *host, int64_t *counts)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    const size_t n = 4 * (size_t)c->Dp;
+    std::vector<double> m(n), pd(n);
+    long long cnt[2], pcnt[2];
+    VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    VSA_CUDA_TRY(cudaMemcpy(m.data(), c->d_m, n * sizeof(double), cudaMemcpyDeviceToHost));
+    VSA_CUDA_TRY(cudaMemcpy(pd.data(), c->d_pending, n * sizeof(double), cudaMemcpyDeviceToHost));
+    VSA_CUDA_TRY(cudaMemcpy(cnt, c->d_counts, sizeof(cnt), cudaMemcpyDeviceToHost));
+    VSA_CUDA_TRY(cudaMemcpy(pcnt, c->d_pcounts, sizeof(pcnt), cudaMemcpyDeviceToHost));
+    if (host) {
+        // undo the centring rotation: m_raw,k = m_centred,k * exp(+i (thx_k c_x + thy_k c_y) / l)
+        for (int cls = 0; cls < 2; ++cls)
+            for (int k = 0; k < c->D; ++k) {
+                const double psi = (c->thx[k] * c->cx + c->thy[k] * c->cy) / c->l;
+                const double cr = cos(psi), si = sin(psi);
+                const size_t o = 2 * ((size_t)cls * c->Dp + k);
+                const double re = m[o] + pd[o], im = m[o + 1] + pd[o + 1];
+                host[2 * ((size_t)cls * c->D + k)] = re * cr - im * si;
+                host[2 * ((size_t)cls * c->D + k) + 1] = re * si + im * cr;
+            }
+    }
+    if (counts) {
+        counts[0] = cnt[0] + pcnt[0];
+        counts[1] = cnt[1] + pcnt[1];
+    }
+    return VSAOGM_OK;
+}
+
+int vsaogm_get_phases(vsaogm_ctx *c, double *host)
+{
+    if (!c || !host) return VSAOGM_EINVAL_ARG;
+    memcpy(host, c->thx.data(), c->D * sizeof(double));
+    memcpy(host + c->D, c->thy.data(), c->D * sizeof(double));
+    return VSAOGM_OK;
+}
+
+int vsaogm_profile_enable(vsaogm_ctx *c, int enable)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    c->prof = enable != 0;
+    return VSAOGM_OK;
+}
+
+int vsaogm_profile_read(vsaogm_ctx *c, double *ms, int64_t *launches)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    prof_harvest(c);
+    for (int i = 0; i < VSAOGM_NKERNELS; ++i) {
+        if (ms) ms[i] = c->prof_ms[i];
+        if (launches) launches[i] = c->prof_n[i];
+        c->prof_ms[i] = 0;
+        c->prof_n[i] = 0;
+    }
+    return VSAOGM_OK;
+}
+
+int64_t vsaogm_launch_count(const vsaogm_ctx *c) { return c ? c->launches : 0; }
+
+int vsaogm_test_gemm(const void *A, const void *B, int32_t M, int32_t N, int32_t K, vsaogm_precision prec, float *C,
+                     void *stream)
+{
+    if (!A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 != 0) return VSAOGM_EINVAL_ARG;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int rc = vsa_gemm_raw(A, B, M, N, K, prec, C, (cudaStream_t)stream, sms);
+    if (rc) return rc;
+    VSA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return VSAOGM_OK;
+}
+
+}  // extern "C"

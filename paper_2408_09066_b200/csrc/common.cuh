@@ -1,0 +1,202 @@
+// common.cuh -- context layout, error plumbing and sm_100a PTX helpers shared
+// by the library's translation units.  Product code only (the oracle never
+// includes anything from here).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "vsaogm.h"
+
+#define VSA_CUDA_TRY(expr)                                              \
+    do {                                                                \
+        cudaError_t _e = (expr);                                        \
+        if (_e != cudaSuccess) return VSAOGM_ECUDA;                     \
+    } while (0)
+
+// Device error-flag bits set by the encode kernel (deferred errors).
+#define VSA_ERRBIT_LABEL 1
+#define VSA_ERRBIT_NONFINITE 2
+
+// Decode GEMM tiling (tcgen05, cta_group::1): 128 x 256 output tile, K chunk
+// of 64 16-bit elements (one 128-byte swizzle row), 4-stage TMA ring.
+#define VSA_BM 128
+#define VSA_BN 256
+#define VSA_BK 64
+#define VSA_STAGES 4
+
+struct ProfRec {
+    int kid;
+    cudaEvent_t a, b;
+};
+
+struct vsaogm_ctx {
+    int device = 0;
+    int num_sms = 148;
+    int32_t D = 0;      // phasor dimensions
+    int32_t Dp = 0;     // D rounded up to 32 (k-group of the interleaved K layout)
+    int32_t Kp = 0;     // 2 * Dp: real contraction length of the decode GEMM
+    double l = 1.0;
+    vsaogm_bounds bounds{};
+    double cx = 0, cy = 0;            // phase origin = bounds centre
+    std::vector<double> thx, thy;     // host fp64 theta
+
+    // device state
+    float *d_wx = nullptr, *d_wy = nullptr;        // theta / l, fp32 rad/m [Dp] (0-padded)
+    double *d_wx64 = nullptr, *d_wy64 = nullptr;   // theta / l, fp64 [Dp]
+    double *d_m = nullptr;                         // committed memories [2][Dp][2]
+    double *d_pending = nullptr;                   // pending memories  [2][Dp][2]
+    long long *d_counts = nullptr;                 // [2]
+    long long *d_pcounts = nullptr;                // pending counts [2]
+    double *d_norm2 = nullptr;                     // ||m_c||^2 [2]
+    int *d_err = nullptr;                          // deferred error bits
+    float2 *d_part = nullptr;                      // encode chunk partials
+    size_t part_cap = 0;                           // in float2
+    long long *d_part_cnt = nullptr;
+    size_t part_cnt_cap = 0;
+    float2 *d_stage_xy = nullptr;                  // host-encode staging
+    uint8_t *d_stage_lab = nullptr;
+    size_t stage_cap = 0;
+
+    // decode tables and buffers
+    void *d_A = nullptr;  size_t A_cap = 0;        // bytes
+    void *d_B = nullptr;  size_t B_cap = 0;
+    bool B_valid = false;
+    double B_x0 = 0, B_res = 0; int32_t B_cols = 0; int B_prec = -1;
+    float *d_hb = nullptr; size_t hb_cap = 0;      // [2][R_ext][cols] fp32
+    float *d_S = nullptr; size_t S_cap = 0;        // host-entropy scratch
+    uint8_t *d_lab = nullptr; size_t lab_cap = 0;
+
+    // last decode geometry
+    bool decoded = false;
+    int32_t g_rows = 0, g_cols = 0, g_r0 = 0, g_r1 = 0, g_rlo = 0, g_rext = 0, g_halo = 0;
+
+    cudaStream_t stream = nullptr;
+    bool pending_taken = false;   // multi-rank mode
+    bool dirty = false;           // pending holds uncommitted work
+
+    // profiling
+    bool prof = false;
+    std::vector<ProfRec> prof_live;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[VSAOGM_NKERNELS] = {0};
+    int64_t prof_n[VSAOGM_NKERNELS] = {0};
+    int64_t launches = 0;
+};
+
+// ---- profiling brackets (api.cu) -------------------------------------------
+int vsa_prof_begin(vsaogm_ctx *c, int kid, cudaEvent_t *a);
+void vsa_prof_end(vsaogm_ctx *c, int kid, cudaEvent_t a);
+
+// ---- launchers implemented in the kernel translation units -----------------
+int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
+int vsa_launch_commit(vsaogm_ctx *c);
+int vsa_launch_norms(vsaogm_ctx *c);
+int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec);
+int vsa_launch_table_A(vsaogm_ctx *c, double y0, double res, int32_t r_lo, int32_t r_ext, int prec);
+int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float inv_scale,
+                           float *hb, float *q, int32_t r_ext, int32_t band_off, int32_t band_rows);
+int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab);
+int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
+                 cudaStream_t s, int num_sms);
+
+// ---- PTX helpers (sm_100a) ---------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// K-major operand tile in shared memory, 128-byte swizzle (matches the TMA
+// SWIZZLE_128B box of 64 16-bit elements per row): 8-row atoms of 1024 B.
+// Descriptor fields (tcgen05 shared-memory matrix descriptor): start address
+// >> 4 in [0,14), leading byte offset >> 4 in [16,30) (unused for swizzled
+// K-major, 1), stride byte offset >> 4 in [32,46) (1024 B between 8-row
+// groups), version 1 in [46,48), swizzle mode 2 (128B) in [61,64).
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr)
+{
+    return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A/B format
+// (bits 7-9, 10-12: 0 = f16, 1 = bf16), both K-major, N >> 3 at bit 17,
+// M >> 4 at bit 24.
+__host__ __device__ __forceinline__ uint32_t make_idesc_f16(int bf16, int M, int N)
+{
+    return (1u << 4) | ((uint32_t)bf16 << 7) | ((uint32_t)bf16 << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+
+#define TMEM_LD_32x32b_X32(taddr, v)                                                                          \
+    asm volatile(                                                                                             \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                                             \
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"                                             \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                            \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),     \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),            \
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),          \
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),          \
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                               \
+        : "r"(taddr))
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -1,0 +1,242 @@
+// encode.cu -- K2 encode/bundle, K3 partial reduction, commit and norms.
+//
+// K2 computes, for every point i (label psi_i) and phasor dimension k,
+//     E_k(x_i, y_i) = exp(i (w^x_k (x_i - c_x) + w^y_k (y_i - c_y))),  w = theta / l,
+// (Eq. 9, length scale Eq. 8 :232-235) and bundles it into
+// class memory psi_i by addition (Eq. 5 :216-219; Alg. 1 :260-285 with delta=1).
+// The phase origin (c_x, c_y) is the bounds centre: a per-k rotation common to
+// every point that cancels in the decode (Eq. 11) and keeps the fp32 phase
+// small.  The kernel is SFU-bound: one MUFU sin + one MUFU cos per phasor.
+//
+// Layout: threads own phasor dimensions k (KT per thread, strided by the block
+// size so the w loads and partial stores are coalesced); the points of the
+// block's chunk are staged through shared memory and read as warp-uniform
+// broadcasts, so the per-point label branch is uniform across the warp.  Each
+// block writes its chunk's fp32 partial sums; K3 adds chunks in a fixed order
+// in fp64 (deterministic, no float atomics).
+#include "common.cuh"
+
+namespace {
+
+constexpr int ENC_THREADS = 128;
+constexpr int ENC_TILE = 256;   // points staged per shared-memory tile
+
+template <int KT>
+__global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
+    const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
+    const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
+    float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
+{
+    __shared__ float4 s_pt[ENC_TILE];
+    __shared__ long long s_cnt[2][ENC_THREADS / 32];
+    const int tid = threadIdx.x;
+    const int kb = blockIdx.x;
+    const int64_t chunk = blockIdx.y;
+    const int kbase = kb * ENC_THREADS * KT + tid;
+
+    float fx[KT], fy[KT];
+    float a0r[KT], a0i[KT], a1r[KT], a1i[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * ENC_THREADS;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+        a0r[j] = a0i[j] = a1r[j] = a1i[j] = 0.f;
+    }
+    long long c0 = 0, c1 = 0;
+    int my_err = 0;
+    const int64_t p0 = chunk * chunk_pts;
+    const int64_t p1 = min(n, p0 + chunk_pts);
+
+    for (int64_t base = p0; base < p1; base += ENC_TILE) {
+        const int cnt = (int)min((int64_t)ENC_TILE, p1 - base);
+        __syncthreads();
+        for (int t = tid; t < cnt; t += ENC_THREADS) {
+            const float2 v = xy[base + t];
+            const int L = lab[base + t];
+            int code = L;
+            if (L > 1) { code = 2; my_err |= VSA_ERRBIT_LABEL; }
+            if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
+            // centred coordinates: fp64 subtraction, one rounding to fp32
+            const float xc = (float)((double)v.x - cx);
+            const float yc = (float)((double)v.y - cy);
+            s_pt[t] = make_float4(xc, yc, __int_as_float(code), 0.f);
+            c0 += (code == 0);
+            c1 += (code == 1);
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int p = 0; p < cnt; ++p) {
+            const float4 P = s_pt[p];                   // warp-uniform broadcast
+            const int code = __float_as_int(P.z);
+            if (code == 0) {
+#pragma unroll
+                for (int j = 0; j < KT; ++j) {
+                    float s, c;
+                    __sincosf(fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
+                    a0r[j] += c;
+                    a0i[j] += s;
+                }
+            } else if (code == 1) {
+#pragma unroll
+                for (int j = 0; j < KT; ++j) {
+                    float s, c;
+                    __sincosf(fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
+                    a1r[j] += c;
+                    a1i[j] += s;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * ENC_THREADS;
+        if (k < Dp) {
+            part[((size_t)chunk * 2 + 0) * Dp + k] = make_float2(a0r[j], a0i[j]);
+            part[((size_t)chunk * 2 + 1) * Dp + k] = make_float2(a1r[j], a1i[j]);
+        }
+    }
+    if (kb == 0) {   // counts and deferred errors once per chunk
+        if (my_err) atomicOr(err, my_err);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        }
+        if ((tid & 31) == 0) { s_cnt[0][tid >> 5] = c0; s_cnt[1][tid >> 5] = c1; }
+        __syncthreads();
+        if (tid < 2) {
+            long long s = 0;
+            for (int w = 0; w < ENC_THREADS / 32; ++w) s += s_cnt[tid][w];
+            part_cnt[chunk * 2 + tid] = s;
+        }
+    }
+}
+
+// K3: pending[c][k] += sum over chunks (fixed order, fp64) of the partials.
+__global__ void k_reduce_partials(const float2 *__restrict__ part, const long long *__restrict__ part_cnt,
+                                  int chunks, int Dp, double *__restrict__ pending, long long *__restrict__ pcount)
+{
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < 2 * Dp) {
+        const int c = idx / Dp, k = idx - c * Dp;
+        double re = 0.0, im = 0.0;
+        const float2 *p = part + (size_t)c * Dp + k;
+#pragma unroll 4
+        for (int ch = 0; ch < chunks; ++ch) {
+            const float2 v = p[(size_t)ch * 2 * Dp];
+            re += v.x;
+            im += v.y;
+        }
+        pending[2 * ((size_t)c * Dp + k)] += re;
+        pending[2 * ((size_t)c * Dp + k) + 1] += im;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 2) {
+        long long s = 0;
+        for (int ch = 0; ch < chunks; ++ch) s += part_cnt[ch * 2 + threadIdx.x];
+        pcount[threadIdx.x] += s;
+    }
+}
+
+// Commit: m += pending, pending = 0 (Alg. 3 result folded into the memories).
+__global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, long long *__restrict__ cnt,
+                         long long *__restrict__ pcnt, int n)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        m[i] += pending[i];
+        pending[i] = 0.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 2) {
+        cnt[threadIdx.x] += pcnt[threadIdx.x];
+        pcnt[threadIdx.x] = 0;
+    }
+}
+
+// ||m_c||^2 for both classes (Eq. 10), fixed-order fp64 block reduction.
+__global__ void k_norms(const double *__restrict__ m, int Dp, double *__restrict__ norm2)
+{
+    __shared__ double s[256];
+    const int c = blockIdx.x;
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < Dp; k += 256) {
+        const double re = m[2 * ((size_t)c * Dp + k)], im = m[2 * ((size_t)c * Dp + k) + 1];
+        acc += re * re + im * im;
+    }
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) norm2[c] = s[0];
+}
+
+}  // namespace
+
+int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
+{
+    const int KT = c->Dp >= 1024 ? 8 : 4;
+    const int kblocks = (c->Dp + ENC_THREADS * KT - 1) / (ENC_THREADS * KT);
+    // one full wave at ~6 resident blocks per SM, at least 64 points per chunk
+    const int64_t target_blocks = (int64_t)c->num_sms * 6;
+    int64_t chunks = (target_blocks + kblocks - 1) / kblocks;
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
+    const int64_t chunk_pts = (n + chunks - 1) / chunks;
+    chunks = (n + chunk_pts - 1) / chunk_pts;
+    const size_t need = (size_t)chunks * 2 * c->Dp;
+    if (need > c->part_cap) {
+        if (c->d_part) cudaFree(c->d_part);
+        if (cudaMalloc(&c->d_part, need * sizeof(float2)) != cudaSuccess) { c->d_part = nullptr; c->part_cap = 0; return VSAOGM_ENOMEM; }
+        c->part_cap = need;
+    }
+    if ((size_t)chunks * 2 > c->part_cnt_cap) {
+        if (c->d_part_cnt) cudaFree(c->d_part_cnt);
+        if (cudaMalloc(&c->d_part_cnt, chunks * 2 * sizeof(long long)) != cudaSuccess) { c->d_part_cnt = nullptr; c->part_cnt_cap = 0; return VSAOGM_ENOMEM; }
+        c->part_cnt_cap = chunks * 2;
+    }
+    cudaEvent_t ev;
+    vsa_prof_begin(c, VSAOGM_K_ENCODE, &ev);
+    dim3 grid(kblocks, (unsigned)chunks);
+    if (KT == 8)
+        k_encode_bundle<8><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy,
+                                                                 c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt, c->d_err);
+    else
+        k_encode_bundle<4><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy,
+                                                                 c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt, c->d_err);
+    VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_ENCODE, ev);
+    c->launches++;
+
+    vsa_prof_begin(c, VSAOGM_K_REDUCE, &ev);
+    const int threads = 256;
+    k_reduce_partials<<<(2 * c->Dp + threads - 1) / threads, threads, 0, c->stream>>>(
+        c->d_part, c->d_part_cnt, (int)chunks, c->Dp, c->d_pending, c->d_pcounts);
+    VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_REDUCE, ev);
+    c->launches++;
+    return VSAOGM_OK;
+}
+
+int vsa_launch_commit(vsaogm_ctx *c)
+{
+    cudaEvent_t ev;
+    vsa_prof_begin(c, VSAOGM_K_COMMIT, &ev);
+    const int n = 4 * c->Dp;
+    k_commit<<<(n + 255) / 256, 256, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, n);
+    VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_COMMIT, ev);
+    c->launches++;
+    return VSAOGM_OK;
+}
+
+int vsa_launch_norms(vsaogm_ctx *c)
+{
+    cudaEvent_t ev;
+    vsa_prof_begin(c, VSAOGM_K_NORMS, &ev);
+    k_norms<<<2, 256, 0, c->stream>>>(c->d_m, c->Dp, c->d_norm2);
+    VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_NORMS, ev);
+    c->launches++;
+    return VSAOGM_OK;
+}

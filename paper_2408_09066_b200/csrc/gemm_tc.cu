@@ -1,0 +1,292 @@
+// gemm_tc.cu -- K5: the decode contraction on the 5th-generation tensor cores.
+//
+//   acc[m][n] = sum_j A[m][j] B[n][j]     (A: [M][K], B: [N][K], 16-bit, K-major)
+//
+// With the tables of tables.cu, row m = (class c, band row i), column n = grid
+// column, acc = D q_c (Eq. 11 after Eq. 10 normalisation).
+// The VSA epilogue applies the Born rule p = q^2, clamped to
+// [0, 1] against rounding, and the per-cell binary entropy H_b(p) that Alg. 2
+// averages; it writes H_b for every decoded row (band +
+// halo) and q for the band's own rows.
+//
+// Kernel structure (persistent, one CTA per SM, 192 threads):
+//   warp 0      TMA producer: 4-stage ring of (A 128x64, B 256x64) tiles, SWIZZLE_128B
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b from a double-buffered TMEM accumulator
+//               (2 x 256 columns), so tile t's epilogue overlaps tile t+1's mainloop.
+// Tiles are visited m-fastest so CTAs running together share a B panel in L2.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int GEMM_THREADS = 192;
+constexpr uint32_t A_TILE_BYTES = VSA_BM * VSA_BK * 2;   // 16 KB
+constexpr uint32_t B_TILE_BYTES = VSA_BN * VSA_BK * 2;   // 32 KB
+constexpr uint32_t STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
+constexpr uint32_t TMEM_COLS = 2 * VSA_BN;                // double-buffered fp32 accumulator
+constexpr size_t GEMM_SMEM = 1024 + (size_t)VSA_STAGES * STAGE_BYTES + 256;
+
+struct Epi {
+    float *C;          // raw mode output [M][N]
+    float inv_scale;   // VSA mode: q = acc * inv_scale
+    float *hb;         // VSA mode: [M][N]
+    float *q;          // VSA mode: [2][band_rows][N] or null
+    int r_ext, band_off, band_rows;
+};
+
+__device__ __forceinline__ float hb_of_p(float p)
+{
+    // binary entropy in bits, 0 log 0 = 0; log1p keeps (1-p) log(1-p) accurate for small p
+    float h = 0.f;
+    if (p > 0.f) h = -p * log2f(p);
+    if (p < 1.f) h -= (1.f - p) * log1pf(-p) * 1.44269504088896341f;
+    return h;
+}
+
+template <int MODE>   // 0 = raw fp32 store (test hook), 1 = VSA epilogue
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_decode_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                  int K, uint32_t idesc, Epi epi)
+{
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + VSA_STAGES * A_TILE_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + VSA_STAGES * B_TILE_BYTES);
+    uint64_t *full = bars;
+    uint64_t *empty = bars + VSA_STAGES;
+    uint64_t *tfull = bars + 2 * VSA_STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int num_m = (M + VSA_BM - 1) / VSA_BM;
+    const int num_n = (N + VSA_BN - 1) / VSA_BN;
+    const int num_tiles = num_m * num_n;
+    const int num_kb = K / VSA_BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < VSA_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+            uint32_t stage = 0, phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int mb = tile % num_m, nb = tile / num_m;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    tma_load_2d(sA + stage * A_TILE_BYTES, &tmA, &full[stage], kb * VSA_BK, mb * VSA_BM);
+                    tma_load_2d(sB + stage * B_TILE_BYTES, &tmB, &full[stage], kb * VSA_BK, nb * VSA_BN);
+                    if (++stage == VSA_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[as], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + as * VSA_BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * A_TILE_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * B_TILE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < VSA_BK / 16; ++k)
+                        tc_mma_f16(d, sw128_kmajor_desc(a0 + 32 * k), sw128_kmajor_desc(b0 + 32 * k), idesc,
+                                   (kb | k) != 0);
+                    tc_commit(&empty[stage]);   // frees the smem slot once these MMAs complete
+                    if (++stage == VSA_STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tfull[as]);          // accumulator ready for the epilogue
+                if (++as == 2) { as = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        // epilogue warps 2..5: warp w may access TMEM lanes [32 (w%4), 32 (w%4) + 32)
+        const int quarter = warp & 3;
+        const int row_in_tile = quarter * 32 + lane;
+        uint32_t as = 0, aphase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int mb = tile % num_m, nb = tile / num_m;
+            mbar_wait(&tfull[as], aphase);
+            tc_fence_after();
+            const int m = mb * VSA_BM + row_in_tile;
+            int cls = 0, i = 0;
+            if (MODE == 1) { cls = m / epi.r_ext; i = m - cls * epi.r_ext; }
+            const bool q_row = MODE == 1 && epi.q && i >= epi.band_off && i < epi.band_off + epi.band_rows;
+#pragma unroll 1
+            for (int cc = 0; cc < VSA_BN / 32; ++cc) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + as * VSA_BN + cc * 32;
+                TMEM_LD_32x32b_X32(taddr, v);
+                tmem_ld_wait();
+                const int n0 = nb * VSA_BN + cc * 32;
+                if (m < M && n0 < N) {
+                    const bool full_chunk = (n0 + 32 <= N) && ((N & 3) == 0);
+                    if (MODE == 0) {
+                        float *dst = epi.C + (size_t)m * N + n0;
+                        if (full_chunk) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                *reinterpret_cast<float4 *>(dst + j) =
+                                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (n0 + j < N) dst[j] = __uint_as_float(v[j]);
+                        }
+                    } else {
+                        float qv[32], hv[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            qv[j] = __uint_as_float(v[j]) * epi.inv_scale;
+                            hv[j] = hb_of_p(fminf(qv[j] * qv[j], 1.f));
+                        }
+                        float *hdst = epi.hb + (size_t)m * N + n0;
+                        float *qdst = q_row ? epi.q + ((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n0
+                                            : nullptr;
+                        if (full_chunk) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                *reinterpret_cast<float4 *>(hdst + j) = make_float4(hv[j], hv[j + 1], hv[j + 2], hv[j + 3]);
+                                if (qdst)
+                                    *reinterpret_cast<float4 *>(qdst + j) =
+                                        make_float4(qv[j], qv[j + 1], qv[j + 2], qv[j + 3]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                if (n0 + j < N) {
+                                    hdst[j] = hv[j];
+                                    if (qdst) qdst[j] = qv[j];
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[as]);
+            if (++as == 2) { as = 0; aphase ^= 1; }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D K-major tensor map: dims {K, rows}, box {64, box_rows}, 128-byte swizzle,
+// out-of-bounds rows are zero-filled (so M, N need no padding).
+int make_map(CUtensorMap *map, const void *ptr, int rows, int K, int box_rows, int prec)
+{
+    auto fn = encode_fn();
+    if (!fn) return VSAOGM_ECUDA;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {VSA_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, prec == VSAOGM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                    const_cast<void *>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? VSAOGM_OK : VSAOGM_ECUDA;
+}
+
+template <int MODE>
+int launch(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms)
+{
+    CUtensorMap ta, tb;
+    int rc = make_map(&ta, A, M, K, VSA_BM, prec);
+    if (rc) return rc;
+    rc = make_map(&tb, B, N, K, VSA_BN, prec);
+    if (rc) return rc;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[MODE]) {
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)GEMM_SMEM));
+        attr_set[MODE] = true;
+    }
+    const int tiles = ((M + VSA_BM - 1) / VSA_BM) * ((N + VSA_BN - 1) / VSA_BN);
+    const int grid = tiles < num_sms ? tiles : num_sms;
+    const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, VSA_BM, VSA_BN);
+    k_decode_gemm<MODE><<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(ta, tb, M, N, K, idesc, epi);
+    VSA_CUDA_TRY(cudaGetLastError());
+    return VSAOGM_OK;
+}
+
+}  // namespace
+
+int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float inv_scale, float *hb, float *q,
+                           int32_t r_ext, int32_t band_off, int32_t band_rows)
+{
+    Epi e{};
+    e.inv_scale = inv_scale;
+    e.hb = hb;
+    e.q = q;
+    e.r_ext = r_ext;
+    e.band_off = band_off;
+    e.band_rows = band_rows;
+    cudaEvent_t ev;
+    vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
+    int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms);
+    if (rc) return rc;
+    vsa_prof_end(c, VSAOGM_K_DECODE_GEMM, ev);
+    c->launches++;
+    return VSAOGM_OK;
+}
+
+int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C, cudaStream_t s,
+                 int num_sms)
+{
+    Epi e{};
+    e.C = C;
+    return launch<0>(A, B, M, N, K, prec, e, s, num_sms);
+}

@@ -1,0 +1,46 @@
+"""Multi-GPU sharding of the hot path.
+
+Two independent partitions, one process per GPU:
+  * encode: rank g bundles the contiguous point slice [g N / G, (g+1) N / G)
+    into its own pending memories; ONE collective, an all-reduce (sum) of the
+    pending memories and counts over NCCL, is Alg. 3's fusion
+    of identically configured agents; every rank then commits;
+  * decode + entropy: rank g owns grid rows [g R / G, (g+1) R / G) and decodes
+    h halo rows on each side (clipped), so the window entropy needs no
+    communication.  Results stay sharded.
+
+The helpers below are pure host logic (tested on CPU with gloo, world 2) plus
+the one all-reduce call.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def point_shard(n: int, rank: int, world: int):
+    """Contiguous equal index range [lo, hi) of n points for `rank`."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def row_band(rows: int, rank: int, world: int):
+    """Row band [r0, r1) of the full grid owned by `rank`."""
+    return rows * rank // world, rows * (rank + 1) // world
+
+
+def decoded_rows(rows: int, r0: int, r1: int, halo: int):
+    """Rows the decode evaluates for band [r0, r1): the band plus halo, clipped."""
+    return max(0, r0 - halo), min(rows, r1 + halo)
+
+
+def allreduce_pending(pending: torch.Tensor, counts: torch.Tensor, group=None):
+    """Sum the pending memories and counts over all ranks (in place)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(pending, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+
+
+def fuse_and_commit(mapper, group=None):
+    """Alg. 3 across ranks, then m += pending on every rank (multi-rank mode)."""
+    allreduce_pending(mapper.pending(), mapper.pending_counts(), group)
+    mapper.commit()

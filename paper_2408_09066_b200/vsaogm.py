@@ -1,0 +1,270 @@
+"""Thin Python binding of include/vsaogm.h (argument marshalling only).
+
+Every step of the hot path runs in the sm_100a kernels of ``libvsaogm.so``;
+this module only converts torch tensors to pointers, passes the current torch
+CUDA stream, and turns error codes into exceptions.  There is no CPU fallback:
+if the in-tree library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libvsaogm.so")
+
+OK, EINVAL_DIM, EINVAL_ARG, EEMPTY, ELABEL, ENONFINITE, ENOMEM, ECUDA, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8
+F16, BF16 = 0, 1
+KERNELS = ("encode", "reduce", "commit", "norms", "table_B", "table_A", "decode_gemm", "entropy")
+
+# every symbol include/vsaogm.h declares
+EXPORTS = (
+    "vsaogm_create", "vsaogm_destroy", "vsaogm_set_stream", "vsaogm_encode_bundle", "vsaogm_encode_bundle_host",
+    "vsaogm_pending", "vsaogm_pending_counts", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
+    "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
+    "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror",
+)
+
+
+class VsaogmError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {strerror(code)} ({code})")
+
+
+class Bounds(ctypes.Structure):
+    _fields_ = [("x_min", ctypes.c_double), ("y_min", ctypes.c_double),
+                ("x_max", ctypes.c_double), ("y_max", ctypes.c_double)]
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("x0", ctypes.c_double), ("y0", ctypes.c_double), ("res", ctypes.c_double),
+                ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+                ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32), ("halo", ctypes.c_int32)]
+
+
+class EntropyParams(ctypes.Structure):
+    _fields_ = [("half_occ", ctypes.c_int32), ("half_emp", ctypes.c_int32), ("disk", ctypes.c_int32),
+                ("rho_occ", ctypes.c_float), ("rho_emp", ctypes.c_float)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the in-tree library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    sig = {
+        "vsaogm_create": ([i32, u64, f64, Bounds, ctypes.POINTER(P)], ctypes.c_int),
+        "vsaogm_destroy": ([P], None),
+        "vsaogm_set_stream": ([P, P], ctypes.c_int),
+        "vsaogm_encode_bundle": ([P, P, P, i64], ctypes.c_int),
+        "vsaogm_encode_bundle_host": ([P, P, P, i64], ctypes.c_int),
+        "vsaogm_pending": ([P, ctypes.POINTER(P), ctypes.POINTER(i64)], ctypes.c_int),
+        "vsaogm_pending_counts": ([P, ctypes.POINTER(P)], ctypes.c_int),
+        "vsaogm_commit": ([P], ctypes.c_int),
+        "vsaogm_reset": ([P], ctypes.c_int),
+        "vsaogm_decode": ([P, ctypes.POINTER(Grid), ctypes.c_int, P], ctypes.c_int),
+        "vsaogm_entropy": ([P, ctypes.POINTER(EntropyParams), P, P], ctypes.c_int),
+        "vsaogm_entropy_host": ([P, ctypes.POINTER(EntropyParams), P, P], ctypes.c_int),
+        "vsaogm_sync": ([P], ctypes.c_int),
+        "vsaogm_get_memory": ([P, P, P], ctypes.c_int),
+        "vsaogm_get_phases": ([P, P], ctypes.c_int),
+        "vsaogm_profile_enable": ([P, ctypes.c_int], ctypes.c_int),
+        "vsaogm_profile_read": ([P, P, P], ctypes.c_int),
+        "vsaogm_launch_count": ([P], i64),
+        "vsaogm_test_gemm": ([P, P, i32, i32, i32, ctypes.c_int, P, P], ctypes.c_int),
+        "vsaogm_strerror": ([ctypes.c_int], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def strerror(code: int) -> str:
+    return load().vsaogm_strerror(code).decode()
+
+
+def _check(rc: int, what: str):
+    if rc != OK:
+        raise VsaogmError(rc, what)
+
+
+def _stream_ptr() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_ptr(a) -> ctypes.c_void_p:
+    """numpy array or CPU torch tensor -> pointer."""
+    if a is None:
+        return ctypes.c_void_p(0)
+    if isinstance(a, torch.Tensor):
+        assert not a.is_cuda and a.is_contiguous()
+        return ctypes.c_void_p(a.data_ptr())
+    assert a.flags["C_CONTIGUOUS"]
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Mapper:
+    """One VSA-OGM context on the current CUDA device (vsaogm_create)."""
+
+    def __init__(self, D: int, seed: int, length_scale: float, bounds):
+        lib = load()
+        self._lib = lib
+        self.D = int(D)
+        self.Dp = (self.D + 31) // 32 * 32
+        ctx = ctypes.c_void_p()
+        _check(lib.vsaogm_create(self.D, ctypes.c_uint64(seed), float(length_scale), Bounds(*map(float, bounds)),
+                                 ctypes.byref(ctx)), "vsaogm_create")
+        self._ctx = ctx
+        self.device = torch.cuda.current_device()
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.vsaogm_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _s(self):
+        _check(self._lib.vsaogm_set_stream(self._ctx, _stream_ptr()), "vsaogm_set_stream")
+
+    # ------------------------------------------------------------------ encode
+    def encode_bundle(self, xy: torch.Tensor, labels: torch.Tensor):
+        """xy: float32 [n, 2] CUDA, labels: uint8 [n] CUDA."""
+        assert xy.is_cuda and xy.dtype == torch.float32 and xy.is_contiguous() and xy.shape[-1] == 2
+        assert labels.is_cuda and labels.dtype == torch.uint8 and labels.is_contiguous()
+        assert labels.numel() == xy.shape[0]
+        self._s()
+        _check(self._lib.vsaogm_encode_bundle(self._ctx, _ptr(xy), _ptr(labels), labels.numel()),
+               "vsaogm_encode_bundle")
+
+    def encode_bundle_host(self, xy, labels):
+        """From host memory (numpy or pinned CPU tensors); copies are queued on the stream."""
+        n = labels.shape[0]
+        self._s()
+        _check(self._lib.vsaogm_encode_bundle_host(self._ctx, _host_ptr(xy), _host_ptr(labels), n),
+               "vsaogm_encode_bundle_host")
+
+    def pending(self) -> torch.Tensor:
+        """fp64 [2, Dp, 2] CUDA view of the pending memories (for all_reduce, Alg. 3)."""
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _check(self._lib.vsaogm_pending(self._ctx, ctypes.byref(p), ctypes.byref(n)), "vsaogm_pending")
+        return _wrap_device(p.value, (2, self.Dp, 2), torch.float64, self.device)
+
+    def pending_counts(self) -> torch.Tensor:
+        p = ctypes.c_void_p()
+        _check(self._lib.vsaogm_pending_counts(self._ctx, ctypes.byref(p)), "vsaogm_pending_counts")
+        return _wrap_device(p.value, (2,), torch.int64, self.device)
+
+    def commit(self):
+        self._s()
+        _check(self._lib.vsaogm_commit(self._ctx), "vsaogm_commit")
+
+    def reset(self):
+        self._s()
+        _check(self._lib.vsaogm_reset(self._ctx), "vsaogm_reset")
+
+    # ------------------------------------------------------------------ decode
+    def decode(self, x0, y0, res, rows, cols, row_begin=0, row_end=None, halo=0, precision=F16, q_out=None):
+        row_end = rows if row_end is None else row_end
+        g = Grid(float(x0), float(y0), float(res), int(rows), int(cols), int(row_begin), int(row_end), int(halo))
+        if q_out is not None:
+            assert q_out.is_cuda and q_out.dtype == torch.float32 and q_out.is_contiguous()
+            assert q_out.numel() == 2 * (row_end - row_begin) * cols
+        self._s()
+        _check(self._lib.vsaogm_decode(self._ctx, ctypes.byref(g), int(precision), _ptr(q_out)), "vsaogm_decode")
+
+    def entropy(self, half_occ, half_emp, rho_occ, rho_emp, disk=0, s_out=None, labels_out=None):
+        p = EntropyParams(int(half_occ), int(half_emp), int(disk), float(rho_occ), float(rho_emp))
+        self._s()
+        _check(self._lib.vsaogm_entropy(self._ctx, ctypes.byref(p), _ptr(s_out), _ptr(labels_out)),
+               "vsaogm_entropy")
+
+    def entropy_host(self, half_occ, half_emp, rho_occ, rho_emp, disk=0, s_host=None, labels_host=None):
+        p = EntropyParams(int(half_occ), int(half_emp), int(disk), float(rho_occ), float(rho_emp))
+        self._s()
+        _check(self._lib.vsaogm_entropy_host(self._ctx, ctypes.byref(p), _host_ptr(s_host), _host_ptr(labels_host)),
+               "vsaogm_entropy_host")
+
+    def sync(self) -> int:
+        """Returns the deferred error code (0, ELABEL, ENONFINITE) without raising."""
+        self._s()
+        rc = self._lib.vsaogm_sync(self._ctx)
+        if rc not in (OK, ELABEL, ENONFINITE):
+            _check(rc, "vsaogm_sync")
+        return rc
+
+    # ------------------------------------------------------------------ hooks
+    def get_memory(self):
+        import numpy as np
+        self._s()
+        m = np.zeros((2, self.D, 2), dtype=np.float64)
+        cnt = np.zeros(2, dtype=np.int64)
+        _check(self._lib.vsaogm_get_memory(self._ctx, _host_ptr(m), _host_ptr(cnt)), "vsaogm_get_memory")
+        return m[..., 0] + 1j * m[..., 1], cnt
+
+    def get_phases(self):
+        import numpy as np
+        out = np.zeros((2, self.D), dtype=np.float64)
+        _check(self._lib.vsaogm_get_phases(self._ctx, _host_ptr(out)), "vsaogm_get_phases")
+        return out[0], out[1]
+
+    def profile_enable(self, on: bool = True):
+        _check(self._lib.vsaogm_profile_enable(self._ctx, int(on)), "vsaogm_profile_enable")
+
+    def profile_read(self):
+        import numpy as np
+        ms = np.zeros(len(KERNELS), dtype=np.float64)
+        n = np.zeros(len(KERNELS), dtype=np.int64)
+        self._s()
+        _check(self._lib.vsaogm_profile_read(self._ctx, _host_ptr(ms), _host_ptr(n)), "vsaogm_profile_read")
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNELS)}
+
+    def launch_count(self) -> int:
+        return int(self._lib.vsaogm_launch_count(self._ctx))
+
+
+def test_gemm(A: torch.Tensor, B: torch.Tensor, precision=F16) -> torch.Tensor:
+    """C = A @ B^T through the decode GEMM kernel (raw epilogue)."""
+    lib = load()
+    M, K = A.shape
+    N = B.shape[0]
+    C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    _check(lib.vsaogm_test_gemm(_ptr(A), _ptr(B), M, N, K, int(precision), _ptr(C), _stream_ptr()),
+           "vsaogm_test_gemm")
+    return C
+
+
+class _CAI:
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": typestr, "version": 2,
+                                         "strides": None}
+
+
+def _wrap_device(ptr: int, shape, dtype, device) -> torch.Tensor:
+    typestr = {torch.float64: "<f8", torch.int64: "<i8"}[dtype]
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CAI(ptr, shape, typestr), device=f"cuda:{device}")

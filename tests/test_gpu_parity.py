@@ -1,0 +1,341 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances (north_star):
+  heatmap   max|q_gpu - q_orc| / max|q_orc| <= 1e-3 (fp16 operands, fp32 accumulate), <= 2e-2 (bf16)
+  labels    agreement >= 99.9 % of compared cells
+  memories  ||m_gpu - m_orc|| / ||m_orc|| <= 1e-4   (fp32 phase + MUFU sincos, derived in DESIGN.md)
+  theta     bit-exact (two independent splitmix64 implementations)
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import label_tau
+from synth.lidar import Scenario
+
+pytestmark = pytest.mark.gpu
+
+Q_TOL = {0: 1e-3, 1: 2e-2}
+M_TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def _mapper(D, l, bounds, seed=0):
+    from paper_2408_09066_b200 import Mapper
+    return Mapper(D, seed, l, bounds)
+
+
+def _cuda(xy, lab):
+    return torch.from_numpy(np.ascontiguousarray(xy)).cuda(), torch.from_numpy(np.ascontiguousarray(lab)).cuda()
+
+
+def _qerr(qg, qo):
+    return max(np.abs(qg[c] - qo[c]).max() / max(np.abs(qo[c]).max(), 1e-300) for c in (0, 1))
+
+
+def _mem_err(mg, mo):
+    return max(np.linalg.norm(mg[c] - mo[c]) / max(np.linalg.norm(mo[c]), 1e-300) for c in (0, 1))
+
+
+# ------------------------------------------------------------------ building blocks
+
+def test_theta_bit_exact():
+    for D, seed in ((512, 0), (100, 7), (16384, 12345)):
+        mp = _mapper(D, 0.3, (0, 0, 1, 1), seed)
+        gx, gy = mp.get_phases()
+        ox, oy = oracle.theta(seed, D)
+        assert np.array_equal(gx, ox) and np.array_equal(gy, oy)
+        mp.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 128), (1000, 777, 640), (4000, 2000, 1024)])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_gemm_vs_torch_fp32(M, N, K, prec):
+    from paper_2408_09066_b200 import test_gemm
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    dt = torch.float16 if prec == 0 else torch.bfloat16
+    A = torch.randn(M, K, device="cuda", generator=g).to(dt)
+    B = torch.randn(N, K, device="cuda", generator=g).to(dt)
+    C = test_gemm(A, B, prec)
+    ref = A.float() @ B.float().T
+    err = (C - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-4, err
+
+
+# ------------------------------------------------------------------ end-to-end configs
+
+def _run_full(name, prec=0, q_out=True):
+    sc = Scenario(name)
+    cfg = sc.cfg
+    xy, lab = sc.all_points()
+    D, l, h = cfg["D"], cfg["l"], cfg["half"]
+    R, C, res = cfg["rows"], cfg["cols"], cfg["res"]
+    tau = label_tau(D)
+    mp = _mapper(D, l, sc.bounds)
+    mp.encode_bundle(*_cuda(xy, lab))
+    q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
+    mp.decode(0.0, 0.0, res, R, C, 0, R, h, precision=prec, q_out=q)
+    S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
+    L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
+    mp.entropy(h, h, tau, -tau, 0, S, L)
+    assert mp.sync() == 0
+    mg, cg = mp.get_memory()
+    mp.close()
+    return sc, xy, lab, mg, cg, q.cpu().numpy().astype(np.float64), S.cpu().numpy(), L.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def c1_oracle():
+    sc = Scenario("C1")
+    cfg = sc.cfg
+    xy, lab = sc.all_points()
+    tx, ty = oracle.theta(0, cfg["D"])
+    m, cnt, _ = oracle.encode(tx, ty, cfg["l"], xy, lab)
+    q = oracle.decode_grid(tx, ty, cfg["l"], m, 0, 0, cfg["res"], 0, cfg["rows"], 0, cfg["cols"])
+    return tx, ty, m, cnt, q
+
+
+def test_c1_memory_heatmap_labels(c1_oracle):
+    tx, ty, mo, co, qo = c1_oracle
+    sc, xy, lab, mg, cg, qg, Sg, Lg = _run_full("C1")
+    assert list(cg) == list(co)
+    assert _mem_err(mg, mo) <= M_TOL
+    assert _qerr(qg, qo) <= Q_TOL[0]
+    h, D = sc.cfg["half"], sc.cfg["D"]
+    tau = label_tau(D)
+    So, Lo = oracle.entropy_grid(qo, h, h, 0, tau, -tau)
+    assert (Lg == Lo).mean() >= 0.999
+    assert np.abs(Sg - So).max() <= 1e-3 * np.abs(So).max() + 1e-6
+
+
+def test_c1_bf16(c1_oracle):
+    _, _, _, _, qo = c1_oracle
+    *_, qg, _, _ = _run_full("C1", prec=1)
+    assert _qerr(qg, qo) <= Q_TOL[1]
+
+
+def test_c2_full_grid():
+    sc, xy, lab, mg, cg, qg, Sg, Lg = _run_full("C2")
+    cfg = sc.cfg
+    tx, ty = oracle.theta(0, cfg["D"])
+    mo, co, _ = oracle.encode(tx, ty, cfg["l"], xy, lab)
+    assert list(cg) == list(co)
+    assert _mem_err(mg, mo) <= M_TOL
+    qo = oracle.decode_grid(tx, ty, cfg["l"], mo, 0, 0, cfg["res"], 0, cfg["rows"], 0, cfg["cols"])
+    assert _qerr(qg, qo) <= Q_TOL[0]
+    tau = label_tau(cfg["D"])
+    So, Lo = oracle.entropy_grid(qo, cfg["half"], cfg["half"], 0, tau, -tau)
+    assert (Lg == Lo).mean() >= 0.999
+
+
+def test_c4_batch_sampled():
+    """C4 at full size (D=8192, 2000x2000 grid, one 100-scan batch) in the bench launch
+    configuration; oracle on sampled cells and their 5x5 neighbourhoods."""
+    sc = Scenario("C4")
+    cfg = sc.cfg
+    xy, lab = sc.batch(0)
+    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
+    tau = label_tau(D)
+    mp = _mapper(D, l, sc.bounds)
+    mp.encode_bundle(*_cuda(xy, lab))
+    q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
+    mp.decode(0.0, 0.0, res, R, C, 0, R, h, q_out=q)
+    L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
+    mp.entropy(h, h, tau, -tau, 0, None, L)
+    assert mp.sync() == 0
+    mg, cg = mp.get_memory()
+    mp.close()
+    qg = q.cpu().numpy()
+    Lg = L.cpu().numpy()
+    tx, ty = oracle.theta(0, D)
+    mo, co, _ = oracle.encode(tx, ty, l, xy, lab)
+    assert list(cg) == list(co)
+    assert _mem_err(mg, mo) <= M_TOL
+    rng = np.random.default_rng(0)
+    # sampled centres (incl. the grid corners / borders) with their full 5x5 windows
+    centres = [(0, 0), (R - 1, C - 1), (0, C - 1), (R - 1, 0)]
+    centres += [tuple(v) for v in rng.integers(0, [R, C], size=(60, 2))]
+    # add cells near the points (where q is large)
+    pts = rng.choice(len(lab), 40, replace=False)
+    centres += [(min(R - 1, max(0, int(xy[i, 1] / res))), min(C - 1, max(0, int(xy[i, 0] / res)))) for i in pts]
+    q_peak = np.abs(qg).reshape(2, -1).max(axis=1)
+    errs, agree = [], []
+    for (r, c) in centres:
+        ra, rb, ca, cb = max(0, r - h), min(R, r + h + 1), max(0, c - h), min(C, c + h + 1)
+        qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, ra, rb, ca, cb)
+        errs.append(max(np.abs(qg[k, ra:rb, ca:cb] - qo[k]).max() / q_peak[k] for k in (0, 1)))
+        _, lo = oracle.entropy_cells(R, C, ra, rb, ca, cb, qo, h, h, 0, tau, -tau, [r], [c])
+        agree.append(lo[0] == Lg[r, c])
+    assert max(errs) <= Q_TOL[0], max(errs)
+    assert np.mean(agree) >= 0.99   # sampled: few cells, one disagreement allowed
+
+
+# ------------------------------------------------------------------ properties and edge cases
+
+def test_single_point_self_similarity_and_empty_class():
+    D, l, res = 1024, 0.25, 0.1
+    mp = _mapper(D, l, (0, 0, 5, 5))
+    r, c = 17, 23
+    pt = np.array([[(c + 0.5) * res, (r + 0.5) * res]], np.float32)
+    mp.encode_bundle(*_cuda(pt, np.array([1], np.uint8)))
+    q = torch.empty((2, 50, 50), dtype=torch.float32, device="cuda")
+    mp.decode(0.0, 0.0, res, 50, 50, 0, 50, 1, q_out=q)
+    mp.entropy(1, 1, 0.0, 0.0)
+    assert mp.sync() == 0
+    qn = q.cpu().numpy()
+    assert abs(qn[1, r, c] - 1.0) < 2e-3
+    assert np.all(qn[0] == 0.0)                  # empty class decodes to 0 (L8)
+    assert np.abs(qn[1]).max() <= 1.0 + 2e-3
+    mp.close()
+
+
+def test_ragged_dims_and_band_stitching():
+    # D not a multiple of 32, grid not a multiple of the tiles, 3 row bands with halo == full grid
+    D, l, res, R, C, h = 100, 0.3, 0.07, 77, 300, 2
+    rng = np.random.default_rng(1)
+    xy = rng.uniform(0, [C * res, R * res], size=(5000, 2)).astype(np.float32)
+    lab = (rng.random(5000) < 0.3).astype(np.uint8)
+    mp = _mapper(D, l, (0, 0, C * res, R * res))
+    mp.encode_bundle(*_cuda(xy, lab))
+    qf = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
+    mp.decode(0, 0, res, R, C, 0, R, h, q_out=qf)
+    Lf = torch.empty((R, C), dtype=torch.uint8, device="cuda")
+    Sf = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
+    mp.entropy(h, h, 0.001, -0.001, 0, Sf, Lf)
+    tx, ty = oracle.theta(0, D)
+    mo, _, _ = oracle.encode(tx, ty, l, xy, lab)
+    qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, 0, R, 0, C)
+    assert _qerr(qf.cpu().numpy(), qo) <= Q_TOL[0]
+    from paper_2408_09066_b200.parallel import row_band
+    for g in range(3):
+        r0, r1 = row_band(R, g, 3)
+        qb = torch.empty((2, r1 - r0, C), dtype=torch.float32, device="cuda")
+        mp.decode(0, 0, res, R, C, r0, r1, h, q_out=qb)
+        Sb = torch.empty((3, r1 - r0, C), dtype=torch.float32, device="cuda")
+        Lb = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
+        mp.entropy(h, h, 0.001, -0.001, 0, Sb, Lb)
+        assert torch.equal(qb, qf[:, r0:r1])
+        assert torch.equal(Lb, Lf[r0:r1])
+        assert torch.allclose(Sb, Sf[:, r0:r1], atol=1e-6)
+    assert mp.sync() == 0
+    mp.close()
+
+
+@pytest.mark.parametrize("disk", [0, 1])
+def test_entropy_disk_and_per_class_radii(disk):
+    sc = Scenario("C1")
+    xy, lab = sc.all_points()
+    cfg = sc.cfg
+    D, l, R, C, res = cfg["D"], cfg["l"], cfg["rows"], cfg["cols"], cfg["res"]
+    h1, h0 = 3, 2
+    mp = _mapper(D, l, sc.bounds)
+    mp.encode_bundle(*_cuda(xy, lab))
+    q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
+    mp.decode(0, 0, res, R, C, 0, R, 3, q_out=q)
+    S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
+    L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
+    mp.entropy(h1, h0, 0.002, -0.002, disk, S, L)
+    assert mp.sync() == 0
+    # oracle entropy on the GPU's own q (isolates the stencil): fp32 vs fp64 sums only
+    So, Lo = oracle.entropy_grid(q.cpu().numpy().astype(np.float64), h1, h0, disk, 0.002, -0.002)
+    assert np.abs(S.cpu().numpy() - So).max() <= 2e-5
+    assert (L.cpu().numpy() == Lo).mean() >= 0.9999
+    mp.close()
+
+
+def test_streaming_equals_one_shot_and_reset():
+    sc = Scenario("C2")
+    xy, lab = sc.all_points()
+    D, l = sc.cfg["D"], sc.cfg["l"]
+    mp = _mapper(D, l, sc.bounds)
+    half = len(lab) // 2
+    mp.encode_bundle(*_cuda(xy[:half], lab[:half]))
+    mp.commit()
+    mp.encode_bundle(*_cuda(xy[half:], lab[half:]))
+    m2, c2 = mp.get_memory()
+    mp.reset()
+    m0, c0 = mp.get_memory()
+    assert np.all(m0 == 0) and list(c0) == [0, 0]
+    mp.encode_bundle(*_cuda(xy, lab))
+    m1, c1 = mp.get_memory()
+    assert list(c1) == list(c2)
+    assert _mem_err(m2, m1) <= 1e-5
+    mp.close()
+
+
+def test_errors_and_deferred_errors():
+    from paper_2408_09066_b200.vsaogm import EEMPTY, ELABEL, ENONFINITE, ESTATE, VsaogmError
+    D, l = 256, 0.3
+    mp = _mapper(D, l, (0, 0, 4, 4))
+    xy = np.array([[1, 1], [2, 2], [np.nan, 1], [3, 3]], np.float32)
+    lab = np.array([1, 7, 0, 0], np.uint8)
+    mp.encode_bundle(*_cuda(xy, lab))
+    assert mp.sync() == ELABEL
+    assert mp.sync() == 0                     # cleared after being reported
+    mg, cg = mp.get_memory()
+    tx, ty = oracle.theta(0, D)
+    mo, co, bad = oracle.encode(tx, ty, l, xy, lab)
+    assert bad == 2 and list(cg) == list(co) == [1, 1]
+    assert _mem_err(mg, mo) <= M_TOL
+    mp.encode_bundle(*_cuda(np.array([[np.inf, 0]], np.float32), np.array([0], np.uint8)))
+    assert mp.sync() == ENONFINITE
+    with pytest.raises(VsaogmError) as e:
+        mp.encode_bundle(torch.empty((0, 2), device="cuda"), torch.empty(0, dtype=torch.uint8, device="cuda"))
+    assert e.value.code == EEMPTY
+    with pytest.raises(VsaogmError) as e:
+        mp.entropy(1, 1, 0.0, 0.0)            # no decode yet
+    assert e.value.code == ESTATE
+    # multi-rank mode: decode refuses uncommitted pending work
+    mp.pending()
+    mp.encode_bundle(*_cuda(xy[:1], lab[:1]))
+    with pytest.raises(VsaogmError) as e:
+        mp.decode(0, 0, 0.1, 10, 10)
+    assert e.value.code == ESTATE
+    mp.commit()
+    mp.decode(0, 0, 0.1, 10, 10)
+    with pytest.raises(VsaogmError):
+        mp.entropy(3, 3, 0.0, 0.0)            # wider than the decode halo
+    mp.close()
+
+
+def test_multi_rank_emulated_on_one_gpu():
+    """G point shards in G contexts, pending summed on the device (the all-reduce),
+    committed: equals the 1-shot memory; decode identical up to rounding."""
+    from paper_2408_09066_b200.parallel import point_shard
+    sc = Scenario("C2")
+    xy, lab = sc.all_points()
+    D, l = sc.cfg["D"], sc.cfg["l"]
+    G = 4
+    ms = [_mapper(D, l, sc.bounds) for _ in range(G)]
+    for g, mp in enumerate(ms):
+        lo, hi = point_shard(len(lab), g, G)
+        mp.encode_bundle(*_cuda(xy[lo:hi], lab[lo:hi]))
+    pend = [mp.pending() for mp in ms]
+    cnts = [mp.pending_counts() for mp in ms]
+    torch.cuda.synchronize()
+    tot = sum(p.clone() for p in pend)
+    totc = sum(c.clone() for c in cnts)
+    for mp, p, c in zip(ms, pend, cnts):
+        p.copy_(tot)
+        c.copy_(totc)
+        mp.commit()
+    one = _mapper(D, l, sc.bounds)
+    one.encode_bundle(*_cuda(xy, lab))
+    m1, c1 = one.get_memory()
+    for mp in ms:
+        mg, cg = mp.get_memory()
+        assert list(cg) == list(c1)
+        assert _mem_err(mg, m1) <= 1e-6
+    for mp in ms + [one]:
+        mp.close()
