@@ -115,11 +115,12 @@ __global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
 
 // K3: pending[c][k] += sum over chunks (fixed order, fp64) of the partials.
 __global__ void k_reduce_partials(const float2 *__restrict__ part, const long long *__restrict__ part_cnt,
-                                  int chunks, int Dp, double *__restrict__ pending, long long *__restrict__ pcount)
+                                  int chunks, int Dp, int D, double *__restrict__ pending, long long *__restrict__ pcount)
 {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < 2 * Dp) {
         const int c = idx / Dp, k = idx - c * Dp;
+        if (k >= D) return;   // padding dimensions (w = 0) stay exactly zero
         double re = 0.0, im = 0.0;
         const float2 *p = part + (size_t)c * Dp + k;
 #pragma unroll 4
@@ -211,7 +212,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     vsa_prof_begin(c, VSAOGM_K_REDUCE, &ev);
     const int threads = 256;
     k_reduce_partials<<<(2 * c->Dp + threads - 1) / threads, threads, 0, c->stream>>>(
-        c->d_part, c->d_part_cnt, (int)chunks, c->Dp, c->d_pending, c->d_pcounts);
+        c->d_part, c->d_part_cnt, (int)chunks, c->Dp, c->D, c->d_pending, c->d_pcounts);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_REDUCE, ev);
     c->launches++;

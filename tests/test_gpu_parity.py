@@ -304,8 +304,11 @@ def test_errors_and_deferred_errors():
     assert e.value.code == ESTATE
     mp.commit()
     mp.decode(0, 0, 0.1, 10, 10)
+    mp.entropy(3, 3, 0.0, 0.0)                # whole grid: no neighbouring band, any window is fine
+    mp.decode(0, 0, 0.1, 10, 10, 0, 5, 2)
+    mp.entropy(2, 2, 0.0, 0.0)
     with pytest.raises(VsaogmError):
-        mp.entropy(3, 3, 0.0, 0.0)            # wider than the decode halo
+        mp.entropy(3, 3, 0.0, 0.0)            # wider than the decode halo of a band
     mp.close()
 
 
