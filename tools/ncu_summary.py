@@ -1,0 +1,97 @@
+#!/usr/bin/env python3
+"""Summarise an ncu capture (--set full .ncu-rep) and a launch list (.csv) into profiles/.
+
+  python tools/ncu_summary.py <tag>        reads gpurun_out/prof_<tag>.ncu-rep, gpurun_out/launches_<tag>.csv
+                                           writes profiles/<tag>_ncu_summary.md, profiles/ncu_traffic.json
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__cycles_elapsed.avg.per_second", "sm clock"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe %"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("launch__registers_per_thread", "regs/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+]
+SHORT = {"k_encode_bundle": "encode", "k_decode_gemm": "decode_gemm", "k_entropy": "entropy",
+         "k_table_A": "table_A", "k_table_B": "table_B", "k_reduce_partials": "reduce", "k_commit": "commit",
+         "k_norms": "norms"}
+
+
+def short(name):
+    for k, v in SHORT.items():
+        if k in name:
+            return v
+    return name[:60]
+
+
+def to_bytes(val, unit):
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    return float(val) * mult
+
+
+def main(tag):
+    rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    lines = [f"# ncu summary `{tag}` (`--set full --clock-control none`, one capture per kernel; cold-cache, serialised)",
+             "", "| kernel | " + " | ".join(m[1] for m in METRICS) + " |", "|---" * (len(METRICS) + 1) + "|"]
+    traffic = {}
+    for r in data:
+        name = short(r[col["Kernel Name"]])
+        vals = []
+        for m, _ in METRICS:
+            i = col.get(m)
+            vals.append(f"{r[i]} {units[i]}".strip() if i is not None else "n/a")
+        lines.append(f"| {name} | " + " | ".join(vals) + " |")
+        rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
+        wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
+        traffic.setdefault(name, rd + wr)
+    launches = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
+    if os.path.exists(launches):
+        txt = open(launches).read()
+        start = txt.find('"ID"')
+        lrows = list(csv.reader(io.StringIO(txt[start:])))
+        h = lrows[0]
+        ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+        tot = defaultdict(float)
+        cnt = defaultdict(int)
+        for r in lrows[1:]:
+            if len(r) <= vi:
+                continue
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
+            v = float(r[vi].replace(",", "")) * scale
+            tot[short(r[ki])] += v
+            cnt[short(r[ki])] += 1
+        s = sum(tot.values())
+        lines += ["", "## Launch list (every launch of the profiled bench command, `gpu__time_duration.sum`)", "",
+                  "| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+        for k in sorted(tot, key=lambda k: -tot[k]):
+            lines.append(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {tot[k] / cnt[k]:.1f} | {tot[k] / s:.3f} |")
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    out = os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md")
+    open(out, "w").write("\n".join(lines) + "\n")
+    json.dump({"tag": tag, **traffic}, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    print(out)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
