@@ -194,9 +194,11 @@ int64_t vsaogm_launch_count(const vsaogm_ctx *ctx);
 
 /* Test hook: the decode GEMM kernel alone.  C[M][N] (float32, row-major) =
  * A[M][K] . B[N][K]^T with A, B 16-bit (precision) K-major device arrays,
- * K a multiple of 64, 1 <= M, N.  Runs on `stream` and synchronises it. */
+ * K a multiple of 64, 1 <= M, N.  kernel: -1 library default, 0 the CTA-pair
+ * (cta_group::2) kernel, 1 the single-CTA kernel.  Runs on `stream` and
+ * synchronises it. */
 int vsaogm_test_gemm(const void *A_dev, const void *B_dev, int32_t M, int32_t N, int32_t K,
-                     vsaogm_precision precision, float *C_dev, void *stream);
+                     vsaogm_precision precision, int32_t kernel, float *C_dev, void *stream);
 
 /* Name of an error code. */
 const char *vsaogm_strerror(int code);

@@ -126,6 +126,7 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
     do {
         if (cudaGetDevice(&c->device) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
         cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+        if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
         c->D = D;
         c->Dp = (D + 31) / 32 * 32;
         c->Kp = 2 * c->Dp;
@@ -139,17 +140,17 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         for (int k = 0; k < D; ++k) c->thx[k] = kPi * (1.0 - 2.0 * ((double)(splitmix64(s) >> 11) * 0x1.0p-53));
         for (int k = 0; k < D; ++k) c->thy[k] = kPi * (1.0 - 2.0 * ((double)(splitmix64(s) >> 11) * 0x1.0p-53));
         std::vector<float> wx(c->Dp, 0.f), wy(c->Dp, 0.f);
-        std::vector<double> wx64(c->Dp, 0.0), wy64(c->Dp, 0.0);
+        std::vector<double> tx(c->Dp, 0.0), ty(c->Dp, 0.0);
         for (int k = 0; k < D; ++k) {
-            wx64[k] = c->thx[k] / length_scale;
-            wy64[k] = c->thy[k] / length_scale;
-            wx[k] = (float)wx64[k];
-            wy[k] = (float)wy64[k];
+            wx[k] = (float)(c->thx[k] / length_scale);             // rad per metre (encode)
+            wy[k] = (float)(c->thy[k] / length_scale);
+            tx[k] = c->thx[k] / (2.0 * kPi * length_scale);       // turns per metre (tables)
+            ty[k] = c->thy[k] / (2.0 * kPi * length_scale);
         }
         if ((rc = dev_alloc_zero(&c->d_wx, c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_wy, c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_wx64, c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_wy64, c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_tx_turns, c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_ty_turns, c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_m, 4 * (size_t)c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_pending, 4 * (size_t)c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_counts, 2))) break;
@@ -158,8 +159,8 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         if ((rc = dev_alloc_zero(&c->d_err, 1))) break;
         if (cudaMemcpy(c->d_wx, wx.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(c->d_wy, wy.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(c->d_wx64, wx64.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(c->d_wy64, wy64.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaMemcpy(c->d_tx_turns, tx.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c->d_ty_turns, ty.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
             rc = VSAOGM_ECUDA;
             break;
         }
@@ -176,7 +177,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
 {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
-    void *ptrs[] = {c->d_wx, c->d_wy, c->d_wx64, c->d_wy64, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
+    void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
                     c->d_norm2, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_S, c->d_lab};
     for (void *p : ptrs)
@@ -408,14 +409,15 @@ int vsaogm_profile_read(vsaogm_ctx *c, double *ms, int64_t *launches)
 
 int64_t vsaogm_launch_count(const vsaogm_ctx *c) { return c ? c->launches : 0; }
 
-int vsaogm_test_gemm(const void *A, const void *B, int32_t M, int32_t N, int32_t K, vsaogm_precision prec, float *C,
-                     void *stream)
+int vsaogm_test_gemm(const void *A, const void *B, int32_t M, int32_t N, int32_t K, vsaogm_precision prec,
+                     int32_t kernel, float *C, void *stream)
 {
-    if (!A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 != 0) return VSAOGM_EINVAL_ARG;
+    if (!A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 != 0 || kernel < -1 || kernel > 1)
+        return VSAOGM_EINVAL_ARG;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int rc = vsa_gemm_raw(A, B, M, N, K, prec, C, (cudaStream_t)stream, sms);
+    int rc = vsa_gemm_raw(A, B, M, N, K, prec, C, (cudaStream_t)stream, sms, kernel);
     if (rc) return rc;
     VSA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     return VSAOGM_OK;

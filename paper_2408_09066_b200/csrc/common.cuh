@@ -41,13 +41,14 @@ struct vsaogm_ctx {
     int32_t Dp = 0;     // D rounded up to 32 (k-group of the interleaved K layout)
     int32_t Kp = 0;     // 2 * Dp: real contraction length of the decode GEMM
     double l = 1.0;
+    int enc_npoly = 2;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta
 
     // device state
     float *d_wx = nullptr, *d_wy = nullptr;        // theta / l, fp32 rad/m [Dp] (0-padded)
-    double *d_wx64 = nullptr, *d_wy64 = nullptr;   // theta / l, fp64 [Dp]
+    double *d_tx_turns = nullptr, *d_ty_turns = nullptr;   // theta / (2 pi l), fp64 turns per metre [Dp]
     double *d_m = nullptr;                         // committed memories [2][Dp][2]
     double *d_pending = nullptr;                   // pending memories  [2][Dp][2]
     long long *d_counts = nullptr;                 // [2]
@@ -102,7 +103,7 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float 
                            float *hb, float *q, int32_t r_ext, int32_t band_off, int32_t band_rows);
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab);
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
-                 cudaStream_t s, int num_sms);
+                 cudaStream_t s, int num_sms, int variant);
 
 // ---- PTX helpers (sm_100a) ---------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -200,3 +201,68 @@ __host__ __device__ __forceinline__ uint32_t make_idesc_f16(int bf16, int M, int
         : "r"(taddr))
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---- CTA-pair (cta_group::2) helpers -----------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// wait with cluster-scope acquire (arrivals may come from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// arrive on the barrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t cta)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(bar)), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+
+// 2-SM TMA load: data lands in this CTA's shared memory, the transaction bytes
+// are counted on the barrier of CTA 0 of the pair (peer bit 24 cleared).
+__device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_mma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// commit the issuing thread's prior tcgen05 ops to the barrier at this offset in both CTAs
+__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar)
+{
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}

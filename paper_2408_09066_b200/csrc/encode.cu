@@ -21,7 +21,48 @@ namespace {
 constexpr int ENC_THREADS = 128;
 constexpr int ENC_TILE = 256;   // points staged per shared-memory tile
 
-template <int KT>
+// sin/cos on the FMA + ALU pipes (no MUFU): quadrant reduction by the
+// magic-number rint, 3-term Cody-Waite pi/2, then the degree-7 / degree-8
+// minimax polynomials of Cephes sinf/cosf (Moshier) on [-pi/4, pi/4]
+// (|error| ~ 1e-7 there, i.e. as accurate as MUFU.SIN/COS).  Used for a
+// fraction of the phasors so the XU (MUFU) pipe and the issue slots are
+// both busy: the encode is SFU-bound otherwise.
+__device__ __forceinline__ void sincos_poly(float phi, float *s_out, float *c_out)
+{
+    const float magic = 12582912.f;                 // 1.5 * 2^23: x + magic rounds x to an integer
+    const float tq = fmaf(phi, 0.636619772367581343f, magic);   // phi * 2/pi + magic
+    const int qi = __float_as_int(tq);              // low bits hold q mod 2^22
+    const float q = tq - magic;
+    float r = fmaf(q, -1.5703125f, phi);
+    r = fmaf(q, -4.837512969970703125e-4f, r);
+    r = fmaf(q, -7.54978995489188216e-8f, r);
+    const float r2 = r * r;
+    float sp = fmaf(r2, -1.9515295891e-4f, 8.3321608736e-3f);
+    sp = fmaf(sp, r2, -1.6666654611e-1f);
+    const float s = fmaf(sp * r2, r, r);
+    float cp = fmaf(r2, 2.443315711809948e-5f, -1.388731625493765e-3f);
+    cp = fmaf(cp, r2, 4.166664568298827e-2f);
+    const float c = fmaf(cp * r2, r2, fmaf(r2, -0.5f, 1.0f));
+    // angle = q pi/2 + r: q=0 (s, c), q=1 (c, -s), q=2 (-s, -c), q=3 (-c, s)
+    const bool sw = qi & 1;
+    float so = sw ? c : s;
+    float co = sw ? s : c;
+    so = __int_as_float(__float_as_int(so) ^ ((qi & 2) << 30));
+    co = __int_as_float(__float_as_int(co) ^ (((qi + 1) & 2) << 30));
+    *s_out = so;
+    *c_out = co;
+}
+
+// Phasor j of KT: the last NPOLY of each thread's KT dimensions use the
+// polynomial, the others MUFU.SIN / MUFU.COS (__sincosf).
+template <int KT, int NPOLY>
+__device__ __forceinline__ void phasor(int j, float phi, float *s, float *c)
+{
+    if (j >= KT - NPOLY) sincos_poly(phi, s, c);
+    else __sincosf(phi, s, c);
+}
+
+template <int KT, int NPOLY>
 __global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
     const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
     const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
@@ -73,7 +114,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
 #pragma unroll
                 for (int j = 0; j < KT; ++j) {
                     float s, c;
-                    __sincosf(fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
+                    phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
                     a0r[j] += c;
                     a0i[j] += s;
                 }
@@ -81,7 +122,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
 #pragma unroll
                 for (int j = 0; j < KT; ++j) {
                     float s, c;
-                    __sincosf(fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
+                    phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
                     a1r[j] += c;
                     a1i[j] += s;
                 }
@@ -113,24 +154,40 @@ __global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
     }
 }
 
-// K3: pending[c][k] += sum over chunks (fixed order, fp64) of the partials.
-__global__ void k_reduce_partials(const float2 *__restrict__ part, const long long *__restrict__ part_cnt,
-                                  int chunks, int Dp, int D, double *__restrict__ pending, long long *__restrict__ pcount)
+// K3: pending[c][k] += sum over chunks of the partials, fp64, fixed order:
+// block (32 k-lanes) x (RED_SLICES chunk slices); slice s sums chunks s, s+S, ...
+// in order, then slice sums are added in slice order (deterministic).
+constexpr int RED_SLICES = 8;
+__global__ void __launch_bounds__(32 * RED_SLICES) k_reduce_partials(
+    const float2 *__restrict__ part, const long long *__restrict__ part_cnt, int chunks, int Dp, int D,
+    double *__restrict__ pending, long long *__restrict__ pcount)
 {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < 2 * Dp) {
-        const int c = idx / Dp, k = idx - c * Dp;
-        if (k >= D) return;   // padding dimensions (w = 0) stay exactly zero
-        double re = 0.0, im = 0.0;
-        const float2 *p = part + (size_t)c * Dp + k;
+    __shared__ double s_re[RED_SLICES][32], s_im[RED_SLICES][32];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int idx = blockIdx.x * 32 + tx;          // over 2 * Dp: (class, k)
+    const bool live = idx < 2 * Dp;
+    double re = 0.0, im = 0.0;
+    if (live) {
+        const float2 *p = part + idx;              // part[(ch*2 + c)*Dp + k] = part[ch*2*Dp + idx]
 #pragma unroll 4
-        for (int ch = 0; ch < chunks; ++ch) {
+        for (int ch = ty; ch < chunks; ch += RED_SLICES) {
             const float2 v = p[(size_t)ch * 2 * Dp];
             re += v.x;
             im += v.y;
         }
-        pending[2 * ((size_t)c * Dp + k)] += re;
-        pending[2 * ((size_t)c * Dp + k) + 1] += im;
+    }
+    s_re[ty][tx] = re;
+    s_im[ty][tx] = im;
+    __syncthreads();
+    if (ty == 0 && live) {
+        const int c = idx / Dp, k = idx - c * Dp;
+        if (k < D) {   // padding dimensions (w = 0 accumulate cos 0 = 1) stay exactly zero
+            double r = 0.0, i = 0.0;
+#pragma unroll
+            for (int s = 0; s < RED_SLICES; ++s) { r += s_re[s][tx]; i += s_im[s][tx]; }
+            pending[2 * (size_t)idx] += r;
+            pending[2 * (size_t)idx + 1] += i;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x < 2) {
         long long s = 0;
@@ -199,19 +256,29 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENCODE, &ev);
     dim3 grid(kblocks, (unsigned)chunks);
-    if (KT == 8)
-        k_encode_bundle<8><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy,
-                                                                 c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt, c->d_err);
-    else
-        k_encode_bundle<4><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy,
-                                                                 c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt, c->d_err);
+#define VSA_ENC_LAUNCH(KT_, NP_)                                                                                 \
+    k_encode_bundle<KT_, NP_><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, n, chunk_pts, c->d_wx, \
+                                                                   c->d_wy, c->cx, c->cy, c->Dp, c->d_part,        \
+                                                                   c->d_part_cnt, c->d_err)
+    if (KT == 8) {
+        switch (c->enc_npoly) {
+        case 0: VSA_ENC_LAUNCH(8, 0); break;
+        case 1: VSA_ENC_LAUNCH(8, 1); break;
+        case 3: VSA_ENC_LAUNCH(8, 3); break;
+        case 4: VSA_ENC_LAUNCH(8, 4); break;
+        default: VSA_ENC_LAUNCH(8, 2); break;
+        }
+    } else {
+        if (c->enc_npoly == 0) VSA_ENC_LAUNCH(4, 0);
+        else VSA_ENC_LAUNCH(4, 1);
+    }
+#undef VSA_ENC_LAUNCH
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENCODE, ev);
     c->launches++;
 
     vsa_prof_begin(c, VSAOGM_K_REDUCE, &ev);
-    const int threads = 256;
-    k_reduce_partials<<<(2 * c->Dp + threads - 1) / threads, threads, 0, c->stream>>>(
+    k_reduce_partials<<<(2 * c->Dp + 31) / 32, 32 * RED_SLICES, 0, c->stream>>>(
         c->d_part, c->d_part_cnt, (int)chunks, c->Dp, c->D, c->d_pending, c->d_pcounts);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_REDUCE, ev);

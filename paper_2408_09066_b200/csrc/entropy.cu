@@ -8,98 +8,123 @@
 //                                                   (Eq. 12 PAPER.md:320-328 + L14)
 //
 // Input is the per-cell H_b(q_c^2) written by the decode epilogue for the band
-// plus halo rows ([2][R_ext][cols] fp32).  Shared-memory tiled: a CTA stages a
-// (TR + 2H) x (TC + 2H) tile of both classes (zeros outside the grid), then
-// box windows use separable sums (row sums in shared memory, then column sums),
-// disk windows sum each footprint row segment directly.  HBM-bound.
+// plus halo rows ([2][R_ext][cols] fp32).  A CTA owns a TR x TC output tile:
+// it stages the (TR + 2H) x (TC + 2H) input tile of both classes in shared
+// memory with coalesced row loads (zeros outside the grid); a box window forms
+// row sums of width 2h+1 then sums 2h+1 of them down the column; a disk sums
+// each footprint row segment directly.  Clipped counts are closed-form.
+// HBM-bound: 8 B read + 1 B written per cell.
 #include "common.cuh"
 
 namespace {
 
-constexpr int TR = 16;    // output rows per CTA
+constexpr int TR = 32;    // output rows per CTA
 constexpr int TC = 128;   // output cols per CTA (one thread per column)
+constexpr int HMAX = 16;
+constexpr int ENT_THREADS = 2 * TC;   // two threads per column, each owning half of the output rows
 
-__global__ void __launch_bounds__(TC) k_entropy(const float *__restrict__ hb, int R, int C, int r_lo, int r_ext,
+__device__ __forceinline__ int isqrt_floor(int t)
+{
+    int w = (int)sqrtf((float)t);
+    while ((w + 1) * (w + 1) <= t) ++w;
+    while (w * w > t) --w;
+    return w;
+}
+
+__global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict__ hb, int R, int C, int r_lo, int r_ext,
                                                 int r0, int band_rows, int h1, int h0, int disk, float rho_occ,
                                                 float rho_emp, float *__restrict__ S, uint8_t *__restrict__ lab)
 {
     extern __shared__ float sm[];
+    __shared__ int s_w[2][2 * HMAX + 1];   // footprint half-width of each window row
     const int H = max(h1, h0);
     const int TW = TC + 2 * H, TH = TR + 2 * H;
-    float *tile[2] = {sm, sm + TH * TW};
-    float *hs = sm + 2 * TH * TW;   // [TH][TC] row sums (box)
-    const int orow0 = r0 + blockIdx.y * TR;   // first output row (full-grid index)
+    float *tile = sm;                      // [2][TH][TW]
+    float *hs = sm + 2 * TH * TW;          // [2][TH][TC] (box: row sums)
+    const int orow0 = r0 + blockIdx.y * TR;
     const int ocol0 = blockIdx.x * TC;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x & (TC - 1);     // column lane
+    const int half = threadIdx.x / TC;          // which half of the output rows
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    for (int cls = 0; cls < 2; ++cls) {
-        const float *src = hb + (size_t)cls * r_ext * C;
-        for (int idx = tid; idx < TH * TW; idx += TC) {
-            const int rr = orow0 - H + idx / TW;
-            const int cc = ocol0 - H + idx % TW;
-            float v = 0.f;
-            if (rr >= 0 && rr < R && cc >= 0 && cc < C) v = src[(size_t)(rr - r_lo) * C + cc];
-            tile[cls][idx] = v;
+    if (threadIdx.x < 2 * (2 * HMAX + 1)) {
+        const int cls = threadIdx.x / (2 * HMAX + 1), j = threadIdx.x % (2 * HMAX + 1);
+        const int h = cls == 1 ? h1 : h0;
+        const int du = j - HMAX;
+        s_w[cls][j] = (du < -h || du > h) ? -1 : (disk ? isqrt_floor(h * h - du * du) : h);
+    }
+    // stage both classes: one warp per (class, row), 5 independent loads per lane in flight
+#pragma unroll 2
+    for (int cr = warp; cr < 2 * TH; cr += ENT_THREADS / 32) {
+        const int cls = cr >= TH, row = cr - cls * TH;
+        const int rr = orow0 - H + row;
+        const bool rin = rr >= 0 && rr < R;
+        const float *srow = hb + (size_t)cls * r_ext * C + (size_t)(rr - r_lo) * C;
+        float v[(TC + 2 * HMAX) / 32];
+#pragma unroll
+        for (int j = 0; j < (TC + 2 * HMAX) / 32; ++j) {
+            const int cc = lane + 32 * j;
+            const int gc = ocol0 - H + cc;
+            v[j] = (rin && cc < TW && gc >= 0 && gc < C) ? __ldg(srow + gc) : 0.f;
         }
+        float *t = tile + cls * TH * TW + row * TW;
+#pragma unroll
+        for (int j = 0; j < (TC + 2 * HMAX) / 32; ++j)
+            if (lane + 32 * j < TW) t[lane + 32 * j] = v[j];
     }
     __syncthreads();
 
     const int col = ocol0 + tid;
-    float Sc[2][TR];
+    if (!disk) {
 #pragma unroll
-    for (int cls = 0; cls < 2; ++cls) {
-        const int h = cls == 1 ? h1 : h0;
-        const float *t = tile[cls];
-        if (!disk) {
-            __syncthreads();
-            for (int idx = tid; idx < TH * TC; idx += TC) {
-                const int row = idx / TC, cc = idx % TC;
+        for (int cls = 0; cls < 2; ++cls) {
+            const int h = cls == 1 ? h1 : h0;
+            const float *t = tile + cls * TH * TW + H + tid;
+            float *o = hs + cls * TH * TC + tid;
+            for (int row = H - h + half; row < TR + H + h; row += 2) {
                 float s = 0.f;
-                for (int dv = -h; dv <= h; ++dv) s += t[row * TW + cc + H + dv];
-                hs[idx] = s;
-            }
-            __syncthreads();
-            const int nc = min(col + h, C - 1) - max(col - h, 0) + 1;
-#pragma unroll
-            for (int r = 0; r < TR; ++r) {
-                float s = 0.f;
-                for (int du = -h; du <= h; ++du) s += hs[(r + H + du) * TC + tid];
-                const int row = orow0 + r;
-                const int nr = min(row + h, R - 1) - max(row - h, 0) + 1;
-                Sc[cls][r] = s / (float)(nr * nc);
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < TR; ++r) {
-                const int row = orow0 + r;
-                float s = 0.f;
-                int cnt = 0;
-                for (int du = -h; du <= h; ++du) {
-                    const int t2 = h * h - du * du;   // exact integer floor(sqrt(t2))
-                    int w = (int)sqrtf((float)t2);
-                    while ((w + 1) * (w + 1) <= t2) ++w;
-                    while (w * w > t2) --w;
-                    const float *tr = t + (r + H + du) * TW + tid + H;
-                    for (int dv = -w; dv <= w; ++dv) s += tr[dv];
-                    if (row + du >= 0 && row + du < R) cnt += min(col + w, C - 1) - max(col - w, 0) + 1;
-                }
-                Sc[cls][r] = cnt > 0 ? s / (float)cnt : 0.f;
+                for (int dv = -h; dv <= h; ++dv) s += t[row * TW + dv];
+                o[row * TC] = s;
             }
         }
+        __syncthreads();
     }
-
-    if (col < C) {
+    const int nc1 = min(col + h1, C - 1) - max(col - h1, 0) + 1;
+    const int nc0 = min(col + h0, C - 1) - max(col - h0, 0) + 1;
+    for (int r = half * (TR / 2); r < (half + 1) * (TR / 2); ++r) {
+        const int row = orow0 + r;
+        const int br = row - r0;
+        if (br >= band_rows) break;
+        float Sc[2];
 #pragma unroll
-        for (int r = 0; r < TR; ++r) {
-            const int row = orow0 + r;
-            const int br = row - r0;
-            if (br >= band_rows) break;
-            const float s1 = Sc[1][r], s0 = Sc[0][r];
-            const float g = s1 - s0;
+        for (int cls = 0; cls < 2; ++cls) {
+            const int h = cls == 1 ? h1 : h0;
+            float s = 0.f;
+            float cnt;
+            if (!disk) {
+                const float *o = hs + cls * TH * TC + tid;
+                for (int du = -h; du <= h; ++du) s += o[(r + H + du) * TC];
+                const int nr = min(row + h, R - 1) - max(row - h, 0) + 1;
+                cnt = (float)(nr * (cls == 1 ? nc1 : nc0));
+            } else {
+                const float *t = tile + cls * TH * TW + H + tid;
+                int n = 0;
+                for (int du = -h; du <= h; ++du) {
+                    const int w = s_w[cls][du + HMAX];
+                    const float *tr = t + (r + H + du) * TW;
+                    for (int dv = -w; dv <= w; ++dv) s += tr[dv];
+                    if (row + du >= 0 && row + du < R) n += min(col + w, C - 1) - max(col - w, 0) + 1;
+                }
+                cnt = (float)n;
+            }
+            Sc[cls] = s / cnt;
+        }
+        if (col < C) {
+            const float g = Sc[1] - Sc[0];
             const size_t o = (size_t)br * C + col;
             if (S) {
-                S[o] = s1;
-                S[(size_t)band_rows * C + o] = s0;
+                S[o] = Sc[1];
+                S[(size_t)band_rows * C + o] = Sc[0];
                 S[(size_t)2 * band_rows * C + o] = g;
             }
             if (lab) lab[o] = g >= rho_occ ? 1 : (g < rho_emp ? 0 : 2);
@@ -113,12 +138,12 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
 {
     const int H = p->half_occ > p->half_emp ? p->half_occ : p->half_emp;
     const int band = c->g_r1 - c->g_r0;
-    const size_t smem = sizeof(float) * (2 * (size_t)(TR + 2 * H) * (TC + 2 * H) + (size_t)(TR + 2 * H) * TC);
-    if (smem > 48 * 1024) VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem = sizeof(float) * (2 * (size_t)(TR + 2 * H) * (TC + 2 * H) + 2 * (size_t)(TR + 2 * H) * TC);
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((c->g_cols + TC - 1) / TC, (band + TR - 1) / TR);
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
-    k_entropy<<<grid, TC, smem, c->stream>>>(c->d_hb, c->g_rows, c->g_cols, c->g_rlo, c->g_rext, c->g_r0, band,
+    k_entropy<<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, c->g_rows, c->g_cols, c->g_rlo, c->g_rext, c->g_r0, band,
                                              p->half_occ, p->half_emp, p->disk, p->rho_occ, p->rho_emp, S, lab);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENTROPY, ev);

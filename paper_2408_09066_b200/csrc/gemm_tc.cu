@@ -9,13 +9,24 @@
 // averages; it writes H_b for every decoded row (band +
 // halo) and q for the band's own rows.
 //
-// Kernel structure (persistent, one CTA per SM, 192 threads):
-//   warp 0      TMA producer: 4-stage ring of (A 128x64, B 256x64) tiles, SWIZZLE_128B
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16)
-//   warps 2..5  epilogue: tcgen05.ld 32x32b from a double-buffered TMEM accumulator
-//               (2 x 256 columns), so tile t's epilogue overlaps tile t+1's mainloop.
-// Tiles are visited m-fastest so CTAs running together share a B panel in L2.
+// Two tcgen05 kernels, both persistent with warp-specialised roles:
+//
+// k_decode_gemm2 (default): CTA pairs (cluster 2x1, cta_group::2), UMMA
+//   M = 256 (128 rows per CTA) x N = BN (BN/2 rows of B per CTA) x K = 16.
+//   Each CTA's TMA producer loads its own A rows and its half of B into a
+//   6-stage ring and counts the bytes on CTA 0's barrier; CTA 0's single MMA
+//   thread issues for the pair and commits (multicast) to both CTAs' "slot
+//   free" and "accumulator ready" barriers; each CTA's 4 epilogue warps drain
+//   its own TMEM half (double-buffered accumulator) and signal CTA 0.  Half the
+//   B bytes per SM relative to the 1-CTA tile (L2 -> SM traffic is the limit).
+//   BN is chosen per problem from {256, 224, 192, 160, 128} to minimise
+//   waves x BN on the 74 SM pairs.
+// k_decode_gemm (1-CTA, M=128 x N=256): the first version, kept as a
+//   measured comparison point (VSAOGM_GEMM=1cta) and for the test hook.
 #include <cudaTypedefs.h>
+
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -25,8 +36,9 @@ constexpr int GEMM_THREADS = 192;
 constexpr uint32_t A_TILE_BYTES = VSA_BM * VSA_BK * 2;   // 16 KB
 constexpr uint32_t B_TILE_BYTES = VSA_BN * VSA_BK * 2;   // 32 KB
 constexpr uint32_t STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
-constexpr uint32_t TMEM_COLS = 2 * VSA_BN;                // double-buffered fp32 accumulator
+constexpr uint32_t TMEM_COLS = 512;                       // double-buffered fp32 accumulator
 constexpr size_t GEMM_SMEM = 1024 + (size_t)VSA_STAGES * STAGE_BYTES + 256;
+constexpr int STAGES2 = 6;                                // 2-CTA ring depth (32 KB / stage at BN=256)
 
 struct Epi {
     float *C;          // raw mode output [M][N]
@@ -45,6 +57,55 @@ __device__ __forceinline__ float hb_of_p(float p)
     return h;
 }
 
+// One thread's 32 consecutive accumulator columns of row m, starting at column n0.
+template <int MODE>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int m, int n0, int M, int N, const Epi &epi)
+{
+    if (m >= M || n0 >= N) return;
+    const bool full_chunk = (n0 + 32 <= N) && ((N & 3) == 0);
+    if (MODE == 0) {
+        float *dst = epi.C + (size_t)m * N + n0;
+        if (full_chunk) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                                   __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n0 + j < N) dst[j] = __uint_as_float(v[j]);
+        }
+        return;
+    }
+    const int cls = m / epi.r_ext;
+    const int i = m - cls * epi.r_ext;
+    const bool q_row = epi.q && i >= epi.band_off && i < epi.band_off + epi.band_rows;
+    float qv[32], hv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        qv[j] = __uint_as_float(v[j]) * epi.inv_scale;
+        hv[j] = hb_of_p(fminf(qv[j] * qv[j], 1.f));
+    }
+    float *hdst = epi.hb + (size_t)m * N + n0;
+    float *qdst = q_row ? epi.q + ((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n0 : nullptr;
+    if (full_chunk) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            *reinterpret_cast<float4 *>(hdst + j) = make_float4(hv[j], hv[j + 1], hv[j + 2], hv[j + 3]);
+            if (qdst) *reinterpret_cast<float4 *>(qdst + j) = make_float4(qv[j], qv[j + 1], qv[j + 2], qv[j + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (n0 + j < N) {
+                hdst[j] = hv[j];
+                if (qdst) qdst[j] = qv[j];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ 1-CTA kernel
 template <int MODE>   // 0 = raw fp32 store (test hook), 1 = VSA epilogue
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_decode_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
@@ -141,60 +202,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_wait(&tfull[as], aphase);
             tc_fence_after();
             const int m = mb * VSA_BM + row_in_tile;
-            int cls = 0, i = 0;
-            if (MODE == 1) { cls = m / epi.r_ext; i = m - cls * epi.r_ext; }
-            const bool q_row = MODE == 1 && epi.q && i >= epi.band_off && i < epi.band_off + epi.band_rows;
 #pragma unroll 1
             for (int cc = 0; cc < VSA_BN / 32; ++cc) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + as * VSA_BN + cc * 32;
                 TMEM_LD_32x32b_X32(taddr, v);
                 tmem_ld_wait();
-                const int n0 = nb * VSA_BN + cc * 32;
-                if (m < M && n0 < N) {
-                    const bool full_chunk = (n0 + 32 <= N) && ((N & 3) == 0);
-                    if (MODE == 0) {
-                        float *dst = epi.C + (size_t)m * N + n0;
-                        if (full_chunk) {
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4)
-                                *reinterpret_cast<float4 *>(dst + j) =
-                                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (n0 + j < N) dst[j] = __uint_as_float(v[j]);
-                        }
-                    } else {
-                        float qv[32], hv[32];
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            qv[j] = __uint_as_float(v[j]) * epi.inv_scale;
-                            hv[j] = hb_of_p(fminf(qv[j] * qv[j], 1.f));
-                        }
-                        float *hdst = epi.hb + (size_t)m * N + n0;
-                        float *qdst = q_row ? epi.q + ((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n0
-                                            : nullptr;
-                        if (full_chunk) {
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
-                                *reinterpret_cast<float4 *>(hdst + j) = make_float4(hv[j], hv[j + 1], hv[j + 2], hv[j + 3]);
-                                if (qdst)
-                                    *reinterpret_cast<float4 *>(qdst + j) =
-                                        make_float4(qv[j], qv[j + 1], qv[j + 2], qv[j + 3]);
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                if (n0 + j < N) {
-                                    hdst[j] = hv[j];
-                                    if (qdst) qdst[j] = qv[j];
-                                }
-                            }
-                        }
-                    }
-                }
+                epilogue_chunk<MODE>(v, m, nb * VSA_BN + cc * 32, M, N, epi);
             }
             tc_fence_before();
             mbar_arrive(&tempty[as]);
@@ -206,6 +220,133 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ 2-CTA kernel
+template <int MODE, int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    k_decode_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, uint32_t idesc, Epi epi)
+{
+    constexpr uint32_t A_BYTES = 128 * VSA_BK * 2;          // this CTA's 128 rows of A
+    constexpr uint32_t BH_BYTES = (BN / 2) * VSA_BK * 2;    // this CTA's half of B
+    constexpr uint32_t ST_BYTES = A_BYTES + BH_BYTES;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + STAGES2 * A_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + STAGES2 * BH_BYTES);
+    uint64_t *full = bars;                  // used in CTA 0: TMA bytes of both CTAs
+    uint64_t *empty = bars + STAGES2;       // both CTAs: slot free (multicast commit)
+    uint64_t *tfull = bars + 2 * STAGES2;   // both CTAs: accumulator ready (multicast commit)
+    uint64_t *tempty = tfull + 2;           // used in CTA 0: 8 epilogue warps of the pair
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+    const int num_m = (M + 255) / 256;
+    const int num_n = (N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int num_kb = K / VSA_BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+            uint32_t stage = 0, phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+                const int mb = tile % num_m, nb = tile / num_m;
+                const int arow = mb * 256 + (int)rank * 128;
+                const int brow = nb * BN + (int)rank * (BN / 2);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    if (rank == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
+                    tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow);
+                    tma_load_2d_2sm(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow);
+                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {
+            uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
+            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+                mbar_wait_cluster(&tempty[as], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + as * 256;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * BH_BYTES);
+#pragma unroll
+                    for (int k = 0; k < VSA_BK / 16; ++k)
+                        tc_mma2_f16(d, sw128_kmajor_desc(a0 + 32 * k), sw128_kmajor_desc(b0 + 32 * k), idesc,
+                                    (kb | k) != 0);
+                    tc_commit2_mc(&empty[stage]);
+                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                }
+                tc_commit2_mc(&tfull[as]);
+                if (++as == 2) { as = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int row_in_tile = (int)rank * 128 + quarter * 32 + lane;
+        uint32_t as = 0, aphase = 0;
+        for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            const int mb = tile % num_m, nb = tile / num_m;
+            mbar_wait_cluster(&tfull[as], aphase);
+            tc_fence_after();
+            const int m = mb * 256 + row_in_tile;
+#pragma unroll 1
+            for (int cc = 0; cc < BN / 32; ++cc) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + as * 256 + cc * 32;
+                TMEM_LD_32x32b_X32(taddr, v);
+                tmem_ld_wait();
+                epilogue_chunk<MODE>(v, m, nb * BN + cc * 32, M, N, epi);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&tempty[as], 0);
+            if (++as == 2) { as = 0; aphase ^= 1; }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                      : "memory");
     }
 }
@@ -241,25 +382,85 @@ int make_map(CUtensorMap *map, const void *ptr, int rows, int K, int box_rows, i
 }
 
 template <int MODE>
-int launch(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms)
+int launch1(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms)
 {
     CUtensorMap ta, tb;
     int rc = make_map(&ta, A, M, K, VSA_BM, prec);
     if (rc) return rc;
     rc = make_map(&tb, B, N, K, VSA_BN, prec);
     if (rc) return rc;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[MODE]) {
-        VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)GEMM_SMEM));
-        attr_set[MODE] = true;
-    }
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
     const int tiles = ((M + VSA_BM - 1) / VSA_BM) * ((N + VSA_BN - 1) / VSA_BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
     const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, VSA_BM, VSA_BN);
     k_decode_gemm<MODE><<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(ta, tb, M, N, K, idesc, epi);
     VSA_CUDA_TRY(cudaGetLastError());
     return VSAOGM_OK;
+}
+
+template <int MODE, int BN>
+int launch2_bn(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s,
+               int num_sms)
+{
+    CUtensorMap ta, tb;
+    int rc = make_map(&ta, A, M, K, 128, prec);
+    if (rc) return rc;
+    rc = make_map(&tb, B, N, K, BN / 2, prec);
+    if (rc) return rc;
+    const size_t smem = 1024 + (size_t)STAGES2 * (128 + BN / 2) * VSA_BK * 2 + 256;
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, 256, BN);
+    k_decode_gemm2<MODE, BN><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, M, N, K, idesc, epi);
+    VSA_CUDA_TRY(cudaGetLastError());
+    return VSAOGM_OK;
+}
+
+// BN minimising (waves x BN): the MMA time of a tile is proportional to BN.
+int pick_bn(int M, int N, int num_sms)
+{
+    static const int cands[] = {256, 224, 192, 160, 128};
+    const int pairs = num_sms / 2;
+    const int num_m = (M + 255) / 256;
+    int best = 256;
+    long best_cost = -1;
+    for (int bn : cands) {
+        const long tiles = (long)num_m * ((N + bn - 1) / bn);
+        const long cost = ((tiles + pairs - 1) / pairs) * bn;
+        if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
+    }
+    return best;
+}
+
+template <int MODE>
+int launch2(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms,
+            int bn)
+{
+    switch (bn) {
+    case 224: return launch2_bn<MODE, 224>(A, B, M, N, K, prec, epi, s, num_sms);
+    case 192: return launch2_bn<MODE, 192>(A, B, M, N, K, prec, epi, s, num_sms);
+    case 160: return launch2_bn<MODE, 160>(A, B, M, N, K, prec, epi, s, num_sms);
+    case 128: return launch2_bn<MODE, 128>(A, B, M, N, K, prec, epi, s, num_sms);
+    default: return launch2_bn<MODE, 256>(A, B, M, N, K, prec, epi, s, num_sms);
+    }
+}
+
+// variant: 0 = 2-CTA (default), 1 = 1-CTA; env VSAOGM_GEMM=1cta selects the latter,
+// VSAOGM_GEMM_BN=<n> pins the 2-CTA tile width.
+template <int MODE>
+int launch(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms,
+           int variant)
+{
+    if (variant < 0) {
+        const char *e = getenv("VSAOGM_GEMM");
+        variant = (e && strcmp(e, "1cta") == 0) ? 1 : 0;
+    }
+    if (variant == 1) return launch1<MODE>(A, B, M, N, K, prec, epi, s, num_sms);
+    int bn = pick_bn(M, N, num_sms);
+    if (const char *e = getenv("VSAOGM_GEMM_BN")) bn = atoi(e);
+    return launch2<MODE>(A, B, M, N, K, prec, epi, s, num_sms, bn);
 }
 
 }  // namespace
@@ -276,7 +477,7 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float 
     e.band_rows = band_rows;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
-    int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms);
+    int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms, -1);
     if (rc) return rc;
     vsa_prof_end(c, VSAOGM_K_DECODE_GEMM, ev);
     c->launches++;
@@ -284,9 +485,9 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float 
 }
 
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C, cudaStream_t s,
-                 int num_sms)
+                 int num_sms, int variant)
 {
     Epi e{};
     e.C = C;
-    return launch<0>(A, B, M, N, K, prec, e, s, num_sms);
+    return launch<0>(A, B, M, N, K, prec, e, s, num_sms, variant);
 }

@@ -17,14 +17,20 @@
 // so that sum_j A[m][j] B[n][j] = s_c H_c = D q_c: the GEMM epilogue multiplies by 1/D.
 // The sqrt(D) keeps |A| ~ 1 on average (16-bit operands stay normal numbers).
 //
-// Phases are reduced in fp64 (w * (x - c) in turns, minus the nearest integer)
-// and evaluated by fp32 sincospi on the reduced argument.
+// One thread owns 8 consecutive k (16-byte stores) and walks TAB_ROWS rows,
+// so theta and the scaled memory are loaded once per thread.  Phases are
+// reduced in fp64 (turns = tau_k * coordinate, minus the nearest integer) and
+// evaluated with MUFU sin/cos on the reduced argument |2 pi f| <= pi.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
 
 namespace {
+
+constexpr int TAB_THREADS = 128;
+constexpr int TAB_KT = 8;
+constexpr int TAB_ROWS = 16;
 
 template <typename T2>
 __device__ __forceinline__ T2 pack2(float a, float b);
@@ -33,64 +39,81 @@ __device__ __forceinline__ __half2 pack2<__half2>(float a, float b) { return __f
 template <>
 __device__ __forceinline__ __nv_bfloat162 pack2<__nv_bfloat162>(float a, float b) { return __floats2bfloat162_rn(a, b); }
 
-__device__ __forceinline__ void phasor64(double w, double d, float *s, float *c)
+template <typename T2>
+__device__ __forceinline__ uint4 pack8(const float *v)
 {
-    const double t = w * d * 0.15915494309189533577;   // turns
-    const double f = t - rint(t);                        // in [-1/2, 1/2]
-    sincospif((float)(2.0 * f), s, c);
+    T2 p[4] = {pack2<T2>(v[0], v[1]), pack2<T2>(v[2], v[3]), pack2<T2>(v[4], v[5]), pack2<T2>(v[6], v[7])};
+    return *reinterpret_cast<uint4 *>(p);
 }
 
-// One thread = one row x one pair of consecutive k (same 32-group).
-template <typename T2>
-__global__ void k_table_B(T2 *__restrict__ B, int cols, int Dp, int D, int Kp, const double *__restrict__ wx,
-                          double x0, double res, double cx)
+__device__ __forceinline__ void phasor_turns(double tau, double coord, float *s, float *c)
 {
-    const int halfD = Dp >> 1;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)cols * halfD) return;
-    const int col = (int)(idx / halfD);
-    const int k = 2 * (int)(idx - (int64_t)col * halfD);
-    const double x = x0 + ((double)col + 0.5) * res - cx;
-    float s0 = 0.f, c0 = 0.f, s1 = 0.f, c1 = 0.f;
-    if (k < D) phasor64(wx[k], x, &s0, &c0);
-    if (k + 1 < D) phasor64(wx[k + 1], x, &s1, &c1);
-    const int g = k >> 5, w = k & 31;
-    T2 *row = B + ((size_t)col * Kp >> 1);
-    row[(64 * g + w) >> 1] = pack2<T2>(c0, c1);
-    row[(64 * g + 32 + w) >> 1] = pack2<T2>(s0, s1);
+    const double t = tau * coord;                                               // turns
+    const double r = __dsub_rn(__dadd_rn(t, 6755399441055744.0), 6755399441055744.0);   // rint(t)
+    const float f = (float)__dsub_rn(t, r);                                     // in [-1/2, 1/2]
+    __sincosf(6.28318530717958648f * f, s, c);
 }
 
-template <typename T2>
-__global__ void k_table_A(T2 *__restrict__ A, int r_ext, int Dp, int D, int Kp, const double *__restrict__ wy,
-                          double y0, double res, int r_lo, double cy, const double *__restrict__ m,
-                          const double *__restrict__ norm2, double sqrtD)
+// IS_A = false: B[row][.] = (Re E | Im E), E = exp(2 pi i tau_k coord_row)
+// IS_A = true : A[c*rows + row][.] = (Re a | -Im a), a = E conj(s_c m_c,k)
+template <typename T2, bool IS_A>
+__global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, int rows, int Dp, int D, int Kp,
+                                                       const double *__restrict__ tau, double base, double res,
+                                                       int row0, const double *__restrict__ m,
+                                                       const double *__restrict__ norm2, double sqrtD)
 {
-    const int halfD = Dp >> 1;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)r_ext * halfD) return;
-    const int i = (int)(idx / halfD);
-    const int k = 2 * (int)(idx - (int64_t)i * halfD);
-    const double y = y0 + ((double)(r_lo + i) + 0.5) * res - cy;
-    float s[2] = {0.f, 0.f}, c[2] = {0.f, 0.f};
-    if (k < D) phasor64(wy[k], y, &s[0], &c[0]);
-    if (k + 1 < D) phasor64(wy[k + 1], y, &s[1], &c[1]);
-    const int g = k >> 5, w = k & 31;
+    const int kq = blockIdx.x * TAB_THREADS + threadIdx.x;
+    const int k0 = kq * TAB_KT;
+    if (k0 >= Dp) return;
+    const int g = k0 >> 5, w = k0 & 31;
+    double tk[TAB_KT];
 #pragma unroll
-    for (int cls = 0; cls < 2; ++cls) {
-        const double n2 = norm2[cls];
-        const float sc = n2 > 0.0 ? (float)(sqrtD / sqrt(n2)) : 0.f;
-        float re[2], nim[2];
+    for (int e = 0; e < TAB_KT; ++e) tk[e] = k0 + e < D ? tau[k0 + e] : 0.0;
+    float mr[2][TAB_KT], mi[2][TAB_KT];
+    if (IS_A) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const float mr = (float)m[2 * ((size_t)cls * Dp + k + e)] * sc;
-            const float mi = (float)m[2 * ((size_t)cls * Dp + k + e) + 1] * sc;
-            // a = (c + i s)(mr - i mi): Re a = c mr + s mi, -Im a = c mi - s mr
-            re[e] = c[e] * mr + s[e] * mi;
-            nim[e] = c[e] * mi - s[e] * mr;
+        for (int cls = 0; cls < 2; ++cls) {
+            const double n2 = norm2[cls];
+            const double sc = n2 > 0.0 ? sqrtD / sqrt(n2) : 0.0;
+#pragma unroll
+            for (int e = 0; e < TAB_KT; ++e) {
+                mr[cls][e] = (float)(m[2 * ((size_t)cls * Dp + k0 + e)] * sc);
+                mi[cls][e] = (float)(m[2 * ((size_t)cls * Dp + k0 + e) + 1] * sc);
+            }
         }
-        T2 *row = A + (((size_t)cls * r_ext + i) * Kp >> 1);
-        row[(64 * g + w) >> 1] = pack2<T2>(re[0], re[1]);
-        row[(64 * g + 32 + w) >> 1] = pack2<T2>(nim[0], nim[1]);
+    }
+    const int i0 = blockIdx.y * TAB_ROWS;
+    const int i1 = min(rows, i0 + TAB_ROWS);
+    // element offsets (in 16-byte units) of this thread's Re and Im octets within a row
+    const size_t re_off = (size_t)(64 * g + w) / 8, im_off = (size_t)(64 * g + 32 + w) / 8;
+    const size_t row_u4 = (size_t)Kp / 8;
+    for (int i = i0; i < i1; ++i) {
+        const double coord = base + ((double)(row0 + i) + 0.5) * res;
+        float cs[TAB_KT], sn[TAB_KT];
+#pragma unroll
+        for (int e = 0; e < TAB_KT; ++e) {
+            phasor_turns(tk[e], coord, &sn[e], &cs[e]);
+            if (k0 + e >= D) cs[e] = sn[e] = 0.f;
+        }
+        if (!IS_A) {
+            uint4 *row = out + (size_t)i * row_u4;
+            row[re_off] = pack8<T2>(cs);
+            row[im_off] = pack8<T2>(sn);
+        } else {
+#pragma unroll
+            for (int cls = 0; cls < 2; ++cls) {
+                float re[TAB_KT], nim[TAB_KT];
+#pragma unroll
+                for (int e = 0; e < TAB_KT; ++e) {
+                    // a = (c + i s)(mr - i mi): Re a = c mr + s mi, -Im a = c mi - s mr
+                    re[e] = cs[e] * mr[cls][e] + sn[e] * mi[cls][e];
+                    nim[e] = cs[e] * mi[cls][e] - sn[e] * mr[cls][e];
+                }
+                uint4 *row = out + ((size_t)cls * rows + i) * row_u4;
+                row[re_off] = pack8<T2>(re);
+                row[im_off] = pack8<T2>(nim);
+            }
+        }
     }
 }
 
@@ -105,6 +128,19 @@ int grow(void **p, size_t *cap, size_t need)
     return VSAOGM_OK;
 }
 
+template <bool IS_A>
+void launch_table(vsaogm_ctx *c, void *out, int rows, const double *tau, double base, double res, int row0, int prec)
+{
+    dim3 grid((c->Dp / TAB_KT + TAB_THREADS - 1) / TAB_THREADS, (rows + TAB_ROWS - 1) / TAB_ROWS);
+    const double sqrtD = sqrt((double)c->D);
+    if (prec == VSAOGM_BF16)
+        k_table<__nv_bfloat162, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>(
+            (uint4 *)out, rows, c->Dp, c->D, c->Kp, tau, base, res, row0, c->d_m, c->d_norm2, sqrtD);
+    else
+        k_table<__half2, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>(
+            (uint4 *)out, rows, c->Dp, c->D, c->Kp, tau, base, res, row0, c->d_m, c->d_norm2, sqrtD);
+}
+
 }  // namespace
 
 int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec)
@@ -114,16 +150,9 @@ int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int p
     const size_t bytes = (size_t)cols * c->Kp * 2;
     int rc = grow(&c->d_B, &c->B_cap, bytes);
     if (rc) return rc;
-    const int64_t nthr = (int64_t)cols * (c->Dp / 2);
-    const int bs = 256;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_TABLE_B, &ev);
-    if (prec == VSAOGM_BF16)
-        k_table_B<__nv_bfloat162><<<(unsigned)((nthr + bs - 1) / bs), bs, 0, c->stream>>>(
-            (__nv_bfloat162 *)c->d_B, cols, c->Dp, c->D, c->Kp, c->d_wx64, x0, res, c->cx);
-    else
-        k_table_B<__half2><<<(unsigned)((nthr + bs - 1) / bs), bs, 0, c->stream>>>(
-            (__half2 *)c->d_B, cols, c->Dp, c->D, c->Kp, c->d_wx64, x0, res, c->cx);
+    launch_table<false>(c, c->d_B, cols, c->d_tx_turns, x0 - c->cx, res, 0, prec);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_TABLE_B, ev);
     c->launches++;
@@ -137,19 +166,9 @@ int vsa_launch_table_A(vsaogm_ctx *c, double y0, double res, int32_t r_lo, int32
     const size_t bytes = (size_t)2 * r_ext * c->Kp * 2;
     int rc = grow(&c->d_A, &c->A_cap, bytes);
     if (rc) return rc;
-    const int64_t nthr = (int64_t)r_ext * (c->Dp / 2);
-    const int bs = 256;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_TABLE_A, &ev);
-    const double sqrtD = sqrt((double)c->D);
-    if (prec == VSAOGM_BF16)
-        k_table_A<__nv_bfloat162><<<(unsigned)((nthr + bs - 1) / bs), bs, 0, c->stream>>>(
-            (__nv_bfloat162 *)c->d_A, r_ext, c->Dp, c->D, c->Kp, c->d_wy64, y0, res, r_lo, c->cy, c->d_m,
-            c->d_norm2, sqrtD);
-    else
-        k_table_A<__half2><<<(unsigned)((nthr + bs - 1) / bs), bs, 0, c->stream>>>(
-            (__half2 *)c->d_A, r_ext, c->Dp, c->D, c->Kp, c->d_wy64, y0, res, r_lo, c->cy, c->d_m, c->d_norm2,
-            sqrtD);
+    launch_table<true>(c, c->d_A, r_ext, c->d_ty_turns, y0 - c->cy, res, r_lo, prec);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_TABLE_A, ev);
     c->launches++;

@@ -81,7 +81,7 @@ def load() -> ctypes.CDLL:
         "vsaogm_profile_enable": ([P, ctypes.c_int], ctypes.c_int),
         "vsaogm_profile_read": ([P, P, P], ctypes.c_int),
         "vsaogm_launch_count": ([P], i64),
-        "vsaogm_test_gemm": ([P, P, i32, i32, i32, ctypes.c_int, P, P], ctypes.c_int),
+        "vsaogm_test_gemm": ([P, P, i32, i32, i32, ctypes.c_int, i32, P, P], ctypes.c_int),
         "vsaogm_strerror": ([ctypes.c_int], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -247,13 +247,13 @@ class Mapper:
         return int(self._lib.vsaogm_launch_count(self._ctx))
 
 
-def test_gemm(A: torch.Tensor, B: torch.Tensor, precision=F16) -> torch.Tensor:
-    """C = A @ B^T through the decode GEMM kernel (raw epilogue)."""
+def test_gemm(A: torch.Tensor, B: torch.Tensor, precision=F16, kernel: int = -1) -> torch.Tensor:
+    """C = A @ B^T through the decode GEMM kernel (raw epilogue); kernel 0 = CTA pair, 1 = single CTA."""
     lib = load()
     M, K = A.shape
     N = B.shape[0]
     C = torch.empty((M, N), dtype=torch.float32, device=A.device)
-    _check(lib.vsaogm_test_gemm(_ptr(A), _ptr(B), M, N, K, int(precision), _ptr(C), _stream_ptr()),
+    _check(lib.vsaogm_test_gemm(_ptr(A), _ptr(B), M, N, K, int(precision), int(kernel), _ptr(C), _stream_ptr()),
            "vsaogm_test_gemm")
     return C
 

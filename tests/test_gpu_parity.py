@@ -59,18 +59,32 @@ def test_theta_bit_exact():
         mp.close()
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 128), (1000, 777, 640), (4000, 2000, 1024)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 128), (1000, 777, 640), (4000, 2000, 1024),
+                                   (257, 33, 192)])
 @pytest.mark.parametrize("prec", [0, 1])
-def test_gemm_vs_torch_fp32(M, N, K, prec):
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_gemm_vs_torch_fp32(M, N, K, prec, kernel):
     from paper_2408_09066_b200 import test_gemm
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     dt = torch.float16 if prec == 0 else torch.bfloat16
     A = torch.randn(M, K, device="cuda", generator=g).to(dt)
     B = torch.randn(N, K, device="cuda", generator=g).to(dt)
-    C = test_gemm(A, B, prec)
+    C = test_gemm(A, B, prec, kernel)
     ref = A.float() @ B.float().T
     err = (C - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-4, err
+
+
+@pytest.mark.parametrize("bn", [256, 224, 192, 160, 128])
+def test_gemm_pair_tile_widths(bn, monkeypatch):
+    from paper_2408_09066_b200 import test_gemm
+    monkeypatch.setenv("VSAOGM_GEMM_BN", str(bn))
+    g = torch.Generator(device="cuda").manual_seed(bn)
+    A = torch.randn(600, 320, device="cuda", generator=g).half()
+    B = torch.randn(1000, 320, device="cuda", generator=g).half()
+    C = test_gemm(A, B, 0, 0)
+    ref = A.float() @ B.float().T
+    assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-4
 
 
 # ------------------------------------------------------------------ end-to-end configs
