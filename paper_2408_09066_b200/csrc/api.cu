@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/vsaogm.h: context, theta, state machine,
 // argument checks, launch sequencing, profiling and test hooks.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -44,6 +45,12 @@ int grow_bytes(void **p, size_t *cap, size_t need)
 bool finite_all(double a, double b, double c, double d) { return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d); }
 
 }  // namespace
+
+void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, int line)
+{
+    static const bool on = getenv("VSAOGM_DEBUG") != nullptr;
+    if (on) fprintf(stderr, "vsaogm: %s failed: %s (%s:%d)\n", expr, cudaGetErrorString(e), file, line);
+}
 
 // ------------------------------------------------------------------ profiling
 
@@ -281,7 +288,8 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     const int32_t r_ext = r_hi - r_lo;
     const int64_t M = 2 * (int64_t)r_ext;
     if (M > (int64_t)1 << 30 || (int64_t)g->cols > (int64_t)1 << 30) return VSAOGM_EINVAL_ARG;
-    if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * g->cols * sizeof(float)))) return rc;
+    const size_t ldh = ((size_t)g->cols + 7) / 8 * 8;   // H_b row stride (16-byte multiple for TMA)
+    if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * ldh * sizeof(float)))) return rc;
     if ((rc = vsa_launch_norms(c))) return rc;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
     if ((rc = vsa_launch_table_A(c, g->y0, g->res, r_lo, r_ext, prec))) return rc;

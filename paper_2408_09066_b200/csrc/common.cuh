@@ -12,10 +12,15 @@
 
 #include "vsaogm.h"
 
-#define VSA_CUDA_TRY(expr)                                              \
-    do {                                                                \
-        cudaError_t _e = (expr);                                        \
-        if (_e != cudaSuccess) return VSAOGM_ECUDA;                     \
+// VSAOGM_DEBUG=1 in the environment prints the failing CUDA call to stderr.
+void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, int line);
+#define VSA_CUDA_TRY(expr)                                                       \
+    do {                                                                         \
+        cudaError_t _e = (expr);                                                 \
+        if (_e != cudaSuccess) {                                                 \
+            vsa_report_cuda_error(_e, #expr, __FILE__, __LINE__);                \
+            return VSAOGM_ECUDA;                                                 \
+        }                                                                        \
     } while (0)
 
 // Device error-flag bits set by the encode kernel (deferred errors).

@@ -8,18 +8,23 @@
 //                                                   (Eq. 12 PAPER.md:320-328 + L14)
 //
 // Input is the per-cell H_b(q_c^2) written by the decode epilogue for the band
-// plus halo rows ([2][R_ext][cols] fp32).  A CTA owns a TR x TC output tile:
-// it stages the (TR + 2H) x (TC + 2H) input tile of both classes in shared
-// memory with coalesced row loads (zeros outside the grid); a box window forms
-// row sums of width 2h+1 then sums 2h+1 of them down the column; a disk sums
-// each footprint row segment directly.  Clipped counts are closed-form.
+// plus halo rows ([2][R_ext][ldh] fp32).  A CTA owns a TR x TC output tile.
+// One 3-D TMA box load stages the (TR + 2H) x (TC + 2H) input tile of both
+// classes in shared memory; coordinates outside the decoded rows / grid
+// columns are zero-filled by the TMA unit, which is exactly the border
+// clipping of the window sums (rows outside the full grid are outside the
+// tensor by construction, L13).  A box window forms row sums of
+// width 2h+1 then sums 2h+1 of them down the column; a disk sums each
+// footprint row segment directly.  Clipped counts are closed-form.
 // HBM-bound: 8 B read + 1 B written per cell.
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace {
 
 constexpr int TR = 32;    // output rows per CTA
-constexpr int TC = 128;   // output cols per CTA (one thread per column)
+constexpr int TC = 128;   // output cols per CTA
 constexpr int HMAX = 16;
 constexpr int ENT_THREADS = 2 * TC;   // two threads per column, each owning half of the output rows
 
@@ -31,9 +36,10 @@ __device__ __forceinline__ int isqrt_floor(int t)
     return w;
 }
 
-__global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict__ hb, int R, int C, int r_lo, int r_ext,
-                                                int r0, int band_rows, int h1, int h0, int disk, float rho_occ,
-                                                float rho_emp, float *__restrict__ S, uint8_t *__restrict__ lab)
+__global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict__ hb, int ldh, int r_ext, int R,
+                                                         int C, int r_lo, int r0, int band_rows, int h1, int h0,
+                                                         int disk, float rho_occ, float rho_emp,
+                                                         float *__restrict__ S, uint8_t *__restrict__ lab)
 {
     extern __shared__ float sm[];
     __shared__ int s_w[2][2 * HMAX + 1];   // footprint half-width of each window row
@@ -45,7 +51,6 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict
     const int ocol0 = blockIdx.x * TC;
     const int tid = threadIdx.x & (TC - 1);     // column lane
     const int half = threadIdx.x / TC;          // which half of the output rows
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x < 2 * (2 * HMAX + 1)) {
         const int cls = threadIdx.x / (2 * HMAX + 1), j = threadIdx.x % (2 * HMAX + 1);
@@ -53,24 +58,25 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict
         const int du = j - HMAX;
         s_w[cls][j] = (du < -h || du > h) ? -1 : (disk ? isqrt_floor(h * h - du * du) : h);
     }
-    // stage both classes: one warp per (class, row), 5 independent loads per lane in flight
-#pragma unroll 2
-    for (int cr = warp; cr < 2 * TH; cr += ENT_THREADS / 32) {
-        const int cls = cr >= TH, row = cr - cls * TH;
-        const int rr = orow0 - H + row;
-        const bool rin = rr >= 0 && rr < R;
-        const float *srow = hb + (size_t)cls * r_ext * C + (size_t)(rr - r_lo) * C;
-        float v[(TC + 2 * HMAX) / 32];
-#pragma unroll
-        for (int j = 0; j < (TC + 2 * HMAX) / 32; ++j) {
-            const int cc = lane + 32 * j;
-            const int gc = ocol0 - H + cc;
-            v[j] = (rin && cc < TW && gc >= 0 && gc < C) ? __ldg(srow + gc) : 0.f;
+    // stage both classes with cp.async (4-byte, zero-fill outside the decoded rows / grid
+    // columns = the window clipping): every element is an independent request in flight
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int cr = warp; cr < 2 * TH; cr += ENT_THREADS / 32) {
+            const int cls = cr >= TH, row = cr - cls * TH;
+            const int rr = orow0 - H + row;               // full-grid row
+            const bool rin = rr >= 0 && rr < R && rr - r_lo < r_ext;
+            const float *srow = hb + ((size_t)cls * r_ext + (size_t)(rin ? rr - r_lo : 0)) * ldh;
+            float *t = tile + cr * TW;
+            for (int cc = lane; cc < TW; cc += 32) {
+                const int gc = ocol0 - H + cc;
+                const bool ok = rin && gc >= 0 && gc < C;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(t + cc)),
+                             "l"(srow + (ok ? gc : 0)), "r"(ok ? 4 : 0)
+                             : "memory");
+            }
         }
-        float *t = tile + cls * TH * TW + row * TW;
-#pragma unroll
-        for (int j = 0; j < (TC + 2 * HMAX) / 32; ++j)
-            if (lane + 32 * j < TW) t[lane + 32 * j] = v[j];
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
 
@@ -137,14 +143,17 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab)
 {
     const int H = p->half_occ > p->half_emp ? p->half_occ : p->half_emp;
+    const int TW = TC + 2 * H, TH = TR + 2 * H;
     const int band = c->g_r1 - c->g_r0;
-    const size_t smem = sizeof(float) * (2 * (size_t)(TR + 2 * H) * (TC + 2 * H) + 2 * (size_t)(TR + 2 * H) * TC);
+    const int ldh = (c->g_cols + 7) / 8 * 8;
+    const size_t smem = sizeof(float) * (2 * (size_t)TH * TW + 2 * (size_t)TH * TC);
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((c->g_cols + TC - 1) / TC, (band + TR - 1) / TR);
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
-    k_entropy<<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, c->g_rows, c->g_cols, c->g_rlo, c->g_rext, c->g_r0, band,
-                                             p->half_occ, p->half_emp, p->disk, p->rho_occ, p->rho_emp, S, lab);
+    k_entropy<<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols, c->g_rlo,
+                                                      c->g_r0, band, p->half_occ, p->half_emp, p->disk, p->rho_occ,
+                                                      p->rho_emp, S, lab);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENTROPY, ev);
     c->launches++;

@@ -43,9 +43,9 @@ constexpr int STAGES2 = 6;                                // 2-CTA ring depth (3
 struct Epi {
     float *C;          // raw mode output [M][N]
     float inv_scale;   // VSA mode: q = acc * inv_scale
-    float *hb;         // VSA mode: [M][N]
+    float *hb;         // VSA mode: [M][ldh], ldh = N rounded up to 8
     float *q;          // VSA mode: [2][band_rows][N] or null
-    int r_ext, band_off, band_rows;
+    int r_ext, band_off, band_rows, ldh;
 };
 
 __device__ __forceinline__ float hb_of_p(float p)
@@ -86,21 +86,26 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int m, i
         qv[j] = __uint_as_float(v[j]) * epi.inv_scale;
         hv[j] = hb_of_p(fminf(qv[j] * qv[j], 1.f));
     }
-    float *hdst = epi.hb + (size_t)m * N + n0;
-    float *qdst = q_row ? epi.q + ((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n0 : nullptr;
-    if (full_chunk) {
+    float *hdst = epi.hb + (size_t)m * epi.ldh + n0;
+    if (n0 + 32 <= N) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4 *>(hdst + j) = make_float4(hv[j], hv[j + 1], hv[j + 2], hv[j + 3]);
-            if (qdst) *reinterpret_cast<float4 *>(qdst + j) = make_float4(qv[j], qv[j + 1], qv[j + 2], qv[j + 3]);
-        }
     } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (n0 + j < N) {
-                hdst[j] = hv[j];
-                if (qdst) qdst[j] = qv[j];
-            }
+        for (int j = 0; j < 32; ++j)
+            if (n0 + j < N) hdst[j] = hv[j];
+    }
+    if (q_row) {
+        float *qdst = epi.q + ((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n0;
+        if (full_chunk) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4 *>(qdst + j) = make_float4(qv[j], qv[j + 1], qv[j + 2], qv[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n0 + j < N) qdst[j] = qv[j];
         }
     }
 }
@@ -475,6 +480,7 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float 
     e.r_ext = r_ext;
     e.band_off = band_off;
     e.band_rows = band_rows;
+    e.ldh = (N + 7) / 8 * 8;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
     int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms, -1);
