@@ -36,6 +36,143 @@ __device__ __forceinline__ int isqrt_floor(int t)
     return w;
 }
 
+__host__ __device__ constexpr int cisqrt(int t, int w = 0) { return (w + 1) * (w + 1) <= t ? cisqrt(t, w + 1) : w; }
+
+// Equal radii h1 = h0 = H <= 8 (every BASELINE config): H and the footprint
+// are compile-time, the tile is staged with 16-byte cp.async (zero-filled
+// outside the decoded rows / grid columns), and each thread keeps the row
+// sums of its 16 output rows (+2H) in registers: no second shared buffer,
+// no barrier between the two passes.
+template <int H, bool DISK>
+__global__ void __launch_bounds__(ENT_THREADS) k_entropy_fixed(const float *__restrict__ hb, int ldh, int r_ext,
+                                                               int R, int C, int r_lo, int r0, int band_rows,
+                                                               float rho_occ, float rho_emp, float *__restrict__ S,
+                                                               uint8_t *__restrict__ lab)
+{
+    constexpr int PADC = (H + 3) / 4 * 4;          // column halo rounded to 16 bytes
+    constexpr int TW = TC + 2 * PADC;              // floats per staged row
+    constexpr int TH = TR + 2 * H;
+    constexpr int CH = TW / 4;                     // 16-byte chunks per staged row
+    constexpr int RPT = TR / 2;                    // output rows per thread
+    extern __shared__ float4 sm4[];
+    float *tile = reinterpret_cast<float *>(sm4);  // [2][TH][TW]
+    const int orow0 = r0 + blockIdx.y * TR;
+    const int ocol0 = blockIdx.x * TC;
+
+    for (int idx = threadIdx.x; idx < 2 * TH * CH; idx += ENT_THREADS) {
+        const int cr = idx / CH, j = idx - cr * CH;
+        const int cls = cr >= TH, row = cr - cls * TH;
+        const int rr = orow0 - H + row;            // full-grid row
+        const int gc = ocol0 - PADC + 4 * j;       // multiple of 4
+        const bool ok = rr >= 0 && rr < R && rr - r_lo < r_ext && gc >= 0 && gc < C;
+        const int nbytes = ok ? 4 * min(4, C - gc) : 0;
+        const float *src = hb + ((size_t)cls * r_ext + (size_t)(ok ? rr - r_lo : 0)) * ldh + (ok ? gc : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(tile + cr * TW + 4 * j)),
+                     "l"(src), "r"(nbytes)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+
+    const int tid = threadIdx.x & (TC - 1);
+    const int half = threadIdx.x / TC;
+    const int col = ocol0 + tid;
+    float Sc[2][RPT];
+#pragma unroll
+    for (int cls = 0; cls < 2; ++cls) {
+        const float *t = tile + cls * TH * TW + (half * RPT) * TW + PADC + tid;
+        if (!DISK) {
+            float hs[RPT + 2 * H];
+#pragma unroll
+            for (int i = 0; i < RPT + 2 * H; ++i) {
+                float s = 0.f;
+#pragma unroll
+                for (int dv = -H; dv <= H; ++dv) s += t[i * TW + dv];
+                hs[i] = s;
+            }
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                float s = 0.f;
+#pragma unroll
+                for (int du = 0; du <= 2 * H; ++du) s += hs[r + du];
+                Sc[cls][r] = s;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                float s = 0.f;
+#pragma unroll
+                for (int du = -H; du <= H; ++du) {
+                    constexpr int dummy = 0;
+                    (void)dummy;
+                    const int w = cisqrt(H * H - du * du);
+#pragma unroll
+                    for (int dv = -w; dv <= w; ++dv) s += t[(r + H + du) * TW + dv];
+                }
+                Sc[cls][r] = s;
+            }
+        }
+    }
+    // clipped counts (closed form) and outputs
+    const int nc = min(col + H, C - 1) - max(col - H, 0) + 1;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int row = orow0 + half * RPT + r;
+        const int br = row - r0;
+        float cnt;
+        if (!DISK) {
+            cnt = (float)((min(row + H, R - 1) - max(row - H, 0) + 1) * nc);
+        } else {
+            int n = 0;
+#pragma unroll
+            for (int du = -H; du <= H; ++du) {
+                const int w = cisqrt(H * H - du * du);
+                if (row + du >= 0 && row + du < R) n += min(col + w, C - 1) - max(col - w, 0) + 1;
+            }
+            cnt = (float)n;
+        }
+        const float inv = 1.0f / cnt;
+        if (col < C && br < band_rows) {
+            const float s1 = Sc[1][r] * inv, s0 = Sc[0][r] * inv;
+            const float g = s1 - s0;
+            const size_t o = (size_t)br * C + col;
+            if (S) {
+                S[o] = s1;
+                S[(size_t)band_rows * C + o] = s0;
+                S[(size_t)2 * band_rows * C + o] = g;
+            }
+            if (lab) lab[o] = g >= rho_occ ? 1 : (g < rho_emp ? 0 : 2);
+        }
+    }
+}
+
+template <int H, bool DISK>
+int launch_fixed(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab, int ldh, dim3 grid)
+{
+    constexpr int PADC = (H + 3) / 4 * 4;
+    const size_t smem = sizeof(float) * 2 * (TR + 2 * H) * (TC + 2 * PADC);
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_fixed<H, DISK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_entropy_fixed<H, DISK><<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols,
+                                                                     c->g_rlo, c->g_r0, c->g_r1 - c->g_r0, p->rho_occ,
+                                                                     p->rho_emp, S, lab);
+    return VSAOGM_OK;
+}
+
+template <bool DISK>
+int dispatch_fixed(int H, vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab, int ldh, dim3 grid)
+{
+    switch (H) {
+    case 1: return launch_fixed<1, DISK>(c, p, S, lab, ldh, grid);
+    case 2: return launch_fixed<2, DISK>(c, p, S, lab, ldh, grid);
+    case 3: return launch_fixed<3, DISK>(c, p, S, lab, ldh, grid);
+    case 4: return launch_fixed<4, DISK>(c, p, S, lab, ldh, grid);
+    case 5: return launch_fixed<5, DISK>(c, p, S, lab, ldh, grid);
+    case 6: return launch_fixed<6, DISK>(c, p, S, lab, ldh, grid);
+    case 7: return launch_fixed<7, DISK>(c, p, S, lab, ldh, grid);
+    default: return launch_fixed<8, DISK>(c, p, S, lab, ldh, grid);
+    }
+}
+
 __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict__ hb, int ldh, int r_ext, int R,
                                                          int C, int r_lo, int r0, int band_rows, int h1, int h0,
                                                          int disk, float rho_occ, float rho_emp,
@@ -147,13 +284,21 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
     const int band = c->g_r1 - c->g_r0;
     const int ldh = (c->g_cols + 7) / 8 * 8;
     const size_t smem = sizeof(float) * (2 * (size_t)TH * TW + 2 * (size_t)TH * TC);
-    VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((c->g_cols + TC - 1) / TC, (band + TR - 1) / TR);
+    const bool fixed = p->half_occ == p->half_emp && H <= 8 && getenv("VSAOGM_ENTROPY_GENERIC") == nullptr;
+    if (!fixed)
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
-    k_entropy<<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols, c->g_rlo,
-                                                      c->g_r0, band, p->half_occ, p->half_emp, p->disk, p->rho_occ,
-                                                      p->rho_emp, S, lab);
+    if (fixed) {
+        int rc = p->disk ? dispatch_fixed<true>(H, c, p, S, lab, ldh, grid)
+                         : dispatch_fixed<false>(H, c, p, S, lab, ldh, grid);
+        if (rc) return rc;
+    } else {
+        k_entropy<<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols, c->g_rlo,
+                                                          c->g_r0, band, p->half_occ, p->half_emp, p->disk,
+                                                          p->rho_occ, p->rho_emp, S, lab);
+    }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENTROPY, ev);
     c->launches++;

@@ -268,6 +268,35 @@ def test_entropy_disk_and_per_class_radii(disk):
     mp.close()
 
 
+@pytest.mark.parametrize("disk", [0, 1])
+@pytest.mark.parametrize("h", [1, 3, 7])
+def test_entropy_equal_radii_fast_path(disk, h):
+    """The compile-time-window kernel (equal radii, h <= 8) vs the oracle stencil on the
+    GPU's own q, on a ragged grid (cols not a multiple of 4 or of the 128-column tile)."""
+    D, l, res, R, C = 256, 0.3, 0.07, 71, 203
+    rng = np.random.default_rng(h + 10 * disk)
+    xy = rng.uniform(0, [C * res, R * res], size=(3000, 2)).astype(np.float32)
+    lab = (rng.random(3000) < 0.4).astype(np.uint8)
+    mp = _mapper(D, l, (0, 0, C * res, R * res))
+    mp.encode_bundle(*_cuda(xy, lab))
+    q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
+    mp.decode(0, 0, res, R, C, 0, R, h, q_out=q)
+    S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
+    L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
+    mp.entropy(h, h, 0.001, -0.001, disk, S, L)
+    assert mp.sync() == 0
+    So, Lo = oracle.entropy_grid(q.cpu().numpy().astype(np.float64), h, h, disk, 0.001, -0.001)
+    assert np.abs(S.cpu().numpy() - So).max() <= 2e-5
+    assert (L.cpu().numpy() == Lo).mean() >= 0.9999
+    # band with halo: same rows as the full grid
+    r0, r1 = 20, 50
+    mp.decode(0, 0, res, R, C, r0, r1, h)
+    Sb = torch.empty((3, r1 - r0, C), dtype=torch.float32, device="cuda")
+    mp.entropy(h, h, 0.001, -0.001, disk, Sb, None)
+    assert torch.allclose(Sb, S[:, r0:r1], atol=1e-6)
+    mp.close()
+
+
 def test_streaming_equals_one_shot_and_reset():
     sc = Scenario("C2")
     xy, lab = sc.all_points()
