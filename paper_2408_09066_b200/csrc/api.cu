@@ -134,6 +134,7 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         if (cudaGetDevice(&c->device) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
         cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
         if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
+        if (const char *e = getenv("VSAOGM_ENC_MINB")) c->enc_minb = atoi(e);     // tuning knob (6 or 8)
         c->D = D;
         c->Dp = (D + 31) / 32 * 32;
         c->Kp = 2 * c->Dp;
@@ -163,6 +164,7 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         if ((rc = dev_alloc_zero(&c->d_counts, 2))) break;
         if ((rc = dev_alloc_zero(&c->d_pcounts, 2))) break;
         if ((rc = dev_alloc_zero(&c->d_norm2, 2))) break;
+        if ((rc = dev_alloc_zero(&c->d_mhat, 2 * (size_t)c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_err, 1))) break;
         if (cudaMemcpy(c->d_wx, wx.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(c->d_wy, wy.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -185,7 +187,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     if (!c) return;
     cudaStreamSynchronize(c->stream);
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
-                    c->d_norm2, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
+                    c->d_norm2, c->d_mhat, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_S, c->d_lab};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -279,10 +281,8 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
         (prec != VSAOGM_F16 && prec != VSAOGM_BF16))
         return VSAOGM_EINVAL_ARG;
     int rc;
-    if (c->dirty) {
-        if (c->pending_taken) return VSAOGM_ESTATE;
-        if ((rc = vsaogm_commit(c))) return rc;
-    }
+    const int do_commit = c->dirty ? 1 : 0;   // single-rank: implicit commit, fused into the norms kernel
+    if (c->dirty && c->pending_taken) return VSAOGM_ESTATE;
     const int32_t r_lo = std::max(0, g->row_begin - g->halo);
     const int32_t r_hi = std::min(g->rows, g->row_end + g->halo);
     const int32_t r_ext = r_hi - r_lo;
@@ -290,7 +290,8 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     if (M > (int64_t)1 << 30 || (int64_t)g->cols > (int64_t)1 << 30) return VSAOGM_EINVAL_ARG;
     const size_t ldh = ((size_t)g->cols + 7) / 8 * 8;   // H_b row stride (16-byte multiple for TMA)
     if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * ldh * sizeof(float)))) return rc;
-    if ((rc = vsa_launch_norms(c))) return rc;
+    if ((rc = vsa_launch_norms(c, do_commit))) return rc;
+    c->dirty = false;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
     if ((rc = vsa_launch_table_A(c, g->y0, g->res, r_lo, r_ext, prec))) return rc;
     if ((rc = vsa_launch_decode_gemm(c, (int32_t)M, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,

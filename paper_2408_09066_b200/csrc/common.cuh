@@ -47,6 +47,7 @@ struct vsaogm_ctx {
     int32_t Kp = 0;     // 2 * Dp: real contraction length of the decode GEMM
     double l = 1.0;
     int enc_npoly = 2;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
+    int enc_minb = 6;   // encode blocks resident per SM (6: 80 regs, 8: <= 64 regs) (tuning knob)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta
@@ -59,6 +60,7 @@ struct vsaogm_ctx {
     long long *d_counts = nullptr;                 // [2]
     long long *d_pcounts = nullptr;                // pending counts [2]
     double *d_norm2 = nullptr;                     // ||m_c||^2 [2]
+    float2 *d_mhat = nullptr;                      // sqrt(D) m_c / ||m_c||, fp32 [2][Dp]
     int *d_err = nullptr;                          // deferred error bits
     float2 *d_part = nullptr;                      // encode chunk partials
     size_t part_cap = 0;                           // in float2
@@ -101,7 +103,7 @@ void vsa_prof_end(vsaogm_ctx *c, int kid, cudaEvent_t a);
 // ---- launchers implemented in the kernel translation units -----------------
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
 int vsa_launch_commit(vsaogm_ctx *c);
-int vsa_launch_norms(vsaogm_ctx *c);
+int vsa_launch_norms(vsaogm_ctx *c, int do_commit);   // [commit +] norms + scaled memory mhat
 int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec);
 int vsa_launch_table_A(vsaogm_ctx *c, double y0, double res, int32_t r_lo, int32_t r_ext, int prec);
 int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float inv_scale,

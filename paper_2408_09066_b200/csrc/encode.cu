@@ -62,8 +62,8 @@ __device__ __forceinline__ void phasor(int j, float phi, float *s, float *c)
     else __sincosf(phi, s, c);
 }
 
-template <int KT, int NPOLY>
-__global__ void __launch_bounds__(ENC_THREADS) k_encode_bundle(
+template <int KT, int NPOLY, int MINB = 6>
+__global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
     const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
     const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
     float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
@@ -211,23 +211,49 @@ __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, l
     }
 }
 
-// ||m_c||^2 for both classes (Eq. 10), fixed-order fp64 block reduction.
-__global__ void k_norms(const double *__restrict__ m, int Dp, double *__restrict__ norm2)
+// Optional commit (m += pending, pending = 0), then ||m_c||^2 for both classes
+// (Eq. 10, fixed-order fp64 block reduction, one block per class), then the
+// scaled conjugate-ready memory mhat_c = sqrt(D) m_c / ||m_c|| (0 for an empty
+// class, L8) in fp32 for the table-A kernel.
+constexpr int NORM_THREADS = 1024;
+__global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restrict__ m, double *__restrict__ pending,
+                                                               long long *__restrict__ cnt, long long *__restrict__ pcnt,
+                                                               int do_commit, int Dp, int D,
+                                                               double *__restrict__ norm2, float2 *__restrict__ mhat)
 {
-    __shared__ double s[256];
+    __shared__ double s[NORM_THREADS];
     const int c = blockIdx.x;
     double acc = 0.0;
-    for (int k = threadIdx.x; k < Dp; k += 256) {
-        const double re = m[2 * ((size_t)c * Dp + k)], im = m[2 * ((size_t)c * Dp + k) + 1];
+    for (int k = threadIdx.x; k < Dp; k += NORM_THREADS) {
+        const size_t o = 2 * ((size_t)c * Dp + k);
+        double re = m[o], im = m[o + 1];
+        if (do_commit) {
+            re += pending[o];
+            im += pending[o + 1];
+            m[o] = re;
+            m[o + 1] = im;
+            pending[o] = 0.0;
+            pending[o + 1] = 0.0;
+        }
         acc += re * re + im * im;
     }
     s[threadIdx.x] = acc;
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
+    for (int o = NORM_THREADS / 2; o > 0; o >>= 1) {
         if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) norm2[c] = s[0];
+    const double n2 = s[0];
+    const double sc = n2 > 0.0 ? sqrt((double)D / n2) : 0.0;
+    if (threadIdx.x == 0) norm2[c] = n2;
+    if (do_commit && c == 0 && threadIdx.x < 2) {
+        cnt[threadIdx.x] += pcnt[threadIdx.x];
+        pcnt[threadIdx.x] = 0;
+    }
+    for (int k = threadIdx.x; k < Dp; k += NORM_THREADS) {
+        const size_t o = 2 * ((size_t)c * Dp + k);
+        mhat[(size_t)c * Dp + k] = make_float2((float)(m[o] * sc), (float)(m[o + 1] * sc));
+    }
 }
 
 }  // namespace
@@ -237,7 +263,9 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     const int KT = c->Dp >= 1024 ? 8 : 4;
     const int kblocks = (c->Dp + ENC_THREADS * KT - 1) / (ENC_THREADS * KT);
     // one full wave at ~6 resident blocks per SM, at least 64 points per chunk
-    const int64_t target_blocks = (int64_t)c->num_sms * 6;
+    // resident blocks per SM: 6 (<= 85 registers, the measured best), 7 or 8 as tuning variants
+    const int minb = (KT == 8 && c->enc_npoly == 2 && (c->enc_minb == 7 || c->enc_minb == 8)) ? c->enc_minb : 6;
+    const int64_t target_blocks = (int64_t)c->num_sms * minb;
     int64_t chunks = (target_blocks + kblocks - 1) / kblocks;
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
     const int64_t chunk_pts = (n + chunks - 1) / chunks;
@@ -256,17 +284,21 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENCODE, &ev);
     dim3 grid(kblocks, (unsigned)chunks);
-#define VSA_ENC_LAUNCH(KT_, NP_)                                                                                 \
-    k_encode_bundle<KT_, NP_><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, n, chunk_pts, c->d_wx, \
-                                                                   c->d_wy, c->cx, c->cy, c->Dp, c->d_part,        \
-                                                                   c->d_part_cnt, c->d_err)
+#define VSA_ENC_LAUNCH(KT_, NP_, ...)                                                                             \
+    k_encode_bundle<KT_, NP_, ##__VA_ARGS__><<<grid, ENC_THREADS, 0, c->stream>>>(                                \
+        (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
+        c->d_err)
     if (KT == 8) {
         switch (c->enc_npoly) {
         case 0: VSA_ENC_LAUNCH(8, 0); break;
         case 1: VSA_ENC_LAUNCH(8, 1); break;
         case 3: VSA_ENC_LAUNCH(8, 3); break;
         case 4: VSA_ENC_LAUNCH(8, 4); break;
-        default: VSA_ENC_LAUNCH(8, 2); break;
+        default:
+            if (minb == 8) VSA_ENC_LAUNCH(8, 2, 8);
+            else if (minb == 7) VSA_ENC_LAUNCH(8, 2, 7);
+            else VSA_ENC_LAUNCH(8, 2);
+            break;
         }
     } else {
         if (c->enc_npoly == 0) VSA_ENC_LAUNCH(4, 0);
@@ -298,11 +330,12 @@ int vsa_launch_commit(vsaogm_ctx *c)
     return VSAOGM_OK;
 }
 
-int vsa_launch_norms(vsaogm_ctx *c)
+int vsa_launch_norms(vsaogm_ctx *c, int do_commit)
 {
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_NORMS, &ev);
-    k_norms<<<2, 256, 0, c->stream>>>(c->d_m, c->Dp, c->d_norm2);
+    k_commit_norms<<<2, NORM_THREADS, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, do_commit,
+                                                      c->Dp, c->D, c->d_norm2, c->d_mhat);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_NORMS, ev);
     c->launches++;

@@ -30,7 +30,7 @@ namespace {
 
 constexpr int TAB_THREADS = 128;
 constexpr int TAB_KT = 8;
-constexpr int TAB_ROWS = 16;
+constexpr int TAB_ROWS = 8;
 
 template <typename T2>
 __device__ __forceinline__ T2 pack2(float a, float b);
@@ -59,8 +59,7 @@ __device__ __forceinline__ void phasor_turns(double tau, double coord, float *s,
 template <typename T2, bool IS_A>
 __global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, int rows, int Dp, int D, int Kp,
                                                        const double *__restrict__ tau, double base, double res,
-                                                       int row0, const double *__restrict__ m,
-                                                       const double *__restrict__ norm2, double sqrtD)
+                                                       int row0, const float2 *__restrict__ mhat)
 {
     const int kq = blockIdx.x * TAB_THREADS + threadIdx.x;
     const int k0 = kq * TAB_KT;
@@ -73,12 +72,11 @@ __global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, 
     if (IS_A) {
 #pragma unroll
         for (int cls = 0; cls < 2; ++cls) {
-            const double n2 = norm2[cls];
-            const double sc = n2 > 0.0 ? sqrtD / sqrt(n2) : 0.0;
 #pragma unroll
             for (int e = 0; e < TAB_KT; ++e) {
-                mr[cls][e] = (float)(m[2 * ((size_t)cls * Dp + k0 + e)] * sc);
-                mi[cls][e] = (float)(m[2 * ((size_t)cls * Dp + k0 + e) + 1] * sc);
+                const float2 v = mhat[(size_t)cls * Dp + k0 + e];   // sqrt(D) m / ||m|| (k_commit_norms)
+                mr[cls][e] = v.x;
+                mi[cls][e] = v.y;
             }
         }
     }
@@ -132,13 +130,12 @@ template <bool IS_A>
 void launch_table(vsaogm_ctx *c, void *out, int rows, const double *tau, double base, double res, int row0, int prec)
 {
     dim3 grid((c->Dp / TAB_KT + TAB_THREADS - 1) / TAB_THREADS, (rows + TAB_ROWS - 1) / TAB_ROWS);
-    const double sqrtD = sqrt((double)c->D);
     if (prec == VSAOGM_BF16)
-        k_table<__nv_bfloat162, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>(
-            (uint4 *)out, rows, c->Dp, c->D, c->Kp, tau, base, res, row0, c->d_m, c->d_norm2, sqrtD);
+        k_table<__nv_bfloat162, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp,
+                                                                            tau, base, res, row0, c->d_mhat);
     else
-        k_table<__half2, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>(
-            (uint4 *)out, rows, c->Dp, c->D, c->Kp, tau, base, res, row0, c->d_m, c->d_norm2, sqrtD);
+        k_table<__half2, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp, tau,
+                                                                     base, res, row0, c->d_mhat);
 }
 
 }  // namespace
