@@ -288,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
             uint32_t stage = 0, phase = 0;
             for (int tile = pair; tile < num_tiles; tile += num_pairs) {
-                const int mb = tile % num_m, nb = tile / num_m;
+                const int nb = tile % num_n, mb = tile / num_n;   // n-fastest: a wave reads A once
                 const int arow = mb * 256 + (int)rank * 128;
                 const int brow = nb * BN + (int)rank * (BN / 2);
                 for (int kb = 0; kb < num_kb; ++kb) {
@@ -328,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int row_in_tile = (int)rank * 128 + quarter * 32 + lane;
         uint32_t as = 0, aphase = 0;
         for (int tile = pair; tile < num_tiles; tile += num_pairs) {
-            const int mb = tile % num_m, nb = tile / num_m;
+            const int nb = tile % num_n, mb = tile / num_n;
             mbar_wait_cluster(&tfull[as], aphase);
             tc_fence_after();
             const int m = mb * 256 + row_in_tile;
