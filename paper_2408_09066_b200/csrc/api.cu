@@ -188,7 +188,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     cudaStreamSynchronize(c->stream);
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
                     c->d_norm2, c->d_mhat, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
-                    c->d_B, c->d_hb, c->d_S, c->d_lab};
+                    c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

@@ -75,7 +75,8 @@ struct vsaogm_ctx {
     void *d_B = nullptr;  size_t B_cap = 0;
     bool B_valid = false;
     double B_x0 = 0, B_res = 0; int32_t B_cols = 0; int B_prec = -1;
-    float *d_hb = nullptr; size_t hb_cap = 0;      // [2][R_ext][cols] fp32
+    float *d_hb = nullptr; size_t hb_cap = 0;      // [2][R_ext][ldh] fp32
+    float *d_ws = nullptr; size_t ws_cap = 0;      // split-K partial sums (bytes)
     float *d_S = nullptr; size_t S_cap = 0;        // host-entropy scratch
     uint8_t *d_lab = nullptr; size_t lab_cap = 0;
 

@@ -46,6 +46,8 @@ struct Epi {
     float *hb;         // VSA mode: [M][ldh], ldh = N rounded up to 8
     float *q;          // VSA mode: [2][band_rows][N] or null
     int r_ext, band_off, band_rows, ldh;
+    float *ws;         // split-K workspace [splits][M][N] fp32
+    int splits, kb_per;
 };
 
 __device__ __forceinline__ float hb_of_p(float p)
@@ -258,6 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const int num_n = (N + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
     const int num_kb = K / VSA_BK;
+    const int S = epi.splits;                 // split-K factor (1 = none)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES2; ++s) {
@@ -287,11 +290,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
             uint32_t stage = 0, phase = 0;
-            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            for (int u = pair; u < num_tiles * S; u += num_pairs) {
+                const int tile = u / S, sk = u - tile * S;
                 const int nb = tile % num_n, mb = tile / num_n;   // n-fastest: a wave reads A once
                 const int arow = mb * 256 + (int)rank * 128;
                 const int brow = nb * BN + (int)rank * (BN / 2);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
                     tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow);
@@ -303,11 +308,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     } else if (warp == 1) {
         if (rank == 0 && lane == 0) {
             uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
-            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            for (int u = pair; u < num_tiles * S; u += num_pairs) {
+                const int sk = u % S;
+                const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
                 mbar_wait_cluster(&tempty[as], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + as * 256;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
@@ -315,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < VSA_BK / 16; ++k)
                         tc_mma2_f16(d, sw128_kmajor_desc(a0 + 32 * k), sw128_kmajor_desc(b0 + 32 * k), idesc,
-                                    (kb | k) != 0);
+                                    (kb != kb0) || (k != 0));
                     tc_commit2_mc(&empty[stage]);
                     if (++stage == STAGES2) { stage = 0; phase ^= 1; }
                 }
@@ -327,18 +334,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int quarter = warp & 3;
         const int row_in_tile = (int)rank * 128 + quarter * 32 + lane;
         uint32_t as = 0, aphase = 0;
-        for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        Epi part = epi;                       // split-K: raw fp32 partial sums to the workspace
+        for (int u = pair; u < num_tiles * S; u += num_pairs) {
+            const int tile = u / S, sk = u - tile * S;
             const int nb = tile % num_n, mb = tile / num_n;
             mbar_wait_cluster(&tfull[as], aphase);
             tc_fence_after();
             const int m = mb * 256 + row_in_tile;
+            part.C = epi.ws + (size_t)sk * M * N;
 #pragma unroll 1
             for (int cc = 0; cc < BN / 32; ++cc) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + as * 256 + cc * 32;
                 TMEM_LD_32x32b_X32(taddr, v);
                 tmem_ld_wait();
-                epilogue_chunk<MODE>(v, m, nb * BN + cc * 32, M, N, epi);
+                if (S == 1) epilogue_chunk<MODE>(v, m, nb * BN + cc * 32, M, N, epi);
+                else epilogue_chunk<0>(v, m, nb * BN + cc * 32, M, N, part);
             }
             tc_fence_before();
             __syncwarp();
@@ -354,6 +365,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                      : "memory");
     }
+}
+
+// split-K: sum the partial accumulators in split order (deterministic), then the epilogue
+template <int MODE>
+__global__ void __launch_bounds__(256) k_splitk_reduce(int M, int N, Epi epi)
+{
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t MN = (size_t)M * N;
+    if (idx >= MN) return;
+    float acc = 0.f;
+    for (int s = 0; s < epi.splits; ++s) acc += epi.ws[(size_t)s * MN + idx];
+    if (MODE == 0) {
+        epi.C[idx] = acc;
+        return;
+    }
+    const int m = (int)(idx / N), n = (int)(idx - (size_t)m * N);
+    const float q = acc * epi.inv_scale;
+    epi.hb[(size_t)m * epi.ldh + n] = hb_of_p(fminf(q * q, 1.f));
+    const int cls = m / epi.r_ext, i = m - cls * epi.r_ext;
+    if (epi.q && i >= epi.band_off && i < epi.band_off + epi.band_rows)
+        epi.q[((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n] = q;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
@@ -404,8 +436,7 @@ int launch1(const void *A, const void *B, int M, int N, int K, int prec, const E
 }
 
 template <int MODE, int BN>
-int launch2_bn(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s,
-               int num_sms)
+int launch2_bn(const void *A, const void *B, int M, int N, int K, int prec, Epi epi, cudaStream_t s, int num_sms)
 {
     CUtensorMap ta, tb;
     int rc = make_map(&ta, A, M, K, 128, prec);
@@ -414,12 +445,17 @@ int launch2_bn(const void *A, const void *B, int M, int N, int K, int prec, cons
     if (rc) return rc;
     const size_t smem = 1024 + (size_t)STAGES2 * (128 + BN / 2) * VSA_BK * 2 + 256;
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
+    const int units = ((M + 255) / 256) * ((N + BN - 1) / BN) * epi.splits;
     const int pairs = num_sms / 2;
-    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    const int grid = 2 * (units < pairs ? units : pairs);
     const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, 256, BN);
     k_decode_gemm2<MODE, BN><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, M, N, K, idesc, epi);
     VSA_CUDA_TRY(cudaGetLastError());
+    if (epi.splits > 1) {
+        const size_t MN = (size_t)M * N;
+        k_splitk_reduce<MODE><<<(unsigned)((MN + 255) / 256), 256, 0, s>>>(M, N, epi);
+        VSA_CUDA_TRY(cudaGetLastError());
+    }
     return VSAOGM_OK;
 }
 
@@ -439,6 +475,26 @@ int pick_bn(int M, int N, int num_sms)
     return best;
 }
 
+// Split-K factor for short problems (few tiles for 74 SM pairs, e.g. the row band of one
+// rank of 8): model time = waves * tile_time / S + partial-sum traffic, tile_time from the
+// measured ~16 TFLOP/s per SM pair, traffic at ~5 TB/s.  S = 1 when the tiles fill the GPU.
+int pick_splits(int M, int N, int K, int bn, int num_sms)
+{
+    const int pairs = num_sms / 2;
+    const long tiles = (long)((M + 255) / 256) * ((N + bn - 1) / bn);
+    const int num_kb = K / VSA_BK;
+    const double t_tile = 2.0 * 256 * bn * (double)K / 16e12 * 1e6;   // us
+    double best_t = -1;
+    int best = 1;
+    for (int S = 1; S <= 16 && S <= num_kb / 4; ++S) {
+        const double waves = (double)((tiles * S + pairs - 1) / pairs);
+        double t = waves * t_tile / S;
+        if (S > 1) t += 2.0 * S * (double)M * N * 4 / 5e12 * 1e6 + 3.0;
+        if (best_t < 0 || t < best_t * 0.97) { best_t = t; best = S; }
+    }
+    return best;
+}
+
 template <int MODE>
 int launch2(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms,
             int bn)
@@ -453,10 +509,11 @@ int launch2(const void *A, const void *B, int M, int N, int K, int prec, const E
 }
 
 // variant: 0 = 2-CTA (default), 1 = 1-CTA; env VSAOGM_GEMM=1cta selects the latter,
-// VSAOGM_GEMM_BN=<n> pins the 2-CTA tile width.
+// VSAOGM_GEMM_BN=<n> pins the 2-CTA tile width, VSAOGM_GEMM_SPLITS=<s> the split-K factor.
+// *ws / *ws_cap: a caller-owned growable workspace for split-K partials.
 template <int MODE>
-int launch(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms,
-           int variant)
+int launch(const void *A, const void *B, int M, int N, int K, int prec, Epi epi, cudaStream_t s, int num_sms,
+           int variant, float **ws, size_t *ws_cap)
 {
     if (variant < 0) {
         const char *e = getenv("VSAOGM_GEMM");
@@ -465,6 +522,23 @@ int launch(const void *A, const void *B, int M, int N, int K, int prec, const Ep
     if (variant == 1) return launch1<MODE>(A, B, M, N, K, prec, epi, s, num_sms);
     int bn = pick_bn(M, N, num_sms);
     if (const char *e = getenv("VSAOGM_GEMM_BN")) bn = atoi(e);
+    int S = pick_splits(M, N, K, bn, num_sms);
+    if (const char *e = getenv("VSAOGM_GEMM_SPLITS")) S = atoi(e);
+    const int num_kb = K / VSA_BK;
+    S = std::max(1, std::min(S, num_kb));
+    epi.kb_per = (num_kb + S - 1) / S;
+    epi.splits = (num_kb + epi.kb_per - 1) / epi.kb_per;   // no empty split
+    if (epi.splits > 1) {
+        const size_t need = (size_t)epi.splits * M * N * sizeof(float);
+        if (need > *ws_cap) {
+            if (*ws) cudaFree(*ws);
+            *ws = nullptr;
+            *ws_cap = 0;
+            if (cudaMalloc(ws, need) != cudaSuccess) { *ws = nullptr; return VSAOGM_ENOMEM; }
+            *ws_cap = need;
+        }
+        epi.ws = *ws;
+    }
     return launch2<MODE>(A, B, M, N, K, prec, epi, s, num_sms, bn);
 }
 
@@ -481,9 +555,11 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float 
     e.band_off = band_off;
     e.band_rows = band_rows;
     e.ldh = (N + 7) / 8 * 8;
+    e.splits = 1;
+    e.kb_per = c->Kp / VSA_BK;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
-    int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms, -1);
+    int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms, -1, &c->d_ws, &c->ws_cap);
     if (rc) return rc;
     vsa_prof_end(c, VSAOGM_K_DECODE_GEMM, ev);
     c->launches++;
@@ -495,5 +571,14 @@ int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, 
 {
     Epi e{};
     e.C = C;
-    return launch<0>(A, B, M, N, K, prec, e, s, num_sms, variant);
+    e.splits = 1;
+    e.kb_per = K / VSA_BK;
+    float *ws = nullptr;
+    size_t cap = 0;
+    int rc = launch<0>(A, B, M, N, K, prec, e, s, num_sms, variant, &ws, &cap);
+    if (ws) {
+        cudaStreamSynchronize(s);
+        cudaFree(ws);
+    }
+    return rc;
 }

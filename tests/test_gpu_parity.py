@@ -75,6 +75,42 @@ def test_gemm_vs_torch_fp32(M, N, K, prec, kernel):
     assert err < 1e-4, err
 
 
+@pytest.mark.parametrize("splits", [2, 3, 7])
+@pytest.mark.parametrize("M,N,K", [(300, 500, 1024), (508, 2000, 4096)])
+def test_gemm_split_k(splits, M, N, K, monkeypatch):
+    from paper_2408_09066_b200 import test_gemm
+    monkeypatch.setenv("VSAOGM_GEMM_SPLITS", str(splits))
+    g = torch.Generator(device="cuda").manual_seed(splits + M)
+    A = torch.randn(M, K, device="cuda", generator=g).half()
+    B = torch.randn(N, K, device="cuda", generator=g).half()
+    C = test_gemm(A, B, 0, 0)
+    ref = A.float() @ B.float().T
+    assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-4
+
+
+def test_decode_band_split_k_matches_unsplit(monkeypatch):
+    """A narrow row band (one rank of 8 at C4 scale) picks split-K automatically; its q and
+    labels equal the forced unsplit decode up to fp32 summation order."""
+    sc = Scenario("C2")
+    xy, lab = sc.all_points()
+    D, l, h, R, C, res = 2048, 0.25, 2, 2000, 2000, 0.02
+    mp = _mapper(D, l, sc.bounds)
+    mp.encode_bundle(*_cuda(xy, lab))
+    out = []
+    for s in (None, "1"):
+        if s:
+            monkeypatch.setenv("VSAOGM_GEMM_SPLITS", s)
+        q = torch.empty((2, 250, C), dtype=torch.float32, device="cuda")
+        mp.decode(0, 0, res, R, C, 750, 1000, h, q_out=q)
+        L = torch.empty((250, C), dtype=torch.uint8, device="cuda")
+        mp.entropy(h, h, 0.001, -0.001, 0, None, L)
+        out.append((q, L))
+    assert mp.sync() == 0
+    assert (out[0][0] - out[1][0]).abs().max().item() <= 1e-5 * out[1][0].abs().max().item() + 1e-7
+    assert (out[0][1] == out[1][1]).float().mean().item() >= 0.9999
+    mp.close()
+
+
 @pytest.mark.parametrize("bn", [256, 224, 192, 160, 128])
 def test_gemm_pair_tile_widths(bn, monkeypatch):
     from paper_2408_09066_b200 import test_gemm
