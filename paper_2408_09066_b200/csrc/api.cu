@@ -135,6 +135,7 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
         if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
         if (const char *e = getenv("VSAOGM_ENC_MINB")) c->enc_minb = atoi(e);     // tuning knob (6 or 8)
+        if (const char *e = getenv("VSAOGM_ENC_KT")) c->enc_kt = atoi(e);         // tuning knob (8 or 16)
         c->D = D;
         c->Dp = (D + 31) / 32 * 32;
         c->Kp = 2 * c->Dp;

@@ -46,8 +46,9 @@ struct vsaogm_ctx {
     int32_t Dp = 0;     // D rounded up to 32 (k-group of the interleaved K layout)
     int32_t Kp = 0;     // 2 * Dp: real contraction length of the decode GEMM
     double l = 1.0;
-    int enc_npoly = 2;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
+    int enc_npoly = 1;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
     int enc_minb = 6;   // encode blocks resident per SM (6: 80 regs, 8: <= 64 regs) (tuning knob)
+    int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta

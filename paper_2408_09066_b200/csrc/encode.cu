@@ -21,36 +21,35 @@ namespace {
 constexpr int ENC_THREADS = 128;
 constexpr int ENC_TILE = 256;   // points staged per shared-memory tile
 
-// sin/cos on the FMA + ALU pipes (no MUFU): quadrant reduction by the
-// magic-number rint, 3-term Cody-Waite pi/2, then the degree-7 / degree-8
-// minimax polynomials of Cephes sinf/cosf (Moshier) on [-pi/4, pi/4]
-// (|error| ~ 1e-7 there, i.e. as accurate as MUFU.SIN/COS).  Used for a
-// fraction of the phasors so the XU (MUFU) pipe and the issue slots are
+// sin/cos on the FMA + ALU pipes (no MUFU), 18 instructions: half-turn
+// reduction phi = q pi + r (q by the magic-number rint, 2-term Cody-Waite pi;
+// |q| < 2^12 keeps q * 3.140625 exact), then near-minimax polynomials on
+// [-pi/2, pi/2] (odd degree 9 / even degree 10, fitted by tools/fit_sincos.py;
+// fp32 Horner max error 1.2e-7, i.e. as accurate as MUFU.SIN/COS), and the
+// sign (-1)^q applied to both by one shift and two xors.  Used for a
+// fraction of the phasors so that the XU (MUFU) pipe and the issue slots are
 // both busy: the encode is SFU-bound otherwise.
 __device__ __forceinline__ void sincos_poly(float phi, float *s_out, float *c_out)
 {
     const float magic = 12582912.f;                 // 1.5 * 2^23: x + magic rounds x to an integer
-    const float tq = fmaf(phi, 0.636619772367581343f, magic);   // phi * 2/pi + magic
+    const float tq = fmaf(phi, 0.318309886183790672f, magic);   // phi / pi + magic
     const int qi = __float_as_int(tq);              // low bits hold q mod 2^22
     const float q = tq - magic;
-    float r = fmaf(q, -1.5703125f, phi);
-    r = fmaf(q, -4.837512969970703125e-4f, r);
-    r = fmaf(q, -7.54978995489188216e-8f, r);
+    float r = fmaf(q, -3.140625f, phi);             // exact (8-bit constant)
+    r = fmaf(q, -9.67653589793e-4f, r);             // pi - 3.140625
     const float r2 = r * r;
-    float sp = fmaf(r2, -1.9515295891e-4f, 8.3321608736e-3f);
-    sp = fmaf(sp, r2, -1.6666654611e-1f);
-    const float s = fmaf(sp * r2, r, r);
-    float cp = fmaf(r2, 2.443315711809948e-5f, -1.388731625493765e-3f);
-    cp = fmaf(cp, r2, 4.166664568298827e-2f);
-    const float c = fmaf(cp * r2, r2, fmaf(r2, -0.5f, 1.0f));
-    // angle = q pi/2 + r: q=0 (s, c), q=1 (c, -s), q=2 (-s, -c), q=3 (-c, s)
-    const bool sw = qi & 1;
-    float so = sw ? c : s;
-    float co = sw ? s : c;
-    so = __int_as_float(__float_as_int(so) ^ ((qi & 2) << 30));
-    co = __int_as_float(__float_as_int(co) ^ (((qi + 1) & 2) << 30));
-    *s_out = so;
-    *c_out = co;
+    float p = fmaf(r2, 2.600054358e-06f, -1.980661473e-04f);
+    p = fmaf(p, r2, 8.333017118e-03f);
+    p = fmaf(p, r2, -1.666665673e-01f);
+    const float s = fmaf(p * r2, r, r);
+    float c = fmaf(r2, -2.607710314e-07f, 2.476188638e-05f);
+    c = fmaf(c, r2, -1.388840377e-03f);
+    c = fmaf(c, r2, 4.166664183e-02f);
+    c = fmaf(c, r2, -5.000000000e-01f);
+    c = fmaf(c, r2, 1.0f);
+    const int sign = qi << 31;                      // (-1)^q
+    *s_out = __int_as_float(__float_as_int(s) ^ sign);
+    *c_out = __int_as_float(__float_as_int(c) ^ sign);
 }
 
 // Phasor j of KT: the last NPOLY of each thread's KT dimensions use the
@@ -68,9 +67,12 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
     const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
     float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
 {
-    __shared__ float4 s_pt[ENC_TILE];
-    __shared__ long long s_cnt[2][ENC_THREADS / 32];
+    constexpr int NW = ENC_THREADS / 32;
+    constexpr int ROUNDS = ENC_TILE / ENC_THREADS;
+    __shared__ float4 s_p0[ENC_TILE], s_p1[ENC_TILE];   // the tile's class-0 / class-1 points, in point order
+    __shared__ int s_g0[ROUNDS * NW], s_g1[ROUNDS * NW];
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const int kb = blockIdx.x;
     const int64_t chunk = blockIdx.y;
     const int kbase = kb * ENC_THREADS * KT + tid;
@@ -92,40 +94,72 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
     for (int64_t base = p0; base < p1; base += ENC_TILE) {
         const int cnt = (int)min((int64_t)ENC_TILE, p1 - base);
         __syncthreads();
-        for (int t = tid; t < cnt; t += ENC_THREADS) {
-            const float2 v = xy[base + t];
-            const int L = lab[base + t];
-            int code = L;
-            if (L > 1) { code = 2; my_err |= VSA_ERRBIT_LABEL; }
-            if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
-            // centred coordinates: fp64 subtraction, one rounding to fp32
-            const float xc = (float)((double)v.x - cx);
-            const float yc = (float)((double)v.y - cy);
-            s_pt[t] = make_float4(xc, yc, __int_as_float(code), 0.f);
-            c0 += (code == 0);
-            c1 += (code == 1);
+        // stage the tile split by label with a deterministic, order-preserving compaction
+        // (ballot + block prefix), so the inner loops carry no per-point label branch
+        float4 rec[ROUNDS];
+        int code_r[ROUNDS];
+        unsigned b0[ROUNDS], b1[ROUNDS];
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int t = tid + r * ENC_THREADS;
+            int code = 2;
+            rec[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < cnt) {
+                const float2 v = xy[base + t];
+                const int L = lab[base + t];
+                code = L;
+                if (L > 1) { code = 2; my_err |= VSA_ERRBIT_LABEL; }
+                if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
+                // centred coordinates: fp64 subtraction, one rounding to fp32
+                rec[r] = make_float4((float)((double)v.x - cx), (float)((double)v.y - cy), 0.f, 0.f);
+            }
+            code_r[r] = code;
+            b0[r] = __ballot_sync(0xffffffffu, code == 0);
+            b1[r] = __ballot_sync(0xffffffffu, code == 1);
+            if (lane == 0) {
+                s_g0[r * NW + warp] = __popc(b0[r]);
+                s_g1[r * NW + warp] = __popc(b1[r]);
+            }
         }
         __syncthreads();
+        int n0 = 0, n1 = 0, o0[ROUNDS], o1[ROUNDS];
+#pragma unroll
+        for (int g = 0; g < ROUNDS * NW; ++g) {
+#pragma unroll
+            for (int r = 0; r < ROUNDS; ++r)
+                if (g == r * NW + warp) { o0[r] = n0; o1[r] = n1; }
+            n0 += s_g0[g];
+            n1 += s_g1[g];
+        }
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            if (code_r[r] == 0) s_p0[o0[r] + __popc(b0[r] & lt)] = rec[r];
+            else if (code_r[r] == 1) s_p1[o1[r] + __popc(b1[r] & lt)] = rec[r];
+        }
+        c0 += n0;   // block totals (every thread has them; thread 0 reports)
+        c1 += n1;
+        __syncthreads();
 #pragma unroll 2
-        for (int p = 0; p < cnt; ++p) {
-            const float4 P = s_pt[p];                   // warp-uniform broadcast
-            const int code = __float_as_int(P.z);
-            if (code == 0) {
+        for (int p = 0; p < n0; ++p) {
+            const float4 P = s_p0[p];                   // warp-uniform broadcast
 #pragma unroll
-                for (int j = 0; j < KT; ++j) {
-                    float s, c;
-                    phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
-                    a0r[j] += c;
-                    a0i[j] += s;
-                }
-            } else if (code == 1) {
+            for (int j = 0; j < KT; ++j) {
+                float s, c;
+                phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
+                a0r[j] += c;
+                a0i[j] += s;
+            }
+        }
+#pragma unroll 2
+        for (int p = 0; p < n1; ++p) {
+            const float4 P = s_p1[p];
 #pragma unroll
-                for (int j = 0; j < KT; ++j) {
-                    float s, c;
-                    phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
-                    a1r[j] += c;
-                    a1i[j] += s;
-                }
+            for (int j = 0; j < KT; ++j) {
+                float s, c;
+                phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &s, &c);
+                a1r[j] += c;
+                a1i[j] += s;
             }
         }
     }
@@ -139,17 +173,9 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
     }
     if (kb == 0) {   // counts and deferred errors once per chunk
         if (my_err) atomicOr(err, my_err);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-        }
-        if ((tid & 31) == 0) { s_cnt[0][tid >> 5] = c0; s_cnt[1][tid >> 5] = c1; }
-        __syncthreads();
-        if (tid < 2) {
-            long long s = 0;
-            for (int w = 0; w < ENC_THREADS / 32; ++w) s += s_cnt[tid][w];
-            part_cnt[chunk * 2 + tid] = s;
+        if (tid == 0) {
+            part_cnt[chunk * 2 + 0] = c0;
+            part_cnt[chunk * 2 + 1] = c1;
         }
     }
 }
@@ -260,11 +286,14 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
 
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
-    const int KT = c->Dp >= 1024 ? 8 : 4;
+    const int KT = (c->enc_kt == 16 && c->Dp >= 2048) ? 16 : (c->Dp >= 1024 ? 8 : 4);
     const int kblocks = (c->Dp + ENC_THREADS * KT - 1) / (ENC_THREADS * KT);
     // one full wave at ~6 resident blocks per SM, at least 64 points per chunk
     // resident blocks per SM: 6 (<= 85 registers, the measured best), 7 or 8 as tuning variants
-    const int minb = (KT == 8 && c->enc_npoly == 2 && (c->enc_minb == 7 || c->enc_minb == 8)) ? c->enc_minb : 6;
+    const int minb = KT == 16 ? 4
+                     : (KT == 8 && (c->enc_npoly == 1 || c->enc_npoly == 2) && (c->enc_minb == 7 || c->enc_minb == 8))
+                         ? c->enc_minb
+                         : 6;
     const int64_t target_blocks = (int64_t)c->num_sms * minb;
     int64_t chunks = (target_blocks + kblocks - 1) / kblocks;
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
@@ -291,14 +320,24 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     if (KT == 8) {
         switch (c->enc_npoly) {
         case 0: VSA_ENC_LAUNCH(8, 0); break;
-        case 1: VSA_ENC_LAUNCH(8, 1); break;
-        case 3: VSA_ENC_LAUNCH(8, 3); break;
-        case 4: VSA_ENC_LAUNCH(8, 4); break;
-        default:
+        case 2:
             if (minb == 8) VSA_ENC_LAUNCH(8, 2, 8);
             else if (minb == 7) VSA_ENC_LAUNCH(8, 2, 7);
             else VSA_ENC_LAUNCH(8, 2);
             break;
+        case 3: VSA_ENC_LAUNCH(8, 3); break;
+        case 4: VSA_ENC_LAUNCH(8, 4); break;
+        default:
+            if (minb == 8) VSA_ENC_LAUNCH(8, 1, 8);
+            else if (minb == 7) VSA_ENC_LAUNCH(8, 1, 7);
+            else VSA_ENC_LAUNCH(8, 1);
+            break;
+        }
+    } else if (KT == 16) {   // tuning variant: 16 dimensions per thread (4 blocks per SM)
+        switch (c->enc_npoly) {
+        case 2: VSA_ENC_LAUNCH(16, 2, 4); break;
+        case 4: VSA_ENC_LAUNCH(16, 4, 4); break;
+        default: VSA_ENC_LAUNCH(16, 3, 4); break;
         }
     } else {
         if (c->enc_npoly == 0) VSA_ENC_LAUNCH(4, 0);
