@@ -263,7 +263,12 @@ def run_native(args):
     my_pts = float(np.mean([len(host_batches[(args.warmup + k) % nb][1]) for k in range(args.steps)]))
     phasors = my_pts * D
     sm_max = pk.get("sm_max_mhz", 1965.0)
-    sfu_peak = 148 * 16 / 2 * sm_max * 1e6          # phasors/s: 16 MUFU/clk/SM, 2 MUFU per phasor
+    sfu_peak = 148 * 16 / 2 * sm_max * 1e6          # MUFU-only: 16 MUFU/clk/SM, 2 MUFU per phasor
+    # combined MUFU + FMA-pipe ceiling: per SM per clock, issue 128
+    # thread-instructions and 16 MUFU; a MUFU phasor costs 7 issue slots + 2 MUFU, an FMA-pipe
+    # phasor 22 issue slots; max m + p s.t. 2m <= 16, 7m + 22p <= 128 -> m = 8, p = 72/22
+    per_clk = 8 + (128 - 7 * 8) / 22
+    alu_peak = 148 * per_clk * sm_max * 1e6
     enc_rate = phasors / (enc_ms * 1e-3)
     clocks = clk.summary()
     # decode GEMM: 2 M N K flops with M = 2 (band + halo rows), N = C, K = 2 Dp
@@ -277,11 +282,13 @@ def run_native(args):
     dominant = "encode" if enc_share >= shares.get("decode_gemm", 0) else "decode_gemm"
     if dominant == "encode":
         roofline = {"kernel": "k_encode_bundle", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
-                    "peak": round(sfu_peak / 1e9, 2), "unit": "Gphasor/s", "frac": round(enc_rate / sfu_peak, 4),
+                    "peak": round(alu_peak / 1e9, 2), "unit": "Gphasor/s", "frac": round(enc_rate / alu_peak, 4),
                     "traffic": traffic.get("encode"),
-                    "peak_basis": f"148 SM x 16 MUFU/clk / 2 MUFU per phasor x {sm_max:.0f} MHz max clock "
-                                  f"(guide unit counts; DESIGN.md)",
-                    "frac_at_measured_clock": (round(enc_rate / (148 * 8 * clocks["sm_mhz"] * 1e6), 4)
+                    "peak_basis": f"combined MUFU+FMA-pipe ceiling {per_clk:.2f} phasors/clk/SM x 148 SM x "
+                                  f"{sm_max:.0f} MHz (guide unit counts: 16 MUFU + 4 issue/clk/SM; DESIGN.md sec. 6)",
+                    "mufu_only_peak": round(sfu_peak / 1e9, 2),
+                    "frac_of_mufu_only": round(enc_rate / sfu_peak, 4),
+                    "frac_at_measured_clock": (round(enc_rate / (148 * per_clk * clocks["sm_mhz"] * 1e6), 4)
                                                if clocks.get("sm_mhz") else None)}
     else:
         roofline = None
