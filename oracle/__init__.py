@@ -56,6 +56,15 @@ def _load():
         lib.oracle_entropy_cells.argtypes = [i32, i32, i32, i32, i32, i32, P, i32, i32, i32,
                                              f64, f64, i64, P, P, P, P]
         lib.oracle_entropy_cells.restype = i64
+        lib.oracle_quadrant_centers.argtypes = [f64, f64, f64, f64, i32, P, P]
+        lib.oracle_quadrant_centers.restype = None
+        lib.oracle_assign_quadrants.argtypes = [f64, f64, f64, f64, i32, i64, P, P, P]
+        lib.oracle_assign_quadrants.restype = None
+        lib.oracle_encode_quadrants.argtypes = [i32, P, P, f64, f64, f64, f64, f64, i32, i64, P, P, P, P, i32]
+        lib.oracle_encode_quadrants.restype = i64
+        lib.oracle_decode_cells_quadrants.argtypes = [i32, P, P, f64, P, f64, f64, f64, f64, i32, f64, f64, f64,
+                                                      i64, P, P, P, P, i32]
+        lib.oracle_decode_cells_quadrants.restype = i64
         _lib = lib
     return _lib
 
@@ -139,6 +148,65 @@ def decode_grid(tx, ty, l, m, x0, y0, res, row_begin, row_end, col_begin, col_en
                          np.arange(col_begin, col_end, dtype=np.int32), indexing="ij")
     q = decode_cells(tx, ty, l, m, x0, y0, res, rr.ravel(), cc.ravel(), nthreads)
     return q.reshape(2, row_end - row_begin, col_end - col_begin)
+
+
+def quadrant_centers(bounds, delta):
+    """getQuadrantCenters() of Alg. 1: (cx, cy) fp64 [delta^2], beta = j delta + i."""
+    cx = np.zeros(delta * delta)
+    cy = np.zeros(delta * delta)
+    _load().oracle_quadrant_centers(*map(float, bounds), delta, _p(cx), _p(cy))
+    return cx, cy
+
+
+def assign_quadrants(bounds, delta, x, y):
+    """Alg. 1 argmin: nearest quadrant centre of each (x, y) (fp64), ties to the lowest index."""
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+    out = np.zeros(x.shape[0], dtype=np.int32)
+    _load().oracle_assign_quadrants(*map(float, bounds), delta, x.shape[0], _p(x), _p(y), _p(out))
+    return out
+
+
+def encode_quadrants(tx, ty, l, bounds, delta, xy, labels, nthreads=None):
+    """Alg. 1 with delta quadrants per axis: m complex128 [2 delta^2, D] (slot 2 beta + psi), counts [2 delta^2]."""
+    tx = np.ascontiguousarray(tx, dtype=np.float64)
+    ty = np.ascontiguousarray(ty, dtype=np.float64)
+    D = tx.shape[0]
+    xy = np.ascontiguousarray(xy, dtype=np.float32).reshape(-1, 2)
+    labels = np.ascontiguousarray(labels, dtype=np.uint8).reshape(-1)
+    ns = 2 * delta * delta
+    mm = np.zeros((ns, D, 2), dtype=np.float64)
+    cnt = np.zeros(ns, dtype=np.int64)
+    bad = _load().oracle_encode_quadrants(D, _p(tx), _p(ty), float(l), *map(float, bounds), delta, xy.shape[0],
+                                          _p(xy), _p(labels), _p(mm), _p(cnt), nthreads or default_threads())
+    return mm[..., 0] + 1j * mm[..., 1], cnt, int(bad)
+
+
+def decode_cells_quadrants(tx, ty, l, m, bounds, delta, x0, y0, res, rows, cols, nthreads=None):
+    """Eq. 11 with delta quadrants: q [2, n] from the cell's own quadrant memories, and beta [n]."""
+    tx = np.ascontiguousarray(tx, dtype=np.float64)
+    ty = np.ascontiguousarray(ty, dtype=np.float64)
+    D = tx.shape[0]
+    mm = np.ascontiguousarray(np.stack([np.real(m), np.imag(m)], axis=-1), dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int32).reshape(-1)
+    cols = np.ascontiguousarray(cols, dtype=np.int32).reshape(-1)
+    n = rows.shape[0]
+    q = np.zeros((2, n), dtype=np.float64)
+    beta = np.zeros(n, dtype=np.int32)
+    viol = _load().oracle_decode_cells_quadrants(D, _p(tx), _p(ty), float(l), _p(mm), *map(float, bounds), delta,
+                                                 float(x0), float(y0), float(res), n, _p(rows), _p(cols), _p(q),
+                                                 _p(beta), nthreads or default_threads())
+    if viol:
+        raise AssertionError(f"oracle: {viol} cells with |q| > 1")
+    return q, beta
+
+
+def decode_grid_quadrants(tx, ty, l, m, bounds, delta, x0, y0, res, row_begin, row_end, col_begin, col_end):
+    rr, cc = np.meshgrid(np.arange(row_begin, row_end, dtype=np.int32),
+                         np.arange(col_begin, col_end, dtype=np.int32), indexing="ij")
+    q, beta = decode_cells_quadrants(tx, ty, l, m, bounds, delta, x0, y0, res, rr.ravel(), cc.ravel())
+    shape = (row_end - row_begin, col_end - col_begin)
+    return q.reshape(2, *shape), beta.reshape(shape)
 
 
 def hb(p: float) -> float:

@@ -27,6 +27,10 @@
  *                L10, L11, L12, L13).
  *   labels     : occupied (1) if S >= rho_occ, empty (0) if S < rho_emp,
  *                unknown (2) otherwise (Eq. 12; L14).
+ *   quadrants  : delta > 1 (sec. III-B-4, Alg. 1): 2 delta^2
+ *                memories; a point goes to slot 2 beta + psi, beta = the
+ *                nearest quadrant centre (ties to the lowest index); a cell
+ *                queries its own quadrant's two memories.
  *
  * Parallelism: pthreads split points (encode; per-thread partial sums added in
  * thread order) or cells (decode).  Results are deterministic for a fixed
@@ -221,6 +225,200 @@ int64_t oracle_decode_cells(int32_t D, const double *tx, const double *ty, doubl
     int64_t viol = 0;
     for (int t = 0; t < nthreads; ++t) { pthread_join(th[t], NULL); viol += jobs[t].range_violations; }
     free(th); free(jobs);
+    return viol;
+}
+
+/* ------------------------------------------------------------------ quadrants (delta > 1) */
+/* Space discretisation (sec. III-B-4): delta x delta equal chunks of
+ * the bounds, 2 delta^2 memories.  getQuadrantCenters() of Alg. 1:
+ * mu_{i,j} = (x_min + (i + 1/2) W / delta, y_min + (j + 1/2) H / delta),
+ * index beta = j delta + i (row-major, x fastest). */
+void oracle_quadrant_centers(double x_min, double y_min, double x_max, double y_max, int32_t delta,
+                             double *cx, double *cy)
+{
+    for (int32_t j = 0; j < delta; ++j)
+        for (int32_t i = 0; i < delta; ++i) {
+            cx[j * delta + i] = x_min + ((double)i + 0.5) * (x_max - x_min) / (double)delta;
+            cy[j * delta + i] = y_min + ((double)j + 0.5) * (y_max - y_min) / (double)delta;
+        }
+}
+
+/* Alg. 1: beta = argmin_k d_L2(point, mu_k) over all delta^2 centres,
+ * ties to the lowest index (coordinate-space distance). */
+static int32_t nearest_quadrant(double x, double y, const double *cx, const double *cy, int32_t nq)
+{
+    int32_t best = 0;
+    double bd = 0.0;
+    for (int32_t k = 0; k < nq; ++k) {
+        double dx = x - cx[k], dy = y - cy[k];
+        double d = dx * dx + dy * dy;
+        if (k == 0 || d < bd) { bd = d; best = k; }
+    }
+    return best;
+}
+
+void oracle_assign_quadrants(double x_min, double y_min, double x_max, double y_max, int32_t delta, int64_t n,
+                             const double *x, const double *y, int32_t *beta)
+{
+    int32_t nq = delta * delta;
+    double *cx = (double *)malloc(sizeof(double) * nq), *cy = (double *)malloc(sizeof(double) * nq);
+    oracle_quadrant_centers(x_min, y_min, x_max, y_max, delta, cx, cy);
+    for (int64_t i = 0; i < n; ++i) beta[i] = nearest_quadrant(x[i], y[i], cx, cy, nq);
+    free(cx);
+    free(cy);
+}
+
+typedef struct {
+    int32_t D;
+    const double *tx, *ty;
+    double l;
+    const float *xy;
+    const uint8_t *lab;
+    const double *cx, *cy;
+    int32_t nq;
+    int64_t i0, i1;
+    double *m;          /* [2 nq][D][2] partial */
+    int64_t *cnt;       /* [2 nq] */
+    int64_t bad;
+} encq_job;
+
+static void *encq_worker(void *arg)
+{
+    encq_job *j = (encq_job *)arg;
+    memset(j->m, 0, sizeof(double) * 4 * (size_t)j->nq * (size_t)j->D);
+    memset(j->cnt, 0, sizeof(int64_t) * 2 * (size_t)j->nq);
+    j->bad = 0;
+    for (int64_t i = j->i0; i < j->i1; ++i) {
+        double x = (double)j->xy[2 * i], y = (double)j->xy[2 * i + 1];
+        int c = j->lab[i];
+        if (c > 1 || !isfinite(x) || !isfinite(y)) { j->bad++; continue; }
+        int32_t beta = nearest_quadrant(x, y, j->cx, j->cy, j->nq);
+        int32_t slot = 2 * beta + c;                     /* Alg. 1: omega_{2 beta + psi} (0-based, L6) */
+        j->cnt[slot]++;
+        double *ms = j->m + (size_t)slot * 2 * j->D;
+        for (int32_t k = 0; k < j->D; ++k) {
+            double a = (j->tx[k] * x + j->ty[k] * y) / j->l;   /* Eq. 9 */
+            ms[2 * k] += cos(a);
+            ms[2 * k + 1] += sin(a);
+        }
+    }
+    return NULL;
+}
+
+/* Alg. 1 with delta >= 1: m [2 delta^2][D][2] and counts [2 delta^2] ADDED to. */
+int64_t oracle_encode_quadrants(int32_t D, const double *tx, const double *ty, double l, double x_min,
+                                double y_min, double x_max, double y_max, int32_t delta, int64_t n,
+                                const float *xy, const uint8_t *labels, double *m, int64_t *counts,
+                                int32_t nthreads)
+{
+    int32_t nq = delta * delta;
+    double *cx = (double *)malloc(sizeof(double) * nq), *cy = (double *)malloc(sizeof(double) * nq);
+    oracle_quadrant_centers(x_min, y_min, x_max, y_max, delta, cx, cy);
+    if (nthreads < 1) nthreads = 1;
+    if (n < (int64_t)nthreads) nthreads = n > 0 ? (int32_t)n : 1;
+    encq_job *jobs = (encq_job *)calloc((size_t)nthreads, sizeof(encq_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    size_t msz = 4 * (size_t)nq * (size_t)D;
+    double *parts = (double *)malloc(sizeof(double) * msz * (size_t)nthreads);
+    int64_t *cparts = (int64_t *)malloc(sizeof(int64_t) * 2 * (size_t)nq * (size_t)nthreads);
+    for (int t = 0; t < nthreads; ++t) {
+        encq_job *j = &jobs[t];
+        j->D = D; j->tx = tx; j->ty = ty; j->l = l; j->xy = xy; j->lab = labels;
+        j->cx = cx; j->cy = cy; j->nq = nq;
+        j->i0 = n * t / nthreads; j->i1 = n * (t + 1) / nthreads;
+        j->m = parts + (size_t)t * msz;
+        j->cnt = cparts + (size_t)t * 2 * nq;
+        pthread_create(&th[t], NULL, encq_worker, j);
+    }
+    int64_t bad = 0;
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    for (int t = 0; t < nthreads; ++t) {          /* fixed thread order */
+        for (size_t e = 0; e < msz; ++e) m[e] += jobs[t].m[e];
+        for (int32_t s = 0; s < 2 * nq; ++s) counts[s] += jobs[t].cnt[s];
+        bad += jobs[t].bad;
+    }
+    free(parts); free(cparts); free(th); free(jobs); free(cx); free(cy);
+    return bad;
+}
+
+typedef struct {
+    int32_t D;
+    const double *tx, *ty;
+    double l;
+    const double *m;
+    const double *norms;     /* [2 nq] */
+    const double *cx, *cy;
+    int32_t nq;
+    double x0, y0, res;
+    const int32_t *rows, *cols;
+    int64_t c0, c1, ncell;
+    double *q;
+    int32_t *beta_out;
+    int64_t viol;
+} decq_job;
+
+static void *decq_worker(void *arg)
+{
+    decq_job *j = (decq_job *)arg;
+    j->viol = 0;
+    for (int64_t e = j->c0; e < j->c1; ++e) {
+        double x = j->x0 + ((double)j->cols[e] + 0.5) * j->res;
+        double y = j->y0 + ((double)j->rows[e] + 0.5) * j->res;
+        int32_t beta = nearest_quadrant(x, y, j->cx, j->cy, j->nq);   /* the cell's own quadrant */
+        if (j->beta_out) j->beta_out[e] = beta;
+        for (int c = 0; c < 2; ++c) {
+            int32_t slot = 2 * beta + c;
+            double q = 0.0;
+            if (j->norms[slot] > 0.0) {
+                const double *ms = j->m + (size_t)slot * 2 * j->D;
+                double H = 0.0;
+                for (int32_t k = 0; k < j->D; ++k) {
+                    double a = (j->tx[k] * x + j->ty[k] * y) / j->l;
+                    H += ms[2 * k] * cos(a) + ms[2 * k + 1] * sin(a);     /* Eq. 11 */
+                }
+                q = H / (sqrt((double)j->D) * j->norms[slot]);
+                if (fabs(q) > 1.0 + 1e-12) j->viol++;
+            }
+            j->q[(size_t)c * j->ncell + e] = q;
+        }
+    }
+    return NULL;
+}
+
+/* Eq. 11 with delta >= 1: each cell queries the memories 2 beta + {0,1} of the
+ * quadrant beta nearest to its centre.  q [2][ncell]; beta_out [ncell] or NULL. */
+int64_t oracle_decode_cells_quadrants(int32_t D, const double *tx, const double *ty, double l, const double *m,
+                                      double x_min, double y_min, double x_max, double y_max, int32_t delta,
+                                      double x0, double y0, double res, int64_t ncell, const int32_t *rows,
+                                      const int32_t *cols, double *q, int32_t *beta_out, int32_t nthreads)
+{
+    int32_t nq = delta * delta;
+    double *cx = (double *)malloc(sizeof(double) * nq), *cy = (double *)malloc(sizeof(double) * nq);
+    oracle_quadrant_centers(x_min, y_min, x_max, y_max, delta, cx, cy);
+    double *norms = (double *)malloc(sizeof(double) * 2 * nq);
+    for (int32_t s = 0; s < 2 * nq; ++s) {                 /* Eq. 10 per memory */
+        double acc = 0.0;
+        for (int32_t k = 0; k < D; ++k) {
+            double re = m[(size_t)s * 2 * D + 2 * k], im = m[(size_t)s * 2 * D + 2 * k + 1];
+            acc += re * re + im * im;
+        }
+        norms[s] = sqrt(acc);
+    }
+    if (nthreads < 1) nthreads = 1;
+    if (ncell < (int64_t)nthreads) nthreads = ncell > 0 ? (int32_t)ncell : 1;
+    decq_job *jobs = (decq_job *)calloc((size_t)nthreads, sizeof(decq_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        decq_job *j = &jobs[t];
+        j->D = D; j->tx = tx; j->ty = ty; j->l = l; j->m = m; j->norms = norms;
+        j->cx = cx; j->cy = cy; j->nq = nq; j->x0 = x0; j->y0 = y0; j->res = res;
+        j->rows = rows; j->cols = cols; j->c0 = ncell * t / nthreads; j->c1 = ncell * (t + 1) / nthreads;
+        j->ncell = ncell; j->q = q; j->beta_out = beta_out;
+        pthread_create(&th[t], NULL, decq_worker, j);
+    }
+    int64_t viol = 0;
+    for (int t = 0; t < nthreads; ++t) { pthread_join(th[t], NULL); viol += jobs[t].viol; }
+    free(th); free(jobs); free(norms); free(cx); free(cy);
     return viol;
 }
 
