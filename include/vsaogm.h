@@ -98,6 +98,19 @@ typedef struct {
 int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds bounds,
                   vsaogm_ctx **out);
 
+/* Space discretisation (sec. III-B-4; Alg. 1 :260-285): as
+ * vsaogm_create with delta x delta equal quadrants of `bounds` (1 <= delta <=
+ * VSAOGM_MAX_DELTA) and 2 delta^2 memories, slot 2 beta + psi.  A point goes to
+ * the quadrant beta = j delta + i whose centre (x_min + (i + 1/2) W / delta,
+ * y_min + (j + 1/2) H / delta) is nearest (fp64 squared distance, ties to the
+ * lowest index; out-of-bounds points to the nearest centre);
+ * a grid cell queries the two memories of the quadrant nearest its centre.
+ * Memories, pending memories and counts are then [2 delta^2] slots instead of
+ * [2] classes in every call below.  vsaogm_create(...) == delta 1. */
+#define VSAOGM_MAX_DELTA 8
+int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds bounds,
+                            int32_t delta, vsaogm_ctx **out);
+
 /* Release every resource of the context (synchronises its stream). NULL is a no-op. */
 void vsaogm_destroy(vsaogm_ctx *ctx);
 
@@ -118,15 +131,16 @@ int vsaogm_encode_bundle_host(vsaogm_ctx *ctx, const float *xy_host, const uint8
                               int64_t n);
 
 /* Expose the pending (not yet committed) memories for a multi-rank all-reduce
- * (Alg. 3 fusion): *dev_ptr = fp64 [2][Dp][2] (class, k,
- * re/im) in the context's centred-phase convention, Dp = D rounded up to a
- * multiple of 32 (padding entries stay zero), *n_doubles = 4 Dp.  After
+ * (Alg. 3 fusion): *dev_ptr = fp64 [S][Dp][2] (slot, k,
+ * re/im; S = 2 delta^2 slots 2 beta + psi, S = 2 classes for delta = 1) in the
+ * context's centred-phase convention, Dp = D rounded up to a multiple of 32
+ * (padding entries stay zero), *n_doubles = 2 S Dp.  After
  * this call the context is in multi-rank mode: vsaogm_decode no longer commits
  * implicitly and returns ESTATE while pending work is uncommitted.  The
  * pointer stays valid for the life of the context. */
 int vsaogm_pending(vsaogm_ctx *ctx, double **dev_ptr, int64_t *n_doubles);
 
-/* Same as vsaogm_pending for the per-class point counts: int64 [2] device. */
+/* Same as vsaogm_pending for the per-slot point counts: int64 [S] device. */
 int vsaogm_pending_counts(vsaogm_ctx *ctx, int64_t **dev_ptr);
 
 /* m += pending; pending = 0 (and the counts). */
@@ -164,9 +178,10 @@ int vsaogm_entropy_host(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, fl
  * ENONFINITE, first one seen since the last sync) or ECUDA, else OK. */
 int vsaogm_sync(vsaogm_ctx *ctx);
 
-/* Test hook (synchronises): committed + pending memories as fp64 [2][D][2]
- * in the raw-coordinate convention of Eq. 9 (the centring rotation undone on
- * the host in fp64), and counts[2].  Either pointer may be NULL. */
+/* Test hook (synchronises): committed + pending memories as fp64 [S][D][2]
+ * (S = 2 delta^2 slots) in the raw-coordinate convention of Eq. 9 (the
+ * centring rotation undone on the host in fp64), and counts[S].  Either
+ * pointer may be NULL. */
 int vsaogm_get_memory(vsaogm_ctx *ctx, double *host, int64_t *counts);
 
 /* Test hook: theta as fp64 [2][D] (x axis, then y axis). */

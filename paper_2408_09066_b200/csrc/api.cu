@@ -121,12 +121,19 @@ const char *vsaogm_strerror(int code)
 
 int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b, vsaogm_ctx **out)
 {
+    return vsaogm_create_quadrants(D, seed, length_scale, b, 1, out);
+}
+
+int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b, int32_t delta,
+                            vsaogm_ctx **out)
+{
     if (!out) return VSAOGM_EINVAL_ARG;
     *out = nullptr;
     if (D < 1) return VSAOGM_EINVAL_DIM;
     if (!(length_scale > 0.0) || !isfinite(length_scale)) return VSAOGM_EINVAL_ARG;
     if (!finite_all(b.x_min, b.y_min, b.x_max, b.y_max) || !(b.x_max > b.x_min) || !(b.y_max > b.y_min))
         return VSAOGM_EINVAL_ARG;
+    if (delta < 1 || delta > VSAOGM_MAX_DELTA) return VSAOGM_EINVAL_ARG;
     vsaogm_ctx *c = new (std::nothrow) vsaogm_ctx();
     if (!c) return VSAOGM_ENOMEM;
     int rc = VSAOGM_OK;
@@ -136,6 +143,18 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
         if (const char *e = getenv("VSAOGM_ENC_MINB")) c->enc_minb = atoi(e);     // tuning knob (6 or 8)
         if (const char *e = getenv("VSAOGM_ENC_KT")) c->enc_kt = atoi(e);         // tuning knob (8 or 16)
+        if (const char *e = getenv("VSAOGM_ENC_SORTED")) c->enc_sorted = atoi(e); // tuning knob (-1 or 1)
+        c->delta = delta;
+        c->nq = delta * delta;
+        c->nslots = 2 * c->nq;
+        // getQuadrantCenters() of Alg. 1, expression order fixed by DESIGN.md (fp64)
+        c->qcx.resize(c->nq);
+        c->qcy.resize(c->nq);
+        for (int j = 0; j < delta; ++j)
+            for (int i = 0; i < delta; ++i) {
+                c->qcx[j * delta + i] = b.x_min + ((double)i + 0.5) * (b.x_max - b.x_min) / (double)delta;
+                c->qcy[j * delta + i] = b.y_min + ((double)j + 0.5) * (b.y_max - b.y_min) / (double)delta;
+            }
         c->D = D;
         c->Dp = (D + 31) / 32 * 32;
         c->Kp = 2 * c->Dp;
@@ -160,12 +179,21 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
         if ((rc = dev_alloc_zero(&c->d_wy, c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_tx_turns, c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_ty_turns, c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_m, 4 * (size_t)c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_pending, 4 * (size_t)c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_counts, 2))) break;
-        if ((rc = dev_alloc_zero(&c->d_pcounts, 2))) break;
-        if ((rc = dev_alloc_zero(&c->d_norm2, 2))) break;
-        if ((rc = dev_alloc_zero(&c->d_mhat, 2 * (size_t)c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_m, 2 * (size_t)c->nslots * c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_pending, 2 * (size_t)c->nslots * c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_counts, c->nslots))) break;
+        if ((rc = dev_alloc_zero(&c->d_pcounts, c->nslots))) break;
+        if ((rc = dev_alloc_zero(&c->d_norm2, c->nslots))) break;
+        if ((rc = dev_alloc_zero(&c->d_mhat, (size_t)c->nslots * c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_qc, 2 * (size_t)c->nq))) break;
+        {
+            std::vector<double> qc(2 * c->nq);
+            for (int k = 0; k < c->nq; ++k) { qc[2 * k] = c->qcx[k]; qc[2 * k + 1] = c->qcy[k]; }
+            if (cudaMemcpy(c->d_qc, qc.data(), qc.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+                rc = VSAOGM_ECUDA;
+                break;
+            }
+        }
         if ((rc = dev_alloc_zero(&c->d_err, 1))) break;
         if (cudaMemcpy(c->d_wx, wx.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(c->d_wy, wy.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -189,7 +217,8 @@ void vsaogm_destroy(vsaogm_ctx *c)
     cudaStreamSynchronize(c->stream);
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
                     c->d_norm2, c->d_mhat, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
-                    c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab};
+                    c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
+                    c->d_sortmeta, c->d_sorted};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -240,7 +269,7 @@ int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
 {
     if (!c || !p) return VSAOGM_EINVAL_ARG;
     *p = c->d_pending;
-    if (n) *n = 4 * (int64_t)c->Dp;
+    if (n) *n = 2 * (int64_t)c->nslots * c->Dp;
     c->pending_taken = true;
     return VSAOGM_OK;
 }
@@ -265,10 +294,10 @@ int vsaogm_commit(vsaogm_ctx *c)
 int vsaogm_reset(vsaogm_ctx *c)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_m, 0, 4 * (size_t)c->Dp * sizeof(double), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pending, 0, 4 * (size_t)c->Dp * sizeof(double), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_counts, 0, 2 * sizeof(long long), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pcounts, 0, 2 * sizeof(long long), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_m, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pending, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_counts, 0, c->nslots * sizeof(long long), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pcounts, 0, c->nslots * sizeof(long long), c->stream));
     c->dirty = false;
     c->decoded = false;
     return VSAOGM_OK;
@@ -288,15 +317,62 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     const int32_t r_hi = std::min(g->rows, g->row_end + g->halo);
     const int32_t r_ext = r_hi - r_lo;
     const int64_t M = 2 * (int64_t)r_ext;
-    if (M > (int64_t)1 << 30 || (int64_t)g->cols > (int64_t)1 << 30) return VSAOGM_EINVAL_ARG;
-    const size_t ldh = ((size_t)g->cols + 7) / 8 * 8;   // H_b row stride (16-byte multiple for TMA)
+    if (M * c->delta > (int64_t)1 << 30 || (int64_t)g->cols > (int64_t)1 << 30) return VSAOGM_EINVAL_ARG;
+    // Decode groups: one per quadrant with decoded cells.  A cell's quadrant is the nearest
+    // centre (fp64, ties to the lower index) along each axis: cell rows of quadrant row j and
+    // cell columns of quadrant column i are contiguous ranges (delta = 1: one group).
+    Groups G{};
+    int slot0[VSA_MAX_GROUPS];
+    {
+        const int dl = c->delta;
+        auto nearest = [&](double v, bool is_y) {
+            int best = 0;
+            double bd = 0.0;
+            for (int k = 0; k < dl; ++k) {
+                const double cc = is_y ? c->qcy[k * dl] : c->qcx[k];
+                const double d = (v - cc) * (v - cc);
+                if (k == 0 || d < bd) { bd = d; best = k; }
+            }
+            return best;
+        };
+        std::vector<int> rlo(dl, INT32_MAX), rhi(dl, -1), clo(dl, INT32_MAX), chi(dl, -1);
+        for (int r = r_lo; r < r_hi; ++r) {
+            const int j = dl == 1 ? 0 : nearest(g->y0 + ((double)r + 0.5) * g->res, true);
+            rlo[j] = std::min(rlo[j], r);
+            rhi[j] = std::max(rhi[j], r);
+        }
+        for (int col = 0; col < g->cols; ++col) {
+            const int i = dl == 1 ? 0 : nearest(g->x0 + ((double)col + 0.5) * g->res, false);
+            clo[i] = std::min(clo[i], col);
+            chi[i] = std::max(chi[i], col);
+        }
+        int a_rows = 0;
+        for (int j = 0; j < dl; ++j) {
+            if (rhi[j] < 0) continue;
+            for (int i = 0; i < dl; ++i) {
+                if (chi[i] < 0) continue;
+                const int k = G.n++;
+                G.nrows[k] = rhi[j] - rlo[j] + 1;
+                G.mrows[k] = 2 * G.nrows[k];
+                G.row0[k] = rlo[j] - r_lo;
+                G.col0[k] = clo[i];
+                G.ncols[k] = chi[i] - clo[i] + 1;
+                G.a_row0[k] = a_rows;
+                slot0[k] = 2 * (j * dl + i);
+                a_rows += G.mrows[k];
+            }
+        }
+    }
+    int a_rows = 0;
+    for (int k = 0; k < G.n; ++k) a_rows = std::max(a_rows, G.a_row0[k] + G.mrows[k]);
+    const size_t ldh = ((size_t)g->cols + 7) / 8 * 8;   // H_b row stride (16-byte multiple)
     if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * ldh * sizeof(float)))) return rc;
     if ((rc = vsa_launch_norms(c, do_commit))) return rc;
     c->dirty = false;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
-    if ((rc = vsa_launch_table_A(c, g->y0, g->res, r_lo, r_ext, prec))) return rc;
-    if ((rc = vsa_launch_decode_gemm(c, (int32_t)M, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,
-                                     g->row_begin - r_lo, g->row_end - g->row_begin)))
+    if ((rc = vsa_launch_table_A(c, G, g->y0, g->res, r_lo, prec, slot0))) return rc;
+    if ((rc = vsa_launch_decode_gemm(c, G, a_rows, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,
+                                     r_lo - g->row_begin, g->row_end - g->row_begin)))
         return rc;
     c->decoded = true;
     c->g_rows = g->rows;
@@ -361,30 +437,29 @@ int vsaogm_sync(vsaogm_ctx *c)
 int vsaogm_get_memory(vsaogm_ctx *c, double *host, int64_t *counts)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
-    const size_t n = 4 * (size_t)c->Dp;
+    const int ns = c->nslots;
+    const size_t n = 2 * (size_t)ns * c->Dp;
     std::vector<double> m(n), pd(n);
-    long long cnt[2], pcnt[2];
+    std::vector<long long> cnt(ns), pcnt(ns);
     VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
     VSA_CUDA_TRY(cudaMemcpy(m.data(), c->d_m, n * sizeof(double), cudaMemcpyDeviceToHost));
     VSA_CUDA_TRY(cudaMemcpy(pd.data(), c->d_pending, n * sizeof(double), cudaMemcpyDeviceToHost));
-    VSA_CUDA_TRY(cudaMemcpy(cnt, c->d_counts, sizeof(cnt), cudaMemcpyDeviceToHost));
-    VSA_CUDA_TRY(cudaMemcpy(pcnt, c->d_pcounts, sizeof(pcnt), cudaMemcpyDeviceToHost));
+    VSA_CUDA_TRY(cudaMemcpy(cnt.data(), c->d_counts, ns * sizeof(long long), cudaMemcpyDeviceToHost));
+    VSA_CUDA_TRY(cudaMemcpy(pcnt.data(), c->d_pcounts, ns * sizeof(long long), cudaMemcpyDeviceToHost));
     if (host) {
         // undo the centring rotation: m_raw,k = m_centred,k * exp(+i (thx_k c_x + thy_k c_y) / l)
-        for (int cls = 0; cls < 2; ++cls)
+        for (int s = 0; s < ns; ++s)
             for (int k = 0; k < c->D; ++k) {
                 const double psi = (c->thx[k] * c->cx + c->thy[k] * c->cy) / c->l;
                 const double cr = cos(psi), si = sin(psi);
-                const size_t o = 2 * ((size_t)cls * c->Dp + k);
+                const size_t o = 2 * ((size_t)s * c->Dp + k);
                 const double re = m[o] + pd[o], im = m[o + 1] + pd[o + 1];
-                host[2 * ((size_t)cls * c->D + k)] = re * cr - im * si;
-                host[2 * ((size_t)cls * c->D + k) + 1] = re * si + im * cr;
+                host[2 * ((size_t)s * c->D + k)] = re * cr - im * si;
+                host[2 * ((size_t)s * c->D + k) + 1] = re * si + im * cr;
             }
     }
-    if (counts) {
-        counts[0] = cnt[0] + pcnt[0];
-        counts[1] = cnt[1] + pcnt[1];
-    }
+    if (counts)
+        for (int s = 0; s < ns; ++s) counts[s] = cnt[s] + pcnt[s];
     return VSAOGM_OK;
 }
 

@@ -34,6 +34,18 @@ void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, in
 #define VSA_BK 64
 #define VSA_STAGES 4
 
+#define VSA_MAX_GROUPS (VSAOGM_MAX_DELTA * VSAOGM_MAX_DELTA)
+
+// Decode GEMM problem groups (one per quadrant with decoded cells; delta = 1: one group).
+// Group g: A-table rows [a_row0, a_row0 + mrows) = class 0 then class 1 blocks of nrows grid
+// rows each (decoded rows row0 .. row0+nrows-1, relative to the first decoded row), times the
+// grid columns [col0, col0 + ncols).
+struct Groups {
+    int n;
+    int a_row0[VSA_MAX_GROUPS], mrows[VSA_MAX_GROUPS], nrows[VSA_MAX_GROUPS], row0[VSA_MAX_GROUPS];
+    int col0[VSA_MAX_GROUPS], ncols[VSA_MAX_GROUPS];
+};
+
 struct ProfRec {
     int kid;
     cudaEvent_t a, b;
@@ -46,6 +58,16 @@ struct vsaogm_ctx {
     int32_t Dp = 0;     // D rounded up to 32 (k-group of the interleaved K layout)
     int32_t Kp = 0;     // 2 * Dp: real contraction length of the decode GEMM
     double l = 1.0;
+    int32_t delta = 1;   // quadrants per axis (sec. III-B-4); delta^2 quadrants
+    int32_t nq = 1;      // delta^2
+    int32_t nslots = 2;  // 2 delta^2 memories, slot = 2 beta + psi
+    std::vector<double> qcx, qcy;                  // quadrant centres (host, fp64)
+    double *d_qc = nullptr;                        // quadrant centres (device) [nq][2]
+    uint8_t *d_slot = nullptr; size_t slot_cap = 0;   // per-point slot (sorted encode)
+    int *d_bhist = nullptr; size_t bhist_cap = 0;     // per-block slot histograms
+    int *d_sortmeta = nullptr;                     // slot totals / starts / vchunk table
+    float2 *d_sorted = nullptr; size_t sorted_cap = 0;
+    int enc_sorted = -1;  // -1: sorted path only for delta > 1; 1: always (tuning knob)
     int enc_npoly = 1;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
     int enc_minb = 6;   // encode blocks resident per SM (6: 80 regs, 8: <= 64 regs) (tuning knob)
     int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
@@ -107,9 +129,10 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
 int vsa_launch_commit(vsaogm_ctx *c);
 int vsa_launch_norms(vsaogm_ctx *c, int do_commit);   // [commit +] norms + scaled memory mhat
 int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec);
-int vsa_launch_table_A(vsaogm_ctx *c, double y0, double res, int32_t r_lo, int32_t r_ext, int prec);
-int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float inv_scale,
-                           float *hb, float *q, int32_t r_ext, int32_t band_off, int32_t band_rows);
+int vsa_launch_table_A(vsaogm_ctx *c, const Groups &G, double y0, double res, int32_t r_lo, int prec,
+                       const int *slot0);
+int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32_t N, int prec, float inv_scale,
+                           float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows);
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab);
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
                  cudaStream_t s, int num_sms, int variant);

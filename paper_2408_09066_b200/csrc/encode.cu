@@ -180,24 +180,157 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
     }
 }
 
+// Quadrant routing (delta > 1; Alg. 1): slot = 2 beta + psi with
+// beta the nearest quadrant centre in fp64 squared distance, ties to the lowest
+// index -- the expression, operation order and rounding DESIGN.md fixes for the decision
+// (explicit _rn intrinsics: no FMA contraction).  255 = invalid point (deferred error).
+__global__ void k_route(const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n,
+                        const double *__restrict__ qc, int nq, uint8_t *__restrict__ slot, int *__restrict__ err)
+{
+    __shared__ double s_qc[2 * VSAOGM_MAX_DELTA * VSAOGM_MAX_DELTA];
+    for (int k = threadIdx.x; k < 2 * nq; k += blockDim.x) s_qc[k] = qc[k];
+    __syncthreads();
+    int my_err = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = xy[i];
+        const int L = lab[i];
+        uint8_t s = 255;
+        if (L > 1) my_err |= VSA_ERRBIT_LABEL;
+        else if (!(isfinite(v.x) && isfinite(v.y))) my_err |= VSA_ERRBIT_NONFINITE;
+        else {
+            const double x = (double)v.x, y = (double)v.y;
+            int best = 0;
+            double bd = 0.0;
+            for (int k = 0; k < nq; ++k) {
+                const double dx = __dsub_rn(x, s_qc[2 * k]), dy = __dsub_rn(y, s_qc[2 * k + 1]);
+                const double d = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+                if (k == 0 || d < bd) { bd = d; best = k; }
+            }
+            s = (uint8_t)(2 * best + L);
+        }
+        slot[i] = s;
+    }
+    if (my_err) atomicOr(err, my_err);
+}
+
+// Slot-filtered encode: block (kb, chunk, z) bundles the points of its chunk whose
+// memory slot is z (slot = label for delta = 1, else the routed 2 beta + psi), so
+// every block keeps one accumulator set.  Same phasor arithmetic as k_encode_bundle;
+// points of other slots are only staged (cost ~0.3 % per slot).
+template <int KT, int NPOLY, int MINB = 6>
+__global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_slots(
+    const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, const uint8_t *__restrict__ slot, int64_t n,
+    int64_t chunk_pts, const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
+    int nslots, float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
+{
+    constexpr int NW = ENC_THREADS / 32;
+    constexpr int ROUNDS = ENC_TILE / ENC_THREADS;
+    __shared__ float4 s_p[ENC_TILE];
+    __shared__ int s_g[ROUNDS * NW];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int kb = blockIdx.x;
+    const int64_t chunk = blockIdx.y;
+    const int z = blockIdx.z;
+    const int kbase = kb * ENC_THREADS * KT + tid;
+
+    float fx[KT], fy[KT], ar[KT], ai[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * ENC_THREADS;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+        ar[j] = ai[j] = 0.f;
+    }
+    long long cnt_z = 0;
+    int my_err = 0;
+    const int64_t p0 = chunk * chunk_pts;
+    const int64_t p1 = min(n, p0 + chunk_pts);
+
+    for (int64_t base = p0; base < p1; base += ENC_TILE) {
+        const int cnt = (int)min((int64_t)ENC_TILE, p1 - base);
+        __syncthreads();
+        float4 rec[ROUNDS];
+        bool mine[ROUNDS];
+        unsigned b[ROUNDS];
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int t = tid + r * ENC_THREADS;
+            mine[r] = false;
+            rec[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < cnt) {
+                const float2 v = xy[base + t];
+                int sl;
+                if (slot) {
+                    sl = slot[base + t];
+                } else {
+                    const int L = lab[base + t];
+                    sl = L;
+                    if (L > 1) { sl = 255; my_err |= VSA_ERRBIT_LABEL; }
+                    if (!(isfinite(v.x) && isfinite(v.y))) { sl = 255; my_err |= VSA_ERRBIT_NONFINITE; }
+                }
+                mine[r] = sl == z;
+                rec[r] = make_float4((float)((double)v.x - cx), (float)((double)v.y - cy), 0.f, 0.f);
+            }
+            b[r] = __ballot_sync(0xffffffffu, mine[r]);
+            if (lane == 0) s_g[r * NW + warp] = __popc(b[r]);
+        }
+        __syncthreads();
+        int nz = 0, o[ROUNDS];
+#pragma unroll
+        for (int g = 0; g < ROUNDS * NW; ++g) {
+#pragma unroll
+            for (int r = 0; r < ROUNDS; ++r)
+                if (g == r * NW + warp) o[r] = nz;
+            nz += s_g[g];
+        }
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r)
+            if (mine[r]) s_p[o[r] + __popc(b[r] & lt)] = rec[r];
+        cnt_z += nz;
+        __syncthreads();
+#pragma unroll 2
+        for (int p = 0; p < nz; ++p) {
+            const float4 P = s_p[p];                    // warp-uniform broadcast
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {
+                float sv, cv;
+                phasor<KT, NPOLY>(j, fmaf(fx[j], P.x, fy[j] * P.y), &sv, &cv);
+                ar[j] += cv;
+                ai[j] += sv;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * ENC_THREADS;
+        if (k < Dp) part[((size_t)chunk * nslots + z) * Dp + k] = make_float2(ar[j], ai[j]);
+    }
+    if (kb == 0) {
+        if (my_err && z == 0) atomicOr(err, my_err);
+        if (tid == 0) part_cnt[chunk * nslots + z] = cnt_z;
+    }
+}
+
 // K3: pending[c][k] += sum over chunks of the partials, fp64, fixed order:
 // block (32 k-lanes) x (RED_SLICES chunk slices); slice s sums chunks s, s+S, ...
 // in order, then slice sums are added in slice order (deterministic).
 constexpr int RED_SLICES = 8;
 __global__ void __launch_bounds__(32 * RED_SLICES) k_reduce_partials(
-    const float2 *__restrict__ part, const long long *__restrict__ part_cnt, int chunks, int Dp, int D,
+    const float2 *__restrict__ part, const long long *__restrict__ part_cnt, int chunks, int nslots, int Dp, int D,
     double *__restrict__ pending, long long *__restrict__ pcount)
 {
     __shared__ double s_re[RED_SLICES][32], s_im[RED_SLICES][32];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int idx = blockIdx.x * 32 + tx;          // over 2 * Dp: (class, k)
-    const bool live = idx < 2 * Dp;
+    const int idx = blockIdx.x * 32 + tx;          // over nslots * Dp: (slot, k)
+    const bool live = idx < nslots * Dp;
     double re = 0.0, im = 0.0;
     if (live) {
-        const float2 *p = part + idx;              // part[(ch*2 + c)*Dp + k] = part[ch*2*Dp + idx]
+        const float2 *p = part + idx;              // part[(ch*nslots + s)*Dp + k] = part[ch*nslots*Dp + idx]
 #pragma unroll 4
         for (int ch = ty; ch < chunks; ch += RED_SLICES) {
-            const float2 v = p[(size_t)ch * 2 * Dp];
+            const float2 v = p[(size_t)ch * nslots * Dp];
             re += v.x;
             im += v.y;
         }
@@ -215,23 +348,23 @@ __global__ void __launch_bounds__(32 * RED_SLICES) k_reduce_partials(
             pending[2 * (size_t)idx + 1] += i;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x < 2) {
+    if (blockIdx.x == 0 && threadIdx.x < nslots) {
         long long s = 0;
-        for (int ch = 0; ch < chunks; ++ch) s += part_cnt[ch * 2 + threadIdx.x];
+        for (int ch = 0; ch < chunks; ++ch) s += part_cnt[ch * nslots + threadIdx.x];
         pcount[threadIdx.x] += s;
     }
 }
 
 // Commit: m += pending, pending = 0 (Alg. 3 result folded into the memories).
 __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, long long *__restrict__ cnt,
-                         long long *__restrict__ pcnt, int n)
+                         long long *__restrict__ pcnt, int n, int nslots)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         m[i] += pending[i];
         pending[i] = 0.0;
     }
-    if (blockIdx.x == 0 && threadIdx.x < 2) {
+    if (blockIdx.x == 0 && threadIdx.x < nslots) {
         cnt[threadIdx.x] += pcnt[threadIdx.x];
         pcnt[threadIdx.x] = 0;
     }
@@ -272,7 +405,7 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
     const double n2 = s[0];
     const double sc = n2 > 0.0 ? sqrt((double)D / n2) : 0.0;
     if (threadIdx.x == 0) norm2[c] = n2;
-    if (do_commit && c == 0 && threadIdx.x < 2) {
+    if (do_commit && c == 0 && threadIdx.x < gridDim.x) {   // one block per slot
         cnt[threadIdx.x] += pcnt[threadIdx.x];
         pcnt[threadIdx.x] = 0;
     }
@@ -286,32 +419,68 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
 
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
-    const int KT = (c->enc_kt == 16 && c->Dp >= 2048) ? 16 : (c->Dp >= 1024 ? 8 : 4);
+    // delta = 1: the label-split kernel (both classes per block); delta > 1 (or the
+    // VSAOGM_ENC_SORTED=1 knob): route points to slots, then slot-filtered blocks
+    const bool slots_path = c->nslots > 2 || c->enc_sorted == 1;
+    const int KT = (!slots_path && c->enc_kt == 16 && c->Dp >= 2048) ? 16 : (c->Dp >= 1024 ? 8 : 4);
     const int kblocks = (c->Dp + ENC_THREADS * KT - 1) / (ENC_THREADS * KT);
     // one full wave at ~6 resident blocks per SM, at least 64 points per chunk
     // resident blocks per SM: 6 (<= 85 registers, the measured best), 7 or 8 as tuning variants
     const int minb = KT == 16 ? 4
-                     : (KT == 8 && (c->enc_npoly == 1 || c->enc_npoly == 2) && (c->enc_minb == 7 || c->enc_minb == 8))
+                     : (!slots_path && KT == 8 && (c->enc_npoly == 1 || c->enc_npoly == 2) &&
+                        (c->enc_minb == 7 || c->enc_minb == 8))
                          ? c->enc_minb
                          : 6;
+    const int zslots = slots_path ? c->nslots : 1;     // grid.z
     const int64_t target_blocks = (int64_t)c->num_sms * minb;
-    int64_t chunks = (target_blocks + kblocks - 1) / kblocks;
+    int64_t chunks = (target_blocks + (int64_t)kblocks * zslots - 1) / ((int64_t)kblocks * zslots);
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
     const int64_t chunk_pts = (n + chunks - 1) / chunks;
     chunks = (n + chunk_pts - 1) / chunk_pts;
-    const size_t need = (size_t)chunks * 2 * c->Dp;
+    const size_t need = (size_t)chunks * c->nslots * c->Dp;
     if (need > c->part_cap) {
         if (c->d_part) cudaFree(c->d_part);
         if (cudaMalloc(&c->d_part, need * sizeof(float2)) != cudaSuccess) { c->d_part = nullptr; c->part_cap = 0; return VSAOGM_ENOMEM; }
         c->part_cap = need;
     }
-    if ((size_t)chunks * 2 > c->part_cnt_cap) {
+    if ((size_t)chunks * c->nslots > c->part_cnt_cap) {
         if (c->d_part_cnt) cudaFree(c->d_part_cnt);
-        if (cudaMalloc(&c->d_part_cnt, chunks * 2 * sizeof(long long)) != cudaSuccess) { c->d_part_cnt = nullptr; c->part_cnt_cap = 0; return VSAOGM_ENOMEM; }
-        c->part_cnt_cap = chunks * 2;
+        if (cudaMalloc(&c->d_part_cnt, chunks * c->nslots * sizeof(long long)) != cudaSuccess) { c->d_part_cnt = nullptr; c->part_cnt_cap = 0; return VSAOGM_ENOMEM; }
+        c->part_cnt_cap = chunks * c->nslots;
     }
     cudaEvent_t ev;
+    const uint8_t *slot = nullptr;
+    if (c->nslots > 2) {
+        if ((size_t)n > c->slot_cap) {
+            if (c->d_slot) cudaFree(c->d_slot);
+            if (cudaMalloc(&c->d_slot, n) != cudaSuccess) { c->d_slot = nullptr; c->slot_cap = 0; return VSAOGM_ENOMEM; }
+            c->slot_cap = n;
+        }
+        vsa_prof_begin(c, VSAOGM_K_ENCODE, &ev);
+        const int rblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->num_sms * 8);
+        k_route<<<rblocks, 256, 0, c->stream>>>((const float2 *)xy, lab, n, c->d_qc, c->nq, c->d_slot, c->d_err);
+        VSA_CUDA_TRY(cudaGetLastError());
+        vsa_prof_end(c, VSAOGM_K_ENCODE, ev);
+        c->launches++;
+        slot = c->d_slot;
+    }
     vsa_prof_begin(c, VSAOGM_K_ENCODE, &ev);
+    if (slots_path) {
+        dim3 grid(kblocks, (unsigned)chunks, (unsigned)zslots);
+#define VSA_ENC_SLOTS(KT_, NP_)                                                                                     \
+    k_encode_slots<KT_, NP_><<<grid, ENC_THREADS, 0, c->stream>>>((const float2 *)xy, lab, slot, n, chunk_pts,       \
+                                                                  c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->nslots, \
+                                                                  c->d_part, c->d_part_cnt, c->d_err)
+        if (KT == 8) {
+            if (c->enc_npoly == 2) VSA_ENC_SLOTS(8, 2);
+            else if (c->enc_npoly == 0) VSA_ENC_SLOTS(8, 0);
+            else VSA_ENC_SLOTS(8, 1);
+        } else {
+            if (c->enc_npoly == 0) VSA_ENC_SLOTS(4, 0);
+            else VSA_ENC_SLOTS(4, 1);
+        }
+#undef VSA_ENC_SLOTS
+    } else {
     dim3 grid(kblocks, (unsigned)chunks);
 #define VSA_ENC_LAUNCH(KT_, NP_, ...)                                                                             \
     k_encode_bundle<KT_, NP_, ##__VA_ARGS__><<<grid, ENC_THREADS, 0, c->stream>>>(                                \
@@ -344,13 +513,14 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
         else VSA_ENC_LAUNCH(4, 1);
     }
 #undef VSA_ENC_LAUNCH
+    }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENCODE, ev);
     c->launches++;
 
     vsa_prof_begin(c, VSAOGM_K_REDUCE, &ev);
-    k_reduce_partials<<<(2 * c->Dp + 31) / 32, 32 * RED_SLICES, 0, c->stream>>>(
-        c->d_part, c->d_part_cnt, (int)chunks, c->Dp, c->D, c->d_pending, c->d_pcounts);
+    k_reduce_partials<<<(c->nslots * c->Dp + 31) / 32, 32 * RED_SLICES, 0, c->stream>>>(
+        c->d_part, c->d_part_cnt, (int)chunks, c->nslots, c->Dp, c->D, c->d_pending, c->d_pcounts);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_REDUCE, ev);
     c->launches++;
@@ -361,8 +531,8 @@ int vsa_launch_commit(vsaogm_ctx *c)
 {
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_COMMIT, &ev);
-    const int n = 4 * c->Dp;
-    k_commit<<<(n + 255) / 256, 256, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, n);
+    const int n = 2 * c->nslots * c->Dp;
+    k_commit<<<(n + 255) / 256, 256, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, n, c->nslots);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_COMMIT, ev);
     c->launches++;
@@ -373,7 +543,7 @@ int vsa_launch_norms(vsaogm_ctx *c, int do_commit)
 {
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_NORMS, &ev);
-    k_commit_norms<<<2, NORM_THREADS, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, do_commit,
+    k_commit_norms<<<c->nslots, NORM_THREADS, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, do_commit,
                                                       c->Dp, c->D, c->d_norm2, c->d_mhat);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_NORMS, ev);

@@ -9,6 +9,12 @@
 // averages; it writes H_b for every decoded row (band +
 // halo) and q for the band's own rows.
 //
+// Grouped problem (quadrant memories, delta > 1, sec. III-B-4): the
+// cells of quadrant (i, j) query that quadrant's memories, so the contraction
+// is a set of GEMMs, one per quadrant: A rows of the quadrant's (class, row)
+// block x B rows (= grid columns) of the quadrant's column range.  `Groups`
+// (passed by value) lists them; delta = 1 is the single group.
+//
 // Two tcgen05 kernels, both persistent with warp-specialised roles:
 //
 // k_decode_gemm2 (default): CTA pairs (cluster 2x1, cta_group::2), UMMA
@@ -20,9 +26,10 @@
 //   its own TMEM half (double-buffered accumulator) and signal CTA 0.  Half the
 //   B bytes per SM relative to the 1-CTA tile (L2 -> SM traffic is the limit).
 //   BN is chosen per problem from {256, 224, 192, 160, 128} to minimise
-//   waves x BN on the 74 SM pairs.
-// k_decode_gemm (1-CTA, M=128 x N=256): the first version, kept as a
-//   measured comparison point (VSAOGM_GEMM=1cta) and for the test hook.
+//   waves x BN on the 74 SM pairs; split-K (fixed-order reduction) when the
+//   tiles cannot fill the GPU.
+// k_decode_gemm (1-CTA, M=128 x N=256, single group): the first version, kept as
+//   a measured comparison point (VSAOGM_GEMM=1cta) and for the test hook.
 #include <cudaTypedefs.h>
 
 #include <stdlib.h>
@@ -41,12 +48,15 @@ constexpr size_t GEMM_SMEM = 1024 + (size_t)VSA_STAGES * STAGE_BYTES + 256;
 constexpr int STAGES2 = 6;                                // 2-CTA ring depth (32 KB / stage at BN=256)
 
 struct Epi {
-    float *C;          // raw mode output [M][N]
-    float inv_scale;   // VSA mode: q = acc * inv_scale
-    float *hb;         // VSA mode: [M][ldh], ldh = N rounded up to 8
-    float *q;          // VSA mode: [2][band_rows][N] or null
-    int r_ext, band_off, band_rows, ldh;
-    float *ws;         // split-K workspace [splits][M][N] fp32
+    float *C;          // MODE 0: raw output, row = group A row, ldc = total columns
+    int ldc;
+    float inv_scale;   // VSA: q = acc * inv_scale
+    float *hb;         // VSA: hb[(c * r_ext + row) * ldh + col]
+    int ldh, r_ext;
+    float *q;          // VSA: q[(c * band_rows + row + q_off) * qcols + col] for band rows, or null
+    int q_off, band_rows, qcols;
+    float *ws;         // split-K partials ws[(s * ws_rows + a_row) * ws_cols + col]
+    int ws_rows, ws_cols;
     int splits, kb_per;
 };
 
@@ -59,64 +69,59 @@ __device__ __forceinline__ float hb_of_p(float p)
     return h;
 }
 
-// One thread's 32 consecutive accumulator columns of row m, starting at column n0.
-template <int MODE>
-__device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int m, int n0, int M, int N, const Epi &epi)
+__device__ __forceinline__ void store32(float *dst, const float *v, int nvalid, bool vec_ok)
 {
-    if (m >= M || n0 >= N) return;
-    const bool full_chunk = (n0 + 32 <= N) && ((N & 3) == 0);
-    if (MODE == 0) {
-        float *dst = epi.C + (size_t)m * N + n0;
-        if (full_chunk) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                                   __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-        } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (n0 + j < N) dst[j] = __uint_as_float(v[j]);
-        }
-        return;
-    }
-    const int cls = m / epi.r_ext;
-    const int i = m - cls * epi.r_ext;
-    const bool q_row = epi.q && i >= epi.band_off && i < epi.band_off + epi.band_rows;
-    float qv[32], hv[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        qv[j] = __uint_as_float(v[j]) * epi.inv_scale;
-        hv[j] = hb_of_p(fminf(qv[j] * qv[j], 1.f));
-    }
-    float *hdst = epi.hb + (size_t)m * epi.ldh + n0;
-    if (n0 + 32 <= N) {
+    if (nvalid == 32 && vec_ok) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4 *>(hdst + j) = make_float4(hv[j], hv[j + 1], hv[j + 2], hv[j + 3]);
+            *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-            if (n0 + j < N) hdst[j] = hv[j];
-    }
-    if (q_row) {
-        float *qdst = epi.q + ((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n0;
-        if (full_chunk) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4 *>(qdst + j) = make_float4(qv[j], qv[j + 1], qv[j + 2], qv[j + 3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (n0 + j < N) qdst[j] = qv[j];
-        }
+            if (j < nvalid) dst[j] = v[j];
     }
 }
 
-// ------------------------------------------------------------------ 1-CTA kernel
+// One thread's 32 consecutive accumulator columns of local row m_l of group g,
+// starting at local column n0.  MODE 0: raw; MODE 1: VSA; MODE 2: split-K partial of split sk.
+template <int MODE>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], const Groups &G, int g, int m_l, int n0,
+                                               int sk, const Epi &e)
+{
+    if (m_l >= G.mrows[g] || n0 >= G.ncols[g]) return;
+    const int nvalid = min(32, G.ncols[g] - n0);
+    const int col = G.col0[g] + n0;
+    float f[32];
+    if (MODE != 1) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        const int a_row = G.a_row0[g] + m_l;
+        float *dst = MODE == 0 ? e.C + (size_t)a_row * e.ldc + col
+                               : e.ws + ((size_t)sk * e.ws_rows + a_row) * e.ws_cols + col;
+        const int ld = MODE == 0 ? e.ldc : e.ws_cols;
+        store32(dst, f, nvalid, ((col | ld) & 3) == 0);
+        return;
+    }
+    const int nr = G.nrows[g];
+    const int cls = m_l >= nr;
+    const int row = G.row0[g] + m_l - cls * nr;
+    float hv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        f[j] = __uint_as_float(v[j]) * e.inv_scale;
+        hv[j] = hb_of_p(fminf(f[j] * f[j], 1.f));
+    }
+    store32(e.hb + ((size_t)cls * e.r_ext + row) * e.ldh + col, hv, nvalid, (col & 3) == 0);
+    const int br = row + e.q_off;
+    if (e.q && br >= 0 && br < e.band_rows)
+        store32(e.q + ((size_t)cls * e.band_rows + br) * e.qcols + col, f, nvalid, ((col | e.qcols) & 3) == 0);
+}
+
+// ------------------------------------------------------------------ 1-CTA kernel (single group)
 template <int MODE>   // 0 = raw fp32 store (test hook), 1 = VSA epilogue
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_decode_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                  int K, uint32_t idesc, Epi epi)
+    k_decode_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ Groups G, int K, uint32_t idesc, Epi epi)
 {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -132,8 +137,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int num_m = (M + VSA_BM - 1) / VSA_BM;
-    const int num_n = (N + VSA_BN - 1) / VSA_BN;
+    const int num_m = (G.mrows[0] + VSA_BM - 1) / VSA_BM;
+    const int num_n = (G.ncols[0] + VSA_BN - 1) / VSA_BN;
     const int num_tiles = num_m * num_n;
     const int num_kb = K / VSA_BK;
 
@@ -170,8 +175,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    tma_load_2d(sA + stage * A_TILE_BYTES, &tmA, &full[stage], kb * VSA_BK, mb * VSA_BM);
-                    tma_load_2d(sB + stage * B_TILE_BYTES, &tmB, &full[stage], kb * VSA_BK, nb * VSA_BN);
+                    tma_load_2d(sA + stage * A_TILE_BYTES, &tmA, &full[stage], kb * VSA_BK,
+                                G.a_row0[0] + mb * VSA_BM);
+                    tma_load_2d(sB + stage * B_TILE_BYTES, &tmB, &full[stage], kb * VSA_BK,
+                                G.col0[0] + nb * VSA_BN);
                     if (++stage == VSA_STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -208,14 +215,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int mb = tile % num_m, nb = tile / num_m;
             mbar_wait(&tfull[as], aphase);
             tc_fence_after();
-            const int m = mb * VSA_BM + row_in_tile;
 #pragma unroll 1
             for (int cc = 0; cc < VSA_BN / 32; ++cc) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + as * VSA_BN + cc * 32;
                 TMEM_LD_32x32b_X32(taddr, v);
                 tmem_ld_wait();
-                epilogue_chunk<MODE>(v, m, nb * VSA_BN + cc * 32, M, N, epi);
+                epilogue_chunk<MODE>(v, G, 0, mb * VSA_BM + row_in_tile, nb * VSA_BN + cc * 32, 0, epi);
             }
             tc_fence_before();
             mbar_arrive(&tempty[as]);
@@ -231,16 +237,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
 }
 
-// ------------------------------------------------------------------ 2-CTA kernel
+// ------------------------------------------------------------------ 2-CTA kernel (grouped, split-K)
+// work unit u -> (tile t = u / S, split sk = u % S); tile t -> group g (prefix of the
+// groups' tile counts) -> n-fastest (mb, nb) inside the group.
+__device__ __forceinline__ void unit_coords(int tile, const int *s_pref, const int *s_tn, int ng, int &g, int &mb,
+                                            int &nb)
+{
+    g = 0;
+    while (g + 1 < ng && tile >= s_pref[g + 1]) ++g;
+    const int lt = tile - s_pref[g];
+    nb = lt % s_tn[g];
+    mb = lt / s_tn[g];
+}
+
 template <int MODE, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
-    k_decode_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, uint32_t idesc, Epi epi)
+    k_decode_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ Groups G, int K, uint32_t idesc, Epi epi)
 {
     constexpr uint32_t A_BYTES = 128 * VSA_BK * 2;          // this CTA's 128 rows of A
     constexpr uint32_t BH_BYTES = (BN / 2) * VSA_BK * 2;    // this CTA's half of B
     constexpr uint32_t ST_BYTES = A_BYTES + BH_BYTES;
     extern __shared__ uint8_t smem_raw[];
+    __shared__ int s_pref[VSA_MAX_GROUPS + 1], s_tn[VSA_MAX_GROUPS];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t *smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
     uint8_t *sA = smem;
@@ -256,13 +275,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
-    const int num_m = (M + 255) / 256;
-    const int num_n = (N + BN - 1) / BN;
-    const int num_tiles = num_m * num_n;
     const int num_kb = K / VSA_BK;
     const int S = epi.splits;                 // split-K factor (1 = none)
+    const int ng = G.n;
 
     if (threadIdx.x == 0) {
+        int t = 0;
+        for (int g = 0; g < ng; ++g) {
+            s_pref[g] = t;
+            s_tn[g] = (G.ncols[g] + BN - 1) / BN;
+            t += ((G.mrows[g] + 255) / 256) * s_tn[g];
+        }
+        s_pref[ng] = t;
         for (int s = 0; s < STAGES2; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -284,17 +308,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const int num_units = s_pref[ng] * S;
 
     if (warp == 0) {
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
             uint32_t stage = 0, phase = 0;
-            for (int u = pair; u < num_tiles * S; u += num_pairs) {
+            for (int u = pair; u < num_units; u += num_pairs) {
                 const int tile = u / S, sk = u - tile * S;
-                const int nb = tile % num_n, mb = tile / num_n;   // n-fastest: a wave reads A once
-                const int arow = mb * 256 + (int)rank * 128;
-                const int brow = nb * BN + (int)rank * (BN / 2);
+                int g, mb, nb;
+                unit_coords(tile, s_pref, s_tn, ng, g, mb, nb);
+                const int arow = G.a_row0[g] + mb * 256 + (int)rank * 128;
+                const int brow = G.col0[g] + nb * BN + (int)rank * (BN / 2);
                 const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
@@ -308,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     } else if (warp == 1) {
         if (rank == 0 && lane == 0) {
             uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
-            for (int u = pair; u < num_tiles * S; u += num_pairs) {
+            for (int u = pair; u < num_units; u += num_pairs) {
                 const int sk = u % S;
                 const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
                 mbar_wait_cluster(&tempty[as], aphase ^ 1);
@@ -334,22 +360,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int quarter = warp & 3;
         const int row_in_tile = (int)rank * 128 + quarter * 32 + lane;
         uint32_t as = 0, aphase = 0;
-        Epi part = epi;                       // split-K: raw fp32 partial sums to the workspace
-        for (int u = pair; u < num_tiles * S; u += num_pairs) {
+        for (int u = pair; u < num_units; u += num_pairs) {
             const int tile = u / S, sk = u - tile * S;
-            const int nb = tile % num_n, mb = tile / num_n;
+            int g, mb, nb;
+            unit_coords(tile, s_pref, s_tn, ng, g, mb, nb);
             mbar_wait_cluster(&tfull[as], aphase);
             tc_fence_after();
-            const int m = mb * 256 + row_in_tile;
-            part.C = epi.ws + (size_t)sk * M * N;
+            const int m_l = mb * 256 + row_in_tile;
 #pragma unroll 1
             for (int cc = 0; cc < BN / 32; ++cc) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + as * 256 + cc * 32;
                 TMEM_LD_32x32b_X32(taddr, v);
                 tmem_ld_wait();
-                if (S == 1) epilogue_chunk<MODE>(v, m, nb * BN + cc * 32, M, N, epi);
-                else epilogue_chunk<0>(v, m, nb * BN + cc * 32, M, N, part);
+                if (S == 1) epilogue_chunk<MODE>(v, G, g, m_l, nb * BN + cc * 32, 0, epi);
+                else epilogue_chunk<2>(v, G, g, m_l, nb * BN + cc * 32, sk, epi);
             }
             tc_fence_before();
             __syncwarp();
@@ -369,23 +394,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 
 // split-K: sum the partial accumulators in split order (deterministic), then the epilogue
 template <int MODE>
-__global__ void __launch_bounds__(256) k_splitk_reduce(int M, int N, Epi epi)
+__global__ void __launch_bounds__(256) k_splitk_reduce(const __grid_constant__ Groups G, Epi e)
 {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t MN = (size_t)M * N;
-    if (idx >= MN) return;
+    const size_t RC = (size_t)e.ws_rows * e.ws_cols;
+    if (idx >= RC) return;
+    const int a_row = (int)(idx / e.ws_cols), col = (int)(idx - (size_t)a_row * e.ws_cols);
+    int g = -1;
+    for (int k = 0; k < G.n; ++k)
+        if (a_row >= G.a_row0[k] && a_row < G.a_row0[k] + G.mrows[k] && col >= G.col0[k] &&
+            col < G.col0[k] + G.ncols[k]) { g = k; break; }
+    if (g < 0) return;
     float acc = 0.f;
-    for (int s = 0; s < epi.splits; ++s) acc += epi.ws[(size_t)s * MN + idx];
+    for (int s = 0; s < e.splits; ++s) acc += e.ws[(size_t)s * RC + idx];
     if (MODE == 0) {
-        epi.C[idx] = acc;
+        e.C[(size_t)a_row * e.ldc + col] = acc;
         return;
     }
-    const int m = (int)(idx / N), n = (int)(idx - (size_t)m * N);
-    const float q = acc * epi.inv_scale;
-    epi.hb[(size_t)m * epi.ldh + n] = hb_of_p(fminf(q * q, 1.f));
-    const int cls = m / epi.r_ext, i = m - cls * epi.r_ext;
-    if (epi.q && i >= epi.band_off && i < epi.band_off + epi.band_rows)
-        epi.q[((size_t)cls * epi.band_rows + (i - epi.band_off)) * N + n] = q;
+    const int m_l = a_row - G.a_row0[g];
+    const int nr = G.nrows[g];
+    const int cls = m_l >= nr;
+    const int row = G.row0[g] + m_l - cls * nr;
+    const float q = acc * e.inv_scale;
+    e.hb[((size_t)cls * e.r_ext + row) * e.ldh + col] = hb_of_p(fminf(q * q, 1.f));
+    const int br = row + e.q_off;
+    if (e.q && br >= 0 && br < e.band_rows) e.q[((size_t)cls * e.band_rows + br) * e.qcols + col] = q;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
@@ -419,56 +452,66 @@ int make_map(CUtensorMap *map, const void *ptr, int rows, int K, int box_rows, i
 }
 
 template <int MODE>
-int launch1(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms)
+int launch1(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, const Epi &epi,
+            cudaStream_t s, int num_sms)
 {
+    if (G.n != 1) return VSAOGM_EINVAL_ARG;
     CUtensorMap ta, tb;
-    int rc = make_map(&ta, A, M, K, VSA_BM, prec);
+    int rc = make_map(&ta, A, a_rows, K, VSA_BM, prec);
     if (rc) return rc;
-    rc = make_map(&tb, B, N, K, VSA_BN, prec);
+    rc = make_map(&tb, B, b_rows, K, VSA_BN, prec);
     if (rc) return rc;
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
-    const int tiles = ((M + VSA_BM - 1) / VSA_BM) * ((N + VSA_BN - 1) / VSA_BN);
+    const int tiles = ((G.mrows[0] + VSA_BM - 1) / VSA_BM) * ((G.ncols[0] + VSA_BN - 1) / VSA_BN);
     const int grid = tiles < num_sms ? tiles : num_sms;
     const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, VSA_BM, VSA_BN);
-    k_decode_gemm<MODE><<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(ta, tb, M, N, K, idesc, epi);
+    k_decode_gemm<MODE><<<grid, GEMM_THREADS, GEMM_SMEM, s>>>(ta, tb, G, K, idesc, epi);
     VSA_CUDA_TRY(cudaGetLastError());
     return VSAOGM_OK;
 }
 
+long group_tiles(const Groups &G, int bn)
+{
+    long t = 0;
+    for (int g = 0; g < G.n; ++g) t += (long)((G.mrows[g] + 255) / 256) * ((G.ncols[g] + bn - 1) / bn);
+    return t;
+}
+
 template <int MODE, int BN>
-int launch2_bn(const void *A, const void *B, int M, int N, int K, int prec, Epi epi, cudaStream_t s, int num_sms)
+int launch2_bn(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, Epi epi,
+               cudaStream_t s, int num_sms)
 {
     CUtensorMap ta, tb;
-    int rc = make_map(&ta, A, M, K, 128, prec);
+    int rc = make_map(&ta, A, a_rows, K, 128, prec);
     if (rc) return rc;
-    rc = make_map(&tb, B, N, K, BN / 2, prec);
+    rc = make_map(&tb, B, b_rows, K, BN / 2, prec);
     if (rc) return rc;
     const size_t smem = 1024 + (size_t)STAGES2 * (128 + BN / 2) * VSA_BK * 2 + 256;
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int units = ((M + 255) / 256) * ((N + BN - 1) / BN) * epi.splits;
+    const long units = group_tiles(G, BN) * epi.splits;
     const int pairs = num_sms / 2;
-    const int grid = 2 * (units < pairs ? units : pairs);
+    const int grid = 2 * (int)(units < pairs ? units : pairs);
+    if (grid == 0) return VSAOGM_OK;
     const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, 256, BN);
-    k_decode_gemm2<MODE, BN><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, M, N, K, idesc, epi);
+    k_decode_gemm2<MODE, BN><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, G, K, idesc, epi);
     VSA_CUDA_TRY(cudaGetLastError());
     if (epi.splits > 1) {
-        const size_t MN = (size_t)M * N;
-        k_splitk_reduce<MODE><<<(unsigned)((MN + 255) / 256), 256, 0, s>>>(M, N, epi);
+        const size_t RC = (size_t)epi.ws_rows * epi.ws_cols;
+        k_splitk_reduce<MODE><<<(unsigned)((RC + 255) / 256), 256, 0, s>>>(G, epi);
         VSA_CUDA_TRY(cudaGetLastError());
     }
     return VSAOGM_OK;
 }
 
 // BN minimising (waves x BN): the MMA time of a tile is proportional to BN.
-int pick_bn(int M, int N, int num_sms)
+int pick_bn(const Groups &G, int num_sms)
 {
     static const int cands[] = {256, 224, 192, 160, 128};
     const int pairs = num_sms / 2;
-    const int num_m = (M + 255) / 256;
     int best = 256;
     long best_cost = -1;
     for (int bn : cands) {
-        const long tiles = (long)num_m * ((N + bn - 1) / bn);
+        const long tiles = group_tiles(G, bn);
         const long cost = ((tiles + pairs - 1) / pairs) * bn;
         if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
     }
@@ -478,10 +521,10 @@ int pick_bn(int M, int N, int num_sms)
 // Split-K factor for short problems (few tiles for 74 SM pairs, e.g. the row band of one
 // rank of 8): model time = waves * tile_time / S + partial-sum traffic, tile_time from the
 // measured ~16 TFLOP/s per SM pair, traffic at ~5 TB/s.  S = 1 when the tiles fill the GPU.
-int pick_splits(int M, int N, int K, int bn, int num_sms)
+int pick_splits(const Groups &G, int ws_rows, int ws_cols, int K, int bn, int num_sms)
 {
     const int pairs = num_sms / 2;
-    const long tiles = (long)((M + 255) / 256) * ((N + bn - 1) / bn);
+    const long tiles = group_tiles(G, bn);
     const int num_kb = K / VSA_BK;
     const double t_tile = 2.0 * 256 * bn * (double)K / 16e12 * 1e6;   // us
     double best_t = -1;
@@ -489,47 +532,49 @@ int pick_splits(int M, int N, int K, int bn, int num_sms)
     for (int S = 1; S <= 16 && S <= num_kb / 4; ++S) {
         const double waves = (double)((tiles * S + pairs - 1) / pairs);
         double t = waves * t_tile / S;
-        if (S > 1) t += 2.0 * S * (double)M * N * 4 / 5e12 * 1e6 + 3.0;
+        if (S > 1) t += 2.0 * S * (double)ws_rows * ws_cols * 4 / 5e12 * 1e6 + 3.0;
         if (best_t < 0 || t < best_t * 0.97) { best_t = t; best = S; }
     }
     return best;
 }
 
 template <int MODE>
-int launch2(const void *A, const void *B, int M, int N, int K, int prec, const Epi &epi, cudaStream_t s, int num_sms,
-            int bn)
+int launch2(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, const Epi &epi,
+            cudaStream_t s, int num_sms, int bn)
 {
     switch (bn) {
-    case 224: return launch2_bn<MODE, 224>(A, B, M, N, K, prec, epi, s, num_sms);
-    case 192: return launch2_bn<MODE, 192>(A, B, M, N, K, prec, epi, s, num_sms);
-    case 160: return launch2_bn<MODE, 160>(A, B, M, N, K, prec, epi, s, num_sms);
-    case 128: return launch2_bn<MODE, 128>(A, B, M, N, K, prec, epi, s, num_sms);
-    default: return launch2_bn<MODE, 256>(A, B, M, N, K, prec, epi, s, num_sms);
+    case 224: return launch2_bn<MODE, 224>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    case 192: return launch2_bn<MODE, 192>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    case 160: return launch2_bn<MODE, 160>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    case 128: return launch2_bn<MODE, 128>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    default: return launch2_bn<MODE, 256>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
     }
 }
 
-// variant: 0 = 2-CTA (default), 1 = 1-CTA; env VSAOGM_GEMM=1cta selects the latter,
-// VSAOGM_GEMM_BN=<n> pins the 2-CTA tile width, VSAOGM_GEMM_SPLITS=<s> the split-K factor.
-// *ws / *ws_cap: a caller-owned growable workspace for split-K partials.
+// variant: 0 = 2-CTA (default), 1 = 1-CTA (single group only); env VSAOGM_GEMM=1cta selects
+// the latter, VSAOGM_GEMM_BN=<n> pins the 2-CTA tile width, VSAOGM_GEMM_SPLITS=<s> the split-K
+// factor.  *ws / *ws_cap: a caller-owned growable workspace for split-K partials.
 template <int MODE>
-int launch(const void *A, const void *B, int M, int N, int K, int prec, Epi epi, cudaStream_t s, int num_sms,
-           int variant, float **ws, size_t *ws_cap)
+int launch(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, Epi epi,
+           cudaStream_t s, int num_sms, int variant, float **ws, size_t *ws_cap)
 {
     if (variant < 0) {
         const char *e = getenv("VSAOGM_GEMM");
-        variant = (e && strcmp(e, "1cta") == 0) ? 1 : 0;
+        variant = (e && strcmp(e, "1cta") == 0 && G.n == 1) ? 1 : 0;
     }
-    if (variant == 1) return launch1<MODE>(A, B, M, N, K, prec, epi, s, num_sms);
-    int bn = pick_bn(M, N, num_sms);
+    if (variant == 1) return launch1<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    int bn = pick_bn(G, num_sms);
     if (const char *e = getenv("VSAOGM_GEMM_BN")) bn = atoi(e);
-    int S = pick_splits(M, N, K, bn, num_sms);
+    epi.ws_rows = a_rows;
+    epi.ws_cols = b_rows;
+    int S = pick_splits(G, a_rows, b_rows, K, bn, num_sms);
     if (const char *e = getenv("VSAOGM_GEMM_SPLITS")) S = atoi(e);
     const int num_kb = K / VSA_BK;
     S = std::max(1, std::min(S, num_kb));
     epi.kb_per = (num_kb + S - 1) / S;
     epi.splits = (num_kb + epi.kb_per - 1) / epi.kb_per;   // no empty split
     if (epi.splits > 1) {
-        const size_t need = (size_t)epi.splits * M * N * sizeof(float);
+        const size_t need = (size_t)epi.splits * a_rows * b_rows * sizeof(float);
         if (need > *ws_cap) {
             if (*ws) cudaFree(*ws);
             *ws = nullptr;
@@ -539,27 +584,28 @@ int launch(const void *A, const void *B, int M, int N, int K, int prec, Epi epi,
         }
         epi.ws = *ws;
     }
-    return launch2<MODE>(A, B, M, N, K, prec, epi, s, num_sms, bn);
+    return launch2<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, bn);
 }
 
 }  // namespace
 
-int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float inv_scale, float *hb, float *q,
-                           int32_t r_ext, int32_t band_off, int32_t band_rows)
+int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32_t N, int prec, float inv_scale,
+                           float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows)
 {
     Epi e{};
     e.inv_scale = inv_scale;
     e.hb = hb;
-    e.q = q;
-    e.r_ext = r_ext;
-    e.band_off = band_off;
-    e.band_rows = band_rows;
     e.ldh = (N + 7) / 8 * 8;
+    e.r_ext = r_ext;
+    e.q = q;
+    e.q_off = q_off;
+    e.band_rows = band_rows;
+    e.qcols = N;
     e.splits = 1;
     e.kb_per = c->Kp / VSA_BK;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
-    int rc = launch<1>(c->d_A, c->d_B, M, N, c->Kp, prec, e, c->stream, c->num_sms, -1, &c->d_ws, &c->ws_cap);
+    int rc = launch<1>(c->d_A, c->d_B, a_rows, N, c->Kp, prec, G, e, c->stream, c->num_sms, -1, &c->d_ws, &c->ws_cap);
     if (rc) return rc;
     vsa_prof_end(c, VSAOGM_K_DECODE_GEMM, ev);
     c->launches++;
@@ -569,13 +615,22 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, int32_t M, int32_t N, int prec, float 
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C, cudaStream_t s,
                  int num_sms, int variant)
 {
+    Groups G{};
+    G.n = 1;
+    G.a_row0[0] = 0;
+    G.mrows[0] = M;
+    G.nrows[0] = M;
+    G.row0[0] = 0;
+    G.col0[0] = 0;
+    G.ncols[0] = N;
     Epi e{};
     e.C = C;
+    e.ldc = N;
     e.splits = 1;
     e.kb_per = K / VSA_BK;
     float *ws = nullptr;
     size_t cap = 0;
-    int rc = launch<0>(A, B, M, N, K, prec, e, s, num_sms, variant, &ws, &cap);
+    int rc = launch<0>(A, B, M, N, K, prec, G, e, s, num_sms, variant, &ws, &cap);
     if (ws) {
         cudaStreamSynchronize(s);
         cudaFree(ws);

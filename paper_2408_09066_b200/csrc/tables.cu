@@ -127,15 +127,16 @@ int grow(void **p, size_t *cap, size_t need)
 }
 
 template <bool IS_A>
-void launch_table(vsaogm_ctx *c, void *out, int rows, const double *tau, double base, double res, int row0, int prec)
+void launch_table(vsaogm_ctx *c, void *out, int rows, const double *tau, double base, double res, int row0, int prec,
+                  const float2 *mhat)
 {
     dim3 grid((c->Dp / TAB_KT + TAB_THREADS - 1) / TAB_THREADS, (rows + TAB_ROWS - 1) / TAB_ROWS);
     if (prec == VSAOGM_BF16)
         k_table<__nv_bfloat162, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp,
-                                                                            tau, base, res, row0, c->d_mhat);
+                                                                            tau, base, res, row0, mhat);
     else
         k_table<__half2, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp, tau,
-                                                                     base, res, row0, c->d_mhat);
+                                                                     base, res, row0, mhat);
 }
 
 }  // namespace
@@ -149,7 +150,7 @@ int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int p
     if (rc) return rc;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_TABLE_B, &ev);
-    launch_table<false>(c, c->d_B, cols, c->d_tx_turns, x0 - c->cx, res, 0, prec);
+    launch_table<false>(c, c->d_B, cols, c->d_tx_turns, x0 - c->cx, res, 0, prec, nullptr);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_TABLE_B, ev);
     c->launches++;
@@ -158,16 +159,24 @@ int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int p
     return VSAOGM_OK;
 }
 
-int vsa_launch_table_A(vsaogm_ctx *c, double y0, double res, int32_t r_lo, int32_t r_ext, int prec)
+// One A block per decode group (quadrant): rows [a_row0, a_row0 + 2 nrows) hold the
+// class-0 then class-1 rows of the group's decoded grid rows, built from the group's
+// memory slots slot0[g], slot0[g] + 1 (delta = 1: one group, slots 0 and 1).
+int vsa_launch_table_A(vsaogm_ctx *c, const Groups &G, double y0, double res, int32_t r_lo, int prec,
+                       const int *slot0)
 {
-    const size_t bytes = (size_t)2 * r_ext * c->Kp * 2;
-    int rc = grow(&c->d_A, &c->A_cap, bytes);
+    size_t rows = 0;
+    for (int g = 0; g < G.n; ++g) rows = std::max(rows, (size_t)(G.a_row0[g] + G.mrows[g]));
+    int rc = grow(&c->d_A, &c->A_cap, rows * c->Kp * 2);
     if (rc) return rc;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_TABLE_A, &ev);
-    launch_table<true>(c, c->d_A, r_ext, c->d_ty_turns, y0 - c->cy, res, r_lo, prec);
+    for (int g = 0; g < G.n; ++g) {
+        launch_table<true>(c, (uint8_t *)c->d_A + (size_t)G.a_row0[g] * c->Kp * 2, G.nrows[g], c->d_ty_turns,
+                           y0 - c->cy, res, r_lo + G.row0[g], prec, c->d_mhat + (size_t)slot0[g] * c->Dp);
+        c->launches++;
+    }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_TABLE_A, ev);
-    c->launches++;
     return VSAOGM_OK;
 }

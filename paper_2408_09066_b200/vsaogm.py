@@ -21,7 +21,7 @@ KERNELS = ("encode", "reduce", "commit", "norms", "table_B", "table_A", "decode_
 
 # every symbol include/vsaogm.h declares
 EXPORTS = (
-    "vsaogm_create", "vsaogm_destroy", "vsaogm_set_stream", "vsaogm_encode_bundle", "vsaogm_encode_bundle_host",
+    "vsaogm_create", "vsaogm_create_quadrants", "vsaogm_destroy", "vsaogm_set_stream", "vsaogm_encode_bundle", "vsaogm_encode_bundle_host",
     "vsaogm_pending", "vsaogm_pending_counts", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
     "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror",
@@ -64,6 +64,7 @@ def load() -> ctypes.CDLL:
     P, i32, i64, u64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
     sig = {
         "vsaogm_create": ([i32, u64, f64, Bounds, ctypes.POINTER(P)], ctypes.c_int),
+        "vsaogm_create_quadrants": ([i32, u64, f64, Bounds, i32, ctypes.POINTER(P)], ctypes.c_int),
         "vsaogm_destroy": ([P], None),
         "vsaogm_set_stream": ([P, P], ctypes.c_int),
         "vsaogm_encode_bundle": ([P, P, P, i64], ctypes.c_int),
@@ -123,16 +124,20 @@ def _host_ptr(a) -> ctypes.c_void_p:
 
 
 class Mapper:
-    """One VSA-OGM context on the current CUDA device (vsaogm_create)."""
+    """One VSA-OGM context on the current CUDA device (vsaogm_create_quadrants; delta = 1 is
+    vsaogm_create).  Memories are indexed by slot 2 beta + psi (beta = quadrant, psi = class)."""
 
-    def __init__(self, D: int, seed: int, length_scale: float, bounds):
+    def __init__(self, D: int, seed: int, length_scale: float, bounds, delta: int = 1):
         lib = load()
         self._lib = lib
         self.D = int(D)
         self.Dp = (self.D + 31) // 32 * 32
+        self.delta = int(delta)
+        self.nslots = 2 * self.delta * self.delta
         ctx = ctypes.c_void_p()
-        _check(lib.vsaogm_create(self.D, ctypes.c_uint64(seed), float(length_scale), Bounds(*map(float, bounds)),
-                                 ctypes.byref(ctx)), "vsaogm_create")
+        _check(lib.vsaogm_create_quadrants(self.D, ctypes.c_uint64(seed), float(length_scale),
+                                           Bounds(*map(float, bounds)), self.delta, ctypes.byref(ctx)),
+               "vsaogm_create_quadrants")
         self._ctx = ctx
         self.device = torch.cuda.current_device()
 
@@ -168,16 +173,16 @@ class Mapper:
                "vsaogm_encode_bundle_host")
 
     def pending(self) -> torch.Tensor:
-        """fp64 [2, Dp, 2] CUDA view of the pending memories (for all_reduce, Alg. 3)."""
+        """fp64 [2 delta^2, Dp, 2] CUDA view of the pending memories (for all_reduce, Alg. 3)."""
         p = ctypes.c_void_p()
         n = ctypes.c_int64()
         _check(self._lib.vsaogm_pending(self._ctx, ctypes.byref(p), ctypes.byref(n)), "vsaogm_pending")
-        return _wrap_device(p.value, (2, self.Dp, 2), torch.float64, self.device)
+        return _wrap_device(p.value, (self.nslots, self.Dp, 2), torch.float64, self.device)
 
     def pending_counts(self) -> torch.Tensor:
         p = ctypes.c_void_p()
         _check(self._lib.vsaogm_pending_counts(self._ctx, ctypes.byref(p)), "vsaogm_pending_counts")
-        return _wrap_device(p.value, (2,), torch.int64, self.device)
+        return _wrap_device(p.value, (self.nslots,), torch.int64, self.device)
 
     def commit(self):
         self._s()
@@ -221,8 +226,8 @@ class Mapper:
     def get_memory(self):
         import numpy as np
         self._s()
-        m = np.zeros((2, self.D, 2), dtype=np.float64)
-        cnt = np.zeros(2, dtype=np.int64)
+        m = np.zeros((self.nslots, self.D, 2), dtype=np.float64)
+        cnt = np.zeros(self.nslots, dtype=np.int64)
         _check(self._lib.vsaogm_get_memory(self._ctx, _host_ptr(m), _host_ptr(cnt)), "vsaogm_get_memory")
         return m[..., 0] + 1j * m[..., 1], cnt
 
