@@ -143,7 +143,9 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
         if (const char *e = getenv("VSAOGM_ENC_MINB")) c->enc_minb = atoi(e);     // tuning knob (6 or 8)
         if (const char *e = getenv("VSAOGM_ENC_KT")) c->enc_kt = atoi(e);         // tuning knob (8 or 16)
-        if (const char *e = getenv("VSAOGM_ENC_SORTED")) c->enc_sorted = atoi(e); // tuning knob (-1 or 1)
+        if (const char *e = getenv("VSAOGM_ENC_PATH")) c->enc_path = atoi(e);     // tuning knob (0, 1, 2)
+        if (const char *e = getenv("VSAOGM_ENC_WAVES")) c->enc_waves = std::max(1, atoi(e));
+        if (const char *e = getenv("VSAOGM_ENC_RUNS_WAVES")) c->enc_runs_waves = std::max(1, atoi(e));
         c->delta = delta;
         c->nq = delta * delta;
         c->nslots = 2 * c->nq;
@@ -218,7 +220,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
                     c->d_norm2, c->d_mhat, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
-                    c->d_sortmeta, c->d_sorted};
+                    c->d_sortmeta, c->d_sorted, c->d_runs};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

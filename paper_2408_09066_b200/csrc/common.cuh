@@ -67,7 +67,12 @@ struct vsaogm_ctx {
     int *d_bhist = nullptr; size_t bhist_cap = 0;     // per-block slot histograms
     int *d_sortmeta = nullptr;                     // slot totals / starts / vchunk table
     float2 *d_sorted = nullptr; size_t sorted_cap = 0;
-    int enc_sorted = -1;  // -1: sorted path only for delta > 1; 1: always (tuning knob)
+    int4 *d_runs = nullptr; size_t runs_cap = 0;      // runs of one slot (sorted encode)
+    // encode path: -1 auto (delta = 1: label-split blocks, measured fastest; delta > 1: sorted
+    // runs); 0 sorted runs; 1 label-split / slot-filtered; 2 slot-filtered (tuning knob)
+    int enc_path = -1;
+    int enc_waves = 16;   // waves of slot-filtered encode blocks (tuning knob)
+    int enc_runs_waves = 4;   // waves of sorted-run encode blocks (tuning knob)
     int enc_npoly = 1;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
     int enc_minb = 6;   // encode blocks resident per SM (6: 80 regs, 8: <= 64 regs) (tuning knob)
     int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
@@ -126,6 +131,7 @@ void vsa_prof_end(vsaogm_ctx *c, int kid, cudaEvent_t a);
 
 // ---- launchers implemented in the kernel translation units -----------------
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
+int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
 int vsa_launch_commit(vsaogm_ctx *c);
 int vsa_launch_norms(vsaogm_ctx *c, int do_commit);   // [commit +] norms + scaled memory mhat
 int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec);
@@ -233,6 +239,37 @@ __host__ __device__ __forceinline__ uint32_t make_idesc_f16(int bf16, int M, int
         : "r"(taddr))
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// sin/cos on the FMA + ALU pipes (no MUFU), 18 instructions: half-turn
+// reduction phi = q pi + r (q by the magic-number rint, 2-term Cody-Waite pi;
+// |q| < 2^12 keeps q * 3.140625 exact), then near-minimax polynomials on
+// [-pi/2, pi/2] (odd degree 9 / even degree 10, fitted by tools/fit_sincos.py;
+// fp32 Horner max error 1.2e-7, i.e. as accurate as MUFU.SIN/COS), and the
+// sign (-1)^q applied to both by one shift and two xors.  Used for a
+// fraction of the phasors so that the XU (MUFU) pipe and the issue slots are
+// both busy: the encode is SFU-bound otherwise.
+__device__ __forceinline__ void sincos_fma(float phi, float *s_out, float *c_out)
+{
+    const float magic = 12582912.f;                 // 1.5 * 2^23: x + magic rounds x to an integer
+    const float tq = fmaf(phi, 0.318309886183790672f, magic);   // phi / pi + magic
+    const int qi = __float_as_int(tq);              // low bits hold q mod 2^22
+    const float q = tq - magic;
+    float r = fmaf(q, -3.140625f, phi);             // exact (8-bit constant)
+    r = fmaf(q, -9.67653589793e-4f, r);             // pi - 3.140625
+    const float r2 = r * r;
+    float p = fmaf(r2, 2.600054358e-06f, -1.980661473e-04f);
+    p = fmaf(p, r2, 8.333017118e-03f);
+    p = fmaf(p, r2, -1.666665673e-01f);
+    const float s = fmaf(p * r2, r, r);
+    float c = fmaf(r2, -2.607710314e-07f, 2.476188638e-05f);
+    c = fmaf(c, r2, -1.388840377e-03f);
+    c = fmaf(c, r2, 4.166664183e-02f);
+    c = fmaf(c, r2, -5.000000000e-01f);
+    c = fmaf(c, r2, 1.0f);
+    const int sign = qi << 31;                      // (-1)^q
+    *s_out = __int_as_float(__float_as_int(s) ^ sign);
+    *c_out = __int_as_float(__float_as_int(c) ^ sign);
+}
 
 // ---- CTA-pair (cta_group::2) helpers -----------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank()

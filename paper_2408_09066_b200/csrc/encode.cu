@@ -21,36 +21,7 @@ namespace {
 constexpr int ENC_THREADS = 128;
 constexpr int ENC_TILE = 256;   // points staged per shared-memory tile
 
-// sin/cos on the FMA + ALU pipes (no MUFU), 18 instructions: half-turn
-// reduction phi = q pi + r (q by the magic-number rint, 2-term Cody-Waite pi;
-// |q| < 2^12 keeps q * 3.140625 exact), then near-minimax polynomials on
-// [-pi/2, pi/2] (odd degree 9 / even degree 10, fitted by tools/fit_sincos.py;
-// fp32 Horner max error 1.2e-7, i.e. as accurate as MUFU.SIN/COS), and the
-// sign (-1)^q applied to both by one shift and two xors.  Used for a
-// fraction of the phasors so that the XU (MUFU) pipe and the issue slots are
-// both busy: the encode is SFU-bound otherwise.
-__device__ __forceinline__ void sincos_poly(float phi, float *s_out, float *c_out)
-{
-    const float magic = 12582912.f;                 // 1.5 * 2^23: x + magic rounds x to an integer
-    const float tq = fmaf(phi, 0.318309886183790672f, magic);   // phi / pi + magic
-    const int qi = __float_as_int(tq);              // low bits hold q mod 2^22
-    const float q = tq - magic;
-    float r = fmaf(q, -3.140625f, phi);             // exact (8-bit constant)
-    r = fmaf(q, -9.67653589793e-4f, r);             // pi - 3.140625
-    const float r2 = r * r;
-    float p = fmaf(r2, 2.600054358e-06f, -1.980661473e-04f);
-    p = fmaf(p, r2, 8.333017118e-03f);
-    p = fmaf(p, r2, -1.666665673e-01f);
-    const float s = fmaf(p * r2, r, r);
-    float c = fmaf(r2, -2.607710314e-07f, 2.476188638e-05f);
-    c = fmaf(c, r2, -1.388840377e-03f);
-    c = fmaf(c, r2, 4.166664183e-02f);
-    c = fmaf(c, r2, -5.000000000e-01f);
-    c = fmaf(c, r2, 1.0f);
-    const int sign = qi << 31;                      // (-1)^q
-    *s_out = __int_as_float(__float_as_int(s) ^ sign);
-    *c_out = __int_as_float(__float_as_int(c) ^ sign);
-}
+__device__ __forceinline__ void sincos_poly(float phi, float *s_out, float *c_out) { sincos_fma(phi, s_out, c_out); }
 
 // Phasor j of KT: the last NPOLY of each thread's KT dimensions use the
 // polynomial, the others MUFU.SIN / MUFU.COS (__sincosf).
@@ -419,9 +390,11 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
 
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
-    // delta = 1: the label-split kernel (both classes per block); delta > 1 (or the
-    // VSAOGM_ENC_SORTED=1 knob): route points to slots, then slot-filtered blocks
-    const bool slots_path = c->nslots > 2 || c->enc_sorted == 1;
+    // default (enc_path 0): counting sort by slot + equal runs (encode_sorted.cu).
+    // Measured alternatives kept as tuning variants: enc_path 1 = label-split blocks
+    // (delta = 1) / slot-filtered blocks (delta > 1); enc_path 2 = slot-filtered always.
+    if (c->enc_path == 0 || (c->enc_path < 0 && c->nslots > 2)) return vsa_launch_encode_sorted(c, xy, lab, n);
+    const bool slots_path = c->nslots > 2 || c->enc_path == 2;
     const int KT = (!slots_path && c->enc_kt == 16 && c->Dp >= 2048) ? 16 : (c->Dp >= 1024 ? 8 : 4);
     const int kblocks = (c->Dp + ENC_THREADS * KT - 1) / (ENC_THREADS * KT);
     // one full wave at ~6 resident blocks per SM, at least 64 points per chunk
@@ -432,7 +405,9 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
                          ? c->enc_minb
                          : 6;
     const int zslots = slots_path ? c->nslots : 1;     // grid.z
-    const int64_t target_blocks = (int64_t)c->num_sms * minb;
+    // slot-filtered blocks carry unequal work (slots hold different point counts): several
+    // waves of smaller blocks even the tail out
+    const int64_t target_blocks = (int64_t)c->num_sms * minb * (slots_path ? c->enc_waves : 1);
     int64_t chunks = (target_blocks + (int64_t)kblocks * zslots - 1) / ((int64_t)kblocks * zslots);
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
     const int64_t chunk_pts = (n + chunks - 1) / chunks;

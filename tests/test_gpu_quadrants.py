@@ -117,20 +117,23 @@ def test_delta1_create_quadrants_equals_create():
     assert torch.equal(outs[0][1], outs[1][1])
 
 
-def test_slot_filtered_encode_matches_label_split(monkeypatch):
-    """delta = 1 through the slot-filtered encode kernel (the delta > 1 kernel) gives the
-    same memories as the default label-split kernel, up to fp32 chunk summation order."""
+@pytest.mark.parametrize("delta", [1, 2])
+def test_encode_paths_agree(monkeypatch, delta):
+    """The three encode paths (0: counting sort by slot + equal runs, the default; 1: label-split
+    blocks for delta = 1 / slot-filtered for delta > 1; 2: slot-filtered blocks) give the same
+    memories up to fp32 chunk summation order, and the same counts."""
     from paper_2408_09066_b200 import Mapper
     sc = Scenario("C2")
     xy, lab = sc.all_points()
     mems = []
-    for knob in (None, "1"):
-        if knob:
-            monkeypatch.setenv("VSAOGM_ENC_SORTED", knob)
-        mp = Mapper(2048, 0, 0.25, sc.bounds)
+    for knob in ("0", "1", "2"):
+        monkeypatch.setenv("VSAOGM_ENC_PATH", knob)
+        mp = Mapper(2048, 0, 0.25, sc.bounds, delta=delta)
         mp.encode_bundle(*_cuda(xy, lab))
         mems.append(mp.get_memory())
         mp.close()
-    assert list(mems[0][1]) == list(mems[1][1])
-    for c in (0, 1):
-        assert np.linalg.norm(mems[0][0][c] - mems[1][0][c]) <= 1e-5 * np.linalg.norm(mems[0][0][c])
+    for other in mems[1:]:
+        assert list(mems[0][1]) == list(other[1])
+        for s in range(2 * delta * delta):
+            if mems[0][1][s]:
+                assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 1e-5 * np.linalg.norm(mems[0][0][s])

@@ -25,14 +25,14 @@ def tau_of(D):
     return -p * math.log2(p) - (1 - p) * math.log2(1 - p)
 
 
-def bench_config(name, reps, pk, points=None, band=None):
+def bench_config(name, reps, pk, points=None, band=None, delta=1):
     sc = Scenario(name)
     cfg = sc.cfg
     xy, lab = points if points is not None else sc.all_points()
     D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
     r0, r1 = band if band else (0, R)
     tau = tau_of(D)
-    mp = Mapper(D, 0, l, sc.bounds)
+    mp = Mapper(D, 0, l, sc.bounds, delta=delta)
     xg, lg = torch.from_numpy(xy).cuda(), torch.from_numpy(lab).cuda()
     L = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -64,7 +64,7 @@ def bench_config(name, reps, pk, points=None, band=None):
     dec_ms = per["norms"] + per["table_A"] + per["decode_gemm"]
     sfu_peak = 148 * 8 * pk["sm_max_mhz"] * 1e6
     out = {
-        "config": name, "points": n, "D": D, "grid": f"{R}x{C}", "band_rows": [r0, r1],
+        "config": name, "delta": delta, "points": n, "D": D, "grid": f"{R}x{C}", "band_rows": [r0, r1],
         "kernel_ms": {k: round(v, 5) for k, v in per.items()},
         "points_bundled_per_s": n / (enc_ms * 1e-3),
         "encode_frac_mufu_roofline": n * D / (per["encode"] * 1e-3) / sfu_peak,
@@ -86,6 +86,9 @@ def main(tag):
            bench_config("C4", 10, pk, points=Scenario("C4").batch(0))]
     sc5 = Scenario("C5")
     res.append(bench_config("C5", 2, pk, points=sc5.all_points(), band=row_band(4000, 0, 8)))
+    # quadrant memories (NEXT #1): the C4 step with delta = 2 and 4
+    for dl in (2, 4):
+        res.append(bench_config("C4", 10, pk, points=Scenario("C4").batch(0), delta=dl))
     path = os.path.join(ROOT, "profiles", f"{tag}_configs.json")
     json.dump(res, open(path, "w"), indent=1)
     print(path)
