@@ -215,6 +215,26 @@ int64_t vsaogm_launch_count(const vsaogm_ctx *ctx);
 int vsaogm_test_gemm(const void *A_dev, const void *B_dev, int32_t M, int32_t N, int32_t K,
                      vsaogm_precision precision, int32_t kernel, float *C_dev, void *stream);
 
+/* Multi-agent fusion (Alg. 3).
+ * vsaogm_export writes the context's state -- committed + pending memories in
+ * the raw-coordinate convention of Eq. 9, per-slot counts, and the fusion
+ * preconditions (D, theta seed, length scale, delta, bounds) -- into `buf` as a
+ * self-describing little-endian container: the 8-byte magic "VSAOGM1\0", a
+ * `key=value` text header terminated by "\n\n", then int64 counts[S] and fp64
+ * memories [S][D][2].  buf == NULL: only *size is set (the bytes needed).
+ * Synchronises the stream.  Errors: EINVAL_ARG (size NULL, or *size too small). */
+int vsaogm_export(vsaogm_ctx *ctx, void *buf, int64_t *size);
+
+/* Fuse an exported state into this context: its memories and counts are ADDED
+ * to this context's committed memories (mode 1; Alg. 3 bundles same-index
+ * memories, Eq. 5) or REPLACE them (mode 0, e.g. a checkpoint restore; pending
+ * work is discarded).  The three fusion conditions (same axis
+ * vectors, same classes, same delta) plus the same D, length scale and bounds
+ * are checked first.  Errors: EINVAL_ARG (malformed container, mode),
+ * EPRECOND (a condition differs; nothing is changed). */
+#define VSAOGM_EPRECOND (-9)     /* fusion precondition violated (Alg. 3)  */
+int vsaogm_import(vsaogm_ctx *ctx, const void *buf, int64_t size, int32_t mode);
+
 /* Name of an error code. */
 const char *vsaogm_strerror(int code);
 

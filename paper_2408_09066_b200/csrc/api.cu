@@ -115,6 +115,7 @@ const char *vsaogm_strerror(int code)
     case VSAOGM_ENOMEM: return "out of memory";
     case VSAOGM_ECUDA: return "CUDA error";
     case VSAOGM_ESTATE: return "call not valid in the current state";
+    case VSAOGM_EPRECOND: return "fusion precondition violated (axis vectors, classes, delta, D, length scale or bounds differ)";
     default: return "unknown error";
     }
 }
@@ -146,6 +147,7 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if (const char *e = getenv("VSAOGM_ENC_PATH")) c->enc_path = atoi(e);     // tuning knob (0, 1, 2)
         if (const char *e = getenv("VSAOGM_ENC_WAVES")) c->enc_waves = std::max(1, atoi(e));
         if (const char *e = getenv("VSAOGM_ENC_RUNS_WAVES")) c->enc_runs_waves = std::max(1, atoi(e));
+        c->seed = seed;
         c->delta = delta;
         c->nq = delta * delta;
         c->nslots = 2 * c->nq;

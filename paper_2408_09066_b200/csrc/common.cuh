@@ -58,6 +58,7 @@ struct vsaogm_ctx {
     int32_t Dp = 0;     // D rounded up to 32 (k-group of the interleaved K layout)
     int32_t Kp = 0;     // 2 * Dp: real contraction length of the decode GEMM
     double l = 1.0;
+    uint64_t seed = 0;   // theta seed (fusion precondition: same axis vectors)
     int32_t delta = 1;   // quadrants per axis (sec. III-B-4); delta^2 quadrants
     int32_t nq = 1;      // delta^2
     int32_t nslots = 2;  // 2 delta^2 memories, slot = 2 beta + psi

@@ -24,8 +24,10 @@ EXPORTS = (
     "vsaogm_create", "vsaogm_create_quadrants", "vsaogm_destroy", "vsaogm_set_stream", "vsaogm_encode_bundle", "vsaogm_encode_bundle_host",
     "vsaogm_pending", "vsaogm_pending_counts", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
-    "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror",
+    "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror", "vsaogm_export",
+    "vsaogm_import",
 )
+EPRECOND = -9
 
 
 class VsaogmError(RuntimeError):
@@ -84,6 +86,8 @@ def load() -> ctypes.CDLL:
         "vsaogm_launch_count": ([P], i64),
         "vsaogm_test_gemm": ([P, P, i32, i32, i32, ctypes.c_int, i32, P, P], ctypes.c_int),
         "vsaogm_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "vsaogm_export": ([P, P, ctypes.POINTER(i64)], ctypes.c_int),
+        "vsaogm_import": ([P, P, i64, i32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -230,6 +234,26 @@ class Mapper:
         cnt = np.zeros(self.nslots, dtype=np.int64)
         _check(self._lib.vsaogm_get_memory(self._ctx, _host_ptr(m), _host_ptr(cnt)), "vsaogm_get_memory")
         return m[..., 0] + 1j * m[..., 1], cnt
+
+    # ------------------------------------------------------------------ fusion (Alg. 3)
+    def export(self) -> bytes:
+        """The state (memories, counts, fusion preconditions) as a 'VSAOGM1' container."""
+        self._s()
+        n = ctypes.c_int64()
+        _check(self._lib.vsaogm_export(self._ctx, None, ctypes.byref(n)), "vsaogm_export")
+        buf = ctypes.create_string_buffer(n.value)
+        _check(self._lib.vsaogm_export(self._ctx, buf, ctypes.byref(n)), "vsaogm_export")
+        return buf.raw[:n.value]
+
+    def fuse(self, blob: bytes):
+        """Alg. 3: add another agent's exported memories to this context's (same preconditions)."""
+        self._s()
+        _check(self._lib.vsaogm_import(self._ctx, blob, len(blob), 1), "vsaogm_import")
+
+    def load(self, blob: bytes):
+        """Replace this context's memories by an exported state (checkpoint restore)."""
+        self._s()
+        _check(self._lib.vsaogm_import(self._ctx, blob, len(blob), 0), "vsaogm_import")
 
     def get_phases(self):
         import numpy as np
