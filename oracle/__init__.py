@@ -56,6 +56,9 @@ def _load():
         lib.oracle_entropy_cells.argtypes = [i32, i32, i32, i32, i32, i32, P, i32, i32, i32,
                                              f64, f64, i64, P, P, P, P]
         lib.oracle_entropy_cells.restype = i64
+        lib.oracle_entropy_hist_cells.argtypes = [i32, i32, i32, i32, i32, i32, P, i32, i32, i32,
+                                                  f64, f64, i64, P, P, P, P]
+        lib.oracle_entropy_hist_cells.restype = i64
         lib.oracle_quadrant_centers.argtypes = [f64, f64, f64, f64, i32, P, P]
         lib.oracle_quadrant_centers.restype = None
         lib.oracle_assign_quadrants.argtypes = [f64, f64, f64, f64, i32, i64, P, P, P]
@@ -233,6 +236,29 @@ def entropy_cells(R, C, ra, rb, ca, cb, q_region, h_occ, h_emp, disk, rho_occ, r
     if viol:
         raise AssertionError(f"oracle: {viol} |q| > 1 values in the entropy region")
     return S, lab
+
+
+def entropy_hist_cells(R, C, ra, rb, ca, cb, p_region, h_occ, h_emp, disk, rho_occ, rho_emp, rows, cols):
+    """Histogram (8-bit grey-level) entropy estimator (NEXT #2) from probabilities p [2, rb-ra, cb-ca]."""
+    p_region = np.ascontiguousarray(p_region, dtype=np.float64)
+    assert p_region.shape == (2, rb - ra, cb - ca)
+    rows = np.ascontiguousarray(rows, dtype=np.int32).reshape(-1)
+    cols = np.ascontiguousarray(cols, dtype=np.int32).reshape(-1)
+    n = rows.shape[0]
+    S = np.zeros((3, n), dtype=np.float64)
+    lab = np.zeros(n, dtype=np.uint8)
+    rc = _load().oracle_entropy_hist_cells(R, C, ra, rb, ca, cb, _p(p_region), h_occ, h_emp, disk, float(rho_occ),
+                                           float(rho_emp), n, _p(rows), _p(cols), _p(S), _p(lab))
+    if rc < 0:
+        raise ValueError("oracle_entropy_hist_cells: a footprint leaves the supplied region")
+    return S, lab
+
+
+def entropy_hist_grid(p, h_occ, h_emp, disk, rho_occ, rho_emp):
+    _, R, C = p.shape
+    rr, cc = np.meshgrid(np.arange(R, dtype=np.int32), np.arange(C, dtype=np.int32), indexing="ij")
+    S, lab = entropy_hist_cells(R, C, 0, R, 0, C, p, h_occ, h_emp, disk, rho_occ, rho_emp, rr.ravel(), cc.ravel())
+    return S.reshape(3, R, C), lab.reshape(R, C)
 
 
 def entropy_grid(q, h_occ, h_emp, disk, rho_occ, rho_emp):

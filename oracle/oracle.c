@@ -439,6 +439,63 @@ static int in_footprint(int du, int dv, int h, int disk)
     return abs(du) <= h && abs(dv) <= h;
 }
 
+/* ---- histogram ("rank") entropy estimator (SPEC.md:375 open question) ----
+ * The paper passes "a disk filter across the heat map image" and applies Shannon
+ * entropy (Alg. 2) without writing the estimator; the
+ * image-processing reading is the entropy of the grey-level histogram inside the
+ * footprint: the probability image is quantised to 8 bits, code = floor(255 p + 1/2)
+ * clipped to [0, 255], and S = -sum_b (n_b/N) log2 (n_b/N) over the N footprint
+ * cells inside the grid.  Codes are taken in fp32 (the kernel's precision) from the
+ * given fp32-representable p: both sides then take the same integer decisions. */
+static int code8(double p)
+{
+    float f = (float)p * 255.0f + 0.5f;
+    int c = (int)floorf(f);
+    return c < 0 ? 0 : (c > 255 ? 255 : c);
+}
+
+/* S [3][n] and labels for target cells from p_region [2][rb-ra][cb-ca] (probabilities,
+ * i.e. already q^2), as oracle_entropy_cells does for the mean estimator. */
+int64_t oracle_entropy_hist_cells(int32_t R, int32_t C, int32_t ra, int32_t rb, int32_t ca, int32_t cb,
+                                  const double *p_region, int32_t h_occ, int32_t h_emp, int32_t disk,
+                                  double rho_occ, double rho_emp, int64_t n, const int32_t *rows,
+                                  const int32_t *cols, double *S, uint8_t *labels)
+{
+    int32_t W = cb - ca, Hh = rb - ra;
+    for (int64_t e = 0; e < n; ++e) {
+        int32_t r = rows[e], c = cols[e];
+        double Sc[2];
+        for (int cls = 0; cls < 2; ++cls) {
+            int h = cls == 1 ? h_occ : h_emp;
+            int64_t hist[256];
+            memset(hist, 0, sizeof hist);
+            int64_t N = 0;
+            for (int du = -h; du <= h; ++du)
+                for (int dv = -h; dv <= h; ++dv) {
+                    if (!in_footprint(du, dv, h, disk)) continue;
+                    int rr = r + du, cc = c + dv;
+                    if (rr < 0 || rr >= R || cc < 0 || cc >= C) continue;   /* L13 */
+                    if (rr < ra || rr >= rb || cc < ca || cc >= cb) return -1;
+                    hist[code8(p_region[(size_t)cls * Hh * W + (size_t)(rr - ra) * W + (cc - ca)])]++;
+                    N++;
+                }
+            double s = 0.0;
+            for (int b = 0; b < 256; ++b)
+                if (hist[b] > 0) {
+                    double f = (double)hist[b] / (double)N;
+                    s -= f * log2(f);
+                }
+            Sc[cls] = s;
+        }
+        double g = Sc[1] - Sc[0];
+        S[e] = Sc[1];
+        S[n + e] = Sc[0];
+        S[2 * n + e] = g;
+        labels[e] = g >= rho_occ ? 1 : (g < rho_emp ? 0 : 2);
+    }
+    return 0;
+}
+
 /* Entropy maps and labels for a list of target cells.
  * q_region: [2][rb-ra][cb-ca] signed similarities of the full-grid region
  * rows [ra, rb) x cols [ca, cb) of an R x C grid.  For each target cell
