@@ -160,6 +160,15 @@ int vsaogm_reset(vsaogm_ctx *ctx);
 int vsaogm_decode(vsaogm_ctx *ctx, const vsaogm_grid *grid, vsaogm_precision precision,
                   float *q_dev);
 
+/* Local-entropy estimator used by the following decodes and entropy calls
+ * (L10):
+ *   0 (default) the window mean of the per-cell binary entropy H_b(p), in bits;
+ *   1 the Shannon entropy, in bits, of the 8-bit grey-level histogram of p in the
+ *     window (p quantised as floor(255 p + 1/2) in fp32) -- the image-processing
+ *     reading of "passing a disk filter ... applying Shannon entropy".
+ * Errors: EINVAL_ARG. */
+int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
+
 /* Local entropy (Alg. 2), global entropy S = S_occ - S_emp, 3-way labels
  * (Eq. 12 + L14) over the band of the last vsaogm_decode.  s_dev: NULL or
  * float32 [3][band][cols] = (S_occ, S_emp, S); labels_dev: NULL or uint8

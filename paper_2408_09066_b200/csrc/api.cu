@@ -222,7 +222,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
                     c->d_norm2, c->d_mhat, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
-                    c->d_sortmeta, c->d_sorted, c->d_runs};
+                    c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -370,7 +370,11 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     int a_rows = 0;
     for (int k = 0; k < G.n; ++k) a_rows = std::max(a_rows, G.a_row0[k] + G.mrows[k]);
     const size_t ldh = ((size_t)g->cols + 7) / 8 * 8;   // H_b row stride (16-byte multiple)
-    if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * ldh * sizeof(float)))) return rc;
+    if (c->estimator == 1) {
+        if ((rc = grow_bytes((void **)&c->d_code, &c->code_cap, (size_t)M * ldh))) return rc;
+    } else if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * ldh * sizeof(float)))) {
+        return rc;
+    }
     if ((rc = vsa_launch_norms(c, do_commit))) return rc;
     c->dirty = false;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
@@ -379,6 +383,7 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
                                      r_lo - g->row_begin, g->row_end - g->row_begin)))
         return rc;
     c->decoded = true;
+    c->g_estimator = c->estimator;
     c->g_rows = g->rows;
     c->g_cols = g->cols;
     c->g_r0 = g->row_begin;
@@ -389,10 +394,17 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     return VSAOGM_OK;
 }
 
+int vsaogm_set_estimator(vsaogm_ctx *c, int32_t estimator)
+{
+    if (!c || (estimator != 0 && estimator != 1)) return VSAOGM_EINVAL_ARG;
+    c->estimator = estimator;
+    return VSAOGM_OK;
+}
+
 static int check_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p)
 {
     if (!c || !p) return VSAOGM_EINVAL_ARG;
-    if (!c->decoded) return VSAOGM_ESTATE;
+    if (!c->decoded || c->g_estimator != c->estimator) return VSAOGM_ESTATE;   // decode again after a switch
     if (p->half_occ < 1 || p->half_emp < 1 || p->half_occ > 16 || p->half_emp > 16 || (p->disk != 0 && p->disk != 1) ||
         !isfinite(p->rho_occ) || !isfinite(p->rho_emp) || p->rho_emp > p->rho_occ)
         return VSAOGM_EINVAL_ARG;

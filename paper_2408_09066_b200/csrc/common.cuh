@@ -106,6 +106,9 @@ struct vsaogm_ctx {
     double B_x0 = 0, B_res = 0; int32_t B_cols = 0; int B_prec = -1;
     float *d_hb = nullptr; size_t hb_cap = 0;      // [2][R_ext][ldh] fp32
     float *d_ws = nullptr; size_t ws_cap = 0;      // split-K partial sums (bytes)
+    int estimator = 0;                             // 0: window mean of H_b(p); 1: 8-bit histogram entropy
+    uint8_t *d_code = nullptr; size_t code_cap = 0;   // [2][R_ext][ldh] 8-bit p (histogram estimator)
+    int g_estimator = 0;                           // estimator of the last decode
     float *d_S = nullptr; size_t S_cap = 0;        // host-entropy scratch
     uint8_t *d_lab = nullptr; size_t lab_cap = 0;
 

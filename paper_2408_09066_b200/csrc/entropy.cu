@@ -275,10 +275,113 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict
     }
 }
 
+// Histogram estimator (NEXT #2): S_c = Shannon entropy (bits) of the 8-bit grey-level
+// histogram of p_c in the clipped footprint.  One thread per output column walks TR rows;
+// each thread owns a 256-bin uint16 histogram in shared memory (bins interleaved across
+// threads: bin b of thread t at [b][t], conflict-free for equal bins), counts the window,
+// then sums n log2 n over the window's bins (table) while clearing them:
+// S = log2 N - (1/N) sum_b n_b log2 n_b.
+constexpr int HT = 128;   // threads (= output columns) per block
+constexpr int HR = 16;    // output rows per block
+__global__ void __launch_bounds__(HT) k_entropy_hist(const uint8_t *__restrict__ code, int ldh, int r_ext, int R, int C,
+                                                     int r_lo, int r0, int band_rows, int h1, int h0, int disk,
+                                                     float rho_occ, float rho_emp, float *__restrict__ S,
+                                                     uint8_t *__restrict__ lab)
+{
+    extern __shared__ uint8_t smh[];
+    const int H = max(h1, h0);
+    const int TW = HT + 2 * H, TH = HR + 2 * H;
+    const int NMAX = (2 * H + 1) * (2 * H + 1);
+    uint16_t *hist = reinterpret_cast<uint16_t *>(smh);                       // [256][HT]
+    float *nlogn = reinterpret_cast<float *>(smh + 256 * HT * 2);             // [NMAX + 1]
+    uint8_t *tile = smh + 256 * HT * 2 + 4 * (NMAX + 1);                      // [2][TH][TW]
+    __shared__ int s_w[2][2 * HMAX + 1];
+    const int tid = threadIdx.x;
+    const int orow0 = r0 + blockIdx.y * HR, ocol0 = blockIdx.x * HT;
+    for (int n = tid; n <= NMAX; n += HT) nlogn[n] = n > 0 ? (float)n * log2f((float)n) : 0.f;
+    for (int k = 0; k < 256; ++k) hist[k * HT + tid] = 0;   // each thread clears its own bins
+    if (tid < 2 * (2 * HMAX + 1)) {
+        const int cls = tid / (2 * HMAX + 1), j = tid % (2 * HMAX + 1);
+        const int h = cls == 1 ? h1 : h0, du = j - HMAX;
+        s_w[cls][j] = (du < -h || du > h) ? -1 : (disk ? isqrt_floor(h * h - du * du) : h);
+    }
+    for (int idx = tid; idx < 2 * TH * TW; idx += HT) {
+        const int cls = idx / (TH * TW), rem = idx - cls * TH * TW;
+        const int row = rem / TW, cc = rem - row * TW;
+        const int rr = orow0 - H + row, gc = ocol0 - H + cc;
+        const bool ok = rr >= 0 && rr < R && rr - r_lo < r_ext && gc >= 0 && gc < C;
+        tile[idx] = ok ? code[((size_t)cls * r_ext + (rr - r_lo)) * ldh + gc] : 0;
+    }
+    __syncthreads();
+    const int col = ocol0 + tid;
+    for (int r = 0; r < HR; ++r) {
+        const int row = orow0 + r;
+        const int br = row - r0;
+        if (br >= band_rows) break;
+        float Sc[2];
+        for (int cls = 0; cls < 2; ++cls) {
+            const uint8_t *t = tile + cls * TH * TW;
+            int n = 0;
+            // count (only cells inside the full grid belong to the clipped footprint)
+            for (int du = -H; du <= H; ++du) {
+                const int w = s_w[cls][du + HMAX];
+                if (w < 0 || row + du < 0 || row + du >= R) continue;
+                const uint8_t *tr = t + (r + H + du) * TW + tid + H;
+                for (int dv = -w; dv <= w; ++dv) {
+                    if (col + dv < 0 || col + dv >= C) continue;
+                    hist[tr[dv] * HT + tid]++;
+                    ++n;
+                }
+            }
+            // sum n log n over the occupied bins, clearing them
+            float s = 0.f;
+            for (int du = -H; du <= H; ++du) {
+                const int w = s_w[cls][du + HMAX];
+                if (w < 0 || row + du < 0 || row + du >= R) continue;
+                const uint8_t *tr = t + (r + H + du) * TW + tid + H;
+                for (int dv = -w; dv <= w; ++dv) {
+                    if (col + dv < 0 || col + dv >= C) continue;
+                    uint16_t &hb = hist[tr[dv] * HT + tid];
+                    s += nlogn[hb];
+                    hb = 0;
+                }
+            }
+            Sc[cls] = n > 0 ? log2f((float)n) - s / (float)n : 0.f;
+        }
+        if (col < C) {
+            const float g = Sc[1] - Sc[0];
+            const size_t o = (size_t)br * C + col;
+            if (S) {
+                S[o] = Sc[1];
+                S[(size_t)band_rows * C + o] = Sc[0];
+                S[(size_t)2 * band_rows * C + o] = g;
+            }
+            if (lab) lab[o] = g >= rho_occ ? 1 : (g < rho_emp ? 0 : 2);
+        }
+    }
+}
+
 }  // namespace
 
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab)
 {
+    if (c->g_estimator == 1) {
+        const int H = p->half_occ > p->half_emp ? p->half_occ : p->half_emp;
+        const int TW = HT + 2 * H, TH = HR + 2 * H, NMAX = (2 * H + 1) * (2 * H + 1);
+        const size_t smem = 256 * HT * 2 + 4 * (size_t)(NMAX + 1) + 2 * (size_t)TH * TW;
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int band = c->g_r1 - c->g_r0;
+        dim3 grid((c->g_cols + HT - 1) / HT, (band + HR - 1) / HR);
+        cudaEvent_t ev;
+        vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
+        k_entropy_hist<<<grid, HT, smem, c->stream>>>(c->d_code, (c->g_cols + 7) / 8 * 8, c->g_rext, c->g_rows,
+                                                      c->g_cols, c->g_rlo, c->g_r0, band, p->half_occ, p->half_emp,
+                                                      p->disk, p->rho_occ, p->rho_emp, S, lab);
+        VSA_CUDA_TRY(cudaGetLastError());
+        vsa_prof_end(c, VSAOGM_K_ENTROPY, ev);
+        c->launches++;
+        return VSAOGM_OK;
+    }
     const int H = p->half_occ > p->half_emp ? p->half_occ : p->half_emp;
     const int TW = TC + 2 * H, TH = TR + 2 * H;
     const int band = c->g_r1 - c->g_r0;

@@ -52,6 +52,7 @@ struct Epi {
     int ldc;
     float inv_scale;   // VSA: q = acc * inv_scale
     float *hb;         // VSA: hb[(c * r_ext + row) * ldh + col]
+    uint8_t *code;     // VSA, histogram estimator: 8-bit p code at the same index (hb unused)
     int ldh, r_ext;
     float *q;          // VSA: q[(c * band_rows + row + q_off) * qcols + col] for band rows, or null
     int q_off, band_rows, qcols;
@@ -67,6 +68,14 @@ __device__ __forceinline__ float hb_of_p(float p)
     if (p > 0.f) h = -p * log2f(p);
     if (p < 1.f) h -= (1.f - p) * log1pf(-p) * 1.44269504088896341f;
     return h;
+}
+
+// 8-bit grey level of a probability: floor(255 p + 1/2) with separately rounded fp32 multiply
+// and add (no FMA contraction), clipped to [0, 255] -- DESIGN.md NEXT #2
+__device__ __forceinline__ uint8_t code8(float p)
+{
+    const int c = __float2int_rd(__fadd_rn(__fmul_rn(p, 255.0f), 0.5f));
+    return (uint8_t)min(255, max(0, c));
 }
 
 __device__ __forceinline__ void store32(float *dst, const float *v, int nvalid, bool vec_ok)
@@ -105,13 +114,22 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], const Gr
     const int nr = G.nrows[g];
     const int cls = m_l >= nr;
     const int row = G.row0[g] + m_l - cls * nr;
-    float hv[32];
+    if (e.code) {   // histogram estimator: 8-bit grey level of p (NEXT #2)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        f[j] = __uint_as_float(v[j]) * e.inv_scale;
-        hv[j] = hb_of_p(fminf(f[j] * f[j], 1.f));
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) * e.inv_scale;
+        uint8_t *cdst = e.code + ((size_t)cls * e.r_ext + row) * e.ldh + col;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) cdst[j] = code8(fminf(f[j] * f[j], 1.f));
+    } else {
+        float hv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            f[j] = __uint_as_float(v[j]) * e.inv_scale;
+            hv[j] = hb_of_p(fminf(f[j] * f[j], 1.f));
+        }
+        store32(e.hb + ((size_t)cls * e.r_ext + row) * e.ldh + col, hv, nvalid, (col & 3) == 0);
     }
-    store32(e.hb + ((size_t)cls * e.r_ext + row) * e.ldh + col, hv, nvalid, (col & 3) == 0);
     const int br = row + e.q_off;
     if (e.q && br >= 0 && br < e.band_rows)
         store32(e.q + ((size_t)cls * e.band_rows + br) * e.qcols + col, f, nvalid, ((col | e.qcols) & 3) == 0);
@@ -416,7 +434,8 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const __grid_constant__ G
     const int cls = m_l >= nr;
     const int row = G.row0[g] + m_l - cls * nr;
     const float q = acc * e.inv_scale;
-    e.hb[((size_t)cls * e.r_ext + row) * e.ldh + col] = hb_of_p(fminf(q * q, 1.f));
+    if (e.code) e.code[((size_t)cls * e.r_ext + row) * e.ldh + col] = code8(fminf(q * q, 1.f));
+    else e.hb[((size_t)cls * e.r_ext + row) * e.ldh + col] = hb_of_p(fminf(q * q, 1.f));
     const int br = row + e.q_off;
     if (e.q && br >= 0 && br < e.band_rows) e.q[((size_t)cls * e.band_rows + br) * e.qcols + col] = q;
 }
@@ -595,6 +614,7 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
     Epi e{};
     e.inv_scale = inv_scale;
     e.hb = hb;
+    e.code = c->estimator == 1 ? c->d_code : nullptr;
     e.ldh = (N + 7) / 8 * 8;
     e.r_ext = r_ext;
     e.q = q;

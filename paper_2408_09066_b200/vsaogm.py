@@ -25,7 +25,7 @@ EXPORTS = (
     "vsaogm_pending", "vsaogm_pending_counts", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
     "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror", "vsaogm_export",
-    "vsaogm_import",
+    "vsaogm_import", "vsaogm_set_estimator",
 )
 EPRECOND = -9
 
@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "vsaogm_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "vsaogm_export": ([P, P, ctypes.POINTER(i64)], ctypes.c_int),
         "vsaogm_import": ([P, P, i64, i32], ctypes.c_int),
+        "vsaogm_set_estimator": ([P, i32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -234,6 +235,10 @@ class Mapper:
         cnt = np.zeros(self.nslots, dtype=np.int64)
         _check(self._lib.vsaogm_get_memory(self._ctx, _host_ptr(m), _host_ptr(cnt)), "vsaogm_get_memory")
         return m[..., 0] + 1j * m[..., 1], cnt
+
+    def set_estimator(self, estimator: int):
+        """0: window mean of H_b(p) (default); 1: 8-bit grey-level histogram entropy (decode again after)."""
+        _check(self._lib.vsaogm_set_estimator(self._ctx, int(estimator)), "vsaogm_set_estimator")
 
     # ------------------------------------------------------------------ fusion (Alg. 3)
     def export(self) -> bytes:
