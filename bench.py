@@ -264,10 +264,13 @@ def run_native(args):
     phasors = my_pts * D
     sm_max = pk.get("sm_max_mhz", 1965.0)
     sfu_peak = 148 * 16 / 2 * sm_max * 1e6          # MUFU-only: 16 MUFU/clk/SM, 2 MUFU per phasor
-    # combined MUFU + FMA-pipe ceiling: per SM per clock, issue 128
-    # thread-instructions and 16 MUFU; a MUFU phasor costs 7 issue slots + 2 MUFU, an FMA-pipe
-    # phasor 22 issue slots; max m + p s.t. 2m <= 16, 7m + 22p <= 128 -> m = 8, p = 72/22
-    per_clk = 8 + (128 - 7 * 8) / 22
+    # combined MUFU + FMA-pipe ceiling of the packed encode, per SM per
+    # clock from the guide's unit counts: 16 MUFU, 128 FMA-pipe lanes.  A MUFU phasor costs
+    # 2 MUFU + 5 FMA lanes (angle 2, FMUL.RZ 1, accumulate 2); a polynomial phasor 16 FMA
+    # lanes (angle 2, sincos_fma2_lite 12, accumulate 2).  max m + p s.t. 2m <= 16,
+    # 5m + 16p <= 128 -> m = 8, p = 88/16 (the ALU pipe, 3 ops per polynomial phasor, and the
+    # issue slots, 5 and 11 per phasor, are not binding there).
+    per_clk = 8 + (128 - 5 * 8) / 16
     alu_peak = 148 * per_clk * sm_max * 1e6
     enc_rate = phasors / (enc_ms * 1e-3)
     clocks = clk.summary()
@@ -281,11 +284,12 @@ def run_native(args):
     enc_share = shares.get("encode", 0)
     dominant = "encode" if enc_share >= shares.get("decode_gemm", 0) else "decode_gemm"
     if dominant == "encode":
-        roofline = {"kernel": "k_encode_bundle", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
+        roofline = {"kernel": "k_encode_bundle_x2", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
                     "peak": round(alu_peak / 1e9, 2), "unit": "Gphasor/s", "frac": round(enc_rate / alu_peak, 4),
                     "traffic": traffic.get("encode"),
                     "peak_basis": f"combined MUFU+FMA-pipe ceiling {per_clk:.2f} phasors/clk/SM x 148 SM x "
-                                  f"{sm_max:.0f} MHz (guide unit counts: 16 MUFU + 4 issue/clk/SM; DESIGN.md sec. 6)",
+                                  f"{sm_max:.0f} MHz (guide unit counts: 16 MUFU + 128 FMA lanes/clk/SM; "
+                                  "DESIGN.md sec. 6)",
                     "mufu_only_peak": round(sfu_peak / 1e9, 2),
                     "frac_of_mufu_only": round(enc_rate / sfu_peak, 4),
                     "frac_at_measured_clock": (round(enc_rate / (148 * per_clk * clocks["sm_mhz"] * 1e6), 4)

@@ -144,6 +144,9 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
         if (const char *e = getenv("VSAOGM_ENC_MINB")) c->enc_minb = atoi(e);     // tuning knob (6 or 8)
         if (const char *e = getenv("VSAOGM_ENC_KT")) c->enc_kt = atoi(e);         // tuning knob (8 or 16)
+        if (const char *e = getenv("VSAOGM_ENC_X2")) c->enc_x2 = atoi(e);         // packed encode (0..3)
+        if (const char *e = getenv("VSAOGM_ENC_X2_WAVES")) c->enc_x2_waves = std::max(1, atoi(e));
+        if (const char *e = getenv("VSAOGM_ENC_X2_NPOLY")) c->enc_x2_npoly = atoi(e);
         if (const char *e = getenv("VSAOGM_ENC_PATH")) c->enc_path = atoi(e);     // tuning knob (0, 1, 2)
         if (const char *e = getenv("VSAOGM_ENC_WAVES")) c->enc_waves = std::max(1, atoi(e));
         if (const char *e = getenv("VSAOGM_ENC_RUNS_WAVES")) c->enc_runs_waves = std::max(1, atoi(e));

@@ -76,6 +76,12 @@ struct vsaogm_ctx {
     int enc_runs_waves = 4;   // waves of sorted-run encode blocks (tuning knob)
     int enc_npoly = 1;  // phasors per 8 evaluated by the FMA polynomial instead of MUFU (tuning knob)
     int enc_minb = 6;   // encode blocks resident per SM (6: 80 regs, 8: <= 64 regs) (tuning knob)
+    // packed fp32x2 encode (k_encode_bundle_x2, delta = 1, D >= 2048): 0 off (scalar kernel),
+    // 1 uniform 4-warp blocks, 2 all-MUFU warps beside enc_x2_npoly-polynomial warps (default,
+    // measured fastest), 3 one-polynomial warps beside enc_x2_npoly-polynomial warps
+    int enc_x2 = 2;
+    int enc_x2_npoly = 6;   // polynomial dimensions of 8 in the second warp role
+    int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
     int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
@@ -274,6 +280,163 @@ __device__ __forceinline__ void sincos_fma(float phi, float *s_out, float *c_out
     *s_out = __int_as_float(__float_as_int(s) ^ sign);
     *c_out = __int_as_float(__float_as_int(c) ^ sign);
 }
+
+// ---- packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2, sm_100a) ----------------
+// Two fp32 lanes in one 64-bit register pair; each lane rounds exactly as the
+// scalar fmaf / __fmul_rn / __fadd_rn would.  One issue slot per two lanes: the
+// encode is bound by the MUFU pipe and the issue slots together, so packing the
+// angle, accumulation and polynomial arithmetic frees issue for more phasors
+// (DESIGN.md section 6).  A scalar operand broadcast as pk2(f, f) compiles to
+// the R.F32 / immediate broadcast form of the packed instruction.
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pk2(float a, float b)
+{
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ void upk2(f32x2 v, float &a, float &b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c)
+{
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// sincos_fma on two angles at once: the same operations in the same order per
+// lane (bit-identical to two sincos_fma calls), 15 packed FMA-pipe instructions
+// plus the per-lane sign xors.
+__device__ __forceinline__ void sincos_fma2(f32x2 phi, f32x2 &s_out, f32x2 &c_out)
+{
+    const float magic = 12582912.f;
+    const f32x2 tq = fma2(phi, bc2(0.318309886183790672f), bc2(magic));
+    const f32x2 q = add2(tq, bc2(-magic));
+    f32x2 r = fma2(q, bc2(-3.140625f), phi);
+    r = fma2(q, bc2(-9.67653589793e-4f), r);
+    const f32x2 r2 = mul2(r, r);
+    f32x2 p = fma2(r2, bc2(2.600054358e-06f), bc2(-1.980661473e-04f));
+    p = fma2(p, r2, bc2(8.333017118e-03f));
+    p = fma2(p, r2, bc2(-1.666665673e-01f));
+    const f32x2 s = fma2(mul2(p, r2), r, r);
+    f32x2 c = fma2(r2, bc2(-2.607710314e-07f), bc2(2.476188638e-05f));
+    c = fma2(c, r2, bc2(-1.388840377e-03f));
+    c = fma2(c, r2, bc2(4.166664183e-02f));
+    c = fma2(c, r2, bc2(-5.000000000e-01f));
+    c = fma2(c, r2, bc2(1.0f));
+    float ta, tb, sa, sb, ca, cb;
+    upk2(tq, ta, tb);
+    upk2(s, sa, sb);
+    upk2(c, ca, cb);
+    const int ga = __float_as_int(ta) << 31, gb = __float_as_int(tb) << 31;
+    s_out = pk2(__int_as_float(__float_as_int(sa) ^ ga), __int_as_float(__float_as_int(sb) ^ gb));
+    c_out = pk2(__int_as_float(__float_as_int(ca) ^ ga), __int_as_float(__float_as_int(cb) ^ gb));
+}
+
+// Cheaper packed sin/cos for the encode's polynomial phasors: one-constant reduction
+// r = phi - q fl(pi) (its error q |pi - fl(pi)| <= |phi| 2.8e-8 is below the fp32 rounding
+// of phi itself, |phi| 6e-8, and below MUFU.SIN's |phi| 3e-8 x 2pi of the RZ turn
+// conversion), odd degree-7 sin (fp32 max error 9.7e-7, MUFU-class) and even degree-8 cos
+// (1.6e-7) near-minimax fits (tools/fit_sincos.py --lite): 12 packed FMA-pipe instructions
+// instead of 15 per two phasors.
+__device__ __forceinline__ void sincos_fma2_lite(f32x2 phi, f32x2 &s_out, f32x2 &c_out)
+{
+    const float magic = 12582912.f;
+    const f32x2 tq = fma2(phi, bc2(0.318309886183790672f), bc2(magic));
+    const f32x2 q = add2(tq, bc2(-magic));
+    const f32x2 r = fma2(q, bc2(-3.14159274101257324f), phi);
+    const f32x2 r2 = mul2(r, r);
+    f32x2 p = fma2(r2, bc2(-1.849217806e-04f), bc2(8.312365972e-03f));
+    p = fma2(p, r2, bc2(-1.666568071e-01f));
+    const f32x2 s = fma2(mul2(p, r2), r, r);
+    f32x2 c = fma2(r2, bc2(2.319438317e-05f), bc2(-1.385592739e-03f));
+    c = fma2(c, r2, bc2(4.166398942e-02f));
+    c = fma2(c, r2, bc2(-4.999993145e-01f));
+    c = fma2(c, r2, bc2(1.0f));
+    float ta, tb, sa, sb, ca, cb;
+    upk2(tq, ta, tb);
+    upk2(s, sa, sb);
+    upk2(c, ca, cb);
+    const int ga = __float_as_int(ta) << 31, gb = __float_as_int(tb) << 31;
+    s_out = pk2(__int_as_float(__float_as_int(sa) ^ ga), __int_as_float(__float_as_int(sb) ^ gb));
+    c_out = pk2(__int_as_float(__float_as_int(ca) ^ ga), __int_as_float(__float_as_int(cb) ^ gb));
+}
+
+// Per-thread phasor accumulators of the packed encode: KT dimensions (KT even) held
+// as KT/2 dimension pairs (j, j+1), the last NPOLY dimensions on the polynomial.
+// One point at a time: the pair's two angles come from one FMUL2 + FFMA2 with the
+// point coordinates broadcast, and the pair's cos / sin sums are two FADD2.  Every
+// dimension sums its points in point order; MUFU dimensions use the scalar kernel's
+// per-lane arithmetic, polynomial pairs the cheaper sincos_fma2_lite.
+template <int KT, int NPOLY>
+struct PhasorAcc {
+    static_assert(KT % 2 == 0, "dimension pairs");
+    static constexpr int NP = KT / 2;
+    f32x2 wx[NP], wy[NP];   // (w_j, w_j+1) per pair
+    f32x2 re[NP], im[NP];   // (sum cos_j, sum cos_j+1), (sum sin_j, sum sin_j+1)
+
+    __device__ __forceinline__ void init(const float *fx, const float *fy)
+    {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            wx[q] = pk2(fx[2 * q], fx[2 * q + 1]);
+            wy[q] = pk2(fy[2 * q], fy[2 * q + 1]);
+            re[q] = im[q] = pk2(0.f, 0.f);
+        }
+    }
+
+    __device__ __forceinline__ void point(float x, float y)
+    {
+        const f32x2 X = bc2(x), Y = bc2(y);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const f32x2 phi = fma2(wx[q], X, mul2(wy[q], Y));   // fmaf(w^x, x, w^y * y) per lane
+            constexpr int J0 = 0;
+            const int j0 = J0 + 2 * q;
+            if (j0 + 1 < KT - NPOLY) {                    // both on MUFU
+                float pa, pb, sa, ca, sb, cb;
+                upk2(phi, pa, pb);
+                __sincosf(pa, &sa, &ca);
+                __sincosf(pb, &sb, &cb);
+                re[q] = add2(re[q], pk2(ca, cb));
+                im[q] = add2(im[q], pk2(sa, sb));
+            } else if (j0 >= KT - NPOLY) {                // both on the polynomial
+                f32x2 S, C;
+                sincos_fma2_lite(phi, S, C);
+                re[q] = add2(re[q], C);
+                im[q] = add2(im[q], S);
+            } else {                                      // MUFU, polynomial
+                float pa, pb, sa, ca, sb, cb;
+                upk2(phi, pa, pb);
+                __sincosf(pa, &sa, &ca);
+                sincos_fma(pb, &sb, &cb);
+                re[q] = add2(re[q], pk2(ca, cb));
+                im[q] = add2(im[q], pk2(sa, sb));
+            }
+        }
+    }
+
+    __device__ __forceinline__ float2 get(int j) const
+    {
+        float a, b, c, d;
+        upk2(re[j >> 1], a, b);
+        upk2(im[j >> 1], c, d);
+        return (j & 1) ? make_float2(b, d) : make_float2(a, c);
+    }
+};
 
 // ---- CTA-pair (cta_group::2) helpers -----------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank()

@@ -151,6 +151,131 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
     }
 }
 
+// Packed variant of K2: the same label-split staging and loop as k_encode_bundle, with
+// each thread's 8 dimensions processed as 4 pairs in fp32x2 instructions (PhasorAcc,
+// common.cuh): the angles, the accumulation and the polynomial phasors take one issue
+// slot per two lanes, and the register footprint is the scalar kernel's.
+//
+// Warp roles: the first half of the block's warps evaluate NPA of their 8 dimensions by
+// polynomial, the second half NPB.  With NPA = 0 (all MUFU) and NPB = 6, every SM
+// sub-partition (warps w and w + 4 of each block) runs one MUFU-bound warp beside one
+// FMA-bound warp: two homogeneous instruction streams that the warp scheduler
+// interleaves, rather than one stream whose MUFU and polynomial phases alternate and
+// stall on each other's latencies.  Each dimension still sums its points in point
+// order with the scalar per-lane arithmetic (only which dimensions use the polynomial
+// differs from k_encode_bundle).
+template <int THREADS, int NPA, int NPB, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_encode_bundle_x2(
+    const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
+    const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
+    float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
+{
+    constexpr int KT = 8;
+    constexpr int NW = THREADS / 32;
+    constexpr int TILE = THREADS >= ENC_TILE ? THREADS : ENC_TILE;
+    constexpr int ROUNDS = TILE / THREADS;
+    __shared__ float2 s_p0[TILE], s_p1[TILE];
+    __shared__ int s_g0[ROUNDS * NW], s_g1[ROUNDS * NW];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const bool role_b = warp >= NW / 2;   // warp-uniform
+    const int kb = blockIdx.x;
+    const int64_t chunk = blockIdx.y;
+    const int kbase = kb * THREADS * KT + tid;
+
+    float fx[KT], fy[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * THREADS;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+    }
+    long long c0 = 0, c1 = 0;
+    int my_err = 0;
+    const int64_t p0 = chunk * chunk_pts;
+    const int64_t p1 = min(n, p0 + chunk_pts);
+
+    // the tile loop, per role (the staging code is common; the bundle loops differ)
+    auto run = [&](auto acc0, auto acc1) {
+        acc0.init(fx, fy);
+        acc1.init(fx, fy);
+        for (int64_t base = p0; base < p1; base += TILE) {
+            const int cnt = (int)min((int64_t)TILE, p1 - base);
+            __syncthreads();
+            float2 rec[ROUNDS];
+            int code_r[ROUNDS];
+            unsigned b0[ROUNDS], b1[ROUNDS];
+#pragma unroll
+            for (int r = 0; r < ROUNDS; ++r) {
+                const int t = tid + r * THREADS;
+                int code = 2;
+                rec[r] = make_float2(0.f, 0.f);
+                if (t < cnt) {
+                    const float2 v = xy[base + t];
+                    const int L = lab[base + t];
+                    code = L;
+                    if (L > 1) { code = 2; my_err |= VSA_ERRBIT_LABEL; }
+                    if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
+                    rec[r] = make_float2((float)((double)v.x - cx), (float)((double)v.y - cy));
+                }
+                code_r[r] = code;
+                b0[r] = __ballot_sync(0xffffffffu, code == 0);
+                b1[r] = __ballot_sync(0xffffffffu, code == 1);
+                if (lane == 0) {
+                    s_g0[r * NW + warp] = __popc(b0[r]);
+                    s_g1[r * NW + warp] = __popc(b1[r]);
+                }
+            }
+            __syncthreads();
+            int n0 = 0, n1 = 0, o0[ROUNDS], o1[ROUNDS];
+#pragma unroll
+            for (int g = 0; g < ROUNDS * NW; ++g) {
+#pragma unroll
+                for (int r = 0; r < ROUNDS; ++r)
+                    if (g == r * NW + warp) { o0[r] = n0; o1[r] = n1; }
+                n0 += s_g0[g];
+                n1 += s_g1[g];
+            }
+            const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int r = 0; r < ROUNDS; ++r) {
+                if (code_r[r] == 0) s_p0[o0[r] + __popc(b0[r] & lt)] = rec[r];
+                else if (code_r[r] == 1) s_p1[o1[r] + __popc(b1[r] & lt)] = rec[r];
+            }
+            c0 += n0;
+            c1 += n1;
+            __syncthreads();
+#pragma unroll 2
+            for (int p = 0; p < n0; ++p) {
+                const float2 P = s_p0[p];   // warp-uniform broadcast
+                acc0.point(P.x, P.y);
+            }
+#pragma unroll 2
+            for (int p = 0; p < n1; ++p) {
+                const float2 P = s_p1[p];
+                acc1.point(P.x, P.y);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int k = kbase + j * THREADS;
+            if (k < Dp) {
+                part[((size_t)chunk * 2 + 0) * Dp + k] = acc0.get(j);
+                part[((size_t)chunk * 2 + 1) * Dp + k] = acc1.get(j);
+            }
+        }
+    };
+    if (role_b) run(PhasorAcc<KT, NPB>{}, PhasorAcc<KT, NPB>{});
+    else run(PhasorAcc<KT, NPA>{}, PhasorAcc<KT, NPA>{});
+    if (kb == 0) {
+        if (my_err) atomicOr(err, my_err);
+        if (tid == 0) {
+            part_cnt[chunk * 2 + 0] = c0;
+            part_cnt[chunk * 2 + 1] = c1;
+        }
+    }
+}
+
 // Quadrant routing (delta > 1; Alg. 1): slot = 2 beta + psi with
 // beta the nearest quadrant centre in fp64 squared distance, ties to the lowest
 // index -- the expression, operation order and rounding DESIGN.md fixes for the decision
@@ -284,45 +409,62 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_slots(
     }
 }
 
-// K3: pending[c][k] += sum over chunks of the partials, fp64, fixed order:
-// block (32 k-lanes) x (RED_SLICES chunk slices); slice s sums chunks s, s+S, ...
-// in order, then slice sums are added in slice order (deterministic).
-constexpr int RED_SLICES = 8;
+// K3: pending[c][k] += sum over chunks of the partials, fp64, fixed order: block =
+// 32 column lanes (two k each: one 16-byte load per chunk row) x RED_SLICES chunk slices;
+// slice s sums chunks s, s+S, ... in order, then the slice sums are added in slice order
+// (deterministic).  Bandwidth-bound: 16 slices keep ~8 loads per thread in flight.
+constexpr int RED_SLICES = 16;
 __global__ void __launch_bounds__(32 * RED_SLICES) k_reduce_partials(
     const float2 *__restrict__ part, const long long *__restrict__ part_cnt, int chunks, int nslots, int Dp, int D,
     double *__restrict__ pending, long long *__restrict__ pcount)
 {
-    __shared__ double s_re[RED_SLICES][32], s_im[RED_SLICES][32];
+    __shared__ double4 s_acc[RED_SLICES][32];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int idx = blockIdx.x * 32 + tx;          // over nslots * Dp: (slot, k)
-    const bool live = idx < nslots * Dp;
-    double re = 0.0, im = 0.0;
+    const int ncol = nslots * Dp / 2;               // float4 columns: (slot, k pair)
+    const int col = blockIdx.x * 32 + tx;
+    const bool live = col < ncol;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (live) {
-        const float2 *p = part + idx;              // part[(ch*nslots + s)*Dp + k] = part[ch*nslots*Dp + idx]
-#pragma unroll 4
+        const float4 *p = reinterpret_cast<const float4 *>(part) + col;
+#pragma unroll 8
         for (int ch = ty; ch < chunks; ch += RED_SLICES) {
-            const float2 v = p[(size_t)ch * nslots * Dp];
-            re += v.x;
-            im += v.y;
+            const float4 v = __ldcs(p + (size_t)ch * ncol);   // read once: evict-first
+            a0 += v.x;
+            a1 += v.y;
+            a2 += v.z;
+            a3 += v.w;
         }
     }
-    s_re[ty][tx] = re;
-    s_im[ty][tx] = im;
+    s_acc[ty][tx] = make_double4(a0, a1, a2, a3);
     __syncthreads();
     if (ty == 0 && live) {
-        const int c = idx / Dp, k = idx - c * Dp;
-        if (k < D) {   // padding dimensions (w = 0 accumulate cos 0 = 1) stay exactly zero
-            double r = 0.0, i = 0.0;
+        double4 r = s_acc[0][tx];
 #pragma unroll
-            for (int s = 0; s < RED_SLICES; ++s) { r += s_re[s][tx]; i += s_im[s][tx]; }
-            pending[2 * (size_t)idx] += r;
-            pending[2 * (size_t)idx + 1] += i;
+        for (int s = 1; s < RED_SLICES; ++s) {
+            const double4 v = s_acc[s][tx];
+            r.x += v.x;
+            r.y += v.y;
+            r.z += v.z;
+            r.w += v.w;
+        }
+        const int idx = 2 * col;                    // (slot, k) of the first of the pair
+        const int c = idx / Dp, k = idx - c * Dp;
+        // padding dimensions (w = 0 accumulate cos 0 = 1) stay exactly zero
+        if (k < D) {
+            pending[2 * (size_t)idx] += r.x;
+            pending[2 * (size_t)idx + 1] += r.y;
+        }
+        if (k + 1 < D) {
+            pending[2 * (size_t)idx + 2] += r.z;
+            pending[2 * (size_t)idx + 3] += r.w;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x < nslots) {
-        long long s = 0;
-        for (int ch = 0; ch < chunks; ++ch) s += part_cnt[ch * nslots + threadIdx.x];
-        pcount[threadIdx.x] += s;
+    if (blockIdx.x == 0) {   // counts: integer sums (exact in any order), chunk-strided over the block
+        for (int sl = 0; sl < nslots; ++sl) {
+            long long s = 0;
+            for (int ch = threadIdx.x; ch < chunks; ch += blockDim.x) s += part_cnt[ch * nslots + sl];
+            if (s) atomicAdd((unsigned long long *)&pcount[sl], (unsigned long long)s);
+        }
     }
 }
 
@@ -396,10 +538,14 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     if (c->enc_path == 0 || (c->enc_path < 0 && c->nslots > 2)) return vsa_launch_encode_sorted(c, xy, lab, n);
     const bool slots_path = c->nslots > 2 || c->enc_path == 2;
     const int KT = (!slots_path && c->enc_kt == 16 && c->Dp >= 2048) ? 16 : (c->Dp >= 1024 ? 8 : 4);
-    const int kblocks = (c->Dp + ENC_THREADS * KT - 1) / (ENC_THREADS * KT);
-    // one full wave at ~6 resident blocks per SM, at least 64 points per chunk
-    // resident blocks per SM: 6 (<= 85 registers, the measured best), 7 or 8 as tuning variants
-    const int minb = KT == 16 ? 4
+    // packed kernel: 128 threads (enc_x2 = 1) or 8-warp role variants (2, 3: 2048 dims per block)
+    const bool x2 = !slots_path && KT == 8 && c->enc_x2 && (c->enc_x2 == 1 || c->Dp >= 2048);
+    const int x2_threads = (x2 && c->enc_x2 >= 2) ? 256 : ENC_THREADS;
+    const int kblocks = (c->Dp + x2_threads * KT - 1) / (x2_threads * KT);
+    // one full wave at ~6 resident blocks per SM (3 for the 256-thread variants), at least 64
+    // points per chunk; 7 or 8 resident blocks as tuning variants of the scalar kernel
+    const int minb = x2 ? (x2_threads == 256 ? 3 : 6)
+                     : KT == 16 ? 4
                      : (!slots_path && KT == 8 && (c->enc_npoly == 1 || c->enc_npoly == 2) &&
                         (c->enc_minb == 7 || c->enc_minb == 8))
                          ? c->enc_minb
@@ -407,7 +553,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     const int zslots = slots_path ? c->nslots : 1;     // grid.z
     // slot-filtered blocks carry unequal work (slots hold different point counts): several
     // waves of smaller blocks even the tail out
-    const int64_t target_blocks = (int64_t)c->num_sms * minb * (slots_path ? c->enc_waves : 1);
+    const int64_t target_blocks = (int64_t)c->num_sms * minb * (slots_path ? c->enc_waves : x2 ? c->enc_x2_waves : 1);
     int64_t chunks = (target_blocks + (int64_t)kblocks * zslots - 1) / ((int64_t)kblocks * zslots);
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
     const int64_t chunk_pts = (n + chunks - 1) / chunks;
@@ -457,11 +603,35 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
 #undef VSA_ENC_SLOTS
     } else {
     dim3 grid(kblocks, (unsigned)chunks);
+#define VSA_ENC_X2(T_, NPA_, NPB_, MB_)                                                                            \
+    k_encode_bundle_x2<T_, NPA_, NPB_, MB_><<<grid, T_, 0, c->stream>>>(                                          \
+        (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
+        c->d_err)
 #define VSA_ENC_LAUNCH(KT_, NP_, ...)                                                                             \
     k_encode_bundle<KT_, NP_, ##__VA_ARGS__><<<grid, ENC_THREADS, 0, c->stream>>>(                                \
         (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
         c->d_err)
-    if (KT == 8) {
+    if (x2 && c->enc_x2 == 1) {   // uniform roles, 4 warps
+        switch (c->enc_x2_npoly) {
+        case 1: VSA_ENC_X2(128, 1, 1, 6); break;
+        case 3: VSA_ENC_X2(128, 3, 3, 6); break;
+        case 4: VSA_ENC_X2(128, 4, 4, 6); break;
+        default: VSA_ENC_X2(128, 2, 2, 6); break;
+        }
+    } else if (x2 && c->enc_x2 == 2) {   // all-MUFU warps beside NPOLY-polynomial warps (default: 6)
+        switch (c->enc_x2_npoly) {
+        case 4: VSA_ENC_X2(256, 0, 4, 3); break;
+        case 5: VSA_ENC_X2(256, 0, 5, 3); break;
+        case 7: VSA_ENC_X2(256, 0, 7, 3); break;
+        case 8: VSA_ENC_X2(256, 0, 8, 3); break;
+        default: VSA_ENC_X2(256, 0, 6, 3); break;
+        }
+    } else if (x2) {   // 1-polynomial warps beside NPOLY-polynomial warps
+        switch (c->enc_x2_npoly) {
+        case 4: VSA_ENC_X2(256, 1, 4, 3); break;
+        default: VSA_ENC_X2(256, 1, 5, 3); break;
+        }
+    } else if (KT == 8) {
         switch (c->enc_npoly) {
         case 0: VSA_ENC_LAUNCH(8, 0); break;
         case 2:
@@ -488,13 +658,14 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
         else VSA_ENC_LAUNCH(4, 1);
     }
 #undef VSA_ENC_LAUNCH
+#undef VSA_ENC_X2
     }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENCODE, ev);
     c->launches++;
 
     vsa_prof_begin(c, VSAOGM_K_REDUCE, &ev);
-    k_reduce_partials<<<(c->nslots * c->Dp + 31) / 32, 32 * RED_SLICES, 0, c->stream>>>(
+    k_reduce_partials<<<(c->nslots * c->Dp / 2 + 31) / 32, 32 * RED_SLICES, 0, c->stream>>>(
         c->d_part, c->d_part_cnt, (int)chunks, c->nslots, c->Dp, c->D, c->d_pending, c->d_pcounts);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_REDUCE, ev);

@@ -193,6 +193,53 @@ __global__ void __launch_bounds__(ENC_T, 6) k_encode_runs(const float2 *__restri
     }
 }
 
+// Packed variant (delta > 1 default for D >= 2048): 8 warps, the first four all-MUFU, the
+// other four with NPB of their 8 dimensions on the polynomial (PhasorAcc, as
+// k_encode_bundle_x2 in encode.cu); one run of one slot per block row.
+template <int NPA, int NPB>
+__global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const float2 *__restrict__ sorted,
+                                                          const int4 *__restrict__ runs,
+                                                          const int *__restrict__ meta, const float *__restrict__ wx,
+                                                          const float *__restrict__ wy, int Dp,
+                                                          float2 *__restrict__ part)
+{
+    constexpr int T = 256, KT = 8;
+    __shared__ float2 s_p[ENC_TILE_S];
+    const int r = blockIdx.y;
+    if (r >= meta[META_NRUNS()]) return;
+    const int4 run = runs[r];
+    const int tid = threadIdx.x;
+    const int kbase = blockIdx.x * T * KT + tid;
+    float fx[KT], fy[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * T;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+    }
+    auto go = [&](auto acc) {
+        acc.init(fx, fy);
+        for (int base = run.y; base < run.z; base += ENC_TILE_S) {
+            const int cnt = min(ENC_TILE_S, run.z - base);
+            __syncthreads();
+            for (int t = tid; t < cnt; t += T) s_p[t] = sorted[base + t];
+            __syncthreads();
+#pragma unroll 2
+            for (int p = 0; p < cnt; ++p) {
+                const float2 P = s_p[p];
+                acc.point(P.x, P.y);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int k = kbase + j * T;
+            if (k < Dp) part[(size_t)r * Dp + k] = acc.get(j);
+        }
+    };
+    if ((tid >> 5) >= 4) go(PhasorAcc<KT, NPB>{});
+    else go(PhasorAcc<KT, NPA>{});
+}
+
 // pending[s][k] += sum over the slot's runs (fixed order, fp64): 32 k-lanes x 8 run slices
 __global__ void __launch_bounds__(256) k_reduce_runs(const float2 *__restrict__ part, const int *__restrict__ meta,
                                                      int nslots, int Dp, int D, double *__restrict__ pending,
@@ -244,10 +291,12 @@ int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab,
     const int ns = c->nslots;
     const int nblk = (int)((n + RT_PTS - 1) / RT_PTS);
     const int KT = c->Dp >= 1024 ? 8 : 4;
-    const int kblocks = (c->Dp + ENC_T * KT - 1) / (ENC_T * KT);
-    // runs per k-block column so that all blocks fit whole waves of 6 per SM; each slot's last
-    // run may be short, so size runs for (target - nslots) and the total never exceeds the target
-    const int64_t target_runs = (int64_t)c->num_sms * 6 * c->enc_runs_waves / kblocks;
+    const bool x2 = c->enc_x2 >= 2 && c->Dp >= 2048;   // packed 8-warp role kernel
+    const int T = x2 ? 256 : ENC_T, per_sm = x2 ? 3 : 6;
+    const int kblocks = (c->Dp + T * KT - 1) / (T * KT);
+    // runs per k-block column so that all blocks fit whole waves of `per_sm` per SM; each slot's
+    // last run may be short, so size runs for (target - nslots) and the total never exceeds it
+    const int64_t target_runs = (int64_t)c->num_sms * per_sm * c->enc_runs_waves / kblocks;
     const int run_pts =
         (int)std::max<int64_t>(64, (n + std::max<int64_t>(1, target_runs - ns) - 1) / std::max<int64_t>(1, target_runs - ns));
     const int64_t max_runs = (n + run_pts - 1) / run_pts + ns;
@@ -271,7 +320,14 @@ int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab,
 #define VSA_RUNS(KT_, NP_)                                                                                         \
     k_encode_runs<KT_, NP_><<<grid, ENC_T, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx, c->d_wy, \
                                                           c->Dp, c->d_part)
-    if (KT == 8) {
+    if (x2) {
+        switch (c->enc_x2_npoly) {
+        case 4: k_encode_runs_x2<0, 4><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
+                                                                    c->d_wy, c->Dp, c->d_part); break;
+        default: k_encode_runs_x2<0, 6><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
+                                                                     c->d_wy, c->Dp, c->d_part); break;
+        }
+    } else if (KT == 8) {
         if (c->enc_npoly == 2) VSA_RUNS(8, 2);
         else if (c->enc_npoly == 0) VSA_RUNS(8, 0);
         else VSA_RUNS(8, 1);

@@ -137,3 +137,26 @@ def test_encode_paths_agree(monkeypatch, delta):
         for s in range(2 * delta * delta):
             if mems[0][1][s]:
                 assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 1e-5 * np.linalg.norm(mems[0][0][s])
+
+
+@pytest.mark.parametrize("delta", [1, 2])
+def test_encode_packed_variants_agree(monkeypatch, delta):
+    """The packed fp32x2 encode kernels (VSAOGM_ENC_X2 = 1: uniform 4-warp blocks; 2: all-MUFU
+    warps beside 6-polynomial warps, the default; 3: 1- beside 5-polynomial warps) agree with
+    the scalar kernel (0) up to fp32 rounding: the polynomial phasors (sincos_fma2_lite, max
+    error 1e-6) and the chunking differ, the counts are exact."""
+    from paper_2408_09066_b200 import Mapper
+    sc = Scenario("C2")
+    xy, lab = sc.all_points()
+    mems = []
+    for knob in ("0", "1", "2", "3"):
+        monkeypatch.setenv("VSAOGM_ENC_X2", knob)
+        mp = Mapper(4096, 3, 0.25, sc.bounds, delta=delta)
+        mp.encode_bundle(*_cuda(xy, lab))
+        mems.append(mp.get_memory())
+        mp.close()
+    for other in mems[1:]:
+        assert list(mems[0][1]) == list(other[1])
+        for s in range(2 * delta * delta):
+            if mems[0][1][s]:
+                assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 1e-5 * np.linalg.norm(mems[0][0][s])
