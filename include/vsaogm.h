@@ -183,6 +183,30 @@ int vsaogm_entropy(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *
 int vsaogm_entropy_host(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *s_host,
                         uint8_t *labels_host);
 
+/* Pipelined host I/O for streaming mapping (one batch per step, Alg. 1 then
+ * Alg. 2): the host<->device copies of step k run on two
+ * internal copy streams and overlap the kernels of steps k-1 and k+1.
+ *
+ * vsaogm_encode_bundle_host_async: as vsaogm_encode_bundle_host, but the
+ * host->device copy of (xy_host float32 [n][2], labels_host uint8 [n]) goes to
+ * one of two device staging slots on the upload stream, and the encode on the
+ * context stream waits for it.  The host arrays must be page-locked for the
+ * copy to be asynchronous, and must stay unmodified until the next
+ * vsaogm_entropy_host_async's ticket has been waited for.
+ *
+ * vsaogm_entropy_host_async: as vsaogm_entropy_host, into one of two device
+ * output slots, then a device->host copy on the download stream; returns at
+ * once with *ticket.  s_host / labels_host (page-locked for overlap) are written
+ * when vsaogm_wait(ctx, *ticket) returns.  A slot is reused two calls later
+ * (the device waits for its previous download first).
+ *
+ * vsaogm_wait: block until step `ticket` has been downloaded; returns a deferred
+ * device error like vsaogm_sync.  Errors: EINVAL_ARG (unknown ticket), ECUDA. */
+int vsaogm_encode_bundle_host_async(vsaogm_ctx *ctx, const float *xy_host, const uint8_t *labels_host, int64_t n);
+int vsaogm_entropy_host_async(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *s_host,
+                              uint8_t *labels_host, int64_t *ticket);
+int vsaogm_wait(vsaogm_ctx *ctx, int64_t ticket);
+
 /* Wait for the context's stream; return a deferred device error (ELABEL or
  * ENONFINITE, first one seen since the last sync) or ECUDA, else OK. */
 int vsaogm_sync(vsaogm_ctx *ctx);

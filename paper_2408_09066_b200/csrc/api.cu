@@ -230,6 +230,21 @@ void vsaogm_destroy(vsaogm_ctx *c)
         if (p) cudaFree(p);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->up) {
+        cudaStreamSynchronize(c->up);
+        cudaStreamSynchronize(c->down);
+        for (int s = 0; s < 2; ++s) {
+            void *q[] = {c->d_in_xy[s], c->d_in_lab[s], c->d_out_S[s], c->d_out_lab[s]};
+            for (void *p : q)
+                if (p) cudaFree(p);
+            cudaEvent_t e[] = {c->ev_up[s], c->ev_used[s], c->ev_out[s], c->ev_down[s]};
+            for (cudaEvent_t x : e)
+                if (x) cudaEventDestroy(x);
+        }
+        cudaStreamDestroy(c->up);
+        cudaStreamDestroy(c->down);
+        if (c->h_err) cudaFreeHost(c->h_err);
+    }
     delete c;
 }
 
@@ -270,6 +285,55 @@ int vsaogm_encode_bundle_host(vsaogm_ctx *c, const float *xy, const uint8_t *lab
     VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_xy, xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
     VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_lab, lab, n, cudaMemcpyHostToDevice, c->stream));
     return vsaogm_encode_bundle(c, (const float *)c->d_stage_xy, c->d_stage_lab, n);
+}
+
+namespace {
+// lazily create the copy streams and slot events of the pipelined host path
+int ensure_pipeline(vsaogm_ctx *c)
+{
+    if (c->up) return VSAOGM_OK;
+    VSA_CUDA_TRY(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking));
+    VSA_CUDA_TRY(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
+    VSA_CUDA_TRY(cudaHostAlloc((void **)&c->h_err, 2 * sizeof(int), cudaHostAllocDefault));
+    c->h_err[0] = c->h_err[1] = 0;
+    for (int s = 0; s < 2; ++s) {
+        VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_up[s], cudaEventDisableTiming));
+        VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_used[s], cudaEventDisableTiming));
+        VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_out[s], cudaEventDisableTiming));
+        VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_down[s], cudaEventDisableTiming));
+    }
+    return VSAOGM_OK;
+}
+
+// grow a slot buffer; the previous user of the slot (recorded event) must be done first
+int grow_slot(void **p, size_t *cap, size_t need, cudaEvent_t busy, bool recorded)
+{
+    if (need <= *cap) return VSAOGM_OK;
+    if (recorded) VSA_CUDA_TRY(cudaEventSynchronize(busy));
+    return grow_bytes(p, cap, need);
+}
+}  // namespace
+
+int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    if (n < 1) return VSAOGM_EEMPTY;
+    if (!xy || !lab) return VSAOGM_EINVAL_ARG;
+    int rc;
+    if ((rc = ensure_pipeline(c))) return rc;
+    const int s = (int)(c->in_seq & 1);
+    const bool used = c->in_seq >= 2;   // slot s was consumed by the encode two calls ago
+    if ((rc = grow_slot((void **)&c->d_in_xy[s], &c->in_xy_cap[s], n * sizeof(float2), c->ev_used[s], used))) return rc;
+    if ((rc = grow_slot((void **)&c->d_in_lab[s], &c->in_lab_cap[s], (size_t)n, c->ev_used[s], used))) return rc;
+    if (used) VSA_CUDA_TRY(cudaStreamWaitEvent(c->up, c->ev_used[s], 0));
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_xy[s], xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->up));
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_lab[s], lab, n, cudaMemcpyHostToDevice, c->up));
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_up[s], c->up));
+    VSA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_up[s], 0));
+    if ((rc = vsaogm_encode_bundle(c, (const float *)c->d_in_xy[s], c->d_in_lab[s], n))) return rc;
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_used[s], c->stream));
+    c->in_seq++;
+    return VSAOGM_OK;
 }
 
 int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
@@ -436,6 +500,44 @@ int vsaogm_entropy_host(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S_
     if (S_host) VSA_CUDA_TRY(cudaMemcpyAsync(S_host, c->d_S, 3 * cells * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     if (lab_host) VSA_CUDA_TRY(cudaMemcpyAsync(lab_host, c->d_lab, cells, cudaMemcpyDeviceToHost, c->stream));
     VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return VSAOGM_OK;
+}
+
+int vsaogm_entropy_host_async(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S_host, uint8_t *lab_host,
+                              int64_t *ticket)
+{
+    int rc = check_entropy(c, p);
+    if (rc) return rc;
+    if (!ticket) return VSAOGM_EINVAL_ARG;
+    if ((rc = ensure_pipeline(c))) return rc;
+    const size_t cells = (size_t)(c->g_r1 - c->g_r0) * c->g_cols;
+    const int s = (int)(c->out_seq & 1);
+    const bool used = c->out_seq >= 2;  // slot s was downloaded two calls ago
+    if (S_host && (rc = grow_slot((void **)&c->d_out_S[s], &c->out_S_cap[s], 3 * cells * sizeof(float), c->ev_down[s], used)))
+        return rc;
+    if (lab_host && (rc = grow_slot((void **)&c->d_out_lab[s], &c->out_lab_cap[s], cells, c->ev_down[s], used)))
+        return rc;
+    if (used) VSA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_down[s], 0));
+    if ((rc = vsa_launch_entropy(c, p, S_host ? c->d_out_S[s] : nullptr, lab_host ? c->d_out_lab[s] : nullptr))) return rc;
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_out[s], c->stream));
+    VSA_CUDA_TRY(cudaStreamWaitEvent(c->down, c->ev_out[s], 0));
+    if (S_host) VSA_CUDA_TRY(cudaMemcpyAsync(S_host, c->d_out_S[s], 3 * cells * sizeof(float), cudaMemcpyDeviceToHost, c->down));
+    if (lab_host) VSA_CUDA_TRY(cudaMemcpyAsync(lab_host, c->d_out_lab[s], cells, cudaMemcpyDeviceToHost, c->down));
+    // deferred error bits as of this step (sticky until vsaogm_sync clears them)
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->h_err + s, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->down));
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_down[s], c->down));
+    *ticket = c->out_seq++;
+    return VSAOGM_OK;
+}
+
+int vsaogm_wait(vsaogm_ctx *c, int64_t ticket)
+{
+    if (!c || ticket < 0 || ticket >= c->out_seq) return VSAOGM_EINVAL_ARG;
+    // the slot's event was recorded for this ticket or a later one (later downloads
+    // complete after earlier ones: one download stream)
+    VSA_CUDA_TRY(cudaEventSynchronize(c->ev_down[ticket & 1]));
+    const int err = c->h_err[ticket & 1];
+    if (err) return (err & VSA_ERRBIT_LABEL) ? VSAOGM_ELABEL : VSAOGM_ENONFINITE;
     return VSAOGM_OK;
 }
 

@@ -118,6 +118,19 @@ struct vsaogm_ctx {
     float *d_S = nullptr; size_t S_cap = 0;        // host-entropy scratch
     uint8_t *d_lab = nullptr; size_t lab_cap = 0;
 
+    // pipelined host I/O (vsaogm_*_host_async): two staging / output slots each, copy streams
+    cudaStream_t up = nullptr, down = nullptr;     // upload (H2D) / download (D2H) streams
+    float2 *d_in_xy[2] = {nullptr, nullptr}; size_t in_xy_cap[2] = {0, 0};
+    uint8_t *d_in_lab[2] = {nullptr, nullptr}; size_t in_lab_cap[2] = {0, 0};
+    float *d_out_S[2] = {nullptr, nullptr}; size_t out_S_cap[2] = {0, 0};
+    uint8_t *d_out_lab[2] = {nullptr, nullptr}; size_t out_lab_cap[2] = {0, 0};
+    cudaEvent_t ev_up[2] = {nullptr, nullptr};       // upload of slot done
+    cudaEvent_t ev_used[2] = {nullptr, nullptr};     // encode has consumed staging slot
+    cudaEvent_t ev_out[2] = {nullptr, nullptr};      // entropy wrote output slot
+    cudaEvent_t ev_down[2] = {nullptr, nullptr};     // download of output slot done
+    int64_t in_seq = 0, out_seq = 0;                 // calls so far (slot = seq & 1)
+    int *h_err = nullptr;                            // pinned [2]: deferred error bits per output slot
+
     // last decode geometry
     bool decoded = false;
     int32_t g_rows = 0, g_cols = 0, g_r0 = 0, g_r1 = 0, g_rlo = 0, g_rext = 0, g_halo = 0;

@@ -25,7 +25,8 @@ EXPORTS = (
     "vsaogm_pending", "vsaogm_pending_counts", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
     "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror", "vsaogm_export",
-    "vsaogm_import", "vsaogm_set_estimator",
+    "vsaogm_import", "vsaogm_set_estimator", "vsaogm_encode_bundle_host_async", "vsaogm_entropy_host_async",
+    "vsaogm_wait",
 )
 EPRECOND = -9
 
@@ -89,6 +90,9 @@ def load() -> ctypes.CDLL:
         "vsaogm_export": ([P, P, ctypes.POINTER(i64)], ctypes.c_int),
         "vsaogm_import": ([P, P, i64, i32], ctypes.c_int),
         "vsaogm_set_estimator": ([P, i32], ctypes.c_int),
+        "vsaogm_encode_bundle_host_async": ([P, P, P, i64], ctypes.c_int),
+        "vsaogm_entropy_host_async": ([P, ctypes.POINTER(EntropyParams), P, P, ctypes.POINTER(i64)], ctypes.c_int),
+        "vsaogm_wait": ([P, i64], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -218,6 +222,33 @@ class Mapper:
         self._s()
         _check(self._lib.vsaogm_entropy_host(self._ctx, ctypes.byref(p), _host_ptr(s_host), _host_ptr(labels_host)),
                "vsaogm_entropy_host")
+
+    # ------------------------------------------------------------------ pipelined host I/O
+    def encode_bundle_host_async(self, xy, labels):
+        """Upload (xy, labels) from page-locked host memory on the context's upload stream and
+        bundle them; the arrays must stay unmodified until the next entropy_host_async ticket
+        has been waited for (vsaogm.h)."""
+        n = labels.shape[0]
+        self._s()
+        _check(self._lib.vsaogm_encode_bundle_host_async(self._ctx, _host_ptr(xy), _host_ptr(labels), n),
+               "vsaogm_encode_bundle_host_async")
+
+    def entropy_host_async(self, half_occ, half_emp, rho_occ, rho_emp, disk=0, s_host=None, labels_host=None) -> int:
+        """Entropy + labels, downloaded on the context's download stream; returns a ticket for wait()."""
+        p = EntropyParams(int(half_occ), int(half_emp), int(disk), float(rho_occ), float(rho_emp))
+        t = ctypes.c_int64()
+        self._s()
+        _check(self._lib.vsaogm_entropy_host_async(self._ctx, ctypes.byref(p), _host_ptr(s_host),
+                                                   _host_ptr(labels_host), ctypes.byref(t)),
+               "vsaogm_entropy_host_async")
+        return t.value
+
+    def wait(self, ticket: int) -> int:
+        """Block until step `ticket`'s outputs are on the host; returns the deferred error code."""
+        rc = self._lib.vsaogm_wait(self._ctx, int(ticket))
+        if rc not in (OK, ELABEL, ENONFINITE):
+            _check(rc, "vsaogm_wait")
+        return rc
 
     def sync(self) -> int:
         """Returns the deferred error code (0, ELABEL, ENONFINITE) without raising."""

@@ -542,3 +542,47 @@ def test_multi_rank_emulated_on_one_gpu():
         assert _mem_err(mg, m1) <= 1e-6
     for mp in ms + [one]:
         mp.close()
+
+
+def test_pipelined_host_steps_match_synchronous():
+    """vsaogm_encode_bundle_host_async / vsaogm_entropy_host_async / vsaogm_wait: a pipelined run
+    of several streaming steps (copies on the upload / download streams, two slots each)
+    returns, per step, the same labels and S as the synchronous host path."""
+    import math
+    from paper_2408_09066_b200 import Mapper
+    sc = Scenario("C2")
+    cfg = sc.cfg
+    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
+    p = 1.0 / (2.0 * D)
+    tau = -p * math.log2(p) - (1 - p) * math.log2(1 - p)
+    xy, lab = sc.all_points()
+    chunks = np.array_split(np.arange(len(lab)), 5)
+    batches = [(torch.from_numpy(np.ascontiguousarray(xy[c])).pin_memory(),
+                torch.from_numpy(np.ascontiguousarray(lab[c])).pin_memory()) for c in chunks]
+    ref = []
+    mp = Mapper(D, 0, l, sc.bounds)
+    for bx, bl in batches:
+        L = torch.empty((R, C), dtype=torch.uint8).pin_memory()
+        S = torch.empty((3, R, C), dtype=torch.float32).pin_memory()
+        mp.encode_bundle_host(bx, bl)
+        mp.decode(0.0, 0.0, res, R, C, 0, R, h)
+        mp.entropy_host(h, h, tau, -tau, 0, S, L)
+        ref.append((L.clone(), S.clone()))
+    mp.close()
+    mp = Mapper(D, 0, l, sc.bounds)
+    outs = [(torch.empty((R, C), dtype=torch.uint8).pin_memory(), torch.empty((3, R, C), dtype=torch.float32).pin_memory())
+            for _ in batches]
+    tickets = []
+    for k, (bx, bl) in enumerate(batches):
+        mp.encode_bundle_host_async(bx, bl)
+        mp.decode(0.0, 0.0, res, R, C, 0, R, h)
+        tickets.append(mp.entropy_host_async(h, h, tau, -tau, 0, outs[k][1], outs[k][0]))
+        if k >= 1:
+            assert mp.wait(tickets[k - 1]) == 0
+            assert torch.equal(outs[k - 1][0], ref[k - 1][0])
+            assert torch.equal(outs[k - 1][1], ref[k - 1][1])
+    assert mp.wait(tickets[-1]) == 0
+    assert torch.equal(outs[-1][0], ref[-1][0]) and torch.equal(outs[-1][1], ref[-1][1])
+    with pytest.raises(Exception):
+        mp.wait(len(batches) + 3)
+    mp.close()
