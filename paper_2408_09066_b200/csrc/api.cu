@@ -192,6 +192,7 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if ((rc = dev_alloc_zero(&c->d_pcounts, c->nslots))) break;
         if ((rc = dev_alloc_zero(&c->d_norm2, c->nslots))) break;
         if ((rc = dev_alloc_zero(&c->d_mhat, (size_t)c->nslots * c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_normpart, (size_t)c->nslots * 16))) break;
         if ((rc = dev_alloc_zero(&c->d_qc, 2 * (size_t)c->nq))) break;
         {
             std::vector<double> qc(2 * c->nq);
@@ -223,7 +224,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     if (!c) return;
     cudaStreamSynchronize(c->stream);
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
-                    c->d_norm2, c->d_mhat, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
+                    c->d_norm2, c->d_mhat, c->d_normpart, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
                     c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code};
     for (void *p : ptrs)

@@ -95,7 +95,8 @@ struct vsaogm_ctx {
     long long *d_counts = nullptr;                 // [2]
     long long *d_pcounts = nullptr;                // pending counts [2]
     double *d_norm2 = nullptr;                     // ||m_c||^2 [2]
-    float2 *d_mhat = nullptr;                      // sqrt(D) m_c / ||m_c||, fp32 [2][Dp]
+    float2 *d_mhat = nullptr;                      // sqrt(D) m_c / ||m_c||, fp32 [S][Dp]
+    double *d_normpart = nullptr;                  // per-block partial ||m_c||^2 [S][16]
     int *d_err = nullptr;                          // deferred error bits
     float2 *d_part = nullptr;                      // encode chunk partials
     size_t part_cap = 0;                           // in float2

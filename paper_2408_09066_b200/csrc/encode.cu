@@ -14,7 +14,11 @@
 // broadcasts, so the per-point label branch is uniform across the warp.  Each
 // block writes its chunk's fp32 partial sums; K3 adds chunks in a fixed order
 // in fp64 (deterministic, no float atomics).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -483,20 +487,25 @@ __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, l
     }
 }
 
-// Optional commit (m += pending, pending = 0), then ||m_c||^2 for both classes
-// (Eq. 10, fixed-order fp64 block reduction, one block per class), then the
-// scaled conjugate-ready memory mhat_c = sqrt(D) m_c / ||m_c|| (0 for an empty
-// class, L8) in fp32 for the table-A kernel.
-constexpr int NORM_THREADS = 1024;
+// Optional commit (m += pending, pending = 0), then ||m_c||^2 per memory slot (Eq. 10) and
+// the scaled conjugate-ready memory mhat_c = sqrt(D) m_c / ||m_c|| (0 for an empty class, L8)
+// in fp32 for the table-A kernel.  Cooperative grid (slot, nb <= NORM_BLOCKS k-ranges; nb
+// shrinks with the slot count so that the grid stays co-resident): each block
+// reduces its range with a fixed tree into normpart[slot][b]; after a grid-wide barrier every
+// block adds its slot's NORM_BLOCKS partials in index order (deterministic, identical in all
+// blocks) and scales its own range.
+constexpr int NORM_THREADS = 256, NORM_BLOCKS = 16;
 __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restrict__ m, double *__restrict__ pending,
                                                                long long *__restrict__ cnt, long long *__restrict__ pcnt,
-                                                               int do_commit, int Dp, int D,
+                                                               int do_commit, int Dp, int D, double *__restrict__ normpart,
                                                                double *__restrict__ norm2, float2 *__restrict__ mhat)
 {
     __shared__ double s[NORM_THREADS];
-    const int c = blockIdx.x;
+    const int c = blockIdx.x, b = blockIdx.y, nb = gridDim.y;
+    const int per = (Dp + nb - 1) / nb;
+    const int k1 = min(Dp, (b + 1) * per);
     double acc = 0.0;
-    for (int k = threadIdx.x; k < Dp; k += NORM_THREADS) {
+    for (int k = b * per + threadIdx.x; k < k1; k += NORM_THREADS) {
         const size_t o = 2 * ((size_t)c * Dp + k);
         double re = m[o], im = m[o + 1];
         if (do_commit) {
@@ -515,16 +524,21 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
         if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
         __syncthreads();
     }
-    const double n2 = s[0];
+    if (threadIdx.x == 0) normpart[c * NORM_BLOCKS + b] = s[0];
+    cg::this_grid().sync();
+    double n2 = 0.0;
+    for (int i = 0; i < nb; ++i) n2 += normpart[c * NORM_BLOCKS + i];
     const double sc = n2 > 0.0 ? sqrt((double)D / n2) : 0.0;
-    if (threadIdx.x == 0) norm2[c] = n2;
-    if (do_commit && c == 0 && threadIdx.x < gridDim.x) {   // one block per slot
-        cnt[threadIdx.x] += pcnt[threadIdx.x];
-        pcnt[threadIdx.x] = 0;
-    }
-    for (int k = threadIdx.x; k < Dp; k += NORM_THREADS) {
+    for (int k = b * per + threadIdx.x; k < k1; k += NORM_THREADS) {
         const size_t o = 2 * ((size_t)c * Dp + k);
         mhat[(size_t)c * Dp + k] = make_float2((float)(m[o] * sc), (float)(m[o + 1] * sc));
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        norm2[c] = n2;
+        if (do_commit) {
+            cnt[c] += pcnt[c];
+            pcnt[c] = 0;
+        }
     }
 }
 
@@ -689,8 +703,16 @@ int vsa_launch_norms(vsaogm_ctx *c, int do_commit)
 {
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_NORMS, &ev);
-    k_commit_norms<<<c->nslots, NORM_THREADS, 0, c->stream>>>(c->d_m, c->d_pending, c->d_counts, c->d_pcounts, do_commit,
-                                                      c->Dp, c->D, c->d_norm2, c->d_mhat);
+    {
+        double *m = c->d_m, *pend = c->d_pending, *np = c->d_normpart, *n2 = c->d_norm2;
+        long long *cnt = c->d_counts, *pcnt = c->d_pcounts;
+        int dc = do_commit, Dp = c->Dp, D = c->D;
+        float2 *mh = c->d_mhat;
+        void *args[] = {&m, &pend, &cnt, &pcnt, &dc, &Dp, &D, &np, &n2, &mh};
+        const int nb = std::max(1, std::min(NORM_BLOCKS, c->num_sms * 4 / c->nslots));
+        VSA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_commit_norms, dim3(c->nslots, nb),
+                                                 dim3(NORM_THREADS), args, 0, c->stream));
+    }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_NORMS, ev);
     c->launches++;

@@ -8,14 +8,13 @@
 //                                                   (Eq. 12 PAPER.md:320-328 + L14)
 //
 // Input is the per-cell H_b(q_c^2) written by the decode epilogue for the band
-// plus halo rows ([2][R_ext][ldh] fp32).  A CTA owns a TR x TC output tile.
-// One 3-D TMA box load stages the (TR + 2H) x (TC + 2H) input tile of both
-// classes in shared memory; coordinates outside the decoded rows / grid
-// columns are zero-filled by the TMA unit, which is exactly the border
-// clipping of the window sums (rows outside the full grid are outside the
-// tensor by construction, L13).  A box window forms row sums of
-// width 2h+1 then sums 2h+1 of them down the column; a disk sums each
-// footprint row segment directly.  Clipped counts are closed-form.
+// plus halo rows ([2][R_ext][ldh] fp32).  Input outside the decoded rows /
+// grid columns reads as zero, which is exactly the border clipping of the
+// window sums (L13); clipped counts are closed-form.  A box window
+// forms row sums of width 2h+1 then sums 2h+1 of them down the column; a disk
+// sums each footprint row segment directly.  Kernels: k_entropy_box4 (box,
+// h <= 4, register rings, no shared memory), k_entropy_fixed (equal radii
+// h <= 8, cp.async-staged tile), k_entropy (any radii).
 // HBM-bound: 8 B read + 1 B written per cell.
 #include <cudaTypedefs.h>
 
@@ -142,6 +141,121 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy_fixed(const float *__re
                 S[(size_t)2 * band_rows * C + o] = g;
             }
             if (lab) lab[o] = g >= rho_occ ? 1 : (g < rho_emp ? 0 : 2);
+        }
+    }
+}
+
+// Box window, H <= 4 (the BASELINE configs' 3x3 / 5x5 / 7x7): the TR x TC tile (+ halo) of
+// both classes is staged with 16-byte cp.async exactly as in k_entropy_fixed; then a thread
+// owns 4 adjacent output columns of BOX_RPT rows: per staged row and class it reads the 12
+// floats c0-4 .. c0+7 (three 16-byte shared loads), forms the 4 horizontal (2H+1)-sums, and
+// keeps the last 2H+1 of them per column in a register ring; each output row is the in-order
+// sum of its ring -- the same additions in the same order as k_entropy_fixed<H, false>, so the
+// result is bit-identical, with ~4x fewer shared-memory instructions.  Labels leave as one
+// 4-byte store, S as float4s.
+constexpr int BOX_RPT = 4;                       // output rows per thread
+constexpr int BOX_CG = TC / 4;                   // column groups (threads across)
+static_assert(BOX_CG * (TR / BOX_RPT) == ENT_THREADS, "one thread per (column group, row strip)");
+
+template <int H>
+__global__ void __launch_bounds__(ENT_THREADS) k_entropy_box4(const float *__restrict__ hb, int ldh, int r_ext,
+                                                             int R, int C, int r_lo, int r0, int band_rows,
+                                                             float rho_occ, float rho_emp, float *__restrict__ S,
+                                                             uint8_t *__restrict__ lab)
+{
+    static_assert(H >= 1 && H <= 4, "halo within one 16-byte chunk");
+    constexpr int W = 2 * H + 1;
+    constexpr int PADC = 4;
+    constexpr int TW = TC + 2 * PADC;
+    constexpr int TH = TR + 2 * H;
+    constexpr int CH = TW / 4;
+    extern __shared__ float4 sm4[];
+    float *tile = reinterpret_cast<float *>(sm4);  // [2][TH][TW]
+    const int orow0 = r0 + blockIdx.y * TR;
+    const int ocol0 = blockIdx.x * TC;
+    for (int idx = threadIdx.x; idx < 2 * TH * CH; idx += ENT_THREADS) {
+        const int cr = idx / CH, j = idx - cr * CH;
+        const int cls = cr >= TH, row = cr - cls * TH;
+        const int rr = orow0 - H + row;
+        const int gc = ocol0 - PADC + 4 * j;
+        const bool ok = rr >= 0 && rr < R && rr - r_lo < r_ext && gc >= 0 && gc < C;
+        const int nbytes = ok ? 4 * min(4, C - gc) : 0;
+        const float *src = hb + ((size_t)cls * r_ext + (size_t)(ok ? rr - r_lo : 0)) * ldh + (ok ? gc : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(tile + cr * TW + 4 * j)),
+                     "l"(src), "r"(nbytes)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+
+    const int cgi = threadIdx.x % BOX_CG, strip = threadIdx.x / BOX_CG;
+    const int c0 = ocol0 + 4 * cgi;
+    if (c0 >= C) return;
+    int nc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) nc[j] = min(c0 + j + H, C - 1) - max(c0 + j - H, 0) + 1;
+    float ring[2][W][4];
+#pragma unroll
+    for (int i = 0; i < BOX_RPT + 2 * H; ++i) {
+#pragma unroll
+        for (int cls = 0; cls < 2; ++cls) {
+            const float4 *t4 = reinterpret_cast<const float4 *>(tile + (cls * TH + strip * BOX_RPT + i) * TW + 4 * cgi);
+            const float4 a = t4[0], b = t4[1], d = t4[2];   // columns c0-4 .. c0+7
+            const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float sh = 0.f;
+#pragma unroll
+                for (int dv = -H; dv <= H; ++dv) sh += x[4 + j + dv];
+                ring[cls][i % W][j] = sh;
+            }
+        }
+        if (i >= 2 * H) {
+            const int row = orow0 + strip * BOX_RPT + i - 2 * H;
+            const int br = row - r0;
+            if (br < band_rows) {
+                const float cntr = (float)(min(row + H, R - 1) - max(row - H, 0) + 1);
+                float g4[4], s14[4], s04[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float sc[2];
+#pragma unroll
+                    for (int cls = 0; cls < 2; ++cls) {
+                        float sv = 0.f;
+#pragma unroll
+                        for (int du = 0; du < W; ++du) sv += ring[cls][(i - 2 * H + du) % W][j];
+                        sc[cls] = sv;
+                    }
+                    const float inv = 1.0f / (cntr * (float)nc[j]);
+                    s14[j] = sc[1] * inv;
+                    s04[j] = sc[0] * inv;
+                    g4[j] = s14[j] - s04[j];
+                }
+                const size_t o = (size_t)br * C + c0;
+                const bool full = c0 + 3 < C && (C & 3) == 0;
+                if (lab) {
+                    uint8_t l4[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) l4[j] = g4[j] >= rho_occ ? 1 : (g4[j] < rho_emp ? 0 : 2);
+                    if (full) *reinterpret_cast<uchar4 *>(lab + o) = make_uchar4(l4[0], l4[1], l4[2], l4[3]);
+                    else
+                        for (int j = 0; j < 4 && c0 + j < C; ++j) lab[o + j] = l4[j];
+                }
+                if (S) {
+                    float *S1 = S + o, *S0 = S + (size_t)band_rows * C + o, *SG = S + (size_t)2 * band_rows * C + o;
+                    if (full) {
+                        *reinterpret_cast<float4 *>(S1) = make_float4(s14[0], s14[1], s14[2], s14[3]);
+                        *reinterpret_cast<float4 *>(S0) = make_float4(s04[0], s04[1], s04[2], s04[3]);
+                        *reinterpret_cast<float4 *>(SG) = make_float4(g4[0], g4[1], g4[2], g4[3]);
+                    } else {
+                        for (int j = 0; j < 4 && c0 + j < C; ++j) {
+                            S1[j] = s14[j];
+                            S0[j] = s04[j];
+                            SG[j] = g4[j];
+                        }
+                    }
+                }
+            }
         }
     }
 }
@@ -393,7 +507,23 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
         VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
-    if (fixed) {
+    if (fixed && !p->disk && H <= 4 && getenv("VSAOGM_ENTROPY_SMEM") == nullptr) {
+#define VSA_BOX(HH)                                                                                                \
+    do {                                                                                                           \
+        const size_t bsm = sizeof(float) * 2 * (TR + 2 * (HH)) * (TC + 8);                                          \
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_box4<HH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)); \
+        k_entropy_box4<HH><<<grid, ENT_THREADS, bsm, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols,     \
+                                                                  c->g_rlo, c->g_r0, band, p->rho_occ, p->rho_emp,  \
+                                                                  S, lab);                                          \
+    } while (0)
+        switch (H) {
+        case 1: VSA_BOX(1); break;
+        case 2: VSA_BOX(2); break;
+        case 3: VSA_BOX(3); break;
+        default: VSA_BOX(4); break;
+        }
+#undef VSA_BOX
+    } else if (fixed) {
         int rc = p->disk ? dispatch_fixed<true>(H, c, p, S, lab, ldh, grid)
                          : dispatch_fixed<false>(H, c, p, S, lab, ldh, grid);
         if (rc) return rc;
