@@ -183,6 +183,18 @@ int vsaogm_entropy(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *
 int vsaogm_entropy_host(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *s_host,
                         uint8_t *labels_host);
 
+/* Encode stream (streaming pipeline): with a non-NULL
+ * `stream` (a cudaStream_t), vsaogm_encode_bundle runs its kernels there
+ * instead of on the context stream.  Ordering stays that of the calls: an
+ * encode waits for the last commit / reset / import / decode's table build
+ * queued on the context stream (so it overlaps the rest of that decode: the
+ * tensor-core GEMM and the entropy), and the next operation on the context
+ * stream that touches the pending memories (decode, commit, reset, pending,
+ * export, sync ...) waits for the encodes queued before it.  The caller orders
+ * the encode inputs against `stream`.  NULL restores single-stream operation.
+ * Errors: EINVAL_ARG, ECUDA. */
+int vsaogm_set_encode_stream(vsaogm_ctx *ctx, void *stream);
+
 /* Pipelined host I/O for streaming mapping (one batch per step, Alg. 1 then
  * Alg. 2): the host<->device copies of step k run on two
  * internal copy streams and overlap the kernels of steps k-1 and k+1.

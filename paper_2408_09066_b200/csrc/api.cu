@@ -147,6 +147,7 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if (const char *e = getenv("VSAOGM_ENC_X2")) c->enc_x2 = atoi(e);         // packed encode (0..3)
         if (const char *e = getenv("VSAOGM_ENC_X2_WAVES")) c->enc_x2_waves = std::max(1, atoi(e));
         if (const char *e = getenv("VSAOGM_ENC_X2_NPOLY")) c->enc_x2_npoly = atoi(e);
+        if (const char *e = getenv("VSAOGM_ENC_X2_MINB")) c->enc_x2_minb = atoi(e);
         if (const char *e = getenv("VSAOGM_ENC_PATH")) c->enc_path = atoi(e);     // tuning knob (0, 1, 2)
         if (const char *e = getenv("VSAOGM_ENC_WAVES")) c->enc_waves = std::max(1, atoi(e));
         if (const char *e = getenv("VSAOGM_ENC_RUNS_WAVES")) c->enc_runs_waves = std::max(1, atoi(e));
@@ -223,6 +224,9 @@ void vsaogm_destroy(vsaogm_ctx *c)
 {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
+    if (c->enc_stream) cudaStreamSynchronize(c->enc_stream);
+    if (c->ev_enc) cudaEventDestroy(c->ev_enc);
+    if (c->ev_main) cudaEventDestroy(c->ev_main);
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
                     c->d_norm2, c->d_mhat, c->d_normpart, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
@@ -256,13 +260,68 @@ int vsaogm_set_stream(vsaogm_ctx *c, void *stream)
     return VSAOGM_OK;
 }
 
+int vsa_join_encode(vsaogm_ctx *c)
+{
+    if (c->enc_stream && c->enc_inflight) {
+        VSA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_enc, 0));
+        c->enc_inflight = false;
+    }
+    return VSAOGM_OK;
+}
+
+int vsa_mark_main(vsaogm_ctx *c)
+{
+    if (c->enc_stream) {
+        VSA_CUDA_TRY(cudaEventRecord(c->ev_main, c->stream));
+        c->main_mark = true;
+    }
+    return VSAOGM_OK;
+}
+
+int vsaogm_set_encode_stream(vsaogm_ctx *c, void *stream)
+{
+    if (!c) return VSAOGM_EINVAL_ARG;
+    int rc;
+    if ((rc = vsa_join_encode(c))) return rc;
+    if (c->enc_stream && (cudaStream_t)stream != c->enc_stream) {
+        // encodes already queued on the old stream must precede anything queued after this call
+        VSA_CUDA_TRY(cudaStreamSynchronize(c->enc_stream));
+    }
+    if (stream && !c->ev_enc) {
+        VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_enc, cudaEventDisableTiming));
+        VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+    }
+    c->enc_stream = (cudaStream_t)stream;
+    c->enc_inflight = false;
+    c->main_mark = false;
+    if (c->enc_stream) {   // the new encode stream starts after everything queued so far
+        VSA_CUDA_TRY(cudaEventRecord(c->ev_main, c->stream));
+        c->main_mark = true;
+    }
+    return VSAOGM_OK;
+}
+
 int vsaogm_encode_bundle(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
     if (n < 1) return VSAOGM_EEMPTY;
     if (!xy || !lab) return VSAOGM_EINVAL_ARG;
-    int rc = vsa_launch_encode(c, xy, lab, n);
-    if (rc) return rc;
+    int rc;
+    if (!c->enc_stream) {
+        if ((rc = vsa_launch_encode(c, xy, lab, n))) return rc;
+    } else {
+        if (c->main_mark) {
+            VSA_CUDA_TRY(cudaStreamWaitEvent(c->enc_stream, c->ev_main, 0));
+            c->main_mark = false;
+        }
+        cudaStream_t main = c->stream;
+        c->stream = c->enc_stream;
+        rc = vsa_launch_encode(c, xy, lab, n);
+        c->stream = main;
+        if (rc) return rc;
+        VSA_CUDA_TRY(cudaEventRecord(c->ev_enc, c->enc_stream));
+        c->enc_inflight = true;
+    }
     c->dirty = true;
     return VSAOGM_OK;
 }
@@ -330,9 +389,10 @@ int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_
     VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_xy[s], xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->up));
     VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_lab[s], lab, n, cudaMemcpyHostToDevice, c->up));
     VSA_CUDA_TRY(cudaEventRecord(c->ev_up[s], c->up));
-    VSA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_up[s], 0));
+    cudaStream_t es = c->enc_stream ? c->enc_stream : c->stream;
+    VSA_CUDA_TRY(cudaStreamWaitEvent(es, c->ev_up[s], 0));
     if ((rc = vsaogm_encode_bundle(c, (const float *)c->d_in_xy[s], c->d_in_lab[s], n))) return rc;
-    VSA_CUDA_TRY(cudaEventRecord(c->ev_used[s], c->stream));
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_used[s], es));
     c->in_seq++;
     return VSAOGM_OK;
 }
@@ -340,6 +400,7 @@ int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_
 int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
 {
     if (!c || !p) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     *p = c->d_pending;
     if (n) *n = 2 * (int64_t)c->nslots * c->Dp;
     c->pending_taken = true;
@@ -349,6 +410,7 @@ int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
 int vsaogm_pending_counts(vsaogm_ctx *c, int64_t **p)
 {
     if (!c || !p) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     *p = (int64_t *)c->d_pcounts;
     c->pending_taken = true;
     return VSAOGM_OK;
@@ -357,22 +419,24 @@ int vsaogm_pending_counts(vsaogm_ctx *c, int64_t **p)
 int vsaogm_commit(vsaogm_ctx *c)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
-    int rc = vsa_launch_commit(c);
-    if (rc) return rc;
+    int rc;
+    if ((rc = vsa_join_encode(c))) return rc;
+    if ((rc = vsa_launch_commit(c))) return rc;
     c->dirty = false;
-    return VSAOGM_OK;
+    return vsa_mark_main(c);
 }
 
 int vsaogm_reset(vsaogm_ctx *c)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_m, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_pending, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_counts, 0, c->nslots * sizeof(long long), c->stream));
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_pcounts, 0, c->nslots * sizeof(long long), c->stream));
     c->dirty = false;
     c->decoded = false;
-    return VSAOGM_OK;
+    return vsa_mark_main(c);
 }
 
 int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, float *q)
@@ -443,10 +507,16 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     } else if ((rc = grow_bytes((void **)&c->d_hb, &c->hb_cap, (size_t)M * ldh * sizeof(float)))) {
         return rc;
     }
+    if ((rc = vsa_join_encode(c))) return rc;
     if ((rc = vsa_launch_norms(c, do_commit))) return rc;
     c->dirty = false;
+    static const bool early = getenv("VSAOGM_PIPE_EARLY") != nullptr;   // tuning knob
+    if (early && (rc = vsa_mark_main(c))) return rc;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
     if ((rc = vsa_launch_table_A(c, G, g->y0, g->res, r_lo, prec, slot0))) return rc;
+    // the next encode (encode stream) may start now: pending is committed and the scaled
+    // memories are consumed; it then shares the SMs with this decode's GEMM
+    if (!early && (rc = vsa_mark_main(c))) return rc;
     if ((rc = vsa_launch_decode_gemm(c, G, a_rows, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,
                                      r_lo - g->row_begin, g->row_end - g->row_begin)))
         return rc;
@@ -545,6 +615,7 @@ int vsaogm_wait(vsaogm_ctx *c, int64_t ticket)
 int vsaogm_sync(vsaogm_ctx *c)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     int err = 0;
     VSA_CUDA_TRY(cudaMemcpyAsync(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -559,6 +630,7 @@ int vsaogm_sync(vsaogm_ctx *c)
 int vsaogm_get_memory(vsaogm_ctx *c, double *host, int64_t *counts)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     const int ns = c->nslots;
     const size_t n = 2 * (size_t)ns * c->Dp;
     std::vector<double> m(n), pd(n);
@@ -603,6 +675,7 @@ int vsaogm_profile_enable(vsaogm_ctx *c, int enable)
 int vsaogm_profile_read(vsaogm_ctx *c, double *ms, int64_t *launches)
 {
     if (!c) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
     prof_harvest(c);
     for (int i = 0; i < VSAOGM_NKERNELS; ++i) {

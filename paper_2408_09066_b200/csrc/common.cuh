@@ -82,6 +82,7 @@ struct vsaogm_ctx {
     int enc_x2 = 2;
     int enc_x2_npoly = 6;   // polynomial dimensions of 8 in the second warp role
     int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
+    int enc_x2_minb = 3;    // resident 8-warp blocks per SM (3: 80 registers; 4: 64, tuning knob)
     int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
@@ -132,6 +133,13 @@ struct vsaogm_ctx {
     int64_t in_seq = 0, out_seq = 0;                 // calls so far (slot = seq & 1)
     int *h_err = nullptr;                            // pinned [2]: deferred error bits per output slot
 
+    // encode stream (vsaogm_set_encode_stream): encodes run there and overlap the previous
+    // decode; ev_enc orders the next commit after them, ev_main orders them after the last
+    // commit / reset / table-A build on the context stream
+    cudaStream_t enc_stream = nullptr;
+    cudaEvent_t ev_enc = nullptr, ev_main = nullptr;
+    bool enc_inflight = false, main_mark = false;
+
     // last decode geometry
     bool decoded = false;
     int32_t g_rows = 0, g_cols = 0, g_r0 = 0, g_r1 = 0, g_rlo = 0, g_rext = 0, g_halo = 0;
@@ -148,6 +156,10 @@ struct vsaogm_ctx {
     int64_t prof_n[VSAOGM_NKERNELS] = {0};
     int64_t launches = 0;
 };
+
+// ---- encode-stream ordering (api.cu) -----------------------------------------
+extern "C" int vsa_join_encode(vsaogm_ctx *c);   // context stream waits for in-flight encodes
+extern "C" int vsa_mark_main(vsaogm_ctx *c);     // later encodes wait for the context stream's work so far
 
 // ---- profiling brackets (api.cu) -------------------------------------------
 int vsa_prof_begin(vsaogm_ctx *c, int kid, cudaEvent_t *a);

@@ -558,7 +558,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     const int kblocks = (c->Dp + x2_threads * KT - 1) / (x2_threads * KT);
     // one full wave at ~6 resident blocks per SM (3 for the 256-thread variants), at least 64
     // points per chunk; 7 or 8 resident blocks as tuning variants of the scalar kernel
-    const int minb = x2 ? (x2_threads == 256 ? 3 : 6)
+    const int minb = x2 ? (x2_threads == 256 ? (c->enc_x2_minb == 4 ? 4 : 3) : 6)
                      : KT == 16 ? 4
                      : (!slots_path && KT == 8 && (c->enc_npoly == 1 || c->enc_npoly == 2) &&
                         (c->enc_minb == 7 || c->enc_minb == 8))
@@ -638,7 +638,10 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
         case 5: VSA_ENC_X2(256, 0, 5, 3); break;
         case 7: VSA_ENC_X2(256, 0, 7, 3); break;
         case 8: VSA_ENC_X2(256, 0, 8, 3); break;
-        default: VSA_ENC_X2(256, 0, 6, 3); break;
+        default:
+            if (c->enc_x2_minb == 4) VSA_ENC_X2(256, 0, 6, 4);
+            else VSA_ENC_X2(256, 0, 6, 3);
+            break;
         }
     } else if (x2) {   // 1-polynomial warps beside NPOLY-polynomial warps
         switch (c->enc_x2_npoly) {

@@ -48,6 +48,7 @@ extern "C" {
 int vsaogm_export(vsaogm_ctx *c, void *buf, int64_t *size)
 {
     if (!c || !size) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
     const std::string h = header(c);
     const int S = c->nslots;
     const int64_t need = 8 + (int64_t)h.size() + 8 * (int64_t)S + 16 * (int64_t)S * c->D;
@@ -73,9 +74,19 @@ int vsaogm_export(vsaogm_ctx *c, void *buf, int64_t *size)
     return rc;
 }
 
+static int import_impl(vsaogm_ctx *c, const void *buf, int64_t size, int32_t mode);
+
 int vsaogm_import(vsaogm_ctx *c, const void *buf, int64_t size, int32_t mode)
 {
     if (!c || !buf || size < 10 || (mode != 0 && mode != 1)) return VSAOGM_EINVAL_ARG;
+    if (int rc = vsa_join_encode(c)) return rc;
+    const int rc_import = import_impl(c, buf, size, mode);
+    if (rc_import == VSAOGM_OK) return vsa_mark_main(c);
+    return rc_import;
+}
+
+static int import_impl(vsaogm_ctx *c, const void *buf, int64_t size, int32_t mode)
+{
     const char *p = (const char *)buf;
     if (memcmp(p, kMagic, 8) != 0) return VSAOGM_EINVAL_ARG;
     const char *end = (const char *)memmem(p + 8, (size_t)size - 8, "\n\n", 2);

@@ -26,7 +26,7 @@ EXPORTS = (
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
     "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror", "vsaogm_export",
     "vsaogm_import", "vsaogm_set_estimator", "vsaogm_encode_bundle_host_async", "vsaogm_entropy_host_async",
-    "vsaogm_wait",
+    "vsaogm_wait", "vsaogm_set_encode_stream",
 )
 EPRECOND = -9
 
@@ -93,6 +93,7 @@ def load() -> ctypes.CDLL:
         "vsaogm_encode_bundle_host_async": ([P, P, P, i64], ctypes.c_int),
         "vsaogm_entropy_host_async": ([P, ctypes.POINTER(EntropyParams), P, P, ctypes.POINTER(i64)], ctypes.c_int),
         "vsaogm_wait": ([P, i64], ctypes.c_int),
+        "vsaogm_set_encode_stream": ([P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -222,6 +223,13 @@ class Mapper:
         self._s()
         _check(self._lib.vsaogm_entropy_host(self._ctx, ctypes.byref(p), _host_ptr(s_host), _host_ptr(labels_host)),
                "vsaogm_entropy_host")
+
+    def set_encode_stream(self, stream):
+        """Run encodes on `stream` (a torch.cuda.Stream, or None for the calling stream) so that
+        they overlap the previous decode (vsaogm.h: vsaogm_set_encode_stream)."""
+        self._s()
+        ptr = ctypes.c_void_p(stream.cuda_stream) if stream is not None else ctypes.c_void_p(None)
+        _check(self._lib.vsaogm_set_encode_stream(self._ctx, ptr), "vsaogm_set_encode_stream")
 
     # ------------------------------------------------------------------ pipelined host I/O
     def encode_bundle_host_async(self, xy, labels):

@@ -617,3 +617,64 @@ def test_pipelined_host_steps_match_synchronous():
     with pytest.raises(Exception):
         mp.wait(len(batches) + 3)
     mp.close()
+
+
+def test_encode_stream_pipeline_matches_serial():
+    """vsaogm_set_encode_stream: encodes on a second (low-priority) stream overlapping the previous
+    decode give, step for step, the labels and S of the one-stream schedule, and the same
+    memories; commit / reset / pending / the async host path keep their call order."""
+    import math
+    from paper_2408_09066_b200 import Mapper
+    sc = Scenario("C2")
+    cfg = sc.cfg
+    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
+    p = 1.0 / (2.0 * D)
+    tau = -p * math.log2(p) - (1 - p) * math.log2(1 - p)
+    xy, lab = sc.all_points()
+    chunks = np.array_split(np.arange(len(lab)), 6)
+    dev = [_cuda(np.ascontiguousarray(xy[c]), np.ascontiguousarray(lab[c])) for c in chunks]
+    pinned = [(torch.from_numpy(np.ascontiguousarray(xy[c])).pin_memory(),
+               torch.from_numpy(np.ascontiguousarray(lab[c])).pin_memory()) for c in chunks]
+
+    def schedule(pipelined):
+        hi, lo = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0)
+        outs = []
+        with torch.cuda.stream(hi):
+            mp = Mapper(D, 0, l, sc.bounds)
+            if pipelined:
+                mp.set_encode_stream(lo)
+            for k in range(4):
+                mp.encode_bundle(*dev[k])
+                if k == 1:
+                    mp.encode_bundle(*dev[4])      # two encodes before one decode
+                mp.decode(0.0, 0.0, res, R, C, 0, R, h)
+                S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
+                L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
+                mp.entropy(h, h, tau, -tau, 0, S, L)
+                outs.append((S, L))
+            mp.encode_bundle(*dev[5])
+            mp.commit()                            # explicit commit, then reset and start again
+            m_commit = mp.get_memory()
+            mp.reset()
+            mp.encode_bundle(*dev[0])
+            pend = mp.pending().clone()            # pending view after the encode
+            mp.commit()
+            labs = torch.empty((R, C), dtype=torch.uint8).pin_memory()
+            mp.encode_bundle_host_async(*pinned[1])
+            mp.commit()                            # multi-rank mode since pending(): explicit commit
+            mp.decode(0.0, 0.0, res, R, C, 0, R, h)
+            t = mp.entropy_host_async(h, h, tau, -tau, 0, None, labs)
+            assert mp.wait(t) == 0
+            torch.cuda.synchronize()
+            mem = mp.get_memory()
+            assert mp.sync() == 0
+            mp.close()
+        return outs, m_commit, pend, labs, mem
+
+    a, b = schedule(False), schedule(True)
+    for (Sa, La), (Sb, Lb) in zip(a[0], b[0]):
+        assert torch.equal(Sa, Sb) and torch.equal(La, Lb)
+    assert np.array_equal(a[1][0], b[1][0]) and list(a[1][1]) == list(b[1][1])
+    assert torch.equal(a[2], b[2])
+    assert torch.equal(a[3], b[3])
+    assert np.array_equal(a[4][0], b[4][0]) and list(a[4][1]) == list(b[4][1])

@@ -33,6 +33,11 @@ def main():
     ldev = torch.empty((R, C), dtype=torch.uint8, device="cuda")
     mp = Mapper(D, 0, l, sc.bounds)
     calls = {"enc": 0.0, "dec": 0.0, "ent": 0.0, "wait": 0.0}
+    hi, lo = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0)
+    use_enc_stream = len(sys.argv) > 2 and sys.argv[2] == "pipe"
+    torch.cuda.set_stream(hi)
+    if use_enc_stream:
+        mp.set_encode_stream(lo)
 
     def step_async(k):
         t0 = time.perf_counter()
@@ -54,7 +59,7 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
-    e0.record()
+    e0.record(hi)
     prev = None
     for k in range(K):
         t = step_async(k)
@@ -64,7 +69,7 @@ def main():
             calls["wait"] += time.perf_counter() - tw
         prev = t
     mp.wait(prev)
-    e1.record()
+    e1.record(hi)
     wall = (time.perf_counter() - t0) * 1e3 / K
     torch.cuda.synchronize()
     print(f"pipelined host: wall {wall:.4f} ms/step, compute stream {e0.elapsed_time(e1) / K:.4f} ms/step; "
@@ -76,12 +81,12 @@ def main():
         mp.entropy(h, h, tau, -tau, 0, None, ldev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e0.record()
+    e0.record(hi)
     for k in range(K):
         mp.encode_bundle(*devb[k % nb])
         mp.decode(0.0, 0.0, res, R, C, 0, R, h, precision=F16)
         mp.entropy(h, h, tau, -tau, 0, None, ldev)
-    e1.record()
+    e1.record(hi)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3 / K
     print(f"device-resident, no per-step sync: wall {wall:.4f} ms/step, compute stream {e0.elapsed_time(e1) / K:.4f}")
