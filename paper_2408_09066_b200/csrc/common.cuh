@@ -78,11 +78,12 @@ struct vsaogm_ctx {
     int enc_minb = 6;   // encode blocks resident per SM (6: 80 regs, 8: <= 64 regs) (tuning knob)
     // packed fp32x2 encode (k_encode_bundle_x2, delta = 1, D >= 2048): 0 off (scalar kernel),
     // 1 uniform 4-warp blocks, 2 all-MUFU warps beside enc_x2_npoly-polynomial warps (default,
-    // measured fastest), 3 one-polynomial warps beside enc_x2_npoly-polynomial warps
+    // measured fastest in the pipelined schedule: (0 | 4), 4 blocks/SM), 3 one-polynomial warps
+    // beside enc_x2_npoly-polynomial warps
     int enc_x2 = 2;
-    int enc_x2_npoly = 6;   // polynomial dimensions of 8 in the second warp role
+    int enc_x2_npoly = 4;   // polynomial dimensions of 8 in the second warp role
     int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
-    int enc_x2_minb = 3;    // resident 8-warp blocks per SM (3: 80 registers; 4: 64, tuning knob)
+    int enc_x2_minb = 4;    // resident 8-warp blocks per SM (4: 64 registers, the default; 3: 80)
     int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_bundle(
 // slot per two lanes, and the register footprint is the scalar kernel's.
 //
 // Warp roles: the first half of the block's warps evaluate NPA of their 8 dimensions by
-// polynomial, the second half NPB.  With NPA = 0 (all MUFU) and NPB = 6, every SM
+// polynomial, the second half NPB.  With NPA = 0 (all MUFU) and NPB = 4 (the default), every SM
 // sub-partition (warps w and w + 4 of each block) runs one MUFU-bound warp beside one
 // FMA-bound warp: two homogeneous instruction streams that the warp scheduler
 // interleaves, rather than one stream whose MUFU and polynomial phases alternate and
@@ -632,10 +632,16 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
         case 4: VSA_ENC_X2(128, 4, 4, 6); break;
         default: VSA_ENC_X2(128, 2, 2, 6); break;
         }
-    } else if (x2 && c->enc_x2 == 2) {   // all-MUFU warps beside NPOLY-polynomial warps (default: 6)
+    } else if (x2 && c->enc_x2 == 2) {   // all-MUFU warps beside NPOLY-polynomial warps (default: 4)
         switch (c->enc_x2_npoly) {
-        case 4: VSA_ENC_X2(256, 0, 4, 3); break;
-        case 5: VSA_ENC_X2(256, 0, 5, 3); break;
+        case 4:
+            if (c->enc_x2_minb == 4) VSA_ENC_X2(256, 0, 4, 4);
+            else VSA_ENC_X2(256, 0, 4, 3);
+            break;
+        case 5:
+            if (c->enc_x2_minb == 4) VSA_ENC_X2(256, 0, 5, 4);
+            else VSA_ENC_X2(256, 0, 5, 3);
+            break;
         case 7: VSA_ENC_X2(256, 0, 7, 3); break;
         case 8: VSA_ENC_X2(256, 0, 8, 3); break;
         default:

@@ -142,7 +142,7 @@ def test_encode_paths_agree(monkeypatch, delta):
 @pytest.mark.parametrize("delta", [1, 2])
 def test_encode_packed_variants_agree(monkeypatch, delta):
     """The packed fp32x2 encode kernels (VSAOGM_ENC_X2 = 1: uniform 4-warp blocks; 2: all-MUFU
-    warps beside 6-polynomial warps, the default; 3: 1- beside 5-polynomial warps) agree with
+    warps beside 4-polynomial warps, the default; 3: 1- beside 5-polynomial warps) agree with
     the scalar kernel (0) up to fp32 rounding: the polynomial phasors (sincos_fma2_lite, max
     error 1e-6) and the chunking differ, the counts are exact."""
     from paper_2408_09066_b200 import Mapper
