@@ -268,8 +268,10 @@ __device__ __forceinline__ void unit_coords(int tile, const int *s_pref, const i
     mb = lt / s_tn[g];
 }
 
+// register cap: <= 80 per thread (15 K per CTA) so that a GEMM CTA and three 8-warp encode
+// blocks fit one SM's register file when the streaming pipeline overlaps them (bench: §10)
 template <int MODE, int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
     k_decode_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ Groups G, int K, uint32_t idesc, Epi epi)
 {
