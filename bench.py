@@ -269,22 +269,28 @@ def run_native(args):
         mp.decode(0.0, 0.0, res, R, C, r0, r1, h, precision=F16)
         return mp.entropy_host_async(h, h, tau, -tau, 0, None, labels_pipe[slot])
 
-    with torch.cuda.stream(hi):                    # encode stream still set: the same pipeline
-        for b in range(min(2, args.warmup)):     # untimed: first calls size the staging / output slots
-            if mp.wait(step_async(b, b % 2)) != 0:
-                raise RuntimeError("deferred device error (e2e warm-up)")
-        barrier()
+    def run_e2e(first, count):
+        """`count` pipelined steps; returns (total wall ms, per-step wall ms between ticket waits)."""
         t0 = time.perf_counter()
-        prev = None
-        for k in range(args.steps):
-            t = step_async(args.warmup + k, k % 2)
+        prev, marks = None, []
+        for k in range(count):
+            t = step_async(first + k, k % 2)
             if prev is not None and mp.wait(prev) != 0:
                 raise RuntimeError("deferred device error (e2e)")
+            marks.append(time.perf_counter())
             prev = t
         if mp.wait(prev) != 0:
             raise RuntimeError("deferred device error (e2e)")
-        e2e_t = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64, device=dev)
+        t1 = time.perf_counter()
+        return (t1 - t0) * 1e3, [(b - a) * 1e3 for a, b in zip(marks, marks[1:])]
+
+    with torch.cuda.stream(hi):                    # encode stream still set: the same pipeline
+        run_e2e(0, max(3, args.warmup))            # untimed: sizes the slots, fills the pipeline
+        barrier()
+        e2e_total, e2e_steps = run_e2e(args.warmup, args.steps)
+        e2e_t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
         mp.set_encode_stream(None)
+    e2e_median = statistics.median(e2e_steps) if e2e_steps else None
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_ms_step = e2e_t.item() / args.steps
@@ -365,6 +371,7 @@ def run_native(args):
         "clocks": clocks,
         "e2e": {"value": round(cells / (e2e_ms_step * 1e-3), 1), "unit": "cells/s",
                 "ms_per_step": round(e2e_ms_step, 4),
+                "ms_per_step_median": round(e2e_median, 4) if e2e_median else None,
                 "h2d_bytes_per_step": int(round(my_pts * 9)),
                 "d2h_bytes_per_step": int(band * C)},
     }

@@ -39,21 +39,36 @@ def main():
     if use_enc_stream:
         mp.set_encode_stream(lo)
 
+    mode = sys.argv[3] if len(sys.argv) > 3 else "both"   # both | up (no download) | down (no upload)
+
     def step_async(k):
         t0 = time.perf_counter()
-        mp.encode_bundle_host_async(*pinned[k % nb])
+        if mode == "down":
+            mp.encode_bundle(*devb[k % nb])
+        else:
+            mp.encode_bundle_host_async(*pinned[k % nb])
         t1 = time.perf_counter()
         mp.decode(0.0, 0.0, res, R, C, 0, R, h, precision=F16)
         t2 = time.perf_counter()
-        t = mp.entropy_host_async(h, h, tau, -tau, 0, None, outs[k % 2])
+        if mode == "up":
+            mp.entropy(h, h, tau, -tau, 0, None, ldev)
+            t = None
+        else:
+            t = mp.entropy_host_async(h, h, tau, -tau, 0, None, outs[k % 2])
         t3 = time.perf_counter()
         calls["enc"] += t1 - t0
         calls["dec"] += t2 - t1
         calls["ent"] += t3 - t2
         return t
 
+    def wait(t):
+        if t is None:
+            torch.cuda.current_stream().synchronize()
+        else:
+            mp.wait(t)
+
     for k in range(3):
-        mp.wait(step_async(k))
+        wait(step_async(k))
     for key in calls:
         calls[key] = 0.0
     torch.cuda.synchronize()
@@ -63,12 +78,13 @@ def main():
     prev = None
     for k in range(K):
         t = step_async(k)
-        if prev is not None:
+        if prev is not None or (mode == "up" and k):
             tw = time.perf_counter()
-            mp.wait(prev)
+            if mode != "up":
+                wait(prev)
             calls["wait"] += time.perf_counter() - tw
         prev = t
-    mp.wait(prev)
+    wait(prev)
     e1.record(hi)
     wall = (time.perf_counter() - t0) * 1e3 / K
     torch.cuda.synchronize()
