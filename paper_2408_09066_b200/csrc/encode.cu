@@ -6,7 +6,11 @@
 // class memory psi_i by addition (Eq. 5 :216-219; Alg. 1 :260-285 with delta=1).
 // The phase origin (c_x, c_y) is the bounds centre: a per-k rotation common to
 // every point that cancels in the decode (Eq. 11) and keeps the fp32 phase
-// small.  The kernel is SFU-bound: one MUFU sin + one MUFU cos per phasor.
+// small.  The kernel is bound by the MUFU (XU) and FMA pipes together: a phasor
+// costs either one MUFU sin + one MUFU cos, or a packed FMA-pipe polynomial
+// (sincos_fma2_lite); the default kernel k_encode_bundle_x2 runs all-MUFU warps
+// beside polynomial warps.  k_encode_bundle (scalar) and
+// k_encode_slots remain as measured variants / the small-D path.
 //
 // Layout: threads own phasor dimensions k (KT per thread, strided by the block
 // size so the w loads and partial stores are coalesced); the points of the
