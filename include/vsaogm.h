@@ -205,14 +205,15 @@ int vsaogm_set_encode_stream(vsaogm_ctx *ctx, void *stream);
  * context stream waits for it (with an encode stream set: the copy is queued on
  * the encode stream itself, ahead of the encode's wait for the previous
  * decode, and the download below follows the entropy on the context stream).  The host arrays must be page-locked for the
- * copy to be asynchronous, and must stay unmodified until the next
- * vsaogm_entropy_host_async's ticket has been waited for.
+ * copy to be asynchronous, and must stay unmodified until the ticket of the
+ * vsaogm_entropy_host_async that follows this call has been waited for.
  *
  * vsaogm_entropy_host_async: as vsaogm_entropy_host, into one of two device
  * output slots, then a device->host copy on the download stream; returns at
  * once with *ticket.  s_host / labels_host (page-locked for overlap) are written
- * when vsaogm_wait(ctx, *ticket) returns.  A slot is reused two calls later
- * (the device waits for its previous download first).
+ * when vsaogm_wait(ctx, *ticket) returns.  There are three staging and three
+ * output slots; a slot is reused three calls later (the device orders the
+ * reuse after its previous download), so up to two steps may be in flight.
  *
  * vsaogm_wait: block until step `ticket` has been downloaded; returns a deferred
  * device error like vsaogm_sync.  Errors: EINVAL_ARG (unknown ticket), ECUDA. */

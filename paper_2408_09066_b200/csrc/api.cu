@@ -238,7 +238,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     if (c->up) {
         cudaStreamSynchronize(c->up);
         cudaStreamSynchronize(c->down);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < VSA_IO_SLOTS; ++s) {
             void *q[] = {c->d_in_xy[s], c->d_in_lab[s], c->d_out_S[s], c->d_out_lab[s]};
             for (void *p : q)
                 if (p) cudaFree(p);
@@ -354,9 +354,9 @@ int ensure_pipeline(vsaogm_ctx *c)
     if (c->up) return VSAOGM_OK;
     VSA_CUDA_TRY(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking));
     VSA_CUDA_TRY(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
-    VSA_CUDA_TRY(cudaHostAlloc((void **)&c->h_err, 2 * sizeof(int), cudaHostAllocDefault));
-    c->h_err[0] = c->h_err[1] = 0;
-    for (int s = 0; s < 2; ++s) {
+    VSA_CUDA_TRY(cudaHostAlloc((void **)&c->h_err, VSA_IO_SLOTS * sizeof(int), cudaHostAllocDefault));
+    for (int s = 0; s < VSA_IO_SLOTS; ++s) c->h_err[s] = 0;
+    for (int s = 0; s < VSA_IO_SLOTS; ++s) {
         VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_up[s], cudaEventDisableTiming));
         VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_used[s], cudaEventDisableTiming));
         VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_out[s], cudaEventDisableTiming));
@@ -381,8 +381,8 @@ int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_
     if (!xy || !lab) return VSAOGM_EINVAL_ARG;
     int rc;
     if ((rc = ensure_pipeline(c))) return rc;
-    const int s = (int)(c->in_seq & 1);
-    const bool used = c->in_seq >= 2;   // slot s was consumed by the encode two calls ago
+    const int s = (int)(c->in_seq % VSA_IO_SLOTS);
+    const bool used = c->in_seq >= VSA_IO_SLOTS;   // slot s was consumed by an earlier encode
     if ((rc = grow_slot((void **)&c->d_in_xy[s], &c->in_xy_cap[s], n * sizeof(float2), c->ev_used[s], used))) return rc;
     if ((rc = grow_slot((void **)&c->d_in_lab[s], &c->in_lab_cap[s], (size_t)n, c->ev_used[s], used))) return rc;
     cudaStream_t es = c->enc_stream ? c->enc_stream : c->stream;
@@ -590,8 +590,8 @@ int vsaogm_entropy_host_async(vsaogm_ctx *c, const vsaogm_entropy_params *p, flo
     if (!ticket) return VSAOGM_EINVAL_ARG;
     if ((rc = ensure_pipeline(c))) return rc;
     const size_t cells = (size_t)(c->g_r1 - c->g_r0) * c->g_cols;
-    const int s = (int)(c->out_seq & 1);
-    const bool used = c->out_seq >= 2;  // slot s was downloaded two calls ago
+    const int s = (int)(c->out_seq % VSA_IO_SLOTS);
+    const bool used = c->out_seq >= VSA_IO_SLOTS;   // slot s was downloaded by an earlier call
     if (S_host && (rc = grow_slot((void **)&c->d_out_S[s], &c->out_S_cap[s], 3 * cells * sizeof(float), c->ev_down[s], used)))
         return rc;
     if (lab_host && (rc = grow_slot((void **)&c->d_out_lab[s], &c->out_lab_cap[s], cells, c->ev_down[s], used)))
@@ -620,8 +620,8 @@ int vsaogm_wait(vsaogm_ctx *c, int64_t ticket)
     if (!c || ticket < 0 || ticket >= c->out_seq) return VSAOGM_EINVAL_ARG;
     // the slot's event was recorded for this ticket or a later one (later downloads
     // complete after earlier ones: one download stream)
-    VSA_CUDA_TRY(cudaEventSynchronize(c->ev_down[ticket & 1]));
-    const int err = c->h_err[ticket & 1];
+    VSA_CUDA_TRY(cudaEventSynchronize(c->ev_down[ticket % VSA_IO_SLOTS]));
+    const int err = c->h_err[ticket % VSA_IO_SLOTS];
     if (err) return (err & VSA_ERRBIT_LABEL) ? VSAOGM_ELABEL : VSAOGM_ENONFINITE;
     return VSAOGM_OK;
 }

@@ -36,6 +36,10 @@ void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, in
 
 #define VSA_MAX_GROUPS (VSAOGM_MAX_DELTA * VSAOGM_MAX_DELTA)
 
+// staging / output slots of the pipelined host I/O (vsaogm_*_host_async): a slot is reused
+// VSA_IO_SLOTS calls later, so the host may keep VSA_IO_SLOTS - 1 steps in flight
+#define VSA_IO_SLOTS 3
+
 // Decode GEMM problem groups (one per quadrant with decoded cells; delta = 1: one group).
 // Group g: A-table rows [a_row0, a_row0 + mrows) = class 0 then class 1 blocks of nrows grid
 // rows each (decoded rows row0 .. row0+nrows-1, relative to the first decoded row), times the
@@ -123,16 +127,16 @@ struct vsaogm_ctx {
 
     // pipelined host I/O (vsaogm_*_host_async): two staging / output slots each, copy streams
     cudaStream_t up = nullptr, down = nullptr;     // upload (H2D) / download (D2H) streams
-    float2 *d_in_xy[2] = {nullptr, nullptr}; size_t in_xy_cap[2] = {0, 0};
-    uint8_t *d_in_lab[2] = {nullptr, nullptr}; size_t in_lab_cap[2] = {0, 0};
-    float *d_out_S[2] = {nullptr, nullptr}; size_t out_S_cap[2] = {0, 0};
-    uint8_t *d_out_lab[2] = {nullptr, nullptr}; size_t out_lab_cap[2] = {0, 0};
-    cudaEvent_t ev_up[2] = {nullptr, nullptr};       // upload of slot done
-    cudaEvent_t ev_used[2] = {nullptr, nullptr};     // encode has consumed staging slot
-    cudaEvent_t ev_out[2] = {nullptr, nullptr};      // entropy wrote output slot
-    cudaEvent_t ev_down[2] = {nullptr, nullptr};     // download of output slot done
-    int64_t in_seq = 0, out_seq = 0;                 // calls so far (slot = seq & 1)
-    int *h_err = nullptr;                            // pinned [2]: deferred error bits per output slot
+    float2 *d_in_xy[VSA_IO_SLOTS] = {}; size_t in_xy_cap[VSA_IO_SLOTS] = {};
+    uint8_t *d_in_lab[VSA_IO_SLOTS] = {}; size_t in_lab_cap[VSA_IO_SLOTS] = {};
+    float *d_out_S[VSA_IO_SLOTS] = {}; size_t out_S_cap[VSA_IO_SLOTS] = {};
+    uint8_t *d_out_lab[VSA_IO_SLOTS] = {}; size_t out_lab_cap[VSA_IO_SLOTS] = {};
+    cudaEvent_t ev_up[VSA_IO_SLOTS] = {};       // upload of slot done
+    cudaEvent_t ev_used[VSA_IO_SLOTS] = {};     // encode has consumed staging slot
+    cudaEvent_t ev_out[VSA_IO_SLOTS] = {};      // entropy wrote output slot
+    cudaEvent_t ev_down[VSA_IO_SLOTS] = {};     // download of output slot done
+    int64_t in_seq = 0, out_seq = 0;            // calls so far (slot = seq % VSA_IO_SLOTS)
+    int *h_err = nullptr;                            // pinned [VSA_IO_SLOTS]: deferred error bits per output slot
 
     // encode stream (vsaogm_set_encode_stream): encodes run there and overlap the previous
     // decode; ev_enc orders the next commit after them, ev_main orders them after the last
