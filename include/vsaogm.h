@@ -201,14 +201,14 @@ int vsaogm_set_encode_stream(vsaogm_ctx *ctx, void *stream);
  *
  * vsaogm_encode_bundle_host_async: as vsaogm_encode_bundle_host, but the
  * host->device copy of (xy_host float32 [n][2], labels_host uint8 [n]) goes to
- * one of two device staging slots on the upload stream, and the encode on the
+ * one of three device staging slots on the upload stream, and the encode on the
  * context stream waits for it (with an encode stream set: the copy is queued on
  * the encode stream itself, ahead of the encode's wait for the previous
  * decode, and the download below follows the entropy on the context stream).  The host arrays must be page-locked for the
  * copy to be asynchronous, and must stay unmodified until the ticket of the
  * vsaogm_entropy_host_async that follows this call has been waited for.
  *
- * vsaogm_entropy_host_async: as vsaogm_entropy_host, into one of two device
+ * vsaogm_entropy_host_async: as vsaogm_entropy_host, into one of three device
  * output slots, then a device->host copy on the download stream; returns at
  * once with *ticket.  s_host / labels_host (page-locked for overlap) are written
  * when vsaogm_wait(ctx, *ticket) returns.  There are three staging and three
