@@ -286,7 +286,7 @@ def run_native(args):
         return (t1 - t0) * 1e3, [(b - a) * 1e3 for a, b in zip(marks, marks[1:])]
 
     with torch.cuda.stream(hi):                    # encode stream still set: the same pipeline
-        run_e2e(0, max(3, args.warmup))            # untimed: sizes the slots, fills the pipeline
+        run_e2e(0, max(3, args.warmup, nb))        # untimed: every distinct batch once (sizes the slots)
         barrier()
         e2e_total, e2e_steps = run_e2e(args.warmup, args.steps)
         e2e_t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)

@@ -365,12 +365,13 @@ int ensure_pipeline(vsaogm_ctx *c)
     return VSAOGM_OK;
 }
 
-// grow a slot buffer; the previous user of the slot (recorded event) must be done first
+// grow a slot buffer (with 25 % headroom: batch sizes vary a little from step to step, and a
+// reallocation synchronises the device); the previous user of the slot must be done first
 int grow_slot(void **p, size_t *cap, size_t need, cudaEvent_t busy, bool recorded)
 {
     if (need <= *cap) return VSAOGM_OK;
     if (recorded) VSA_CUDA_TRY(cudaEventSynchronize(busy));
-    return grow_bytes(p, cap, need);
+    return grow_bytes(p, cap, need + need / 4);
 }
 }  // namespace
 
