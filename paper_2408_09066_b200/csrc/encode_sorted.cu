@@ -279,6 +279,7 @@ int grow_t(T **p, size_t *cap, size_t need)
     if (*p) cudaFree(*p);
     *p = nullptr;
     *cap = 0;
+    need += need / 4;   // headroom: batch sizes vary, and a reallocation synchronises the device
     if (cudaMalloc(p, need * sizeof(T)) != cudaSuccess) { *p = nullptr; return VSAOGM_ENOMEM; }
     *cap = need;
     return VSAOGM_OK;
