@@ -131,17 +131,18 @@ int vsaogm_encode_bundle_host(vsaogm_ctx *ctx, const float *xy_host, const uint8
                               int64_t n);
 
 /* Expose the pending (not yet committed) memories for a multi-rank all-reduce
- * (Alg. 3 fusion): *dev_ptr = fp64 [S][Dp][2] (slot, k,
+ * (Alg. 3 fusion): *dev_ptr = ONE contiguous fp64 buffer of
+ * *n_doubles = 2 S Dp + S values: the pending memories [S][Dp][2] (slot, k,
  * re/im; S = 2 delta^2 slots 2 beta + psi, S = 2 classes for delta = 1) in the
  * context's centred-phase convention, Dp = D rounded up to a multiple of 32
- * (padding entries stay zero), *n_doubles = 2 S Dp.  After
+ * (padding entries stay zero), followed by the S pending point counts as
+ * integer-valued doubles (exact below 2^53).  A multi-rank job sums the whole
+ * buffer with a single all-reduce (sum) and then calls vsaogm_commit.  After
  * this call the context is in multi-rank mode: vsaogm_decode no longer commits
  * implicitly and returns ESTATE while pending work is uncommitted.  The
- * pointer stays valid for the life of the context. */
+ * pointer stays valid for the life of the context; the buffer is ordered on
+ * the context stream (encodes queued on an encode stream are joined first). */
 int vsaogm_pending(vsaogm_ctx *ctx, double **dev_ptr, int64_t *n_doubles);
-
-/* Same as vsaogm_pending for the per-slot point counts: int64 [S] device. */
-int vsaogm_pending_counts(vsaogm_ctx *ctx, int64_t **dev_ptr);
 
 /* m += pending; pending = 0 (and the counts). */
 int vsaogm_commit(vsaogm_ctx *ctx);
@@ -168,6 +169,16 @@ int vsaogm_decode(vsaogm_ctx *ctx, const vsaogm_grid *grid, vsaogm_precision pre
  *     reading of "passing a disk filter ... applying Shannon entropy".
  * Errors: EINVAL_ARG. */
 int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
+
+/* Tuning variants (measurement and test hook; the defaults are the measured best and no
+ * environment variable changes them).  Sets the integer knob `key` of this context for
+ * later calls: "enc_x2" (encode kernel family), "enc_x2_npoly", "enc_x2_minb",
+ * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
+ * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
+ * CTA pair, 1 single CTA), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,
+ * else the split-K factor), "pipe_early" (0/1), "entropy_kernel"
+ * (0 auto).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
+int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);
 
 /* Local entropy (Alg. 2), global entropy S = S_occ - S_emp, 3-way labels
  * (Eq. 12 + L14) over the band of the last vsaogm_decode.  s_dev: NULL or
@@ -216,7 +227,11 @@ int vsaogm_set_encode_stream(vsaogm_ctx *ctx, void *stream);
  * reuse after its previous download), so up to two steps may be in flight.
  *
  * vsaogm_wait: block until step `ticket` has been downloaded; returns a deferred
- * device error like vsaogm_sync.  Errors: EINVAL_ARG (unknown ticket), ECUDA. */
+ * device error like vsaogm_sync (the error bits are sticky until vsaogm_sync and are
+ * snapshotted after the step's entropy; with an encode stream set, the next step's
+ * encode may already have run, so an error can be reported one step early).
+ * Errors: EINVAL_ARG (unknown ticket), ECUDA.  Switching the encode stream
+ * (vsaogm_set_encode_stream) synchronises the copy streams of this pipeline. */
 int vsaogm_encode_bundle_host_async(vsaogm_ctx *ctx, const float *xy_host, const uint8_t *labels_host, int64_t n);
 int vsaogm_entropy_host_async(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, float *s_host,
                               uint8_t *labels_host, int64_t *ticket);
@@ -258,10 +273,12 @@ int64_t vsaogm_launch_count(const vsaogm_ctx *ctx);
 /* Test hook: the decode GEMM kernel alone.  C[M][N] (float32, row-major) =
  * A[M][K] . B[N][K]^T with A, B 16-bit (precision) K-major device arrays,
  * K a multiple of 64, 1 <= M, N.  kernel: -1 library default, 0 the CTA-pair
- * (cta_group::2) kernel, 1 the single-CTA kernel.  Runs on `stream` and
- * synchronises it. */
+ * (cta_group::2) kernel, 1 the single-CTA kernel; bn (0 auto, else 128..256 in
+ * steps of 32) and splits (0 auto, else the split-K factor) pin the CTA-pair
+ * kernel's tile width and split-K.  Runs on `stream` and synchronises it. */
 int vsaogm_test_gemm(const void *A_dev, const void *B_dev, int32_t M, int32_t N, int32_t K,
-                     vsaogm_precision precision, int32_t kernel, float *C_dev, void *stream);
+                     vsaogm_precision precision, int32_t kernel, int32_t bn, int32_t splits, float *C_dev,
+                     void *stream);
 
 /* Multi-agent fusion (Alg. 3).
  * vsaogm_export writes the context's state -- committed + pending memories in

@@ -141,16 +141,6 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
     do {
         if (cudaGetDevice(&c->device) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
         cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
-        if (const char *e = getenv("VSAOGM_ENC_NPOLY")) c->enc_npoly = atoi(e);   // tuning knob (0..4)
-        if (const char *e = getenv("VSAOGM_ENC_MINB")) c->enc_minb = atoi(e);     // tuning knob (6 or 8)
-        if (const char *e = getenv("VSAOGM_ENC_KT")) c->enc_kt = atoi(e);         // tuning knob (8 or 16)
-        if (const char *e = getenv("VSAOGM_ENC_X2")) c->enc_x2 = atoi(e);         // packed encode (0..3)
-        if (const char *e = getenv("VSAOGM_ENC_X2_WAVES")) c->enc_x2_waves = std::max(1, atoi(e));
-        if (const char *e = getenv("VSAOGM_ENC_X2_NPOLY")) c->enc_x2_npoly = atoi(e);
-        if (const char *e = getenv("VSAOGM_ENC_X2_MINB")) c->enc_x2_minb = atoi(e);
-        if (const char *e = getenv("VSAOGM_ENC_PATH")) c->enc_path = atoi(e);     // tuning knob (0, 1, 2)
-        if (const char *e = getenv("VSAOGM_ENC_WAVES")) c->enc_waves = std::max(1, atoi(e));
-        if (const char *e = getenv("VSAOGM_ENC_RUNS_WAVES")) c->enc_runs_waves = std::max(1, atoi(e));
         c->seed = seed;
         c->delta = delta;
         c->nq = delta * delta;
@@ -188,9 +178,9 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if ((rc = dev_alloc_zero(&c->d_tx_turns, c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_ty_turns, c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_m, 2 * (size_t)c->nslots * c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_pending, 2 * (size_t)c->nslots * c->Dp))) break;
+        if ((rc = dev_alloc_zero(&c->d_pending, 2 * (size_t)c->nslots * c->Dp + c->nslots))) break;
+        c->d_pcounts = c->d_pending + 2 * (size_t)c->nslots * c->Dp;
         if ((rc = dev_alloc_zero(&c->d_counts, c->nslots))) break;
-        if ((rc = dev_alloc_zero(&c->d_pcounts, c->nslots))) break;
         if ((rc = dev_alloc_zero(&c->d_norm2, c->nslots))) break;
         if ((rc = dev_alloc_zero(&c->d_mhat, (size_t)c->nslots * c->Dp))) break;
         if ((rc = dev_alloc_zero(&c->d_normpart, (size_t)c->nslots * 16))) break;
@@ -227,7 +217,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     if (c->enc_stream) cudaStreamSynchronize(c->enc_stream);
     if (c->ev_enc) cudaEventDestroy(c->ev_enc);
     if (c->ev_main) cudaEventDestroy(c->ev_main);
-    void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts, c->d_pcounts,
+    void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts,
                     c->d_norm2, c->d_mhat, c->d_normpart, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
                     c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code};
@@ -287,6 +277,14 @@ int vsaogm_set_encode_stream(vsaogm_ctx *c, void *stream)
         // encodes already queued on the old stream must precede anything queued after this call
         VSA_CUDA_TRY(cudaStreamSynchronize(c->enc_stream));
     }
+    // the pipelined host I/O orders slot reuse differently with and without an encode stream
+    // (api.cu: vsaogm_*_host_async); drain its copy streams so that no slot's previous user is
+    // left unordered across the switch
+    if (c->up && (cudaStream_t)stream != c->enc_stream) {
+        VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        VSA_CUDA_TRY(cudaStreamSynchronize(c->up));
+        VSA_CUDA_TRY(cudaStreamSynchronize(c->down));
+    }
     if (stream && !c->ev_enc) {
         VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_enc, cudaEventDisableTiming));
         VSA_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
@@ -342,8 +340,20 @@ int vsaogm_encode_bundle_host(vsaogm_ctx *c, const float *xy, const uint8_t *lab
             return VSAOGM_ENOMEM;
         c->stage_cap = n;
     }
-    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_xy, xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
-    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_lab, lab, n, cudaMemcpyHostToDevice, c->stream));
+    // the copies go on the stream the encode runs on: with an encode stream, after its wait for
+    // the context stream's last mark (a previous reader of the staging buffers may be an encode
+    // queued on the context stream before the encode stream was set); consecutive host encodes
+    // then reuse the buffers in stream order
+    cudaStream_t es = c->stream;
+    if (c->enc_stream) {
+        es = c->enc_stream;
+        if (c->main_mark) {
+            VSA_CUDA_TRY(cudaStreamWaitEvent(c->enc_stream, c->ev_main, 0));
+            c->main_mark = false;
+        }
+    }
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_xy, xy, n * sizeof(float2), cudaMemcpyHostToDevice, es));
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_stage_lab, lab, n, cudaMemcpyHostToDevice, es));
     return vsaogm_encode_bundle(c, (const float *)c->d_stage_xy, c->d_stage_lab, n);
 }
 
@@ -411,16 +421,7 @@ int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
     if (!c || !p) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     *p = c->d_pending;
-    if (n) *n = 2 * (int64_t)c->nslots * c->Dp;
-    c->pending_taken = true;
-    return VSAOGM_OK;
-}
-
-int vsaogm_pending_counts(vsaogm_ctx *c, int64_t **p)
-{
-    if (!c || !p) return VSAOGM_EINVAL_ARG;
-    if (int rc = vsa_join_encode(c)) return rc;
-    *p = (int64_t *)c->d_pcounts;
+    if (n) *n = 2 * (int64_t)c->nslots * c->Dp + c->nslots;
     c->pending_taken = true;
     return VSAOGM_OK;
 }
@@ -440,9 +441,8 @@ int vsaogm_reset(vsaogm_ctx *c)
     if (!c) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_m, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pending, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pending, 0, (2 * (size_t)c->nslots * c->Dp + c->nslots) * sizeof(double), c->stream));
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_counts, 0, c->nslots * sizeof(long long), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_pcounts, 0, c->nslots * sizeof(long long), c->stream));
     c->dirty = false;
     c->decoded = false;
     return vsa_mark_main(c);
@@ -519,7 +519,7 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     if ((rc = vsa_join_encode(c))) return rc;
     if ((rc = vsa_launch_norms(c, do_commit))) return rc;
     c->dirty = false;
-    static const bool early = getenv("VSAOGM_PIPE_EARLY") != nullptr;   // tuning knob
+    const bool early = c->pipe_early != 0;   // tuning variant
     if (early && (rc = vsa_mark_main(c))) return rc;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
     if ((rc = vsa_launch_table_A(c, G, g->y0, g->res, r_lo, prec, slot0))) return rc;
@@ -546,6 +546,39 @@ int vsaogm_set_estimator(vsaogm_ctx *c, int32_t estimator)
     if (!c || (estimator != 0 && estimator != 1)) return VSAOGM_EINVAL_ARG;
     c->estimator = estimator;
     return VSAOGM_OK;
+}
+
+int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
+{
+    if (!c || !key) return VSAOGM_EINVAL_ARG;
+    struct Knob {
+        const char *name;
+        int *field;
+        int lo, hi;
+    } knobs[] = {
+        {"enc_x2", &c->enc_x2, 0, 3},
+        {"enc_x2_npoly", &c->enc_x2_npoly, 0, 8},
+        {"enc_x2_minb", &c->enc_x2_minb, 3, 4},
+        {"enc_x2_waves", &c->enc_x2_waves, 1, 64},
+        {"enc_npoly", &c->enc_npoly, 0, 4},
+        {"enc_minb", &c->enc_minb, 6, 8},
+        {"enc_kt", &c->enc_kt, 8, 16},
+        {"enc_path", &c->enc_path, -1, 2},
+        {"enc_waves", &c->enc_waves, 1, 64},
+        {"enc_runs_waves", &c->enc_runs_waves, 1, 64},
+        {"gemm_variant", &c->gemm_variant, -1, 1},
+        {"gemm_bn", &c->gemm_bn, 0, 256},
+        {"gemm_splits", &c->gemm_splits, 0, 64},
+        {"pipe_early", &c->pipe_early, 0, 1},
+        {"entropy_kernel", &c->entropy_kernel, 0, 3},
+    };
+    for (const Knob &k : knobs)
+        if (strcmp(k.name, key) == 0) {
+            if (value < k.lo || value > k.hi) return VSAOGM_EINVAL_ARG;
+            *k.field = (int)value;
+            return VSAOGM_OK;
+        }
+    return VSAOGM_EINVAL_ARG;
 }
 
 static int check_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p)
@@ -649,12 +682,13 @@ int vsaogm_get_memory(vsaogm_ctx *c, double *host, int64_t *counts)
     const int ns = c->nslots;
     const size_t n = 2 * (size_t)ns * c->Dp;
     std::vector<double> m(n), pd(n);
-    std::vector<long long> cnt(ns), pcnt(ns);
+    std::vector<long long> cnt(ns);
+    std::vector<double> pcnt(ns);
     VSA_CUDA_TRY(cudaStreamSynchronize(c->stream));
     VSA_CUDA_TRY(cudaMemcpy(m.data(), c->d_m, n * sizeof(double), cudaMemcpyDeviceToHost));
     VSA_CUDA_TRY(cudaMemcpy(pd.data(), c->d_pending, n * sizeof(double), cudaMemcpyDeviceToHost));
     VSA_CUDA_TRY(cudaMemcpy(cnt.data(), c->d_counts, ns * sizeof(long long), cudaMemcpyDeviceToHost));
-    VSA_CUDA_TRY(cudaMemcpy(pcnt.data(), c->d_pcounts, ns * sizeof(long long), cudaMemcpyDeviceToHost));
+    VSA_CUDA_TRY(cudaMemcpy(pcnt.data(), c->d_pcounts, ns * sizeof(double), cudaMemcpyDeviceToHost));
     if (host) {
         // undo the centring rotation: m_raw,k = m_centred,k * exp(+i (thx_k c_x + thy_k c_y) / l)
         for (int s = 0; s < ns; ++s)
@@ -668,7 +702,7 @@ int vsaogm_get_memory(vsaogm_ctx *c, double *host, int64_t *counts)
             }
     }
     if (counts)
-        for (int s = 0; s < ns; ++s) counts[s] = cnt[s] + pcnt[s];
+        for (int s = 0; s < ns; ++s) counts[s] = cnt[s] + (long long)pcnt[s];
     return VSAOGM_OK;
 }
 
@@ -705,14 +739,16 @@ int vsaogm_profile_read(vsaogm_ctx *c, double *ms, int64_t *launches)
 int64_t vsaogm_launch_count(const vsaogm_ctx *c) { return c ? c->launches : 0; }
 
 int vsaogm_test_gemm(const void *A, const void *B, int32_t M, int32_t N, int32_t K, vsaogm_precision prec,
-                     int32_t kernel, float *C, void *stream)
+                     int32_t kernel, int32_t bn, int32_t splits, float *C, void *stream)
 {
     if (!A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 != 0 || kernel < -1 || kernel > 1)
         return VSAOGM_EINVAL_ARG;
+    if (bn != 0 && (bn < 128 || bn > 256 || bn % 32 != 0)) return VSAOGM_EINVAL_ARG;
+    if (splits < 0) return VSAOGM_EINVAL_ARG;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int rc = vsa_gemm_raw(A, B, M, N, K, prec, C, (cudaStream_t)stream, sms, kernel);
+    int rc = vsa_gemm_raw(A, B, M, N, K, prec, C, (cudaStream_t)stream, sms, kernel, bn, splits);
     if (rc) return rc;
     VSA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     return VSAOGM_OK;

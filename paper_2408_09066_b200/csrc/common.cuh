@@ -36,8 +36,8 @@ void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, in
 
 #define VSA_MAX_GROUPS (VSAOGM_MAX_DELTA * VSAOGM_MAX_DELTA)
 
-// staging / output slots of the pipelined host I/O (vsaogm_*_host_async): a slot is reused
-// VSA_IO_SLOTS calls later, so the host may keep VSA_IO_SLOTS - 1 steps in flight
+// staging / output slots of the pipelined host I/O (vsaogm_*_host_async): three of each; a slot
+// is reused VSA_IO_SLOTS calls later, so the host may keep VSA_IO_SLOTS - 1 steps in flight
 #define VSA_IO_SLOTS 3
 
 // Decode GEMM problem groups (one per quadrant with decoded cells; delta = 1: one group).
@@ -89,6 +89,12 @@ struct vsaogm_ctx {
     int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
     int enc_x2_minb = 4;    // resident 8-warp blocks per SM (4: 64 registers, the default; 3: 80)
     int enc_kt = 8;     // phasor dimensions per encode thread (8, or 16 as a tuning variant)
+    // decode / pipeline / entropy tuning variants (vsaogm_set_tuning; defaults = measured best)
+    int gemm_variant = -1;  // -1 auto (CTA pair), 0 CTA pair, 1 single CTA (one group only)
+    int gemm_bn = 0;        // 0 auto, else the CTA-pair tile width (128..256, multiple of 32)
+    int gemm_splits = 0;    // 0 auto, else the split-K factor
+    int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
+    int entropy_kernel = 0; // 0 auto; 1 generic kernel; 2 staged fixed-radius kernel
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta
@@ -97,9 +103,11 @@ struct vsaogm_ctx {
     float *d_wx = nullptr, *d_wy = nullptr;        // theta / l, fp32 rad/m [Dp] (0-padded)
     double *d_tx_turns = nullptr, *d_ty_turns = nullptr;   // theta / (2 pi l), fp64 turns per metre [Dp]
     double *d_m = nullptr;                         // committed memories [2][Dp][2]
-    double *d_pending = nullptr;                   // pending memories  [2][Dp][2]
-    long long *d_counts = nullptr;                 // [2]
-    long long *d_pcounts = nullptr;                // pending counts [2]
+    // pending memories [S][Dp][2] followed by the S pending point counts (integer-valued fp64),
+    // one contiguous buffer so that a multi-rank job sums both with ONE all-reduce (Alg. 3)
+    double *d_pending = nullptr;
+    long long *d_counts = nullptr;                 // [S]
+    double *d_pcounts = nullptr;                   // = d_pending + 2 S Dp (not a separate allocation)
     double *d_norm2 = nullptr;                     // ||m_c||^2 [2]
     float2 *d_mhat = nullptr;                      // sqrt(D) m_c / ||m_c||, fp32 [S][Dp]
     double *d_normpart = nullptr;                  // per-block partial ||m_c||^2 [S][16]
@@ -125,7 +133,7 @@ struct vsaogm_ctx {
     float *d_S = nullptr; size_t S_cap = 0;        // host-entropy scratch
     uint8_t *d_lab = nullptr; size_t lab_cap = 0;
 
-    // pipelined host I/O (vsaogm_*_host_async): two staging / output slots each, copy streams
+    // pipelined host I/O (vsaogm_*_host_async): three staging / output slots each, copy streams
     cudaStream_t up = nullptr, down = nullptr;     // upload (H2D) / download (D2H) streams
     float2 *d_in_xy[VSA_IO_SLOTS] = {}; size_t in_xy_cap[VSA_IO_SLOTS] = {};
     uint8_t *d_in_lab[VSA_IO_SLOTS] = {}; size_t in_lab_cap[VSA_IO_SLOTS] = {};
@@ -182,7 +190,8 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
                            float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows);
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab);
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
-                 cudaStream_t s, int num_sms, int variant);
+                 cudaStream_t s, int num_sms, int variant, int bn = 0, int splits = 0);
+// staged host-encode / I/O helpers: comments in api.cu
 
 // ---- PTX helpers (sm_100a) ---------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p)

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(ENC_THREADS, MINB) k_encode_slots(
 constexpr int RED_SLICES = 16;
 __global__ void __launch_bounds__(32 * RED_SLICES) k_reduce_partials(
     const float2 *__restrict__ part, const long long *__restrict__ part_cnt, int chunks, int nslots, int Dp, int D,
-    double *__restrict__ pending, long long *__restrict__ pcount)
+    double *__restrict__ pending, double *__restrict__ pcount)
 {
     __shared__ double4 s_acc[RED_SLICES][32];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -467,18 +467,18 @@ __global__ void __launch_bounds__(32 * RED_SLICES) k_reduce_partials(
             pending[2 * (size_t)idx + 3] += r.w;
         }
     }
-    if (blockIdx.x == 0) {   // counts: integer sums (exact in any order), chunk-strided over the block
+    if (blockIdx.x == 0) {   // counts: integer sums (exact in any order: integer-valued fp64 < 2^53)
         for (int sl = 0; sl < nslots; ++sl) {
             long long s = 0;
             for (int ch = threadIdx.x; ch < chunks; ch += blockDim.x) s += part_cnt[ch * nslots + sl];
-            if (s) atomicAdd((unsigned long long *)&pcount[sl], (unsigned long long)s);
+            if (s) atomicAdd(&pcount[sl], (double)s);
         }
     }
 }
 
 // Commit: m += pending, pending = 0 (Alg. 3 result folded into the memories).
 __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, long long *__restrict__ cnt,
-                         long long *__restrict__ pcnt, int n, int nslots)
+                         double *__restrict__ pcnt, int n, int nslots)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
@@ -486,8 +486,8 @@ __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, l
         pending[i] = 0.0;
     }
     if (blockIdx.x == 0 && threadIdx.x < nslots) {
-        cnt[threadIdx.x] += pcnt[threadIdx.x];
-        pcnt[threadIdx.x] = 0;
+        cnt[threadIdx.x] += (long long)pcnt[threadIdx.x];
+        pcnt[threadIdx.x] = 0.0;
     }
 }
 
@@ -500,7 +500,7 @@ __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, l
 // blocks) and scales its own range.
 constexpr int NORM_THREADS = 256, NORM_BLOCKS = 16;
 __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restrict__ m, double *__restrict__ pending,
-                                                               long long *__restrict__ cnt, long long *__restrict__ pcnt,
+                                                               long long *__restrict__ cnt, double *__restrict__ pcnt,
                                                                int do_commit, int Dp, int D, double *__restrict__ normpart,
                                                                double *__restrict__ norm2, float2 *__restrict__ mhat)
 {
@@ -540,8 +540,8 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
     if (b == 0 && threadIdx.x == 0) {
         norm2[c] = n2;
         if (do_commit) {
-            cnt[c] += pcnt[c];
-            pcnt[c] = 0;
+            cnt[c] += (long long)pcnt[c];
+            pcnt[c] = 0.0;
         }
     }
 }
@@ -718,7 +718,8 @@ int vsa_launch_norms(vsaogm_ctx *c, int do_commit)
     vsa_prof_begin(c, VSAOGM_K_NORMS, &ev);
     {
         double *m = c->d_m, *pend = c->d_pending, *np = c->d_normpart, *n2 = c->d_norm2;
-        long long *cnt = c->d_counts, *pcnt = c->d_pcounts;
+        long long *cnt = c->d_counts;
+        double *pcnt = c->d_pcounts;
         int dc = do_commit, Dp = c->Dp, D = c->D;
         float2 *mh = c->d_mhat;
         void *args[] = {&m, &pend, &cnt, &pcnt, &dc, &Dp, &D, &np, &n2, &mh};

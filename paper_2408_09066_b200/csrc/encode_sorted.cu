@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const float2 *__restr
 // pending[s][k] += sum over the slot's runs (fixed order, fp64): 32 k-lanes x 8 run slices
 __global__ void __launch_bounds__(256) k_reduce_runs(const float2 *__restrict__ part, const int *__restrict__ meta,
                                                      int nslots, int Dp, int D, double *__restrict__ pending,
-                                                     long long *__restrict__ pcount)
+                                                     double *__restrict__ pcount)
 {
     __shared__ double s_re[8][32], s_im[8][32];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256) k_reduce_runs(const float2 *__restrict__ 
         pending[2 * (size_t)idx] += a;
         pending[2 * (size_t)idx + 1] += b;
     }
-    if (blockIdx.x == 0 && threadIdx.x < nslots) pcount[threadIdx.x] += meta[META_TOTAL() + threadIdx.x];
+    if (blockIdx.x == 0 && threadIdx.x < nslots) pcount[threadIdx.x] += (double)meta[META_TOTAL() + threadIdx.x];
 }
 
 template <typename T>

@@ -502,12 +502,12 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
     const int ldh = (c->g_cols + 7) / 8 * 8;
     const size_t smem = sizeof(float) * (2 * (size_t)TH * TW + 2 * (size_t)TH * TC);
     dim3 grid((c->g_cols + TC - 1) / TC, (band + TR - 1) / TR);
-    const bool fixed = p->half_occ == p->half_emp && H <= 8 && getenv("VSAOGM_ENTROPY_GENERIC") == nullptr;
+    const bool fixed = p->half_occ == p->half_emp && H <= 8 && c->entropy_kernel != 1;
     if (!fixed)
         VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
-    if (fixed && !p->disk && H <= 4 && getenv("VSAOGM_ENTROPY_SMEM") == nullptr) {
+    if (fixed && !p->disk && H <= 4 && c->entropy_kernel != 2) {
 #define VSA_BOX(HH)                                                                                                \
     do {                                                                                                           \
         const size_t bsm = sizeof(float) * 2 * (TR + 2 * (HH)) * (TC + 8);                                          \

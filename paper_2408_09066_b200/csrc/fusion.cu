@@ -154,7 +154,7 @@ static int import_impl(vsaogm_ctx *c, const void *buf, int64_t size, int32_t mod
             rc = VSAOGM_ECUDA;
             break;
         }
-        if (mode == 0 && cudaMemset(c->d_pcounts, 0, S * sizeof(long long)) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
+        if (mode == 0 && cudaMemset(c->d_pcounts, 0, S * sizeof(double)) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
         if (cudaStreamSynchronize(c->stream) != cudaSuccess) { rc = VSAOGM_ECUDA; break; }
         if (mode == 0) c->dirty = false;
     } while (0);

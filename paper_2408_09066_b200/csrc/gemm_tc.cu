@@ -572,24 +572,21 @@ int launch2(const void *A, const void *B, int a_rows, int b_rows, int K, int pre
     }
 }
 
-// variant: 0 = 2-CTA (default), 1 = 1-CTA (single group only); env VSAOGM_GEMM=1cta selects
-// the latter, VSAOGM_GEMM_BN=<n> pins the 2-CTA tile width, VSAOGM_GEMM_SPLITS=<s> the split-K
-// factor.  *ws / *ws_cap: a caller-owned growable workspace for split-K partials.
+// variant: -1 / 0 = 2-CTA (default), 1 = 1-CTA (single group only); bn_force > 0 pins the
+// 2-CTA tile width, splits_force > 0 the split-K factor (vsaogm_set_tuning).  *ws / *ws_cap:
+// a caller-owned growable workspace for split-K partials.
 template <int MODE>
 int launch(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, Epi epi,
-           cudaStream_t s, int num_sms, int variant, float **ws, size_t *ws_cap)
+           cudaStream_t s, int num_sms, int variant, float **ws, size_t *ws_cap, int bn_force = 0,
+           int splits_force = 0)
 {
-    if (variant < 0) {
-        const char *e = getenv("VSAOGM_GEMM");
-        variant = (e && strcmp(e, "1cta") == 0 && G.n == 1) ? 1 : 0;
-    }
-    if (variant == 1) return launch1<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    if (variant == 1 && G.n == 1) return launch1<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
     int bn = pick_bn(G, num_sms);
-    if (const char *e = getenv("VSAOGM_GEMM_BN")) bn = atoi(e);
+    if (bn_force > 0) bn = bn_force;
     epi.ws_rows = a_rows;
     epi.ws_cols = b_rows;
     int S = pick_splits(G, a_rows, b_rows, K, bn, num_sms);
-    if (const char *e = getenv("VSAOGM_GEMM_SPLITS")) S = atoi(e);
+    if (splits_force > 0) S = splits_force;
     const int num_kb = K / VSA_BK;
     S = std::max(1, std::min(S, num_kb));
     epi.kb_per = (num_kb + S - 1) / S;
@@ -627,7 +624,8 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
     e.kb_per = c->Kp / VSA_BK;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
-    int rc = launch<1>(c->d_A, c->d_B, a_rows, N, c->Kp, prec, G, e, c->stream, c->num_sms, -1, &c->d_ws, &c->ws_cap);
+    int rc = launch<1>(c->d_A, c->d_B, a_rows, N, c->Kp, prec, G, e, c->stream, c->num_sms, c->gemm_variant, &c->d_ws,
+                       &c->ws_cap, c->gemm_bn, c->gemm_splits);
     if (rc) return rc;
     vsa_prof_end(c, VSAOGM_K_DECODE_GEMM, ev);
     c->launches++;
@@ -635,7 +633,7 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
 }
 
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C, cudaStream_t s,
-                 int num_sms, int variant)
+                 int num_sms, int variant, int bn, int splits)
 {
     Groups G{};
     G.n = 1;
@@ -652,7 +650,7 @@ int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, 
     e.kb_per = K / VSA_BK;
     float *ws = nullptr;
     size_t cap = 0;
-    int rc = launch<0>(A, B, M, N, K, prec, G, e, s, num_sms, variant, &ws, &cap);
+    int rc = launch<0>(A, B, M, N, K, prec, G, e, s, num_sms, variant, &ws, &cap, bn, splits);
     if (ws) {
         cudaStreamSynchronize(s);
         cudaFree(ws);

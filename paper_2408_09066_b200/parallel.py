@@ -3,8 +3,9 @@
 Two independent partitions, one process per GPU:
   * encode: rank g bundles the contiguous point slice [g N / G, (g+1) N / G)
     into its own pending memories; ONE collective, an all-reduce (sum) of the
-    pending memories and counts over NCCL, is Alg. 3's fusion
-    of identically configured agents; every rank then commits;
+    library's packed pending buffer (memories + counts, 16 Dp + 16 bytes at
+    delta = 1) over NCCL, is Alg. 3's fusion of identically
+    configured agents; every rank then commits;
   * decode + entropy: rank g owns grid rows [g R / G, (g+1) R / G) and decodes
     h halo rows on each side (clipped), so the window entropy needs no
     communication.  Results stay sharded.
@@ -33,14 +34,23 @@ def decoded_rows(rows: int, r0: int, r1: int, halo: int):
     return max(0, r0 - halo), min(rows, r1 + halo)
 
 
-def allreduce_pending(pending: torch.Tensor, counts: torch.Tensor, group=None):
-    """Sum the pending memories and counts over all ranks (in place)."""
+def allreduce_pending(buf: torch.Tensor, group=None):
+    """Sum the packed pending buffer (memories, then the per-slot point counts as
+    integer-valued doubles; vsaogm.h: vsaogm_pending) over all ranks, in place: ONE
+    collective per batch (Alg. 3 fusion)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(pending, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
 
 
-def fuse_and_commit(mapper, group=None):
-    """Alg. 3 across ranks, then m += pending on every rank (multi-rank mode)."""
-    allreduce_pending(mapper.pending(), mapper.pending_counts(), group)
+def fuse_and_commit(mapper, group=None, timer=None):
+    """Alg. 3 across ranks, then m += pending on every rank (multi-rank mode).
+
+    `timer`, if given, is a pair of CUDA events recorded on the current stream around the
+    collective (the bench's all-reduce latency)."""
+    buf = mapper.pending_buffer()
+    if timer is not None:
+        timer[0].record()
+    allreduce_pending(buf, group)
+    if timer is not None:
+        timer[1].record()
     mapper.commit()

@@ -22,11 +22,11 @@ KERNELS = ("encode", "reduce", "commit", "norms", "table_B", "table_A", "decode_
 # every symbol include/vsaogm.h declares
 EXPORTS = (
     "vsaogm_create", "vsaogm_create_quadrants", "vsaogm_destroy", "vsaogm_set_stream", "vsaogm_encode_bundle", "vsaogm_encode_bundle_host",
-    "vsaogm_pending", "vsaogm_pending_counts", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
+    "vsaogm_pending", "vsaogm_commit", "vsaogm_reset", "vsaogm_decode", "vsaogm_entropy",
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
     "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror", "vsaogm_export",
     "vsaogm_import", "vsaogm_set_estimator", "vsaogm_encode_bundle_host_async", "vsaogm_entropy_host_async",
-    "vsaogm_wait", "vsaogm_set_encode_stream",
+    "vsaogm_wait", "vsaogm_set_encode_stream", "vsaogm_set_tuning",
 )
 EPRECOND = -9
 
@@ -73,7 +73,6 @@ def load() -> ctypes.CDLL:
         "vsaogm_encode_bundle": ([P, P, P, i64], ctypes.c_int),
         "vsaogm_encode_bundle_host": ([P, P, P, i64], ctypes.c_int),
         "vsaogm_pending": ([P, ctypes.POINTER(P), ctypes.POINTER(i64)], ctypes.c_int),
-        "vsaogm_pending_counts": ([P, ctypes.POINTER(P)], ctypes.c_int),
         "vsaogm_commit": ([P], ctypes.c_int),
         "vsaogm_reset": ([P], ctypes.c_int),
         "vsaogm_decode": ([P, ctypes.POINTER(Grid), ctypes.c_int, P], ctypes.c_int),
@@ -85,7 +84,7 @@ def load() -> ctypes.CDLL:
         "vsaogm_profile_enable": ([P, ctypes.c_int], ctypes.c_int),
         "vsaogm_profile_read": ([P, P, P], ctypes.c_int),
         "vsaogm_launch_count": ([P], i64),
-        "vsaogm_test_gemm": ([P, P, i32, i32, i32, ctypes.c_int, i32, P, P], ctypes.c_int),
+        "vsaogm_test_gemm": ([P, P, i32, i32, i32, ctypes.c_int, i32, i32, i32, P, P], ctypes.c_int),
         "vsaogm_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "vsaogm_export": ([P, P, ctypes.POINTER(i64)], ctypes.c_int),
         "vsaogm_import": ([P, P, i64, i32], ctypes.c_int),
@@ -94,6 +93,7 @@ def load() -> ctypes.CDLL:
         "vsaogm_entropy_host_async": ([P, ctypes.POINTER(EntropyParams), P, P, ctypes.POINTER(i64)], ctypes.c_int),
         "vsaogm_wait": ([P, i64], ctypes.c_int),
         "vsaogm_set_encode_stream": ([P, P], ctypes.c_int),
+        "vsaogm_set_tuning": ([P, ctypes.c_char_p, i64], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -182,17 +182,23 @@ class Mapper:
         _check(self._lib.vsaogm_encode_bundle_host(self._ctx, _host_ptr(xy), _host_ptr(labels), n),
                "vsaogm_encode_bundle_host")
 
-    def pending(self) -> torch.Tensor:
-        """fp64 [2 delta^2, Dp, 2] CUDA view of the pending memories (for all_reduce, Alg. 3)."""
+    def pending_buffer(self) -> torch.Tensor:
+        """fp64 [2 S Dp + S] CUDA view of the whole pending buffer: memories then the S point
+        counts (integer-valued doubles) -- the one tensor a multi-rank job all-reduces (Alg. 3)."""
         p = ctypes.c_void_p()
         n = ctypes.c_int64()
+        self._s()
         _check(self._lib.vsaogm_pending(self._ctx, ctypes.byref(p), ctypes.byref(n)), "vsaogm_pending")
-        return _wrap_device(p.value, (self.nslots, self.Dp, 2), torch.float64, self.device)
+        assert n.value == 2 * self.nslots * self.Dp + self.nslots
+        return _wrap_device(p.value, (n.value,), torch.float64, self.device)
+
+    def pending(self) -> torch.Tensor:
+        """fp64 [S, Dp, 2] view of the pending memories (S = 2 delta^2 slots)."""
+        return self.pending_buffer()[: 2 * self.nslots * self.Dp].view(self.nslots, self.Dp, 2)
 
     def pending_counts(self) -> torch.Tensor:
-        p = ctypes.c_void_p()
-        _check(self._lib.vsaogm_pending_counts(self._ctx, ctypes.byref(p)), "vsaogm_pending_counts")
-        return _wrap_device(p.value, (self.nslots,), torch.int64, self.device)
+        """fp64 [S] view of the pending point counts (integer-valued)."""
+        return self.pending_buffer()[2 * self.nslots * self.Dp:]
 
     def commit(self):
         self._s()
@@ -275,6 +281,10 @@ class Mapper:
         _check(self._lib.vsaogm_get_memory(self._ctx, _host_ptr(m), _host_ptr(cnt)), "vsaogm_get_memory")
         return m[..., 0] + 1j * m[..., 1], cnt
 
+    def set_tuning(self, key: str, value: int):
+        """Set a tuning variant of this context (vsaogm.h: vsaogm_set_tuning)."""
+        _check(self._lib.vsaogm_set_tuning(self._ctx, key.encode(), int(value)), f"vsaogm_set_tuning({key})")
+
     def set_estimator(self, estimator: int):
         """0: window mean of H_b(p) (default); 1: 8-bit grey-level histogram entropy (decode again after)."""
         _check(self._lib.vsaogm_set_estimator(self._ctx, int(estimator)), "vsaogm_set_estimator")
@@ -320,13 +330,16 @@ class Mapper:
         return int(self._lib.vsaogm_launch_count(self._ctx))
 
 
-def test_gemm(A: torch.Tensor, B: torch.Tensor, precision=F16, kernel: int = -1) -> torch.Tensor:
-    """C = A @ B^T through the decode GEMM kernel (raw epilogue); kernel 0 = CTA pair, 1 = single CTA."""
+def test_gemm(A: torch.Tensor, B: torch.Tensor, precision=F16, kernel: int = -1, bn: int = 0,
+              splits: int = 0) -> torch.Tensor:
+    """C = A @ B^T through the decode GEMM kernel (raw epilogue); kernel 0 = CTA pair, 1 = single CTA;
+    bn / splits pin the CTA-pair tile width / split-K factor (0 = auto)."""
     lib = load()
     M, K = A.shape
     N = B.shape[0]
     C = torch.empty((M, N), dtype=torch.float32, device=A.device)
-    _check(lib.vsaogm_test_gemm(_ptr(A), _ptr(B), M, N, K, int(precision), int(kernel), _ptr(C), _stream_ptr()),
+    _check(lib.vsaogm_test_gemm(_ptr(A), _ptr(B), M, N, K, int(precision), int(kernel), int(bn), int(splits), _ptr(C),
+                                _stream_ptr()),
            "vsaogm_test_gemm")
     return C
 

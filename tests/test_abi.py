@@ -58,7 +58,8 @@ def test_strerror_and_host_validation(lib):
     assert lib.vsaogm_create(16, 0, 0.2, Bounds(0.0, 0.0, 0.0, 10.0), ctypes.byref(ctx)) == EINVAL_ARG
     assert lib.vsaogm_create(16, 0, 0.2, Bounds(0.0, 0.0, float("nan"), 10.0), ctypes.byref(ctx)) == EINVAL_ARG
     assert lib.vsaogm_encode_bundle(None, None, None, 5) == EINVAL_ARG
-    assert lib.vsaogm_test_gemm(None, None, 1, 1, 64, 0, -1, None, None) == EINVAL_ARG
+    assert lib.vsaogm_test_gemm(None, None, 1, 1, 64, 0, -1, 0, 0, None, None) == EINVAL_ARG
+    assert lib.vsaogm_set_tuning(None, b"gemm_bn", 0) == EINVAL_ARG
 
 
 def test_oracle_and_product_share_no_code():

@@ -77,18 +77,17 @@ def test_gemm_vs_torch_fp32(M, N, K, prec, kernel):
 
 @pytest.mark.parametrize("splits", [2, 3, 7])
 @pytest.mark.parametrize("M,N,K", [(300, 500, 1024), (508, 2000, 4096)])
-def test_gemm_split_k(splits, M, N, K, monkeypatch):
+def test_gemm_split_k(splits, M, N, K):
     from paper_2408_09066_b200 import test_gemm
-    monkeypatch.setenv("VSAOGM_GEMM_SPLITS", str(splits))
     g = torch.Generator(device="cuda").manual_seed(splits + M)
     A = torch.randn(M, K, device="cuda", generator=g).half()
     B = torch.randn(N, K, device="cuda", generator=g).half()
-    C = test_gemm(A, B, 0, 0)
+    C = test_gemm(A, B, 0, 0, splits=splits)
     ref = A.float() @ B.float().T
     assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-4
 
 
-def test_decode_band_split_k_matches_unsplit(monkeypatch):
+def test_decode_band_split_k_matches_unsplit():
     """A narrow row band (one rank of 8 at C4 scale) picks split-K automatically; its q and
     labels equal the forced unsplit decode up to fp32 summation order."""
     sc = Scenario("C2")
@@ -99,7 +98,7 @@ def test_decode_band_split_k_matches_unsplit(monkeypatch):
     out = []
     for s in (None, "1"):
         if s:
-            monkeypatch.setenv("VSAOGM_GEMM_SPLITS", s)
+            mp.set_tuning("gemm_splits", int(s))
         q = torch.empty((2, 250, C), dtype=torch.float32, device="cuda")
         mp.decode(0, 0, res, R, C, 750, 1000, h, q_out=q)
         L = torch.empty((250, C), dtype=torch.uint8, device="cuda")
@@ -112,13 +111,12 @@ def test_decode_band_split_k_matches_unsplit(monkeypatch):
 
 
 @pytest.mark.parametrize("bn", [256, 224, 192, 160, 128])
-def test_gemm_pair_tile_widths(bn, monkeypatch):
+def test_gemm_pair_tile_widths(bn):
     from paper_2408_09066_b200 import test_gemm
-    monkeypatch.setenv("VSAOGM_GEMM_BN", str(bn))
     g = torch.Generator(device="cuda").manual_seed(bn)
     A = torch.randn(600, 320, device="cuda", generator=g).half()
     B = torch.randn(1000, 320, device="cuda", generator=g).half()
-    C = test_gemm(A, B, 0, 0)
+    C = test_gemm(A, B, 0, 0, bn=bn)
     ref = A.float() @ B.float().T
     assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-4
 
@@ -470,7 +468,7 @@ def test_entropy_box_register_kernel_bit_identical(h, monkeypatch):
     outs = []
     for env in (None, "1"):
         if env:
-            monkeypatch.setenv("VSAOGM_ENTROPY_SMEM", env)
+            mp.set_tuning("entropy_kernel", 2)
         for (r0, r1) in ((0, R), (21, 58)):
             mp.decode(0, 0, res, R, C, r0, r1, h, q_out=q if (r0, r1) == (0, R) else None)
             S = torch.empty((3, r1 - r0, C), dtype=torch.float32, device="cuda")
@@ -577,7 +575,7 @@ def test_multi_rank_emulated_on_one_gpu():
 
 def test_pipelined_host_steps_match_synchronous():
     """vsaogm_encode_bundle_host_async / vsaogm_entropy_host_async / vsaogm_wait: a pipelined run
-    of several streaming steps (copies on the upload / download streams, two slots each)
+    of several streaming steps (copies on the upload / download streams, three slots each)
     returns, per step, the same labels and S as the synchronous host path."""
     import math
     from paper_2408_09066_b200 import Mapper
@@ -644,9 +642,13 @@ def test_encode_stream_pipeline_matches_serial():
             if pipelined:
                 mp.set_encode_stream(lo)
             for k in range(4):
-                mp.encode_bundle(*dev[k])
+                if k == 2:
+                    mp.encode_bundle_host(*pinned[k])   # library-owned staging buffers
+                else:
+                    mp.encode_bundle(*dev[k])
                 if k == 1:
-                    mp.encode_bundle(*dev[4])      # two encodes before one decode
+                    mp.encode_bundle_host(*pinned[4])   # two encodes before one decode, the second
+                    mp.encode_bundle_host(*pinned[3])   # and third reusing the staging buffers
                 mp.decode(0.0, 0.0, res, R, C, 0, R, h)
                 S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
                 L = torch.empty((R, C), dtype=torch.uint8, device="cuda")

@@ -127,8 +127,8 @@ def test_encode_paths_agree(monkeypatch, delta):
     xy, lab = sc.all_points()
     mems = []
     for knob in ("0", "1", "2"):
-        monkeypatch.setenv("VSAOGM_ENC_PATH", knob)
         mp = Mapper(2048, 0, 0.25, sc.bounds, delta=delta)
+        mp.set_tuning("enc_path", int(knob))
         mp.encode_bundle(*_cuda(xy, lab))
         mems.append(mp.get_memory())
         mp.close()
@@ -150,8 +150,8 @@ def test_encode_packed_variants_agree(monkeypatch, delta):
     xy, lab = sc.all_points()
     mems = []
     for knob in ("0", "1", "2", "3"):
-        monkeypatch.setenv("VSAOGM_ENC_X2", knob)
         mp = Mapper(4096, 3, 0.25, sc.bounds, delta=delta)
+        mp.set_tuning("enc_x2", int(knob))
         mp.encode_bundle(*_cuda(xy, lab))
         mems.append(mp.get_memory())
         mp.close()

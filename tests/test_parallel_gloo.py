@@ -35,9 +35,11 @@ def _worker(rank, world, port, out):
     tx, ty = oracle.theta(0, D)
     lo, hi = point_shard(len(lab), rank, world)
     m, cnt, _ = oracle.encode(tx, ty, l, xy[lo:hi], lab[lo:hi], nthreads=2)
-    pend = torch.from_numpy(np.stack([m.real, m.imag], axis=-1).copy())
-    cnts = torch.from_numpy(cnt.copy())
-    allreduce_pending(pend, cnts)
+    # the library's packed pending layout: memories [2][D][2], then the counts as doubles
+    buf = torch.from_numpy(np.concatenate([np.stack([m.real, m.imag], axis=-1).ravel(), cnt.astype(np.float64)]))
+    allreduce_pending(buf)
+    pend = buf[: 4 * D].view(2, D, 2)
+    cnts = buf[4 * D:].to(torch.int64)
     mfull = pend[..., 0].numpy() + 1j * pend[..., 1].numpy()
     r0, r1 = row_band(R, rank, world)
     ra, rb = decoded_rows(R, r0, r1, h)
