@@ -10,12 +10,17 @@ tensor cores, and compute the 5x5 local-entropy map and labels.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL): points of each batch
-are sharded (contiguous ranges) with one all-reduce of the pending memories
-(Alg. 3), and grid rows are sharded into bands with halo rows; `value` is the
-whole-job throughput (cells of the full grid per second).  --impl reference
-times the fp64 CPU oracle (the only reference that exists for this tier) on a
-bounded sample of the same workload.
+N > 1 runs one process per GPU over NCCL: under torchrun (WORLD_SIZE set) as
+launched, otherwise bench.py re-executes itself under torch.distributed.run
+with N processes (and fails if fewer than N GPUs are visible).  Points of each
+batch are sharded (contiguous ranges) with ONE all-reduce of the library's
+packed pending buffer (memories + counts; Alg. 3), and grid rows are sharded
+into bands with halo rows; `value` is the whole-job throughput (cells of the
+full grid per second).  The line also carries a `c5` object: the largest
+config (C5: 10M points, D = 16384, 4000^2 grid, 7x7) at the same N, and a
+`bf16` object (the bf16-operand decode, reported separately).  --impl
+reference times the fp64 CPU oracle (the only reference that exists for this
+tier) on complete sampled units of the same workload.
 """
 from __future__ import annotations
 
@@ -114,6 +119,28 @@ def dist_env():
     return world, rank, local
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without a torchrun environment: re-execute under torch.distributed.run."""
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} GPU(s) visible", file=sys.stderr)
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def workload_config(sc, n_pts_mean, world):
     cfg = sc.cfg
     return {
@@ -122,7 +149,7 @@ def workload_config(sc, n_pts_mean, world):
         "D": cfg["D"], "length_scale_m": cfg["l"], "grid": f"{cfg['rows']}x{cfg['cols']}@{cfg['res']}m",
         "points_per_step": int(round(n_pts_mean)), "cells_per_step": cfg["rows"] * cfg["cols"],
         "window": f"{2 * cfg['half'] + 1}x{2 * cfg['half'] + 1} box",
-        "decode_operands": "f16 (fp32 accumulate in TMEM)",
+        "decode_operands": "f16 (fp32 accumulate in TMEM); the bf16-operand decode is the `bf16` object",
         "l2": "pipelined value and e2e: inputs larger than L2 (per-step working set: table A 131 MB written + "
               "read, table B 65 MB, H_b 32 MB > 126 MB L2); serial sub-line: flushed between steps (256 MiB write)",
         "parallelism": "single GPU" if world == 1 else f"points sharded x{world} + NCCL all-reduce of memories; "
@@ -146,8 +173,8 @@ def run_native(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2408_09066_b200 import F16, Mapper
-    from paper_2408_09066_b200.parallel import fuse_and_commit, point_shard, row_band
+    from paper_2408_09066_b200 import BF16, F16, Mapper
+    from paper_2408_09066_b200.parallel import decoded_rows, fuse_and_commit, point_shard, row_band
     from synth.lidar import Scenario
 
     world, rank, local = dist_env()
@@ -176,30 +203,29 @@ def run_native(args):
     r0, r1 = row_band(R, rank, world)
     band = r1 - r0
     labels_dev = torch.empty((band, C), dtype=torch.uint8, device=dev)
-    labels_host = torch.empty((band, C), dtype=torch.uint8).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     mp = Mapper(D, 0, l, sc.bounds)
+    ar_ms = []                                   # all-reduce durations (serial loop, world > 1)
 
-    def step(b, host=False):
-        if host:
-            xy, lab = pinned[b % nb]
-            mp.encode_bundle_host(xy, lab)
-        else:
-            xy, lab = dev_batches[b % nb]
-            mp.encode_bundle(xy, lab)
+    def step(b, precision=F16, ar_timer=None):
+        xy, lab = dev_batches[b % nb]
+        mp.encode_bundle(xy, lab)
         if world > 1:
-            fuse_and_commit(mp)
-        mp.decode(0.0, 0.0, res, R, C, r0, r1, h, precision=F16)
-        if host:
-            mp.entropy_host(h, h, tau, -tau, 0, None, labels_host)
-        else:
-            mp.entropy(h, h, tau, -tau, 0, None, labels_dev)
+            fuse_and_commit(mp, timer=ar_timer)
+        mp.decode(0.0, 0.0, res, R, C, r0, r1, h, precision=precision)
+        mp.entropy(h, h, tau, -tau, 0, None, labels_dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
     # warm-up (untimed)
     for b in range(args.warmup):
@@ -208,16 +234,19 @@ def run_native(args):
     if mp.sync() != 0:
         raise RuntimeError("deferred device error during warm-up")
 
-    # Two timed regions of K steps each (barrier + synchronize on both sides, max over ranks),
-    # NVML clocks sampled through both:
+    # Timed regions of K steps each (barrier + synchronize on both sides, max over ranks),
+    # NVML clocks sampled through all of them:
     # (1) serial: one stream, per-step CUDA events, L2 flushed between steps (outside the
-    #     events) -- the per-kernel times, shares and rooflines come from here;
+    #     events) -- the per-kernel times, shares, rooflines and the all-reduce latency come
+    #     from here;
     # (2) pipelined streaming (the headline `value`): vsaogm_set_encode_stream puts the encodes
     #     on a low-priority stream, where the encode of batch k+1 overlaps the GEMM + entropy of
     #     batch k (high-priority stream); CUDA events around the K steps; no flush -- the step's
-    #     working set (tables A 131 MB + B 65 MB, H_b 32 MB) exceeds the 126 MB L2.
+    #     working set (tables A 131 MB + B 65 MB, H_b 32 MB) exceeds the 126 MB L2;
+    # (3) bf16: the serial loop with bf16 decode operands (north_star: reported separately).
     stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ar_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     mp.profile_read()              # clear
     mp.profile_enable(True)
     with ClockSampler(dev.index) as clk:
@@ -225,10 +254,25 @@ def run_native(args):
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
-            step(args.warmup + k)
+            step(args.warmup + k, ar_timer=ar_evs[k] if world > 1 else None)
             evs[k][1].record(stream)
         barrier()
         prof = mp.profile_read()
+
+        # bf16-operand decode, same serial loop (fewer steps)
+        kb = max(3, min(args.steps, 20))
+        bevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kb)]
+        for b in range(2):
+            step(b, precision=BF16)
+        barrier()
+        mp.profile_read()
+        for k in range(kb):
+            flush.zero_()
+            bevs[k][0].record(stream)
+            step(args.warmup + k, precision=BF16)
+            bevs[k][1].record(stream)
+        barrier()
+        prof_bf16 = mp.profile_read()
         mp.profile_enable(False)
 
         hi, lo = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0)
@@ -249,16 +293,18 @@ def run_native(args):
             barrier()
             launches = mp.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    t_ms = torch.tensor([sum(step_ms), p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-    serial_ms_per_step = t_ms[0].item() / args.steps
-    ms_per_step = t_ms[1].item() / args.steps
+    bf16_ms = [a.elapsed_time(b) for a, b in bevs]
+    ar_ms = [a.elapsed_time(b) for a, b in ar_evs] if world > 1 else []
+    serial_total, pipe_total, bf16_total, ar_median = max_over_ranks(
+        [sum(step_ms), p0.elapsed_time(p1), sum(bf16_ms), statistics.median(ar_ms) if ar_ms else 0.0])
+    serial_ms_per_step = serial_total / args.steps
+    ms_per_step = pipe_total / args.steps
+    bf16_ms_per_step = bf16_total / kb
 
-    # end-to-end through the public pipelined host API: every step uploads its batch from pinned
-    # host memory (upload stream), bundles, decodes, and downloads the labels to pinned host
-    # memory (download stream); step k's copies overlap the kernels of steps k-1 / k+1.  Wall
-    # clock over all K steps, including the final wait; max over ranks.
+    # end to end through the public pipelined host API: every step uploads its batch from pinned
+    # host memory, bundles, decodes, and downloads the labels to pinned host memory; step k's
+    # copies overlap the kernels of steps k-1 / k+1.  Wall clock over all K steps, including
+    # the final wait; max over ranks.
     labels_pipe = [torch.empty((band, C), dtype=torch.uint8).pin_memory() for _ in range(3)]
 
     def step_async(b, slot):
@@ -286,17 +332,18 @@ def run_native(args):
         return (t1 - t0) * 1e3, [(b - a) * 1e3 for a, b in zip(marks, marks[1:])]
 
     with torch.cuda.stream(hi):                    # encode stream still set: the same pipeline
-        run_e2e(0, max(3, args.warmup, nb))        # untimed: every distinct batch once (sizes the slots)
+        # untimed: lcm(3 slots, nb batches) steps, so every (slot, batch) pair is visited and
+        # every slot is sized before the timed region (no reallocation inside it)
+        run_e2e(0, max(args.warmup, 3 * nb // math.gcd(3, nb)))
         barrier()
         e2e_total, e2e_steps = run_e2e(args.warmup, args.steps)
-        e2e_t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
         mp.set_encode_stream(None)
     e2e_median = statistics.median(e2e_steps) if e2e_steps else None
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_ms_step = e2e_t.item() / args.steps
+    e2e_ms_step = max_over_ranks([e2e_total])[0] / args.steps
     if mp.sync() != 0:
         raise RuntimeError("deferred device error")
+    mp.close()
+    del dev_batches, flush
 
     cells = R * C
     n_mean = float(np.mean([n_total[(args.warmup + k) % nb] for k in range(args.steps)]))
@@ -304,68 +351,62 @@ def run_native(args):
     pk, pk_kind = peaks()
 
     # per-kernel averages (this rank) and rooflines
-    def avg(name):
-        ms, n = prof[name]
+    def avg(p, name):
+        ms, n = p[name]
         return ms / n if n else float("nan")
-    enc_ms, gemm_ms = avg("encode"), avg("decode_gemm")
+    enc_ms, gemm_ms = avg(prof, "encode"), avg(prof, "decode_gemm")
     shares = {k: round(v[0] / max(1e-12, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
-    # encode (dominant): SFU-bound; algorithmic work = D phasors (1 MUFU sin + 1 MUFU cos) per point
+    # encode (dominant): ALU-bound; algorithmic work = D phasors per point
     my_pts = float(np.mean([len(host_batches[(args.warmup + k) % nb][1]) for k in range(args.steps)]))
     phasors = my_pts * D
     sm_max = pk.get("sm_max_mhz", 1965.0)
-    sfu_peak = 148 * 16 / 2 * sm_max * 1e6          # MUFU-only: 16 MUFU/clk/SM, 2 MUFU per phasor
-    # combined MUFU + FMA-pipe ceiling of the packed encode, per SM per
-    # clock from the guide's unit counts: 16 MUFU, 128 FMA-pipe lanes.  A MUFU phasor costs
-    # 2 MUFU + 5 FMA lanes (angle 2, FMUL.RZ 1, accumulate 2); a polynomial phasor 16 FMA
-    # lanes (angle 2, sincos_fma2_lite 12, accumulate 2).  max m + p s.t. 2m <= 16,
-    # 5m + 16p <= 128 -> m = 8, p = 88/16 (the ALU pipe, 3 ops per polynomial phasor, and the
-    # issue slots, 5 and 11 per phasor, are not binding there).
-    per_clk = 8 + (128 - 5 * 8) / 16
-    alu_peak = 148 * per_clk * sm_max * 1e6
+    enc_roof = encode_ceiling(sm_max)
     enc_rate = phasors / (enc_ms * 1e-3)
     clocks = clk.summary()
     # decode GEMM: 2 M N K flops with M = 2 (band + halo rows), N = C, K = 2 Dp
-    from paper_2408_09066_b200.parallel import decoded_rows
     ra, rb = decoded_rows(R, r0, r1, h)
     Dp = (D + 31) // 32 * 32
     flops = 2.0 * (2 * (rb - ra)) * C * (2 * Dp)
     gemm_tf = flops / (gemm_ms * 1e-3) / 1e12
     traffic = load_ncu_traffic()
-    enc_share = shares.get("encode", 0)
-    dominant = "encode" if enc_share >= shares.get("decode_gemm", 0) else "decode_gemm"
-    if dominant == "encode":
-        roofline = {"kernel": "k_encode_bundle_x2", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
-                    "peak": round(alu_peak / 1e9, 2), "unit": "Gphasor/s", "frac": round(enc_rate / alu_peak, 4),
-                    "traffic": traffic.get("encode"),
-                    "peak_basis": f"combined MUFU+FMA-pipe ceiling {per_clk:.2f} phasors/clk/SM x 148 SM x "
-                                  f"{sm_max:.0f} MHz (guide unit counts: 16 MUFU + 128 FMA lanes/clk/SM; "
-                                  "DESIGN.md sec. 6)",
-                    "mufu_only_peak": round(sfu_peak / 1e9, 2),
-                    "frac_of_mufu_only": round(enc_rate / sfu_peak, 4),
-                    "frac_at_measured_clock": (round(enc_rate / (148 * per_clk * clocks["sm_mhz"] * 1e6), 4)
-                                               if clocks.get("sm_mhz") else None)}
-    else:
-        roofline = None
-    gemm_roof = {"kernel": "k_decode_gemm", "bound": "tensor", "achieved": round(gemm_tf, 1),
-                 "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                 "frac": round(gemm_tf / pk["bf16_tflops_sustained"], 4),
-                 "frac_of_burst": round(gemm_tf / pk["bf16_tflops"], 4), "traffic": traffic.get("decode_gemm"),
-                 "peak_basis": f"MEASURED_PEAKS.json ({pk_kind}) bf16 sustained; fp16 dense = bf16 dense"}
-    if roofline is None:
-        roofline = gemm_roof
+    dominant = "encode" if shares.get("encode", 0) >= shares.get("decode_gemm", 0) else "decode_gemm"
+    # the GEMM is timed per launch (~0.2 ms) inside a short loop, not a seconds-long run:
+    # its denominator is the BURST tensor peak (also reported against sustained)
+    gemm_roof = {"kernel": "k_decode_gemm2", "bound": "tensor", "achieved": round(gemm_tf, 1),
+                 "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(gemm_tf / pk["bf16_tflops"], 4),
+                 "frac_of_sustained": round(gemm_tf / pk["bf16_tflops_sustained"], 4),
+                 "traffic": traffic.get("decode_gemm"),
+                 "peak_basis": f"MEASURED_PEAKS.json ({pk_kind}) bf16 burst (fp16 dense = bf16 dense)"}
+    enc_line = {"kernel": "k_encode_bundle_x2", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
+                "peak": round(enc_roof["combined"] / 1e9, 2), "unit": "Gphasor/s",
+                "frac": round(enc_rate / enc_roof["combined"], 4), "traffic": traffic.get("encode"),
+                "peak_basis": enc_roof["basis"], "mufu_only_peak": round(enc_roof["mufu_only"] / 1e9, 2),
+                "frac_of_mufu_only": round(enc_rate / enc_roof["mufu_only"], 4),
+                "frac_at_measured_clock": (round(enc_rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
+                                           if clocks.get("sm_mhz") else None)}
+    roofline = enc_line if dominant == "encode" else gemm_roof
+    gemm_bf16_ms = avg(prof_bf16, "decode_gemm")
+    gemm_bf16_tf = flops / (gemm_bf16_ms * 1e-3) / 1e12
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (decode MMA operands f16, fp32 accumulate)",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f16 MMA operands, fp32 accumulate (decode); fp32 (encode phases / sincos / sums)",
         "data": "synthetic", "config": workload_config(sc, n_mean, world),
         "points_bundled_per_s": round(n_mean / (ms_per_step * 1e-3), 1),
         "decode_cells_per_s_gemm_only": round(cells / (gemm_ms * 1e-3), 1),
-        "decode_pct_tensor_peak": round(100 * gemm_tf / pk["bf16_tflops_sustained"], 2),
-        "roofline": roofline, "decode_roofline": gemm_roof,
+        "decode_pct_tensor_peak": round(100 * gemm_tf / pk["bf16_tflops"], 2),
+        "roofline": roofline, "decode_roofline": gemm_roof, "encode_roofline": enc_line,
         "schedule": "pipelined: encode of batch k+1 (low-priority stream) overlaps the GEMM + entropy of batch k",
         "serial": {"ms_per_step": round(serial_ms_per_step, 4), "value": round(cells / (serial_ms_per_step * 1e-3), 1),
                    "note": "one stream, L2 flushed between steps; kernel_ms_per_step and the rooflines are from here"},
+        "bf16": {"ms_per_step": round(bf16_ms_per_step, 4), "value": round(cells / (bf16_ms_per_step * 1e-3), 1),
+                 "unit": "cells/s", "steps": kb, "decode_gemm_ms": round(gemm_bf16_ms, 5),
+                 "decode_tflops": round(gemm_bf16_tf, 1), "frac_of_burst": round(gemm_bf16_tf / pk["bf16_tflops"], 4),
+                 "note": "serial loop, bf16 decode operands (fp32 accumulate); parity bound 2e-2 (north_star)"},
+        "allreduce_us": round(1e3 * ar_median, 2) if world > 1 else None,
+        "allreduce_bytes": (2 * 2 * Dp + 2) * 8,
         "kernel_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in prof.items()},
         "kernel_time_share": shares,
         "gpu_launches": int(launches),
@@ -376,67 +417,185 @@ def run_native(args):
                 "h2d_bytes_per_step": int(round(my_pts * 9)),
                 "d2h_bytes_per_step": int(band * C)},
     }
+    if not args.no_c5:
+        line["c5"] = run_c5(args, world, rank, dev, barrier, max_over_ranks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, budget_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    mp.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+def encode_ceiling(sm_mhz):
+    """ALU ceiling of the packed encode, per SM per clock from the guide's
+    unit counts: 16 MUFU, 128 FMA-pipe lanes.  A MUFU phasor costs 2 MUFU + 5 FMA lanes (angle
+    2, FMUL.RZ 1, accumulate 2); a polynomial phasor 16 FMA lanes (angle 2, sincos_fma2_lite 12,
+    accumulate 2).  max m + p s.t. 2m <= 16, 5m + 16p <= 128 -> m = 8, p = 88/16."""
+    per_clk = 8 + (128 - 5 * 8) / 16
+    return {"combined": 148 * per_clk * sm_mhz * 1e6, "mufu_only": 148 * 16 / 2 * sm_mhz * 1e6,
+            "basis": f"combined MUFU+FMA-pipe ceiling {per_clk:.2f} phasors/clk/SM x 148 SM x {sm_mhz:.0f} MHz "
+                     "(guide unit counts: 16 MUFU + 128 FMA lanes/clk/SM; DESIGN.md sec. 6)"}
+
+
+def run_c5(args, world, rank, dev, barrier, max_over_ranks):
+    """The largest config (BASELINE configs[4], C5) at this world size: each rank bundles its
+    contiguous 1/N of the 10M points at D = 16384, ONE all-reduce of the packed pending buffer,
+    commit, decode of its 1/N row band (+3 halo rows) of the 4000 x 4000 grid, 7x7 entropy and
+    labels.  A step rebuilds the map from zero (reset).  Total work is fixed: strong scaling."""
+    import torch
+    from paper_2408_09066_b200 import F16, Mapper
+    from paper_2408_09066_b200.parallel import decoded_rows, fuse_and_commit, point_shard, row_band
+    from synth.lidar import Scenario
+
+    sc = Scenario("C5")
+    cfg = sc.cfg
+    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
+    tau = label_tau(D)
+    xy, lab = sc.all_points()
+    n = len(lab)
+    lo, hi = point_shard(n, rank, world)
+    xy_d = torch.from_numpy(np.ascontiguousarray(xy[lo:hi])).to(dev)
+    lab_d = torch.from_numpy(np.ascontiguousarray(lab[lo:hi])).to(dev)
+    r0, r1 = row_band(R, rank, world)
+    labels = torch.empty((r1 - r0, C), dtype=torch.uint8, device=dev)
+    mp = Mapper(D, 0, l, sc.bounds)
+    stream = torch.cuda.current_stream()
+
+    def step(ar_timer=None):
+        mp.reset()
+        mp.encode_bundle(xy_d, lab_d)
+        if world > 1:
+            fuse_and_commit(mp, timer=ar_timer)
+        mp.decode(0.0, 0.0, res, R, C, r0, r1, h, precision=F16)
+        mp.entropy(h, h, tau, -tau, 0, None, labels)
+
+    step()
+    barrier()
+    if mp.sync() != 0:
+        raise RuntimeError("deferred device error (C5)")
+    K = args.c5_steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ar = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    mp.profile_read()
+    mp.profile_enable(True)
+    barrier()
+    for k in range(K):
+        evs[k][0].record(stream)
+        step(ar[k] if world > 1 else None)
+        evs[k][1].record(stream)
+    barrier()
+    prof = mp.profile_read()
+    mp.profile_enable(False)
+    mp.close()
+    tot = sum(a.elapsed_time(b) for a, b in evs)
+    ar_med = statistics.median([a.elapsed_time(b) for a, b in ar]) if world > 1 else 0.0
+    enc_ms = (prof["encode"][0] + prof["reduce"][0]) / K
+    gemm_ms = prof["decode_gemm"][0] / K
+    tot, ar_med, enc_max, gemm_max = max_over_ranks([tot, ar_med, enc_ms, gemm_ms])
+    ms = tot / K
+    ra, rb = decoded_rows(R, r0, r1, h)
+    Dp = (D + 31) // 32 * 32
+    gemm_tf = 2.0 * (2 * (rb - ra)) * C * (2 * Dp) / (gemm_ms * 1e-3) / 1e12
+    pk, _ = peaks()
+    return {
+        "workload": "C5: 10M labelled points (occupied:free ~ 1:2) bundled at D=16384 (points sharded), one "
+                    "all-reduce, 4000x4000 grid at 0.05 m decoded by row bands (+3 halo rows), 7x7 entropy + labels",
+        "n_points": n, "cells": R * C, "steps": K, "ms_per_step": round(ms, 4),
+        "value": round(R * C / (ms * 1e-3), 1), "unit": "cells/s",
+        "points_bundled_per_s": round(n / (ms * 1e-3), 1),
+        "encode_ms": round(enc_max, 4), "decode_gemm_ms": round(gemm_max, 4),
+        "decode_tflops_rank0": round(gemm_tf, 1), "decode_frac_of_burst_rank0": round(gemm_tf / pk["bf16_tflops"], 4),
+        "allreduce_us": round(1e3 * ar_med, 2) if world > 1 else None,
+        "kernel_ms_per_step_rank0": {k: round(v[0] / K, 5) for k, v in prof.items()},
+        "scaling": "strong", "timing": "CUDA events per step, max over ranks; no L2 flush (per-step working set "
+                                      "> 1 GB: table B 262 MB, table A 66-525 MB, H_b 16-128 MB, partials)",
+    }
+
+
 # ------------------------------------------------------------------ oracle (CPU) timing
-_ORACLE_INPUTS = {}
+_ORACLE = {}
 
 
-def oracle_step_estimate(sc, budget_s, seed=0):
-    """Time the fp64 oracle on a bounded sample of the C4 step and extrapolate
-    linearly to one full step.  Returns (seconds per step, sample description, threads)."""
+def oracle_units(sc, batch_ids, n_centres, seed0=0):
+    """The fp64 oracle on COMPLETE units of the C4 step, measured (no time is extrapolated):
+    for each batch id, the full encode of that batch (all its points), then the full decode
+    (every cell of every window) + entropy + labels of `n_centres` seeded centres with their
+    (2h+1)^2 windows.  Returns a list of (t_encode_s, t_decode_s, n_points, decoded_cells)."""
     import oracle
     cfg = sc.cfg
     D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
     nthreads = oracle.default_threads()
-    if "batch0" not in _ORACLE_INPUTS:
-        _ORACLE_INPUTS["batch0"] = sc.batch(0)
-        _ORACLE_INPUTS["theta"] = oracle.theta(0, D)
-    xy, lab = _ORACLE_INPUTS["batch0"]
-    tx, ty = _ORACLE_INPUTS["theta"]
-    rng = np.random.default_rng(seed)
-    # probe the per-item cost, then size each sample to ~budget/2 seconds
-    t0 = time.perf_counter()
-    oracle.encode(tx, ty, l, xy[:2000], lab[:2000], nthreads=nthreads)
-    per_pt = (time.perf_counter() - t0) / 2000
-    n_enc = int(min(len(lab), max(2000, budget_s / 2 / per_pt)))
-    t0 = time.perf_counter()
-    m, _, _ = oracle.encode(tx, ty, l, xy[:n_enc], lab[:n_enc], nthreads=nthreads)
-    t_enc = time.perf_counter() - t0
-    # decode: sampled cells with their entropy windows ((2h+1)^2 cells each) -> per-cell cost
-    per_cell = per_pt   # same D sincos per item
-    n_win = max(4, int(budget_s / 2 / per_cell / (2 * h + 1) ** 2))
-    cells = rng.integers(h, [R - h, C - h], size=(n_win, 2))
-    t0 = time.perf_counter()
+    if "theta" not in _ORACLE:
+        _ORACLE["theta"] = oracle.theta(0, D)
+    tx, ty = _ORACLE["theta"]
     tau = label_tau(D)
     w = 2 * h + 1
     du, dv = np.meshgrid(np.arange(-h, h + 1), np.arange(-h, h + 1), indexing="ij")
-    rows = (cells[:, 0, None] + du.ravel()[None, :]).ravel()
-    cols = (cells[:, 1, None] + dv.ravel()[None, :]).ravel()
-    q_all = oracle.decode_cells(tx, ty, l, m, 0, 0, res, rows, cols, nthreads=nthreads).reshape(2, n_win, w, w)
-    for e, (r, c) in enumerate(cells):
-        oracle.entropy_cells(R, C, r - h, r + h + 1, c - h, c + h + 1, q_all[:, e], h, h, 0, tau, -tau, [r], [c])
-    t_dec = time.perf_counter() - t0
-    n_dec_cells = n_win * (2 * h + 1) ** 2
-    step_s = t_enc * (len(lab) / n_enc) + t_dec * (R * C / n_dec_cells)
-    sample = (f"oracle on C4 batch 0: encode {n_enc} of {len(lab)} points ({t_enc:.1f} s), decode+entropy "
-              f"of {n_win} cells via their {2 * h + 1}x{2 * h + 1} windows = {n_dec_cells} decoded cells "
-              f"({t_dec:.1f} s); extrapolated linearly to one full step ({len(lab)} points + {R * C} cells)")
-    return step_s, sample, nthreads, len(lab)
+    out = []
+    for i, b in enumerate(batch_ids):
+        key = ("batch", b)
+        if key not in _ORACLE:
+            _ORACLE[key] = sc.batch(b)
+        xy, lab = _ORACLE[key]
+        t0 = time.perf_counter()
+        m, _, _ = oracle.encode(tx, ty, l, xy, lab, nthreads=nthreads)
+        t_enc = time.perf_counter() - t0
+        rng = np.random.default_rng(seed0 + i)
+        cells = rng.integers(h, [R - h, C - h], size=(n_centres, 2))
+        t0 = time.perf_counter()
+        rows = (cells[:, 0, None] + du.ravel()[None, :]).ravel()
+        cols = (cells[:, 1, None] + dv.ravel()[None, :]).ravel()
+        q_all = oracle.decode_cells(tx, ty, l, m, 0, 0, res, rows, cols, nthreads=nthreads).reshape(2, n_centres, w, w)
+        for e, (r, c) in enumerate(cells):
+            oracle.entropy_cells(R, C, r - h, r + h + 1, c - h, c + h + 1, q_all[:, e], h, h, 0, tau, -tau, [r], [c])
+        t_dec = time.perf_counter() - t0
+        out.append((t_enc, t_dec, len(lab), n_centres * w * w))
+    return out, nthreads
+
+
+def oracle_rate(units, cells_per_step):
+    """Whole-step-equivalent rate from measured complete units: the measured encode of a whole
+    batch plus the measured per-decoded-cell cost times the grid's cells (each grid cell is
+    decoded once per step on the GPU)."""
+    t_enc = float(np.mean([u[0] for u in units]))
+    per_cell = sum(u[1] for u in units) / sum(u[3] for u in units)
+    return cells_per_step / (t_enc + per_cell * cells_per_step), t_enc, per_cell
+
+
+def size_centres(sc, budget_s, t_enc_hint=None):
+    """Centres per unit so that one unit (full batch encode + windows) takes ~budget_s here."""
+    import oracle
+    cfg = sc.cfg
+    D, l, h, res = cfg["D"], cfg["l"], cfg["half"], cfg["res"]
+    if "theta" not in _ORACLE:
+        _ORACLE["theta"] = oracle.theta(0, D)
+    tx, ty = _ORACLE["theta"]
+    xy, lab = sc.batch(0)
+    nthreads = oracle.default_threads()
+    t0 = time.perf_counter()
+    m, _, _ = oracle.encode(tx, ty, l, xy[:4000], lab[:4000], nthreads=nthreads)
+    per_pt = (time.perf_counter() - t0) / 4000
+    t0 = time.perf_counter()
+    oracle.decode_cells(tx, ty, l, m, 0, 0, res, np.arange(2000) % 50, np.arange(2000) // 50, nthreads=nthreads)
+    per_cell = (time.perf_counter() - t0) / 2000
+    t_enc = per_pt * len(lab)
+    left = max(0.25 * budget_s, budget_s - t_enc)
+    return int(np.clip(left / (per_cell * (2 * h + 1) ** 2), 200, 10000))
 
 
 def cpu_baseline(sc, budget_s=20.0):
     cfg = sc.cfg
-    step_s, sample, nthreads, _ = oracle_step_estimate(sc, budget_s)
-    return {"value": round(cfg["rows"] * cfg["cols"] / step_s, 1), "unit": "cells/s", "cores": nthreads,
-            "kind": "oracle", "sample": sample}
+    cells = cfg["rows"] * cfg["cols"]
+    n_c = size_centres(sc, budget_s)
+    units, nthreads = oracle_units(sc, [0], n_c)
+    value, t_enc, per_cell = oracle_rate(units, cells)
+    return {"value": round(value, 1), "unit": "cells/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"complete units, measured: full fp64 encode of C4 batch 0 ({units[0][2]} points, "
+                      f"{t_enc:.2f} s) + full decode/entropy/labels of {n_c} seeded centres with their "
+                      f"{2 * cfg['half'] + 1}x{2 * cfg['half'] + 1} windows ({units[0][3]} decoded cells, "
+                      f"{units[0][1]:.2f} s = {per_cell * 1e6:.1f} us/cell); value = cells / (encode + "
+                      f"per-cell cost x {cells} cells), the whole-step-equivalent rate"}
 
 
 def run_reference(args):
@@ -447,22 +606,30 @@ def run_reference(args):
     sc = Scenario(CONFIG)
     cfg = sc.cfg
     cells = cfg["rows"] * cfg["cols"]
-    # the whole --steps K --warmup W run is bounded to ~3 x cpu_seconds of CPU time
-    budget = max(0.3, 3 * args.cpu_seconds / max(1, args.steps + args.warmup))
-    times = []
-    for k in range(args.warmup + args.steps):
-        step_s, sample, nthreads, n_pts = oracle_step_estimate(sc, budget, seed=k)
-        if k >= args.warmup:
-            times.append(step_s)
-    ms = 1e3 * float(np.mean(times))
-    value = cells / (ms * 1e-3)
+    nb = min(N_DISTINCT_BATCHES, args.steps + args.warmup)
+    # the whole --steps K --warmup W run is bounded to ~3 min of host time: one unit per step
+    budget = float(np.clip(180.0 / max(1, args.steps + args.warmup), 1.0, 20.0))
+    n_c = size_centres(sc, budget)
+    oracle_units(sc, [b % nb for b in range(args.warmup)], n_c, seed0=1000)          # warm-up, untimed
+    batch_ids = [(args.warmup + k) % nb for k in range(args.steps)]                 # the GPU arm's batches
+    t0 = time.perf_counter()
+    units, nthreads = oracle_units(sc, batch_ids, n_c)
+    wall = time.perf_counter() - t0
+    value, t_enc, per_cell = oracle_rate(units, cells)
+    n_mean = float(np.mean([u[2] for u in units]))
+    ms = 1e3 * wall / args.steps
+    sample = (f"each step one complete unit, measured: the full fp64 encode of the step's C4 batch (the GPU "
+              f"arm's batch set; mean {n_mean:.0f} points, {t_enc:.2f} s) + the full decode/entropy/labels of "
+              f"{n_c} seeded centres with their windows ({per_cell * 1e6:.1f} us per decoded cell); ms_per_step "
+              f"= measured wall time of those units; value = cells / (encode + per-cell cost x {cells} cells), "
+              f"the whole-step-equivalent rate of the measured units")
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": workload_config(sc, n_pts, 1),
+        "config": workload_config(sc, n_mean, world),
         "cpu_baseline": {"value": round(value, 2), "unit": "cells/s", "cores": nthreads, "kind": "oracle",
-                         "sample": sample + " (each step a bounded sample)"},
+                         "sample": sample},
         "e2e": {"value": round(value, 2), "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -476,9 +643,15 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.impl == "native" and "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} overrides --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     else:

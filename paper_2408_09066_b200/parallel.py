@@ -39,7 +39,13 @@ def allreduce_pending(buf: torch.Tensor, group=None):
     integer-valued doubles; vsaogm.h: vsaogm_pending) over all ranks, in place: ONE
     collective per batch (Alg. 3 fusion)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        if buf.is_cuda and dist.get_backend(group) == "gloo":
+            # gloo (CPU tests, several ranks sharing one GPU): host round trip, same sum
+            host = buf.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+            buf.copy_(host)
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
 
 
 def fuse_and_commit(mapper, group=None, timer=None):

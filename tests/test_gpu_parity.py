@@ -187,137 +187,7 @@ def test_c2_full_grid():
     assert (Lg == Lo).mean() >= 0.999
 
 
-def test_c4_batch_sampled():
-    """C4 at full size (D=8192, 2000x2000 grid, one 100-scan batch) in the bench launch
-    configuration; oracle on sampled cells and their 5x5 neighbourhoods."""
-    sc = Scenario("C4")
-    cfg = sc.cfg
-    xy, lab = sc.batch(0)
-    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
-    tau = label_tau(D)
-    mp = _mapper(D, l, sc.bounds)
-    mp.encode_bundle(*_cuda(xy, lab))
-    q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
-    mp.decode(0.0, 0.0, res, R, C, 0, R, h, q_out=q)
-    L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
-    mp.entropy(h, h, tau, -tau, 0, None, L)
-    assert mp.sync() == 0
-    mg, cg = mp.get_memory()
-    mp.close()
-    qg = q.cpu().numpy()
-    Lg = L.cpu().numpy()
-    tx, ty = oracle.theta(0, D)
-    mo, co, _ = oracle.encode(tx, ty, l, xy, lab)
-    assert list(cg) == list(co)
-    assert _mem_err(mg, mo) <= M_TOL
-    rng = np.random.default_rng(0)
-    # sampled centres (incl. the grid corners / borders) with their full 5x5 windows
-    centres = [(0, 0), (R - 1, C - 1), (0, C - 1), (R - 1, 0)]
-    centres += [tuple(v) for v in rng.integers(0, [R, C], size=(60, 2))]
-    # add cells near the points (where q is large)
-    pts = rng.choice(len(lab), 40, replace=False)
-    centres += [(min(R - 1, max(0, int(xy[i, 1] / res))), min(C - 1, max(0, int(xy[i, 0] / res)))) for i in pts]
-    q_peak = np.abs(qg).reshape(2, -1).max(axis=1)
-    errs, agree = [], []
-    for (r, c) in centres:
-        ra, rb, ca, cb = max(0, r - h), min(R, r + h + 1), max(0, c - h), min(C, c + h + 1)
-        qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, ra, rb, ca, cb)
-        errs.append(max(np.abs(qg[k, ra:rb, ca:cb] - qo[k]).max() / q_peak[k] for k in (0, 1)))
-        _, lo = oracle.entropy_cells(R, C, ra, rb, ca, cb, qo, h, h, 0, tau, -tau, [r], [c])
-        agree.append(lo[0] == Lg[r, c])
-    assert max(errs) <= Q_TOL[0], max(errs)
-    assert np.mean(agree) >= 0.99   # sampled: few cells, one disagreement allowed
-
-
-def _sampled_windows(mp_q, mp_L, mo, tx, ty, l, res, R, C, h, tau, centres, row_off=0):
-    """Oracle q on each centre's (2h+1)^2 window and its label; returns (max peak-normalised
-    q error, label agreement).  mp_q, mp_L are the GPU band arrays starting at full-grid row row_off."""
-    q_peak = np.abs(mp_q).reshape(2, -1).max(axis=1)
-    errs, agree = [], []
-    for (r, c) in centres:
-        ra, rb, ca, cb = max(0, r - h), min(R, r + h + 1), max(0, c - h), min(C, c + h + 1)
-        qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, ra, rb, ca, cb)
-        ga, gb = max(ra, row_off), min(rb, row_off + mp_q.shape[1])
-        if gb > ga:
-            errs.append(max(np.abs(mp_q[k, ga - row_off:gb - row_off, ca:cb] - qo[k, ga - ra:gb - ra]).max()
-                            / q_peak[k] for k in (0, 1)))
-        if row_off <= r < row_off + mp_L.shape[0]:
-            _, lo = oracle.entropy_cells(R, C, ra, rb, ca, cb, qo, h, h, 0, tau, -tau, [r], [c])
-            agree.append(lo[0] == mp_L[r - row_off, c])
-    return max(errs), float(np.mean(agree))
-
-
-def test_c3_sampled_fp16_and_bf16():
-    """C3 (2.04M points, D=4096, 1000x1000 grid): full GPU decode in fp16 and bf16 operands,
-    oracle on sampled cells; BASELINE C3 asks for the fp16-vs-bf16 comparison."""
-    sc = Scenario("C3")
-    cfg = sc.cfg
-    xy, lab = sc.all_points()
-    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
-    tau = label_tau(D)
-    mp = _mapper(D, l, sc.bounds)
-    mp.encode_bundle(*_cuda(xy, lab))
-    out = {}
-    for prec in (0, 1):
-        q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
-        mp.decode(0.0, 0.0, res, R, C, 0, R, h, precision=prec, q_out=q)
-        L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
-        mp.entropy(h, h, tau, -tau, 0, None, L)
-        assert mp.sync() == 0
-        out[prec] = (q.cpu().numpy(), L.cpu().numpy())
-    mg, cg = mp.get_memory()
-    mp.close()
-    tx, ty = oracle.theta(0, D)
-    mo, co, _ = oracle.encode(tx, ty, l, xy, lab)
-    assert list(cg) == list(co)
-    assert _mem_err(mg, mo) <= M_TOL
-    rng = np.random.default_rng(3)
-    centres = [(0, 0), (R - 1, C - 1)] + [tuple(v) for v in rng.integers(0, [R, C], size=(40, 2))]
-    pts = rng.choice(len(lab), 40, replace=False)
-    centres += [(min(R - 1, int(xy[i, 1] / res)), min(C - 1, int(xy[i, 0] / res))) for i in pts]
-    e16, a16 = _sampled_windows(*out[0], mo, tx, ty, l, res, R, C, h, tau, centres)
-    ebf, _ = _sampled_windows(*out[1], mo, tx, ty, l, res, R, C, h, tau, centres)
-    assert e16 <= Q_TOL[0], e16
-    assert ebf <= Q_TOL[1], ebf
-    assert a16 >= 0.98
-    # fp16 and bf16 decodes agree on labels almost everywhere (reported separately in DESIGN.md)
-    assert (out[0][1] == out[1][1]).mean() >= 0.99
-
-
-def test_c5_band_sampled():
-    """C5 scale on one GPU: D=16384, 4000x4000 grid @ 0.05 m, row band 0 of 8 with a 7x7
-    window (halo 3), points = the first 150 scans of the C5 world; oracle on sampled cells
-    incl. the band's interior boundary rows."""
-    from paper_2408_09066_b200.parallel import row_band
-    sc = Scenario("C5")
-    cfg = sc.cfg
-    xy, lab = sc.scans(0, 150)
-    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], cfg["cols"], cfg["res"]
-    tau = label_tau(D)
-    r0, r1 = row_band(R, 3, 8)
-    mp = _mapper(D, l, sc.bounds)
-    mp.encode_bundle(*_cuda(xy, lab))
-    q = torch.empty((2, r1 - r0, C), dtype=torch.float32, device="cuda")
-    mp.decode(0.0, 0.0, res, R, C, r0, r1, h, q_out=q)
-    L = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
-    mp.entropy(h, h, tau, -tau, 0, None, L)
-    assert mp.sync() == 0
-    mg, cg = mp.get_memory()
-    mp.close()
-    tx, ty = oracle.theta(0, D)
-    mo, co, _ = oracle.encode(tx, ty, l, xy, lab)
-    assert list(cg) == list(co)
-    assert _mem_err(mg, mo) <= M_TOL
-    rng = np.random.default_rng(5)
-    centres = [(r0, 0), (r0, C - 1), (r1 - 1, 7), (r1 - 1, C - 1), (r0 + 1, 100), (r1 - 2, 200)]
-    centres += [(int(a), int(b)) for a, b in zip(rng.integers(r0, r1, 40), rng.integers(0, C, 40))]
-    inband = [i for i in range(len(lab)) if r0 * res <= xy[i, 1] < r1 * res]
-    for i in rng.choice(inband, min(30, len(inband)), replace=False):
-        centres.append((int(xy[i, 1] / res), min(C - 1, int(xy[i, 0] / res))))
-    err, agree = _sampled_windows(q.cpu().numpy(), L.cpu().numpy(), mo, tx, ty, l, res, R, C, h, tau, centres,
-                                  row_off=r0)
-    assert err <= Q_TOL[0], err
-    assert agree >= 0.98
+# C3 / C4 (streamed, bench schedule) / C5 at full size: tests/test_gpu_parity_large.py
 
 
 def test_nccl_fuse_and_commit_single_rank():
