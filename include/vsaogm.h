@@ -172,12 +172,14 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
 
 /* Tuning variants (measurement and test hook; the defaults are the measured best and no
  * environment variable changes them).  Sets the integer knob `key` of this context for
- * later calls: "enc_x2" (encode kernel family), "enc_x2_npoly", "enc_x2_minb",
+ * later calls: "enc_x2" (encode kernel family; 4 = the pair kernel, the default),
+ * "enc_pairs_npoly", "enc_pairs_minb", "enc_x2_npoly", "enc_x2_minb",
  * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
  * CTA pair, 1 single CTA), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,
  * else the split-K factor), "pipe_early" (0/1), "entropy_kernel"
- * (0 auto).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
+ * (0 auto, 1 the generic staged kernel), "entropy_rw" (0 auto, else output rows per
+ * work item of the streamed entropy kernel).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
 int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);
 
 /* Local entropy (Alg. 2), global entropy S = S_occ - S_emp, 3-way labels

@@ -556,8 +556,10 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
         int *field;
         int lo, hi;
     } knobs[] = {
-        {"enc_x2", &c->enc_x2, 0, 3},
+        {"enc_x2", &c->enc_x2, 0, 4},
         {"enc_x2_npoly", &c->enc_x2_npoly, 0, 8},
+        {"enc_pairs_npoly", &c->enc_pairs_npoly, 0, 8},
+        {"enc_pairs_minb", &c->enc_pairs_minb, 3, 4},
         {"enc_x2_minb", &c->enc_x2_minb, 3, 4},
         {"enc_x2_waves", &c->enc_x2_waves, 1, 64},
         {"enc_npoly", &c->enc_npoly, 0, 4},
@@ -570,7 +572,8 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
         {"gemm_bn", &c->gemm_bn, 0, 256},
         {"gemm_splits", &c->gemm_splits, 0, 64},
         {"pipe_early", &c->pipe_early, 0, 1},
-        {"entropy_kernel", &c->entropy_kernel, 0, 3},
+        {"entropy_kernel", &c->entropy_kernel, 0, 1},
+        {"entropy_rw", &c->entropy_rw, 0, 1 << 20},
     };
     for (const Knob &k : knobs)
         if (strcmp(k.name, key) == 0) {

@@ -84,7 +84,10 @@ struct vsaogm_ctx {
     // 1 uniform 4-warp blocks, 2 all-MUFU warps beside enc_x2_npoly-polynomial warps (default,
     // measured fastest in the pipelined schedule: (0 | 4), 4 blocks/SM), 3 one-polynomial warps
     // beside enc_x2_npoly-polynomial warps
-    int enc_x2 = 2;
+    // 4: the pair (half-angle) kernel k_encode_pairs, all-MUFU warps beside enc_x2_npoly-FMA warps
+    int enc_x2 = 4;
+    int enc_pairs_npoly = 4;  // FMA-pipe dimensions of 8 in the pair kernel's second warp role
+    int enc_pairs_minb = 3;   // resident pair-kernel blocks per SM (3: 80 registers, no spills)
     int enc_x2_npoly = 4;   // polynomial dimensions of 8 in the second warp role
     int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
     int enc_x2_minb = 4;    // resident 8-warp blocks per SM (4: 64 registers, the default; 3: 80)
@@ -94,7 +97,8 @@ struct vsaogm_ctx {
     int gemm_bn = 0;        // 0 auto, else the CTA-pair tile width (128..256, multiple of 32)
     int gemm_splits = 0;    // 0 auto, else the split-K factor
     int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
-    int entropy_kernel = 0; // 0 auto; 1 generic kernel; 2 staged fixed-radius kernel
+    int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
+    int entropy_rw = 0;     // 0 auto, else output rows per streamed work item (test hook)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta
@@ -192,6 +196,10 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
                  cudaStream_t s, int num_sms, int variant, int bn = 0, int splits = 0);
 // staged host-encode / I/O helpers: comments in api.cu
+
+// cuTensorMapEncodeTiled from the driver (gemm_tc.cu), nullptr if unavailable
+#include <cudaTypedefs.h>
+PFN_cuTensorMapEncodeTiled_v12000 vsa_tmap_encode_fn();
 
 // ---- PTX helpers (sm_100a) ---------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -475,6 +483,130 @@ struct PhasorAcc {
         upk2(re[j >> 1], a, b);
         upk2(im[j >> 1], c, d);
         return (j & 1) ? make_float2(b, d) : make_float2(a, c);
+    }
+};
+
+// Packed cos only, same reduction and cos polynomial as sincos_fma2_lite: 8 packed FMA-pipe
+// instructions plus the sign xors, for the half-difference factor of the pair encode.
+__device__ __forceinline__ f32x2 cos_fma2_lite(f32x2 phi)
+{
+    const float magic = 12582912.f;
+    const f32x2 tq = fma2(phi, bc2(0.318309886183790672f), bc2(magic));
+    const f32x2 q = add2(tq, bc2(-magic));
+    const f32x2 r = fma2(q, bc2(-3.14159274101257324f), phi);
+    const f32x2 r2 = mul2(r, r);
+    f32x2 c = fma2(r2, bc2(2.319438317e-05f), bc2(-1.385592739e-03f));
+    c = fma2(c, r2, bc2(4.166398942e-02f));
+    c = fma2(c, r2, bc2(-4.999993145e-01f));
+    c = fma2(c, r2, bc2(1.0f));
+    float ta, tb, ca, cb;
+    upk2(tq, ta, tb);
+    upk2(c, ca, cb);
+    return pk2(__int_as_float(__float_as_int(ca) ^ (__float_as_int(ta) << 31)),
+               __int_as_float(__float_as_int(cb) ^ (__float_as_int(tb) << 31)));
+}
+
+// Block barrier without .aligned (PTX barrier.sync): legal when the warps of a block reach it
+// from different (warp-uniform) code paths, e.g. the role-templated loops of the encode.
+__device__ __forceinline__ void block_sync_any() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
+// Pair accumulators of the half-angle encode: two points a, b of one
+// class contribute
+//     e^{i phi_a} + e^{i phi_b} = 2 cos(delta) e^{i sigma},
+//     sigma = w^x xbar + w^y ybar,  delta = w^x dx + w^y dy,
+//     xbar = (x_a + x_b) / 2,  dx = (x_a - x_b) / 2  (same for y),
+// i.e. three sin/cos evaluations per two phasors instead of four.  A thread holds KT
+// dimensions as KT/2 packed pairs; re/im accumulate cos(delta) (cos sigma, sin sigma), i.e.
+// HALF the sum (the factor 2 is applied once, exactly, when the partials are stored).  The
+// last NPOLY dimensions evaluate all three on the FMA pipe (sincos_fma2_lite, cos_fma2_lite),
+// the others on MUFU.  A single leftover point adds (1/2) e^{i phi}.
+// The thread's KT phase rates (w^x, w^y) as KT/2 packed pairs, shared by its accumulators.
+template <int KT>
+struct PairW {
+    f32x2 wx[KT / 2], wy[KT / 2];
+    __device__ __forceinline__ void init(const float *fx, const float *fy)
+    {
+#pragma unroll
+        for (int q = 0; q < KT / 2; ++q) {
+            wx[q] = pk2(fx[2 * q], fx[2 * q + 1]);
+            wy[q] = pk2(fy[2 * q], fy[2 * q + 1]);
+        }
+    }
+};
+
+template <int KT, int NPOLY>
+struct PairAcc {
+    static_assert(KT % 2 == 0, "dimension pairs");
+    static constexpr int NP = KT / 2;
+    f32x2 re[NP], im[NP];
+
+    __device__ __forceinline__ void init()
+    {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) re[q] = im[q] = pk2(0.f, 0.f);
+    }
+
+    // P = (xbar, ybar, dx, dy), centred metres
+    __device__ __forceinline__ void pair(const PairW<KT> &w, float4 P)
+    {
+        const f32x2 X = bc2(P.x), Y = bc2(P.y), DX = bc2(P.z), DY = bc2(P.w);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const f32x2 sg = fma2(w.wx[q], X, mul2(w.wy[q], Y));    // sigma per lane
+            const f32x2 dl = fma2(w.wx[q], DX, mul2(w.wy[q], DY));  // delta per lane
+            const int j0 = 2 * q;
+            if (j0 + 1 < KT - NPOLY) {                            // both on MUFU
+                float sa, sb, da, db, ssa, csa, ssb, csb;
+                upk2(sg, sa, sb);
+                upk2(dl, da, db);
+                __sincosf(sa, &ssa, &csa);
+                __sincosf(sb, &ssb, &csb);
+                const f32x2 cd = pk2(__cosf(da), __cosf(db));
+                re[q] = fma2(cd, pk2(csa, csb), re[q]);
+                im[q] = fma2(cd, pk2(ssa, ssb), im[q]);
+            } else if (j0 >= KT - NPOLY) {                        // both on the FMA pipe
+                f32x2 S, C;
+                sincos_fma2_lite(sg, S, C);
+                const f32x2 cd = cos_fma2_lite(dl);
+                re[q] = fma2(cd, C, re[q]);
+                im[q] = fma2(cd, S, im[q]);
+            } else {                                              // MUFU, FMA pipe
+                float sa, sb, da, db, ssa, csa, ssb, csb;
+                upk2(sg, sa, sb);
+                upk2(dl, da, db);
+                __sincosf(sa, &ssa, &csa);
+                sincos_fma(sb, &ssb, &csb);
+                float sdb, cdb;
+                sincos_fma(db, &sdb, &cdb);
+                const f32x2 cd = pk2(__cosf(da), cdb);
+                re[q] = fma2(cd, pk2(csa, csb), re[q]);
+                im[q] = fma2(cd, pk2(ssa, ssb), im[q]);
+            }
+        }
+    }
+
+    // a single (leftover) point: + (1/2) e^{i phi}, MUFU
+    __device__ __forceinline__ void single(const PairW<KT> &w, float x, float y)
+    {
+        const f32x2 X = bc2(x), Y = bc2(y), H = bc2(0.5f);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            float pa, pb, sa, ca, sb, cb;
+            upk2(fma2(w.wx[q], X, mul2(w.wy[q], Y)), pa, pb);
+            __sincosf(pa, &sa, &ca);
+            __sincosf(pb, &sb, &cb);
+            re[q] = fma2(H, pk2(ca, cb), re[q]);
+            im[q] = fma2(H, pk2(sa, sb), im[q]);
+        }
+    }
+
+    // the dimension's full sum (2 x the half sum; exact scaling)
+    __device__ __forceinline__ float2 get(int j) const
+    {
+        float a, b, c, d;
+        upk2(re[j >> 1], a, b);
+        upk2(im[j >> 1], c, d);
+        return (j & 1) ? make_float2(2.f * b, 2.f * d) : make_float2(2.f * a, 2.f * c);
     }
 };
 

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_bundle_x2(
         acc1.init(fx, fy);
         for (int64_t base = p0; base < p1; base += TILE) {
             const int cnt = (int)min((int64_t)TILE, p1 - base);
-            __syncthreads();
+            block_sync_any();
             float2 rec[ROUNDS];
             int code_r[ROUNDS];
             unsigned b0[ROUNDS], b1[ROUNDS];
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_bundle_x2(
                     s_g1[r * NW + warp] = __popc(b1[r]);
                 }
             }
-            __syncthreads();
+            block_sync_any();
             int n0 = 0, n1 = 0, o0[ROUNDS], o1[ROUNDS];
 #pragma unroll
             for (int g = 0; g < ROUNDS * NW; ++g) {
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_bundle_x2(
             }
             c0 += n0;
             c1 += n1;
-            __syncthreads();
+            block_sync_any();
 #pragma unroll 2
             for (int p = 0; p < n0; ++p) {
                 const float2 P = s_p0[p];   // warp-uniform broadcast
@@ -275,6 +275,124 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_bundle_x2(
     };
     if (role_b) run(PhasorAcc<KT, NPB>{}, PhasorAcc<KT, NPB>{});
     else run(PhasorAcc<KT, NPA>{}, PhasorAcc<KT, NPA>{});
+    if (kb == 0) {
+        if (my_err) atomicOr(err, my_err);
+        if (tid == 0) {
+            part_cnt[chunk * 2 + 0] = c0;
+            part_cnt[chunk * 2 + 1] = c1;
+        }
+    }
+}
+
+// Pair (half-angle) variant of K2, the default for delta = 1 and D >= 2048: the label-split
+// staging of k_encode_bundle_x2, with the coordinates kept centred in fp64 in shared memory;
+// consecutive points of one class in the tile form pairs whose mean and half-difference
+// (xbar, ybar, dx, dy) are computed in fp64 and rounded once to fp32; the bundle loop then
+// adds 2 cos(delta) e^{i sigma} per pair (PairAcc, common.cuh): 1.5 MUFU ops per phasor
+// instead of 2.  An odd last point of a class in a tile is added on its own.  Warp roles as in
+// k_encode_bundle_x2 (warps 0-3: NPA, warps 4-7: NPB of 8 dimensions on the FMA pipe).  Every
+// block barrier is the non-.aligned barrier.sync, reached from both roles' code.
+template <int THREADS, int NPA, int NPB, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs(
+    const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
+    const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
+    float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
+{
+    constexpr int KT = 8;
+    constexpr int NW = THREADS / 32;
+    constexpr int TILE = THREADS;
+    __shared__ double2 s_p[2][TILE];          // the tile's centred points, split by class, in order
+    __shared__ float4 s_q[2][TILE / 2];       // pair records (xbar, ybar, dx, dy)
+    __shared__ int s_g0[NW], s_g1[NW];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const bool role_b = warp >= NW / 2;   // warp-uniform
+    const int kb = blockIdx.x;
+    const int64_t chunk = blockIdx.y;
+    const int kbase = kb * THREADS * KT + tid;
+
+    float fx[KT], fy[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * THREADS;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+    }
+    long long c0 = 0, c1 = 0;
+    int my_err = 0;
+    const int64_t p0 = chunk * chunk_pts;
+    const int64_t p1 = min(n, p0 + chunk_pts);
+
+    PairW<KT> w;
+    w.init(fx, fy);
+    auto run = [&](auto acc0, auto acc1) {
+        acc0.init();
+        acc1.init();
+        for (int64_t base = p0; base < p1; base += TILE) {
+            const int cnt = (int)min((int64_t)TILE, p1 - base);
+            block_sync_any();
+            int code = 2;
+            double2 rec = make_double2(0.0, 0.0);
+            if (tid < cnt) {
+                const float2 v = xy[base + tid];
+                const int L = lab[base + tid];
+                code = L;
+                if (L > 1) { code = 2; my_err |= VSA_ERRBIT_LABEL; }
+                if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
+                rec = make_double2((double)v.x - cx, (double)v.y - cy);
+            }
+            const unsigned b0 = __ballot_sync(0xffffffffu, code == 0);
+            const unsigned b1 = __ballot_sync(0xffffffffu, code == 1);
+            if (lane == 0) {
+                s_g0[warp] = __popc(b0);
+                s_g1[warp] = __popc(b1);
+            }
+            block_sync_any();
+            int n0 = 0, n1 = 0, o0 = 0, o1 = 0;
+#pragma unroll
+            for (int g = 0; g < NW; ++g) {
+                if (g == warp) { o0 = n0; o1 = n1; }
+                n0 += s_g0[g];
+                n1 += s_g1[g];
+            }
+            const unsigned lt = (1u << lane) - 1u;
+            if (code == 0) s_p[0][o0 + __popc(b0 & lt)] = rec;
+            else if (code == 1) s_p[1][o1 + __popc(b1 & lt)] = rec;
+            c0 += n0;
+            c1 += n1;
+            block_sync_any();
+            const int np0 = n0 >> 1, np1 = n1 >> 1;
+            if (tid < np0 + np1) {                            // pair records, fp64 then one rounding
+                const int cls = tid >= np0, i = cls ? tid - np0 : tid;
+                const double2 a = s_p[cls][2 * i], b = s_p[cls][2 * i + 1];
+                s_q[cls][i] = make_float4((float)(0.5 * (a.x + b.x)), (float)(0.5 * (a.y + b.y)),
+                                          (float)(0.5 * (a.x - b.x)), (float)(0.5 * (a.y - b.y)));
+            }
+            block_sync_any();
+#pragma unroll 1
+            for (int p = 0; p < np0; ++p) acc0.pair(w, s_q[0][p]);   // warp-uniform broadcasts
+            if (n0 & 1) {
+                const double2 a = s_p[0][n0 - 1];
+                acc0.single(w, (float)a.x, (float)a.y);
+            }
+#pragma unroll 1
+            for (int p = 0; p < np1; ++p) acc1.pair(w, s_q[1][p]);
+            if (n1 & 1) {
+                const double2 a = s_p[1][n1 - 1];
+                acc1.single(w, (float)a.x, (float)a.y);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int k = kbase + j * THREADS;
+            if (k < Dp) {
+                part[((size_t)chunk * 2 + 0) * Dp + k] = acc0.get(j);
+                part[((size_t)chunk * 2 + 1) * Dp + k] = acc1.get(j);
+            }
+        }
+    };
+    if (role_b) run(PairAcc<KT, NPB>{}, PairAcc<KT, NPB>{});
+    else run(PairAcc<KT, NPA>{}, PairAcc<KT, NPA>{});
     if (kb == 0) {
         if (my_err) atomicOr(err, my_err);
         if (tid == 0) {
@@ -562,7 +680,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     const int kblocks = (c->Dp + x2_threads * KT - 1) / (x2_threads * KT);
     // one full wave at ~6 resident blocks per SM (3 for the 256-thread variants), at least 64
     // points per chunk; 7 or 8 resident blocks as tuning variants of the scalar kernel
-    const int minb = x2 ? (x2_threads == 256 ? (c->enc_x2_minb == 4 ? 4 : 3) : 6)
+    const int minb = x2 ? (x2_threads == 256 ? (c->enc_x2 == 4 ? c->enc_pairs_minb : (c->enc_x2_minb == 4 ? 4 : 3)) : 6)
                      : KT == 16 ? 4
                      : (!slots_path && KT == 8 && (c->enc_npoly == 1 || c->enc_npoly == 2) &&
                         (c->enc_minb == 7 || c->enc_minb == 8))
@@ -629,7 +747,20 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     k_encode_bundle<KT_, NP_, ##__VA_ARGS__><<<grid, ENC_THREADS, 0, c->stream>>>(                                \
         (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
         c->d_err)
-    if (x2 && c->enc_x2 == 1) {   // uniform roles, 4 warps
+#define VSA_ENC_PAIRS(NPB_, MB_)                                                                                   \
+    k_encode_pairs<256, 0, NPB_, MB_><<<grid, 256, 0, c->stream>>>(                                               \
+        (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
+        c->d_err)
+    if (x2 && c->enc_x2 == 4) {   // pairs (half-angle): all-MUFU warps beside NPOLY-FMA-pipe warps
+        const bool mb4 = c->enc_pairs_minb == 4;
+        switch (c->enc_pairs_npoly) {
+        case 0: if (mb4) VSA_ENC_PAIRS(0, 4); else VSA_ENC_PAIRS(0, 3); break;
+        case 2: if (mb4) VSA_ENC_PAIRS(2, 4); else VSA_ENC_PAIRS(2, 3); break;
+        case 6: if (mb4) VSA_ENC_PAIRS(6, 4); else VSA_ENC_PAIRS(6, 3); break;
+        case 8: if (mb4) VSA_ENC_PAIRS(8, 4); else VSA_ENC_PAIRS(8, 3); break;
+        default: if (mb4) VSA_ENC_PAIRS(4, 4); else VSA_ENC_PAIRS(4, 3); break;
+        }
+    } else if (x2 && c->enc_x2 == 1) {   // uniform roles, 4 warps
         switch (c->enc_x2_npoly) {
         case 1: VSA_ENC_X2(128, 1, 1, 6); break;
         case 3: VSA_ENC_X2(128, 3, 3, 6); break;
@@ -686,6 +817,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     }
 #undef VSA_ENC_LAUNCH
 #undef VSA_ENC_X2
+#undef VSA_ENC_PAIRS
     }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENCODE, ev);

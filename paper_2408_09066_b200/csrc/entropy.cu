@@ -12,10 +12,10 @@
 // grid columns reads as zero, which is exactly the border clipping of the
 // window sums (L13); clipped counts are closed-form.  A box window
 // forms row sums of width 2h+1 then sums 2h+1 of them down the column; a disk
-// sums each footprint row segment directly.  Kernels: k_entropy_box4 (box,
-// h <= 4, register rings, no shared memory), k_entropy_fixed (equal radii
-// h <= 8, cp.async-staged tile), k_entropy (any radii).
-// HBM-bound: 8 B read + 1 B written per cell.
+// sums each footprint row segment directly.  Kernels: k_entropy_stream (box,
+// equal radii h <= 4: the BASELINE windows; TMA-streamed warps, register
+// rings), k_entropy (any radii / disks, cp.async-staged tile), k_entropy_hist
+// (the histogram estimator).  HBM-bound: 8 B read + 1 B written per cell.
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -35,255 +35,181 @@ __device__ __forceinline__ int isqrt_floor(int t)
     return w;
 }
 
-__host__ __device__ constexpr int cisqrt(int t, int w = 0) { return (w + 1) * (w + 1) <= t ? cisqrt(t, w + 1) : w; }
 
-// Equal radii h1 = h0 = H <= 8 (every BASELINE config): H and the footprint
-// are compile-time, the tile is staged with 16-byte cp.async (zero-filled
-// outside the decoded rows / grid columns), and each thread keeps the row
-// sums of its 16 output rows (+2H) in registers: no second shared buffer,
-// no barrier between the two passes.
-template <int H, bool DISK>
-__global__ void __launch_bounds__(ENT_THREADS) k_entropy_fixed(const float *__restrict__ hb, int ldh, int r_ext,
-                                                               int R, int C, int r_lo, int r0, int band_rows,
-                                                               float rho_occ, float rho_emp, float *__restrict__ S,
-                                                               uint8_t *__restrict__ lab)
+// Box window, equal radii h1 = h0 = H <= 4 (every BASELINE config: 3x3 / 5x5 / 7x7), the
+// HBM-bound hot kernel.  Persistent warps, each streaming a work item = one 128-column strip x
+// `rw` output rows of the band from top to bottom:
+//   * lane 0 keeps a private ring of ST_NST TMA stages in flight (cp.async.bulk.tensor.3d, box
+//     136 columns x ST_RS rows x both classes, 4 halo columns on each side; the tensor map's
+//     bounds are the decoded rows x grid columns, so the TMA zero-fill IS the window clipping of
+//     DESIGN.md L13) on per-stage mbarriers -- no block barriers, every warp independent;
+//   * each lane owns 4 adjacent columns: per staged row and class it reads its own float4,
+//     gets the H neighbour columns on each side by warp shuffles (the strip's edge lanes read
+//     the staged halo), forms the 4 horizontal (2H+1)-sums and keeps the last 2H+1 of them in a
+//     register ring; each output row is the in-order sum of its ring (the additions and their
+//     order of the generic kernel, so the result is bit-identical to it);
+//   * labels leave as one 4-byte store per lane (128 B per warp row), S as float4s.
+// Each staged row is read from shared memory once per class (16 B per lane); halo rows of
+// neighbouring items are re-read from L2, not DRAM (items run concurrently).
+constexpr int ST_RS = 4;                          // staged rows per TMA stage
+constexpr int ST_NST = 4;                         // stages per warp ring
+constexpr int ST_W = 136;                         // staged floats per row (4 + 128 + 4)
+constexpr int ST_WARPS = 4;                       // warps per block
+constexpr int ST_BLOCKS_PER_SM = 2;
+constexpr int ST_STAGE_FLOATS = 2 * ST_RS * ST_W; // [class][row][col]
+constexpr int ST_STAGE_BYTES = ST_STAGE_FLOATS * 4;
+constexpr size_t ST_SMEM = (size_t)ST_WARPS * ST_NST * ST_STAGE_BYTES;
+
+struct StreamArgs {
+    int R, C, r_lo;            // full grid; first decoded row (tensor-map row 0)
+    int r0, band_rows;         // band: full-grid rows [r0, r0 + band_rows)
+    int strips, chunks, rw;    // work items = strips x chunks of rw output rows
+    float rho_occ, rho_emp;
+    float *S;
+    uint8_t *lab;
+};
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2)
 {
-    constexpr int PADC = (H + 3) / 4 * 4;          // column halo rounded to 16 bytes
-    constexpr int TW = TC + 2 * PADC;              // floats per staged row
-    constexpr int TH = TR + 2 * H;
-    constexpr int CH = TW / 4;                     // 16-byte chunks per staged row
-    constexpr int RPT = TR / 2;                    // output rows per thread
-    extern __shared__ float4 sm4[];
-    float *tile = reinterpret_cast<float *>(sm4);  // [2][TH][TW]
-    const int orow0 = r0 + blockIdx.y * TR;
-    const int ocol0 = blockIdx.x * TC;
-
-    for (int idx = threadIdx.x; idx < 2 * TH * CH; idx += ENT_THREADS) {
-        const int cr = idx / CH, j = idx - cr * CH;
-        const int cls = cr >= TH, row = cr - cls * TH;
-        const int rr = orow0 - H + row;            // full-grid row
-        const int gc = ocol0 - PADC + 4 * j;       // multiple of 4
-        const bool ok = rr >= 0 && rr < R && rr - r_lo < r_ext && gc >= 0 && gc < C;
-        const int nbytes = ok ? 4 * min(4, C - gc) : 0;
-        const float *src = hb + ((size_t)cls * r_ext + (size_t)(ok ? rr - r_lo : 0)) * ldh + (ok ? gc : 0);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(tile + cr * TW + 4 * j)),
-                     "l"(src), "r"(nbytes)
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-
-    const int tid = threadIdx.x & (TC - 1);
-    const int half = threadIdx.x / TC;
-    const int col = ocol0 + tid;
-    float Sc[2][RPT];
-#pragma unroll
-    for (int cls = 0; cls < 2; ++cls) {
-        const float *t = tile + cls * TH * TW + (half * RPT) * TW + PADC + tid;
-        if (!DISK) {
-            float hs[RPT + 2 * H];
-#pragma unroll
-            for (int i = 0; i < RPT + 2 * H; ++i) {
-                float s = 0.f;
-#pragma unroll
-                for (int dv = -H; dv <= H; ++dv) s += t[i * TW + dv];
-                hs[i] = s;
-            }
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                float s = 0.f;
-#pragma unroll
-                for (int du = 0; du <= 2 * H; ++du) s += hs[r + du];
-                Sc[cls][r] = s;
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                float s = 0.f;
-#pragma unroll
-                for (int du = -H; du <= H; ++du) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
-                    const int w = cisqrt(H * H - du * du);
-#pragma unroll
-                    for (int dv = -w; dv <= w; ++dv) s += t[(r + H + du) * TW + dv];
-                }
-                Sc[cls][r] = s;
-            }
-        }
-    }
-    // clipped counts (closed form) and outputs
-    const int nc = min(col + H, C - 1) - max(col - H, 0) + 1;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-        const int row = orow0 + half * RPT + r;
-        const int br = row - r0;
-        float cnt;
-        if (!DISK) {
-            cnt = (float)((min(row + H, R - 1) - max(row - H, 0) + 1) * nc);
-        } else {
-            int n = 0;
-#pragma unroll
-            for (int du = -H; du <= H; ++du) {
-                const int w = cisqrt(H * H - du * du);
-                if (row + du >= 0 && row + du < R) n += min(col + w, C - 1) - max(col - w, 0) + 1;
-            }
-            cnt = (float)n;
-        }
-        const float inv = 1.0f / cnt;
-        if (col < C && br < band_rows) {
-            const float s1 = Sc[1][r] * inv, s0 = Sc[0][r] * inv;
-            const float g = s1 - s0;
-            const size_t o = (size_t)br * C + col;
-            if (S) {
-                S[o] = s1;
-                S[(size_t)band_rows * C + o] = s0;
-                S[(size_t)2 * band_rows * C + o] = g;
-            }
-            if (lab) lab[o] = g >= rho_occ ? 1 : (g < rho_emp ? 0 : 2);
-        }
-    }
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
 }
 
-// Box window, H <= 4 (the BASELINE configs' 3x3 / 5x5 / 7x7): the TR x TC tile (+ halo) of
-// both classes is staged with 16-byte cp.async exactly as in k_entropy_fixed; then a thread
-// owns 4 adjacent output columns of BOX_RPT rows: per staged row and class it reads the 12
-// floats c0-4 .. c0+7 (three 16-byte shared loads), forms the 4 horizontal (2H+1)-sums, and
-// keeps the last 2H+1 of them per column in a register ring; each output row is the in-order
-// sum of its ring -- the same additions in the same order as k_entropy_fixed<H, false>, so the
-// result is bit-identical, with ~4x fewer shared-memory instructions.  Labels leave as one
-// 4-byte store, S as float4s.
-constexpr int BOX_RPT = 4;                       // output rows per thread
-constexpr int BOX_CG = TC / 4;                   // column groups (threads across)
-static_assert(BOX_CG * (TR / BOX_RPT) == ENT_THREADS, "one thread per (column group, row strip)");
-
 template <int H>
-__global__ void __launch_bounds__(ENT_THREADS) k_entropy_box4(const float *__restrict__ hb, int ldh, int r_ext,
-                                                             int R, int C, int r_lo, int r0, int band_rows,
-                                                             float rho_occ, float rho_emp, float *__restrict__ S,
-                                                             uint8_t *__restrict__ lab)
+__global__ void __launch_bounds__(ST_WARPS * 32, ST_BLOCKS_PER_SM)
+    k_entropy_stream(const __grid_constant__ CUtensorMap tm, const StreamArgs a)
 {
-    static_assert(H >= 1 && H <= 4, "halo within one 16-byte chunk");
+    static_assert(H >= 1 && H <= 4, "halo within one float4 per side");
     constexpr int W = 2 * H + 1;
-    constexpr int PADC = 4;
-    constexpr int TW = TC + 2 * PADC;
-    constexpr int TH = TR + 2 * H;
-    constexpr int CH = TW / 4;
-    extern __shared__ float4 sm4[];
-    float *tile = reinterpret_cast<float *>(sm4);  // [2][TH][TW]
-    const int orow0 = r0 + blockIdx.y * TR;
-    const int ocol0 = blockIdx.x * TC;
-    for (int idx = threadIdx.x; idx < 2 * TH * CH; idx += ENT_THREADS) {
-        const int cr = idx / CH, j = idx - cr * CH;
-        const int cls = cr >= TH, row = cr - cls * TH;
-        const int rr = orow0 - H + row;
-        const int gc = ocol0 - PADC + 4 * j;
-        const bool ok = rr >= 0 && rr < R && rr - r_lo < r_ext && gc >= 0 && gc < C;
-        const int nbytes = ok ? 4 * min(4, C - gc) : 0;
-        const float *src = hb + ((size_t)cls * r_ext + (size_t)(ok ? rr - r_lo : 0)) * ldh + (ok ? gc : 0);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(tile + cr * TW + 4 * j)),
-                     "l"(src), "r"(nbytes)
-                     : "memory");
+    extern __shared__ __align__(128) float sm_st[];
+    __shared__ __align__(8) uint64_t bars[ST_WARPS][ST_NST];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *ring_smem = sm_st + (size_t)warp * ST_NST * ST_STAGE_FLOATS;
+    uint64_t *bar = bars[warp];
+    if (lane == 0) {
+        for (int s = 0; s < ST_NST; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-
-    const int cgi = threadIdx.x % BOX_CG, strip = threadIdx.x / BOX_CG;
-    const int c0 = ocol0 + 4 * cgi;
-    if (c0 >= C) return;
-    int nc[4];
+    __syncwarp();
+    const int items = a.strips * a.chunks;
+    const int nwarps = gridDim.x * ST_WARPS;
+    uint32_t g = 0;   // stages this warp has consumed (slot g % ST_NST, phase (g / ST_NST) & 1)
+    for (int it = blockIdx.x * ST_WARPS + warp; it < items; it += nwarps) {
+        const int strip = it % a.strips, chunk = it / a.strips;
+        const int col0 = strip * 128;
+        const int oA = chunk * a.rw;                          // band-relative output rows [oA, oB)
+        const int oB = min(a.band_rows, oA + a.rw);
+        const int rA = a.r0 + oA;                             // full-grid row of output oA
+        const int nstaged = (oB - oA) + 2 * H;                // staged rows rA - H .. rB - 1 + H
+        const int nst = (nstaged + ST_RS - 1) / ST_RS;
+        auto issue = [&](int t) {                             // local stage t -> slot (g + t) % ST_NST
+            const uint32_t slot = (g + t) % ST_NST;
+            mbar_expect_tx(&bar[slot], ST_STAGE_BYTES);
+            tma_load_3d(ring_smem + slot * ST_STAGE_FLOATS, &tm, &bar[slot], col0 - 4,
+                        rA - H + t * ST_RS - a.r_lo, 0);
+        };
+        if (lane == 0)
+            for (int t = 0; t < min(nst, ST_NST); ++t) issue(t);
+        const int c0 = col0 + 4 * lane;
+        int nc[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) nc[j] = min(c0 + j + H, C - 1) - max(c0 + j - H, 0) + 1;
-    float ring[2][W][4];
+        for (int j = 0; j < 4; ++j) nc[j] = min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1;
+        const bool cols_live = c0 < a.C;
+        const bool full4 = c0 + 3 < a.C && (a.C & 3) == 0;
+        float ring[2][W][4];
+        for (int ib = 0; ib < nstaged; ib += W) {
 #pragma unroll
-    for (int i = 0; i < BOX_RPT + 2 * H; ++i) {
-#pragma unroll
-        for (int cls = 0; cls < 2; ++cls) {
-            const float4 *t4 = reinterpret_cast<const float4 *>(tile + (cls * TH + strip * BOX_RPT + i) * TW + 4 * cgi);
-            const float4 a = t4[0], b = t4[1], d = t4[2];   // columns c0-4 .. c0+7
-            const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float sh = 0.f;
-#pragma unroll
-                for (int dv = -H; dv <= H; ++dv) sh += x[4 + j + dv];
-                ring[cls][i % W][j] = sh;
-            }
-        }
-        if (i >= 2 * H) {
-            const int row = orow0 + strip * BOX_RPT + i - 2 * H;
-            const int br = row - r0;
-            if (br < band_rows) {
-                const float cntr = (float)(min(row + H, R - 1) - max(row - H, 0) + 1);
-                float g4[4], s14[4], s04[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float sc[2];
+            for (int u = 0; u < W; ++u) {
+                const int i = ib + u;                         // staged row (ring slot u = i % W)
+                if (i < nstaged) {
+                    const int t = i / ST_RS, rr = i - t * ST_RS;
+                    const uint32_t slot = (g + t) % ST_NST;
+                    if (rr == 0) mbar_wait(&bar[slot], ((g + t) / ST_NST) & 1u);
+                    const float *stage = ring_smem + slot * ST_STAGE_FLOATS;
 #pragma unroll
                     for (int cls = 0; cls < 2; ++cls) {
-                        float sv = 0.f;
+                        const float *rp = stage + (cls * ST_RS + rr) * ST_W;
+                        const float4 v = *reinterpret_cast<const float4 *>(rp + 4 + 4 * lane);
+                        float4 L, Rt;
+                        L.x = __shfl_up_sync(0xffffffffu, v.x, 1);
+                        L.y = __shfl_up_sync(0xffffffffu, v.y, 1);
+                        L.z = __shfl_up_sync(0xffffffffu, v.z, 1);
+                        L.w = __shfl_up_sync(0xffffffffu, v.w, 1);
+                        Rt.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+                        Rt.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+                        Rt.z = __shfl_down_sync(0xffffffffu, v.z, 1);
+                        Rt.w = __shfl_down_sync(0xffffffffu, v.w, 1);
+                        if (lane == 0) L = *reinterpret_cast<const float4 *>(rp);
+                        if (lane == 31) Rt = *reinterpret_cast<const float4 *>(rp + 132);
+                        const float x[12] = {L.x, L.y, L.z, L.w, v.x, v.y, v.z, v.w, Rt.x, Rt.y, Rt.z, Rt.w};
 #pragma unroll
-                        for (int du = 0; du < W; ++du) sv += ring[cls][(i - 2 * H + du) % W][j];
-                        sc[cls] = sv;
+                        for (int j = 0; j < 4; ++j) {
+                            float sh = 0.f;
+#pragma unroll
+                            for (int dv = -H; dv <= H; ++dv) sh += x[4 + j + dv];
+                            ring[cls][u][j] = sh;
+                        }
                     }
-                    const float inv = 1.0f / (cntr * (float)nc[j]);
-                    s14[j] = sc[1] * inv;
-                    s04[j] = sc[0] * inv;
-                    g4[j] = s14[j] - s04[j];
-                }
-                const size_t o = (size_t)br * C + c0;
-                const bool full = c0 + 3 < C && (C & 3) == 0;
-                if (lab) {
-                    uint8_t l4[4];
+                    if (rr == ST_RS - 1 || i == nstaged - 1) {   // stage consumed: refill its slot
+                        __syncwarp();
+                        if (lane == 0 && t + ST_NST < nst) {
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            issue(t + ST_NST);
+                        }
+                    }
+                    if (i >= 2 * H && cols_live) {
+                        const int o = oA + i - 2 * H;             // band-relative output row
+                        const int row = a.r0 + o;
+                        const float cntr = (float)(min(row + H, a.R - 1) - max(row - H, 0) + 1);
+                        float g4[4], s14[4], s04[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) l4[j] = g4[j] >= rho_occ ? 1 : (g4[j] < rho_emp ? 0 : 2);
-                    if (full) *reinterpret_cast<uchar4 *>(lab + o) = make_uchar4(l4[0], l4[1], l4[2], l4[3]);
-                    else
-                        for (int j = 0; j < 4 && c0 + j < C; ++j) lab[o + j] = l4[j];
-                }
-                if (S) {
-                    float *S1 = S + o, *S0 = S + (size_t)band_rows * C + o, *SG = S + (size_t)2 * band_rows * C + o;
-                    if (full) {
-                        *reinterpret_cast<float4 *>(S1) = make_float4(s14[0], s14[1], s14[2], s14[3]);
-                        *reinterpret_cast<float4 *>(S0) = make_float4(s04[0], s04[1], s04[2], s04[3]);
-                        *reinterpret_cast<float4 *>(SG) = make_float4(g4[0], g4[1], g4[2], g4[3]);
-                    } else {
-                        for (int j = 0; j < 4 && c0 + j < C; ++j) {
-                            S1[j] = s14[j];
-                            S0[j] = s04[j];
-                            SG[j] = g4[j];
+                        for (int j = 0; j < 4; ++j) {
+                            float sc[2];
+#pragma unroll
+                            for (int cls = 0; cls < 2; ++cls) {
+                                float sv = 0.f;
+#pragma unroll
+                                for (int du = 0; du < W; ++du) sv += ring[cls][(u + 1 + du) % W][j];
+                                sc[cls] = sv;
+                            }
+                            const float inv = 1.0f / (cntr * (float)nc[j]);
+                            s14[j] = sc[1] * inv;
+                            s04[j] = sc[0] * inv;
+                            g4[j] = s14[j] - s04[j];
+                        }
+                        const size_t off = (size_t)o * a.C + c0;
+                        if (a.lab) {
+                            uint8_t l4[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) l4[j] = g4[j] >= a.rho_occ ? 1 : (g4[j] < a.rho_emp ? 0 : 2);
+                            if (full4) *reinterpret_cast<uchar4 *>(a.lab + off) = make_uchar4(l4[0], l4[1], l4[2], l4[3]);
+                            else
+                                for (int j = 0; j < 4 && c0 + j < a.C; ++j) a.lab[off + j] = l4[j];
+                        }
+                        if (a.S) {
+                            float *S1 = a.S + off, *S0 = a.S + (size_t)a.band_rows * a.C + off,
+                                  *SG = a.S + (size_t)2 * a.band_rows * a.C + off;
+                            if (full4) {
+                                *reinterpret_cast<float4 *>(S1) = make_float4(s14[0], s14[1], s14[2], s14[3]);
+                                *reinterpret_cast<float4 *>(S0) = make_float4(s04[0], s04[1], s04[2], s04[3]);
+                                *reinterpret_cast<float4 *>(SG) = make_float4(g4[0], g4[1], g4[2], g4[3]);
+                            } else {
+                                for (int j = 0; j < 4 && c0 + j < a.C; ++j) {
+                                    S1[j] = s14[j];
+                                    S0[j] = s04[j];
+                                    SG[j] = g4[j];
+                                }
+                            }
                         }
                     }
                 }
             }
         }
-    }
-}
-
-template <int H, bool DISK>
-int launch_fixed(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab, int ldh, dim3 grid)
-{
-    constexpr int PADC = (H + 3) / 4 * 4;
-    const size_t smem = sizeof(float) * 2 * (TR + 2 * H) * (TC + 2 * PADC);
-    VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_fixed<H, DISK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_entropy_fixed<H, DISK><<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols,
-                                                                     c->g_rlo, c->g_r0, c->g_r1 - c->g_r0, p->rho_occ,
-                                                                     p->rho_emp, S, lab);
-    return VSAOGM_OK;
-}
-
-template <bool DISK>
-int dispatch_fixed(int H, vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab, int ldh, dim3 grid)
-{
-    switch (H) {
-    case 1: return launch_fixed<1, DISK>(c, p, S, lab, ldh, grid);
-    case 2: return launch_fixed<2, DISK>(c, p, S, lab, ldh, grid);
-    case 3: return launch_fixed<3, DISK>(c, p, S, lab, ldh, grid);
-    case 4: return launch_fixed<4, DISK>(c, p, S, lab, ldh, grid);
-    case 5: return launch_fixed<5, DISK>(c, p, S, lab, ldh, grid);
-    case 6: return launch_fixed<6, DISK>(c, p, S, lab, ldh, grid);
-    case 7: return launch_fixed<7, DISK>(c, p, S, lab, ldh, grid);
-    default: return launch_fixed<8, DISK>(c, p, S, lab, ldh, grid);
+        g += nst;
     }
 }
 
@@ -374,7 +300,7 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict
                 }
                 cnt = (float)n;
             }
-            Sc[cls] = s / cnt;
+            Sc[cls] = s * (1.0f / cnt);   // as the streamed kernel: bit-identical box results
         }
         if (col < C) {
             const float g = Sc[1] - Sc[0];
@@ -497,37 +423,63 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
         return VSAOGM_OK;
     }
     const int H = p->half_occ > p->half_emp ? p->half_occ : p->half_emp;
-    const int TW = TC + 2 * H, TH = TR + 2 * H;
     const int band = c->g_r1 - c->g_r0;
     const int ldh = (c->g_cols + 7) / 8 * 8;
-    const size_t smem = sizeof(float) * (2 * (size_t)TH * TW + 2 * (size_t)TH * TC);
-    dim3 grid((c->g_cols + TC - 1) / TC, (band + TR - 1) / TR);
-    const bool fixed = p->half_occ == p->half_emp && H <= 8 && c->entropy_kernel != 1;
-    if (!fixed)
-        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaEvent_t ev;
-    vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
-    if (fixed && !p->disk && H <= 4 && c->entropy_kernel != 2) {
-#define VSA_BOX(HH)                                                                                                \
-    do {                                                                                                           \
-        const size_t bsm = sizeof(float) * 2 * (TR + 2 * (HH)) * (TC + 8);                                          \
-        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_box4<HH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)); \
-        k_entropy_box4<HH><<<grid, ENT_THREADS, bsm, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols,     \
-                                                                  c->g_rlo, c->g_r0, band, p->rho_occ, p->rho_emp,  \
-                                                                  S, lab);                                          \
-    } while (0)
+    const bool stream_k = p->half_occ == p->half_emp && !p->disk && H <= 4 && c->entropy_kernel != 1;
+    if (stream_k) {
+        // tensor map over the decoded H_b rows: dims {cols, r_ext, 2 classes}; out-of-bounds
+        // boxes are zero-filled (the window clipping)
+        auto fn = vsa_tmap_encode_fn();
+        if (!fn) return VSAOGM_ECUDA;
+        CUtensorMap tm;
+        cuuint64_t dims[3] = {(cuuint64_t)c->g_cols, (cuuint64_t)c->g_rext, 2};
+        cuuint64_t strides[2] = {(cuuint64_t)ldh * 4, (cuuint64_t)c->g_rext * ldh * 4};
+        cuuint32_t box[3] = {(cuuint32_t)ST_W, (cuuint32_t)ST_RS, 2};
+        cuuint32_t estr[3] = {1, 1, 1};
+        if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->d_hb, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return VSAOGM_ECUDA;
+        StreamArgs sa;
+        sa.R = c->g_rows;
+        sa.C = c->g_cols;
+        sa.r_lo = c->g_rlo;
+        sa.r0 = c->g_r0;
+        sa.band_rows = band;
+        sa.strips = (c->g_cols + 127) / 128;
+        // one wave of work items over the resident warps; at least 16 output rows per item so
+        // that the 2H halo rows stay a small fraction of the staged rows
+        const int warps = c->num_sms * ST_BLOCKS_PER_SM * ST_WARPS;
+        sa.rw = std::max(16, (int)(((int64_t)band * sa.strips + warps - 1) / warps));
+        if (c->entropy_rw > 0) sa.rw = c->entropy_rw;
+        sa.chunks = (band + sa.rw - 1) / sa.rw;
+        sa.rho_occ = p->rho_occ;
+        sa.rho_emp = p->rho_emp;
+        sa.S = S;
+        sa.lab = lab;
+        const int items = sa.strips * sa.chunks;
+        const int blocks = std::min((items + ST_WARPS - 1) / ST_WARPS, c->num_sms * ST_BLOCKS_PER_SM);
+        vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
         switch (H) {
-        case 1: VSA_BOX(1); break;
-        case 2: VSA_BOX(2); break;
-        case 3: VSA_BOX(3); break;
-        default: VSA_BOX(4); break;
+#define VSA_ST(HH)                                                                                                 \
+    case HH:                                                                                                       \
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_stream<HH>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                          (int)ST_SMEM));                                                          \
+        k_entropy_stream<HH><<<blocks, ST_WARPS * 32, ST_SMEM, c->stream>>>(tm, sa);                               \
+        break;
+            VSA_ST(1)
+            VSA_ST(2)
+            VSA_ST(3)
+            VSA_ST(4)
+#undef VSA_ST
         }
-#undef VSA_BOX
-    } else if (fixed) {
-        int rc = p->disk ? dispatch_fixed<true>(H, c, p, S, lab, ldh, grid)
-                         : dispatch_fixed<false>(H, c, p, S, lab, ldh, grid);
-        if (rc) return rc;
     } else {
+        const int TW = TC + 2 * H, TH = TR + 2 * H;
+        const size_t smem = sizeof(float) * (2 * (size_t)TH * TW + 2 * (size_t)TH * TC);
+        dim3 grid((c->g_cols + TC - 1) / TC, (band + TR - 1) / TR);
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
         k_entropy<<<grid, ENT_THREADS, smem, c->stream>>>(c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols, c->g_rlo,
                                                           c->g_r0, band, p->half_occ, p->half_emp, p->disk,
                                                           p->rho_occ, p->rho_emp, S, lab);

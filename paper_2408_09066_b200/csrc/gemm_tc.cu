@@ -37,6 +37,19 @@
 
 #include "common.cuh"
 
+PFN_cuTensorMapEncodeTiled_v12000 vsa_tmap_encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
 namespace {
 
 constexpr int GEMM_THREADS = 192;
@@ -442,18 +455,7 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const __grid_constant__ G
     if (e.q && br >= 0 && br < e.band_rows) e.q[((size_t)cls * e.band_rows + br) * e.qcols + col] = q;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
-{
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() { return vsa_tmap_encode_fn(); }
 
 // 2-D K-major tensor map: dims {K, rows}, box {64, box_rows}, 128-byte swizzle,
 // out-of-bounds rows are zero-filled (so M, N need no padding).

@@ -324,34 +324,38 @@ def test_entropy_equal_radii_fast_path(disk, h):
 
 
 @pytest.mark.parametrize("h", [1, 2, 3, 4])
-def test_entropy_box_register_kernel_bit_identical(h, monkeypatch):
-    """k_entropy_box4 (box, h <= 4, no shared memory) equals the cp.async-staged fixed-window
-    kernel bit for bit (same additions in the same order), on a ragged grid (203 columns: not a
-    multiple of 4) and on a band with halo rows; both match the oracle stencil."""
-    D, l, res, R, C = 256, 0.3, 0.07, 75, 203
+@pytest.mark.parametrize("R,C,rw", [(75, 203, 0), (75, 203, 3), (300, 1000, 0), (300, 1000, 5)])
+def test_entropy_stream_kernel_bit_identical(h, R, C, rw):
+    """k_entropy_stream (TMA-streamed warps, box, h <= 4) equals the generic staged kernel bit
+    for bit (same additions in the same order) on ragged grids (203 columns: not a multiple of
+    4; 1000: a partial last strip), on bands with halo rows, and with short work items (rw) so
+    that every warp streams several items through its stage ring; both match the oracle."""
+    D, l, res = 256, 0.3, 0.07
     rng = np.random.default_rng(100 + h)
     xy = rng.uniform(0, [C * res, R * res], size=(3000, 2)).astype(np.float32)
     lab = (rng.random(3000) < 0.4).astype(np.uint8)
     mp = _mapper(D, l, (0, 0, C * res, R * res))
     mp.encode_bundle(*_cuda(xy, lab))
     q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
+    mp.set_tuning("entropy_rw", rw)
     outs = []
-    for env in (None, "1"):
-        if env:
-            mp.set_tuning("entropy_kernel", 2)
-        for (r0, r1) in ((0, R), (21, 58)):
+    for kernel in (0, 1):
+        mp.set_tuning("entropy_kernel", kernel)
+        for (r0, r1) in ((0, R), (21, 58), (R - 17, R)):
             mp.decode(0, 0, res, R, C, r0, r1, h, q_out=q if (r0, r1) == (0, R) else None)
             S = torch.empty((3, r1 - r0, C), dtype=torch.float32, device="cuda")
             L = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
             mp.entropy(h, h, 0.001, -0.001, 0, S, L)
             outs.append((S.cpu(), L.cpu()))
     assert mp.sync() == 0
-    for a, b in zip(outs[:2], outs[2:]):
+    for a, b in zip(outs[:3], outs[3:]):
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
     So, Lo = oracle.entropy_grid(q.cpu().numpy().astype(np.float64), h, h, 0, 0.001, -0.001)
     assert np.abs(outs[0][0].numpy() - So).max() <= 2e-5
     assert (outs[0][1].numpy() == Lo).mean() >= 0.9999
+    assert torch.equal(outs[1][1], outs[0][1][21:58]) and torch.equal(outs[2][1], outs[0][1][R - 17:])
     mp.close()
+
 
 def test_streaming_equals_one_shot_and_reset():
     sc = Scenario("C2")
