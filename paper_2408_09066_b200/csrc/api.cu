@@ -128,6 +128,7 @@ int vsaogm_create(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b
 int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaogm_bounds b, int32_t delta,
                             vsaogm_ctx **out)
 {
+    VSA_NVTX();
     if (!out) return VSAOGM_EINVAL_ARG;
     *out = nullptr;
     if (D < 1) return VSAOGM_EINVAL_DIM;
@@ -212,6 +213,7 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
 
 void vsaogm_destroy(vsaogm_ctx *c)
 {
+    VSA_NVTX();
     if (!c) return;
     cudaStreamSynchronize(c->stream);
     if (c->enc_stream) cudaStreamSynchronize(c->enc_stream);
@@ -270,6 +272,7 @@ int vsa_mark_main(vsaogm_ctx *c)
 
 int vsaogm_set_encode_stream(vsaogm_ctx *c, void *stream)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     int rc;
     if ((rc = vsa_join_encode(c))) return rc;
@@ -301,6 +304,7 @@ int vsaogm_set_encode_stream(vsaogm_ctx *c, void *stream)
 
 int vsaogm_encode_bundle(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     if (n < 1) return VSAOGM_EEMPTY;
     if (!xy || !lab) return VSAOGM_EINVAL_ARG;
@@ -326,6 +330,7 @@ int vsaogm_encode_bundle(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int
 
 int vsaogm_encode_bundle_host(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     if (n < 1) return VSAOGM_EEMPTY;
     if (!xy || !lab) return VSAOGM_EINVAL_ARG;
@@ -387,6 +392,7 @@ int grow_slot(void **p, size_t *cap, size_t need, cudaEvent_t busy, bool recorde
 
 int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     if (n < 1) return VSAOGM_EEMPTY;
     if (!xy || !lab) return VSAOGM_EINVAL_ARG;
@@ -418,6 +424,7 @@ int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_
 
 int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
 {
+    VSA_NVTX();
     if (!c || !p) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     *p = c->d_pending;
@@ -428,6 +435,7 @@ int vsaogm_pending(vsaogm_ctx *c, double **p, int64_t *n)
 
 int vsaogm_commit(vsaogm_ctx *c)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     int rc;
     if ((rc = vsa_join_encode(c))) return rc;
@@ -438,6 +446,7 @@ int vsaogm_commit(vsaogm_ctx *c)
 
 int vsaogm_reset(vsaogm_ctx *c)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_m, 0, 2 * (size_t)c->nslots * c->Dp * sizeof(double), c->stream));
@@ -450,6 +459,7 @@ int vsaogm_reset(vsaogm_ctx *c)
 
 int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, float *q)
 {
+    VSA_NVTX();
     if (!c || !g) return VSAOGM_EINVAL_ARG;
     if (!(g->res > 0.0) || !isfinite(g->res) || !isfinite(g->x0) || !isfinite(g->y0) || g->rows < 1 ||
         g->cols < 1 || g->row_begin < 0 || g->row_end > g->rows || g->row_begin >= g->row_end || g->halo < 0 ||
@@ -600,6 +610,7 @@ static int check_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p)
 
 int vsaogm_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab)
 {
+    VSA_NVTX();
     int rc = check_entropy(c, p);
     if (rc) return rc;
     return vsa_launch_entropy(c, p, S, lab);
@@ -607,6 +618,7 @@ int vsaogm_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint
 
 int vsaogm_entropy_host(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S_host, uint8_t *lab_host)
 {
+    VSA_NVTX();
     int rc = check_entropy(c, p);
     if (rc) return rc;
     const size_t cells = (size_t)(c->g_r1 - c->g_r0) * c->g_cols;
@@ -622,6 +634,7 @@ int vsaogm_entropy_host(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S_
 int vsaogm_entropy_host_async(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S_host, uint8_t *lab_host,
                               int64_t *ticket)
 {
+    VSA_NVTX();
     int rc = check_entropy(c, p);
     if (rc) return rc;
     if (!ticket) return VSAOGM_EINVAL_ARG;
@@ -654,6 +667,7 @@ int vsaogm_entropy_host_async(vsaogm_ctx *c, const vsaogm_entropy_params *p, flo
 
 int vsaogm_wait(vsaogm_ctx *c, int64_t ticket)
 {
+    VSA_NVTX();
     if (!c || ticket < 0 || ticket >= c->out_seq) return VSAOGM_EINVAL_ARG;
     // the slot's event was recorded for this ticket or a later one (later downloads
     // complete after earlier ones: one download stream)
@@ -665,6 +679,7 @@ int vsaogm_wait(vsaogm_ctx *c, int64_t ticket)
 
 int vsaogm_sync(vsaogm_ctx *c)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     int err = 0;
@@ -680,6 +695,7 @@ int vsaogm_sync(vsaogm_ctx *c)
 
 int vsaogm_get_memory(vsaogm_ctx *c, double *host, int64_t *counts)
 {
+    VSA_NVTX();
     if (!c) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     const int ns = c->nslots;

@@ -12,6 +12,15 @@
 
 #include "vsaogm.h"
 
+// NVTX range per C-ABI call (header-only NVTX v3: a no-op unless a profiler is attached), so
+// nsys / ncu timelines show vsaogm_encode_bundle, vsaogm_decode, ... around their kernels.
+#include <nvtx3/nvToolsExt.h>
+struct VsaNvtxRange {
+    explicit VsaNvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~VsaNvtxRange() { nvtxRangePop(); }
+};
+#define VSA_NVTX() VsaNvtxRange vsa_nvtx_range_(__func__)
+
 // VSAOGM_DEBUG=1 in the environment prints the failing CUDA call to stderr.
 void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, int line);
 #define VSA_CUDA_TRY(expr)                                                       \

@@ -47,6 +47,7 @@ extern "C" {
 
 int vsaogm_export(vsaogm_ctx *c, void *buf, int64_t *size)
 {
+    VSA_NVTX();
     if (!c || !size) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     const std::string h = header(c);
@@ -78,6 +79,7 @@ static int import_impl(vsaogm_ctx *c, const void *buf, int64_t size, int32_t mod
 
 int vsaogm_import(vsaogm_ctx *c, const void *buf, int64_t size, int32_t mode)
 {
+    VSA_NVTX();
     if (!c || !buf || size < 10 || (mode != 0 && mode != 1)) return VSAOGM_EINVAL_ARG;
     if (int rc = vsa_join_encode(c)) return rc;
     const int rc_import = import_impl(c, buf, size, mode);
