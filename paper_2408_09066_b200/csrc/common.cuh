@@ -105,6 +105,7 @@ struct vsaogm_ctx {
     int gemm_variant = -1;  // -1 auto (CTA pair), 0 CTA pair, 1 single CTA (one group only)
     int gemm_bn = 0;        // 0 auto, else the CTA-pair tile width (128..256, multiple of 32)
     int gemm_splits = 0;    // 0 auto, else the split-K factor
+    int gemm_l2_hints = 1;  // TMA L2 eviction hints in the decode GEMM (A evict-first, B evict-last)
     int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
     int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
     int entropy_rw = 0;     // 0 auto, else output rows per streamed work item (test hook)
@@ -660,6 +661,20 @@ __device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *ma
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
         "%3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+
+// as tma_load_2d_2sm with an L2 eviction-priority hint (64-bit cache policy: the encodings of
+// createpolicy.fractional evict_first / evict_last with fraction 1.0)
+constexpr uint64_t VSA_L2_EVICT_FIRST = 0x12F0000000000000ull;
+constexpr uint64_t VSA_L2_EVICT_LAST = 0x14F0000000000000ull;
+__device__ __forceinline__ void tma_load_2d_2sm_hint(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                                     uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu), "l"(policy)
         : "memory");
 }
 

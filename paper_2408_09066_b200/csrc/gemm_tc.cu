@@ -72,6 +72,7 @@ struct Epi {
     float *ws;         // split-K partials ws[(s * ws_rows + a_row) * ws_cols + col]
     int ws_rows, ws_cols;
     int splits, kb_per;
+    int l2_hints;      // TMA loads with L2 eviction hints (A evict-first, B evict-last)
 };
 
 __device__ __forceinline__ float hb_of_p(float p)
@@ -358,8 +359,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
-                    tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow);
-                    tma_load_2d_2sm(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow);
+                    if (epi.l2_hints) {
+                        // A (each panel read by one wave) evict-first; B (every panel re-read by
+                        // the next wave, 66 MB at C4 < 126 MB L2) evict-last: B is read from DRAM once
+                        tma_load_2d_2sm_hint(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow,
+                                             VSA_L2_EVICT_FIRST);
+                        tma_load_2d_2sm_hint(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow,
+                                             VSA_L2_EVICT_LAST);
+                    } else {
+                        tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow);
+                        tma_load_2d_2sm(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow);
+                    }
                     if (++stage == STAGES2) { stage = 0; phase ^= 1; }
                 }
             }
@@ -624,6 +634,7 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
     e.qcols = N;
     e.splits = 1;
     e.kb_per = c->Kp / VSA_BK;
+    e.l2_hints = c->gemm_l2_hints;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
     int rc = launch<1>(c->d_A, c->d_B, a_rows, N, c->Kp, prec, G, e, c->stream, c->num_sms, c->gemm_variant, &c->d_ws,
