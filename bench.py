@@ -377,11 +377,12 @@ def run_native(args):
                  "frac_of_sustained": round(gemm_tf / pk["bf16_tflops_sustained"], 4),
                  "traffic": traffic.get("decode_gemm"),
                  "peak_basis": f"MEASURED_PEAKS.json ({pk_kind}) bf16 burst (fp16 dense = bf16 dense)"}
-    enc_line = {"kernel": "k_encode_bundle_x2", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
+    enc_line = {"kernel": "k_encode_pairs", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
                 "peak": round(enc_roof["combined"] / 1e9, 2), "unit": "Gphasor/s",
                 "frac": round(enc_rate / enc_roof["combined"], 4), "traffic": traffic.get("encode"),
                 "peak_basis": enc_roof["basis"], "mufu_only_peak": round(enc_roof["mufu_only"] / 1e9, 2),
                 "frac_of_mufu_only": round(enc_rate / enc_roof["mufu_only"], 4),
+                "frac_of_mufu_only_single_point": round(enc_rate / enc_roof["mufu_only_single"], 4),
                 "frac_at_measured_clock": (round(enc_rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
                                            if clocks.get("sm_mhz") else None)}
     roofline = enc_line if dominant == "encode" else gemm_roof
@@ -428,14 +429,21 @@ def run_native(args):
 
 
 def encode_ceiling(sm_mhz):
-    """ALU ceiling of the packed encode, per SM per clock from the guide's
-    unit counts: 16 MUFU, 128 FMA-pipe lanes.  A MUFU phasor costs 2 MUFU + 5 FMA lanes (angle
-    2, FMUL.RZ 1, accumulate 2); a polynomial phasor 16 FMA lanes (angle 2, sincos_fma2_lite 12,
-    accumulate 2).  max m + p s.t. 2m <= 16, 5m + 16p <= 128 -> m = 8, p = 88/16."""
-    per_clk = 8 + (128 - 5 * 8) / 16
-    return {"combined": 148 * per_clk * sm_mhz * 1e6, "mufu_only": 148 * 16 / 2 * sm_mhz * 1e6,
-            "basis": f"combined MUFU+FMA-pipe ceiling {per_clk:.2f} phasors/clk/SM x 148 SM x {sm_mhz:.0f} MHz "
-                     "(guide unit counts: 16 MUFU + 128 FMA lanes/clk/SM; DESIGN.md sec. 6)"}
+    """ALU ceiling of the pair (half-angle) encode k_encode_pairs, per SM
+    per clock from the guide's unit counts: 16 MUFU, 128 FMA-pipe lanes.  Per two phasors of
+    one pair (one dimension): a MUFU pair costs 3 MUFU (sin + cos of the mean angle, cos of the
+    half difference) and 8 FMA lanes (two angles 4, two FMUL.RZ 2, accumulate 2); an FMA-pipe
+    pair costs 26 lanes (angles 4, sincos_fma2_lite 12, cos_fma2_lite 8, accumulate 2).  Per
+    phasor: MUFU 1.5 + 4 lanes, or 13 lanes.  max m + p s.t. 1.5 m <= 16, 4 m + 13 p <= 128
+    -> m = 32/3, p = (128 - 128/3)/13.  Also reported: the MUFU-only ceilings of the pair
+    scheme (16/1.5 per clock) and of one point at a time (16/2, the method's 2 sin/cos per
+    phasor)."""
+    m = 16 / 1.5
+    per_clk = m + (128 - 4 * m) / 13
+    return {"combined": 148 * per_clk * sm_mhz * 1e6, "mufu_only": 148 * m * sm_mhz * 1e6,
+            "mufu_only_single": 148 * 8 * sm_mhz * 1e6,
+            "basis": f"combined MUFU+FMA-pipe ceiling of the pair encode {per_clk:.2f} phasors/clk/SM x 148 SM x "
+                     f"{sm_mhz:.0f} MHz (guide unit counts: 16 MUFU + 128 FMA lanes/clk/SM; DESIGN.md sec. 6)"}
 
 
 def run_c5(args, world, rank, dev, barrier, max_over_ranks):

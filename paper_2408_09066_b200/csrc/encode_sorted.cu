@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const float2 *__restr
         acc.init(fx, fy);
         for (int base = run.y; base < run.z; base += ENC_TILE_S) {
             const int cnt = min(ENC_TILE_S, run.z - base);
-            __syncthreads();
+            block_sync_any();   // reached from both warp roles: non-.aligned
             for (int t = tid; t < cnt; t += T) s_p[t] = sorted[base + t];
-            __syncthreads();
+            block_sync_any();   // reached from both warp roles: non-.aligned
 #pragma unroll 2
             for (int p = 0; p < cnt; ++p) {
                 const float2 P = s_p[p];
