@@ -173,7 +173,7 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
 /* Tuning variants (measurement and test hook; the defaults are the measured best and no
  * environment variable changes them).  Sets the integer knob `key` of this context for
  * later calls: "enc_x2" (encode kernel family; 4 = the pair kernel, the default),
- * "enc_pairs_npoly", "enc_pairs_minb", "enc_x2_npoly", "enc_x2_minb",
+ * "enc_pairs_npoly", "enc_pairs_minb", "enc_pairs_split", "enc_x2_npoly", "enc_x2_minb",
  * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
  * CTA pair, 1 single CTA), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,

@@ -195,6 +195,7 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
             }
         }
         if ((rc = dev_alloc_zero(&c->d_err, 1))) break;
+        if ((rc = dev_alloc_zero(&c->d_ent_ctr, 2))) break;
         if (cudaMemcpy(c->d_wx, wx.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(c->d_wy, wy.data(), c->Dp * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(c->d_tx_turns, tx.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -220,7 +221,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
     if (c->ev_enc) cudaEventDestroy(c->ev_enc);
     if (c->ev_main) cudaEventDestroy(c->ev_main);
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts,
-                    c->d_norm2, c->d_mhat, c->d_normpart, c->d_err, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
+                    c->d_norm2, c->d_mhat, c->d_normpart, c->d_err, c->d_ent_ctr, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
                     c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code};
     for (void *p : ptrs)
@@ -570,6 +571,7 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
         {"enc_x2_npoly", &c->enc_x2_npoly, 0, 8},
         {"enc_pairs_npoly", &c->enc_pairs_npoly, 0, 8},
         {"enc_pairs_minb", &c->enc_pairs_minb, 3, 4},
+        {"enc_pairs_split", &c->enc_pairs_split, 0, 1},
         {"enc_x2_minb", &c->enc_x2_minb, 3, 4},
         {"enc_x2_waves", &c->enc_x2_waves, 1, 64},
         {"enc_npoly", &c->enc_npoly, 0, 4},

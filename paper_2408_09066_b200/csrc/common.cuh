@@ -80,7 +80,7 @@ struct vsaogm_ctx {
     uint8_t *d_slot = nullptr; size_t slot_cap = 0;   // per-point slot (sorted encode)
     int *d_bhist = nullptr; size_t bhist_cap = 0;     // per-block slot histograms
     int *d_sortmeta = nullptr;                     // slot totals / starts / vchunk table
-    float2 *d_sorted = nullptr; size_t sorted_cap = 0;
+    double2 *d_sorted = nullptr; size_t sorted_cap = 0;   // centred fp64 coordinates in slot order
     int4 *d_runs = nullptr; size_t runs_cap = 0;      // runs of one slot (sorted encode)
     // encode path: -1 auto (delta = 1: label-split blocks, measured fastest; delta > 1: sorted
     // runs); 0 sorted runs; 1 label-split / slot-filtered; 2 slot-filtered (tuning knob)
@@ -97,6 +97,7 @@ struct vsaogm_ctx {
     int enc_x2 = 4;
     int enc_pairs_npoly = 4;  // FMA-pipe dimensions of 8 in the pair kernel's second warp role
     int enc_pairs_minb = 3;   // resident pair-kernel blocks per SM (3: 80 registers, no spills)
+    int enc_pairs_split = 1;  // 1 (default): one class per block (k_encode_pairs1, 64 registers, 4 per SM)
     int enc_x2_npoly = 4;   // polynomial dimensions of 8 in the second warp role
     int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
     int enc_x2_minb = 4;    // resident 8-warp blocks per SM (4: 64 registers, the default; 3: 80)
@@ -126,6 +127,7 @@ struct vsaogm_ctx {
     float2 *d_mhat = nullptr;                      // sqrt(D) m_c / ||m_c||, fp32 [S][Dp]
     double *d_normpart = nullptr;                  // per-block partial ||m_c||^2 [S][16]
     int *d_err = nullptr;                          // deferred error bits
+    int *d_ent_ctr = nullptr;                      // streamed entropy work queue [2]: next item, warps done
     float2 *d_part = nullptr;                      // encode chunk partials
     size_t part_cap = 0;                           // in float2
     long long *d_part_cnt = nullptr;

@@ -402,6 +402,100 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs(
     }
 }
 
+// One class per block (grid.z = class): the pair kernel with a single accumulator set, 16
+// registers lighter (64 registers, 4 blocks per SM without spills, so that three blocks fit
+// beside a decode-GEMM CTA in the pipelined schedule).  Every block stages the whole tile and
+// keeps its class's points (in order), so the per-dimension sums are those of k_encode_pairs.
+template <int THREADS, int NPA, int NPB, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs1(
+    const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
+    const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
+    float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
+{
+    constexpr int KT = 8;
+    constexpr int NW = THREADS / 32;
+    constexpr int TILE = THREADS;
+    __shared__ double2 s_p[TILE];             // the tile's centred points of this class, in order
+    __shared__ float4 s_q[TILE / 2];          // pair records (xbar, ybar, dx, dy)
+    __shared__ int s_g[NW];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const bool role_b = warp >= NW / 2;   // warp-uniform
+    const int kb = blockIdx.x;
+    const int64_t chunk = blockIdx.y;
+    const int cls = blockIdx.z;
+    const int kbase = kb * THREADS * KT + tid;
+
+    float fx[KT], fy[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * THREADS;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+    }
+    long long cn = 0;
+    int my_err = 0;
+    const int64_t p0 = chunk * chunk_pts;
+    const int64_t p1 = min(n, p0 + chunk_pts);
+    PairW<KT> w;
+    w.init(fx, fy);
+
+    auto run = [&](auto acc) {
+        acc.init();
+        for (int64_t base = p0; base < p1; base += TILE) {
+            const int cnt = (int)min((int64_t)TILE, p1 - base);
+            block_sync_any();
+            bool mine = false;
+            double2 rec = make_double2(0.0, 0.0);
+            if (tid < cnt) {
+                const float2 v = xy[base + tid];
+                const int L = lab[base + tid];
+                int code = L;
+                if (L > 1) { code = 2; my_err |= VSA_ERRBIT_LABEL; }
+                if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
+                mine = code == cls;
+                rec = make_double2((double)v.x - cx, (double)v.y - cy);
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, mine);
+            if (lane == 0) s_g[warp] = __popc(b);
+            block_sync_any();
+            int nc = 0, o = 0;
+#pragma unroll
+            for (int g = 0; g < NW; ++g) {
+                if (g == warp) o = nc;
+                nc += s_g[g];
+            }
+            if (mine) s_p[o + __popc(b & ((1u << lane) - 1u))] = rec;
+            cn += nc;
+            block_sync_any();
+            const int np = nc >> 1;
+            if (tid < np) {                                   // pair records, fp64 then one rounding
+                const double2 a = s_p[2 * tid], bb = s_p[2 * tid + 1];
+                s_q[tid] = make_float4((float)(0.5 * (a.x + bb.x)), (float)(0.5 * (a.y + bb.y)),
+                                       (float)(0.5 * (a.x - bb.x)), (float)(0.5 * (a.y - bb.y)));
+            }
+            block_sync_any();
+#pragma unroll 1
+            for (int p = 0; p < np; ++p) acc.pair(w, s_q[p]);     // warp-uniform broadcasts
+            if (nc & 1) {
+                const double2 a = s_p[nc - 1];
+                acc.single(w, (float)a.x, (float)a.y);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int k = kbase + j * THREADS;
+            if (k < Dp) part[((size_t)chunk * 2 + cls) * Dp + k] = acc.get(j);
+        }
+    };
+    if (role_b) run(PairAcc<KT, NPB>{});
+    else run(PairAcc<KT, NPA>{});
+    if (kb == 0) {
+        if (my_err && cls == 0) atomicOr(err, my_err);
+        if (tid == 0) part_cnt[chunk * 2 + cls] = cn;
+    }
+}
+
 // Quadrant routing (delta > 1; Alg. 1): slot = 2 beta + psi with
 // beta the nearest quadrant centre in fp64 squared distance, ties to the lowest
 // index -- the expression, operation order and rounding DESIGN.md fixes for the decision
@@ -689,8 +783,12 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     const int zslots = slots_path ? c->nslots : 1;     // grid.z
     // slot-filtered blocks carry unequal work (slots hold different point counts): several
     // waves of smaller blocks even the tail out
-    const int64_t target_blocks = (int64_t)c->num_sms * minb * (slots_path ? c->enc_waves : x2 ? c->enc_x2_waves : 1);
-    int64_t chunks = (target_blocks + (int64_t)kblocks * zslots - 1) / ((int64_t)kblocks * zslots);
+    const bool split1 = x2 && c->enc_x2 == 4 && c->enc_pairs_split;   // grid.z = 2 classes
+    const int minb_eff = split1 ? 4 : minb;
+    const int64_t target_blocks =
+        (int64_t)c->num_sms * minb_eff * (slots_path ? c->enc_waves : x2 ? c->enc_x2_waves : 1);
+    int64_t chunks = (target_blocks + (int64_t)kblocks * zslots * (split1 ? 2 : 1) - 1) /
+                     ((int64_t)kblocks * zslots * (split1 ? 2 : 1));
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (n + 63) / 64));
     const int64_t chunk_pts = (n + chunks - 1) / chunks;
     chunks = (n + chunk_pts - 1) / chunk_pts;
@@ -751,7 +849,19 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     k_encode_pairs<256, 0, NPB_, MB_><<<grid, 256, 0, c->stream>>>(                                               \
         (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
         c->d_err)
-    if (x2 && c->enc_x2 == 4) {   // pairs (half-angle): all-MUFU warps beside NPOLY-FMA-pipe warps
+#define VSA_ENC_PAIRS1(NPB_, MB_)                                                                                  \
+    k_encode_pairs1<256, 0, NPB_, MB_><<<dim3(grid.x, grid.y, 2), 256, 0, c->stream>>>(                            \
+        (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, c->d_part, c->d_part_cnt,  \
+        c->d_err)
+    if (x2 && c->enc_x2 == 4 && c->enc_pairs_split) {   // pairs, one class per block
+        switch (c->enc_pairs_npoly) {
+        case 0: VSA_ENC_PAIRS1(0, 4); break;
+        case 2: VSA_ENC_PAIRS1(2, 4); break;
+        case 6: VSA_ENC_PAIRS1(6, 4); break;
+        case 8: VSA_ENC_PAIRS1(8, 4); break;
+        default: VSA_ENC_PAIRS1(4, 4); break;
+        }
+    } else if (x2 && c->enc_x2 == 4) {   // pairs (half-angle): all-MUFU warps beside NPOLY-FMA-pipe warps
         const bool mb4 = c->enc_pairs_minb == 4;
         switch (c->enc_pairs_npoly) {
         case 0: if (mb4) VSA_ENC_PAIRS(0, 4); else VSA_ENC_PAIRS(0, 3); break;
@@ -818,6 +928,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
 #undef VSA_ENC_LAUNCH
 #undef VSA_ENC_X2
 #undef VSA_ENC_PAIRS
+#undef VSA_ENC_PAIRS1
     }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_ENCODE, ev);

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(1024) k_sort_plan(int *__restrict__ bhist, int
 __global__ void __launch_bounds__(RT_THREADS) k_scatter(const float2 *__restrict__ xy, const uint8_t *__restrict__ slot,
                                                         int64_t n, int nslots, const int *__restrict__ boff,
                                                         const int *__restrict__ meta, double cx, double cy,
-                                                        float2 *__restrict__ sorted)
+                                                        double2 *__restrict__ sorted)
 {
     constexpr int NW = RT_THREADS / 32;
     __shared__ int s_run[MAX_SLOTS];
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_scatter(const float2 *__restrict
             for (int w = 0; w < warp; ++w) off += s_w[w][s];
             const int pos = meta[META_SSTART() + s] + boff[(size_t)blockIdx.x * nslots + s] + off + rank;
             const float2 v = xy[i];
-            sorted[pos] = make_float2((float)((double)v.x - cx), (float)((double)v.y - cy));
+            sorted[pos] = make_double2((double)v.x - cx, (double)v.y - cy);
         }
         __syncthreads();
         for (int k = threadIdx.x; k < nslots; k += RT_THREADS) {
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(RT_THREADS) k_scatter(const float2 *__restrict
 }
 
 template <int KT, int NPOLY>
-__global__ void __launch_bounds__(ENC_T, 6) k_encode_runs(const float2 *__restrict__ sorted, const int4 *__restrict__ runs,
+__global__ void __launch_bounds__(ENC_T, 6) k_encode_runs(const double2 *__restrict__ sorted, const int4 *__restrict__ runs,
                                                           const int *__restrict__ meta, const float *__restrict__ wx,
                                                           const float *__restrict__ wy, int Dp,
                                                           float2 *__restrict__ part)
@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(ENC_T, 6) k_encode_runs(const float2 *__restri
     for (int base = run.y; base < run.z; base += ENC_TILE_S) {
         const int cnt = min(ENC_TILE_S, run.z - base);
         __syncthreads();
-        for (int t = tid; t < cnt; t += ENC_T) s_p[t] = sorted[base + t];
+        for (int t = tid; t < cnt; t += ENC_T) {
+            const double2 v = sorted[base + t];
+            s_p[t] = make_float2((float)v.x, (float)v.y);
+        }
         __syncthreads();
 #pragma unroll 2
         for (int p = 0; p < cnt; ++p) {
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(ENC_T, 6) k_encode_runs(const float2 *__restri
 // other four with NPB of their 8 dimensions on the polynomial (PhasorAcc, as
 // k_encode_bundle_x2 in encode.cu); one run of one slot per block row.
 template <int NPA, int NPB>
-__global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const float2 *__restrict__ sorted,
+__global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const double2 *__restrict__ sorted,
                                                           const int4 *__restrict__ runs,
                                                           const int *__restrict__ meta, const float *__restrict__ wx,
                                                           const float *__restrict__ wy, int Dp,
@@ -222,7 +225,10 @@ __global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const float2 *__restr
         for (int base = run.y; base < run.z; base += ENC_TILE_S) {
             const int cnt = min(ENC_TILE_S, run.z - base);
             block_sync_any();   // reached from both warp roles: non-.aligned
-            for (int t = tid; t < cnt; t += T) s_p[t] = sorted[base + t];
+            for (int t = tid; t < cnt; t += T) {
+                const double2 v = sorted[base + t];
+                s_p[t] = make_float2((float)v.x, (float)v.y);
+            }
             block_sync_any();   // reached from both warp roles: non-.aligned
 #pragma unroll 2
             for (int p = 0; p < cnt; ++p) {
@@ -238,6 +244,62 @@ __global__ void __launch_bounds__(256, 3) k_encode_runs_x2(const float2 *__restr
     };
     if ((tid >> 5) >= 4) go(PhasorAcc<KT, NPB>{});
     else go(PhasorAcc<KT, NPA>{});
+}
+
+// Pair (half-angle) variant, the default for D >= 2048 (PairAcc,
+// common.cuh): a run holds points of one slot in index order; consecutive points form pairs
+// whose mean and half-difference are computed from the fp64 centred coordinates and rounded
+// once; an odd last point of a run is added on its own.  8 warps, the first four all-MUFU, the
+// other four NPB of 8 dimensions on the FMA pipe; 64 registers, 4 blocks per SM.
+template <int NPB>
+__global__ void __launch_bounds__(256, 4) k_encode_runs_pairs(const double2 *__restrict__ sorted,
+                                                              const int4 *__restrict__ runs,
+                                                              const int *__restrict__ meta, const float *__restrict__ wx,
+                                                              const float *__restrict__ wy, int Dp,
+                                                              float2 *__restrict__ part)
+{
+    constexpr int T = 256, KT = 8;
+    __shared__ float4 s_q[ENC_TILE_S / 2];
+    __shared__ double2 s_last;
+    const int r = blockIdx.y;
+    if (r >= meta[META_NRUNS()]) return;
+    const int4 run = runs[r];
+    const int tid = threadIdx.x;
+    const int kbase = blockIdx.x * T * KT + tid;
+    float fx[KT], fy[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = kbase + j * T;
+        fx[j] = k < Dp ? wx[k] : 0.f;
+        fy[j] = k < Dp ? wy[k] : 0.f;
+    }
+    PairW<KT> w;
+    w.init(fx, fy);
+    auto go = [&](auto acc) {
+        acc.init();
+        for (int base = run.y; base < run.z; base += ENC_TILE_S) {
+            const int cnt = min(ENC_TILE_S, run.z - base);
+            const int np = cnt >> 1;
+            block_sync_any();   // reached from both warp roles: non-.aligned
+            for (int t = tid; t < np; t += T) {
+                const double2 a = sorted[base + 2 * t], b = sorted[base + 2 * t + 1];
+                s_q[t] = make_float4((float)(0.5 * (a.x + b.x)), (float)(0.5 * (a.y + b.y)),
+                                     (float)(0.5 * (a.x - b.x)), (float)(0.5 * (a.y - b.y)));
+            }
+            if (tid == 0 && (cnt & 1)) s_last = sorted[base + cnt - 1];
+            block_sync_any();
+#pragma unroll 1
+            for (int p = 0; p < np; ++p) acc.pair(w, s_q[p]);
+            if (cnt & 1) acc.single(w, (float)s_last.x, (float)s_last.y);
+        }
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int k = kbase + j * T;
+            if (k < Dp) part[(size_t)r * Dp + k] = acc.get(j);
+        }
+    };
+    if ((tid >> 5) >= 4) go(PairAcc<KT, NPB>{});
+    else go(PairAcc<KT, 0>{});
 }
 
 // pending[s][k] += sum over the slot's runs (fixed order, fp64): 32 k-lanes x 8 run slices
@@ -292,8 +354,9 @@ int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab,
     const int ns = c->nslots;
     const int nblk = (int)((n + RT_PTS - 1) / RT_PTS);
     const int KT = c->Dp >= 1024 ? 8 : 4;
-    const bool x2 = c->enc_x2 >= 2 && c->Dp >= 2048;   // packed 8-warp role kernel
-    const int T = x2 ? 256 : ENC_T, per_sm = x2 ? 3 : 6;
+    const bool pairs = c->enc_x2 == 4 && c->Dp >= 2048;  // pair kernel (default)
+    const bool x2 = c->enc_x2 >= 2 && c->Dp >= 2048;     // packed 8-warp role kernels
+    const int T = x2 ? 256 : ENC_T, per_sm = pairs ? 4 : x2 ? 3 : 6;
     const int kblocks = (c->Dp + T * KT - 1) / (T * KT);
     // runs per k-block column so that all blocks fit whole waves of `per_sm` per SM; each slot's
     // last run may be short, so size runs for (target - nslots) and the total never exceeds it
@@ -321,7 +384,18 @@ int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab,
 #define VSA_RUNS(KT_, NP_)                                                                                         \
     k_encode_runs<KT_, NP_><<<grid, ENC_T, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx, c->d_wy, \
                                                           c->Dp, c->d_part)
-    if (x2) {
+    if (pairs) {
+        switch (c->enc_pairs_npoly) {
+        case 0: k_encode_runs_pairs<0><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
+                                                                    c->d_wy, c->Dp, c->d_part); break;
+        case 2: k_encode_runs_pairs<2><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
+                                                                    c->d_wy, c->Dp, c->d_part); break;
+        case 6: k_encode_runs_pairs<6><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
+                                                                    c->d_wy, c->Dp, c->d_part); break;
+        default: k_encode_runs_pairs<4><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
+                                                                     c->d_wy, c->Dp, c->d_part); break;
+        }
+    } else if (x2) {
         switch (c->enc_x2_npoly) {
         case 4: k_encode_runs_x2<0, 4><<<grid, 256, 0, c->stream>>>(c->d_sorted, c->d_runs, c->d_sortmeta, c->d_wx,
                                                                     c->d_wy, c->Dp, c->d_part); break;

@@ -36,37 +36,50 @@ __device__ __forceinline__ int isqrt_floor(int t)
 }
 
 
-// Box window, equal radii h1 = h0 = H <= 4 (every BASELINE config: 3x3 / 5x5 / 7x7), the
-// HBM-bound hot kernel.  Persistent warps, each streaming a work item = one 128-column strip x
-// `rw` output rows of the band from top to bottom:
-//   * lane 0 keeps a private ring of ST_NST TMA stages in flight (cp.async.bulk.tensor.3d, box
-//     136 columns x ST_RS rows x both classes, 4 halo columns on each side; the tensor map's
-//     bounds are the decoded rows x grid columns, so the TMA zero-fill IS the window clipping of
-//     DESIGN.md L13) on per-stage mbarriers -- no block barriers, every warp independent;
-//   * each lane owns 4 adjacent columns: per staged row and class it reads its own float4,
-//     gets the H neighbour columns on each side by warp shuffles (the strip's edge lanes read
-//     the staged halo), forms the 4 horizontal (2H+1)-sums and keeps the last 2H+1 of them in a
-//     register ring; each output row is the in-order sum of its ring (the additions and their
-//     order of the generic kernel, so the result is bit-identical to it);
-//   * labels leave as one 4-byte store per lane (128 B per warp row), S as float4s.
-// Each staged row is read from shared memory once per class (16 B per lane); halo rows of
-// neighbouring items are re-read from L2, not DRAM (items run concurrently).
-constexpr int ST_RS = 4;                          // staged rows per TMA stage
-constexpr int ST_NST = 4;                         // stages per warp ring
-constexpr int ST_W = 136;                         // staged floats per row (4 + 128 + 4)
+// Box window, equal radii h1 = h0 = H <= 4 (every BASELINE config: 3x3 / 5x5 / 7x7), labels
+// only (the streaming step's output; a request for the S maps takes the generic kernel).
+// HBM-bound: 8 B read + 1 B written per cell.  Persistent warps take work items from a device
+// queue; an item is one 256-column strip x `rw` output rows of the band, streamed top to
+// bottom:
+//   * lane 0 keeps a private ring of NST = 2H+1 TMA stages of RS rows in flight, each two
+//     cp.async.bulk.tensor.3d boxes of 136 columns x RS rows x both classes (columns -4..131
+//     and 124..259 of the strip: 4 halo columns on each side; a box is at most 256 wide); the
+//     tensor map's bounds are the decoded rows x grid columns, so the TMA zero-fill IS the
+//     window clipping of DESIGN.md L13; per-stage mbarriers, no block barriers, every warp
+//     independent;
+//   * rows go in blocks of U = RS NST rows, U a multiple of W = 2H+1, so the stage slot, the
+//     row inside the stage and the register-ring slot of every row are compile-time;
+//   * each lane owns 8 adjacent columns: per staged row and class it reads its two float4s,
+//     gets the H neighbour columns on each side by warp shuffles (edge lanes: the staged
+//     halo), forms the horizontal (2H+1)-sums as packed fp32x2 sums, and the class difference
+//     d = h_occ - h_emp; a running vertical sum V += d_new - d_old (the last W differences in
+//     registers) gives S = S_occ - S_emp = V / count for the row W-1 above, then the label.
+// Against the fp64 definition the fp32 rounding of these sums is <= 2e-6 in S.
 constexpr int ST_WARPS = 4;                       // warps per block
-constexpr int ST_BLOCKS_PER_SM = 2;
-constexpr int ST_STAGE_FLOATS = 2 * ST_RS * ST_W; // [class][row][col]
-constexpr int ST_STAGE_BYTES = ST_STAGE_FLOATS * 4;
-constexpr size_t ST_SMEM = (size_t)ST_WARPS * ST_NST * ST_STAGE_BYTES;
+constexpr int ST_COLS = 256;                      // output columns per strip (8 per lane)
+constexpr int ST_W = 136;                         // staged floats per box row (4 + 128 + 4)
+
+template <int H>
+struct StCfg {
+    static constexpr int W = 2 * H + 1;
+    static constexpr int RS = 1;                              // rows per stage
+    static constexpr int NST = W;                             // stages per ring
+    static constexpr int U = RS * NST;                        // rows per block (multiple of W)
+    static constexpr int BOX_FLOATS = (2 * RS * ST_W + 31) / 32 * 32;     // [class][row][col], 128 B aligned
+    static constexpr int STAGE_FLOATS = 2 * BOX_FLOATS;       // two boxes: strip columns -4.. and 124..
+    static constexpr int STAGE_BYTES = 2 * 2 * RS * ST_W * 4; // TMA bytes per stage
+    static constexpr int WARP_BYTES = NST * STAGE_FLOATS * 4;
+    static constexpr int BLOCK_SMEM = ST_WARPS * WARP_BYTES;
+    static constexpr int BLOCKS_PER_SM = 200 * 1024 / BLOCK_SMEM < 4 ? 200 * 1024 / BLOCK_SMEM : 4;
+};
 
 struct StreamArgs {
     int R, C, r_lo;            // full grid; first decoded row (tensor-map row 0)
     int r0, band_rows;         // band: full-grid rows [r0, r0 + band_rows)
     int strips, chunks, rw;    // work items = strips x chunks of rw output rows
     float rho_occ, rho_emp;
-    float *S;
     uint8_t *lab;
+    int *ctr;                  // [0] next item, [1] warps done (reset by the last warp)
 };
 
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2)
@@ -78,138 +91,167 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// label of one cell (Eq. 12 + L14): 1 occupied if S >= rho_occ, 0 empty if S < rho_emp, else 2
+__device__ __forceinline__ uint32_t label_of(float g, float rho_occ, float rho_emp)
+{
+    return g >= rho_occ ? 1u : (g < rho_emp ? 0u : 2u);
+}
+
 template <int H>
-__global__ void __launch_bounds__(ST_WARPS * 32, ST_BLOCKS_PER_SM)
+__global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
     k_entropy_stream(const __grid_constant__ CUtensorMap tm, const StreamArgs a)
 {
     static_assert(H >= 1 && H <= 4, "halo within one float4 per side");
-    constexpr int W = 2 * H + 1;
+    using Cfg = StCfg<H>;
+    constexpr int W = Cfg::W, RS = Cfg::RS, NST = Cfg::NST, U = Cfg::U;
     extern __shared__ __align__(128) float sm_st[];
-    __shared__ __align__(8) uint64_t bars[ST_WARPS][ST_NST];
+    __shared__ __align__(8) uint64_t bars[ST_WARPS][NST];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float *ring_smem = sm_st + (size_t)warp * ST_NST * ST_STAGE_FLOATS;
+    float *ring_smem = sm_st + (size_t)warp * NST * Cfg::STAGE_FLOATS;
     uint64_t *bar = bars[warp];
     if (lane == 0) {
-        for (int s = 0; s < ST_NST; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncwarp();
     const int items = a.strips * a.chunks;
-    const int nwarps = gridDim.x * ST_WARPS;
-    uint32_t g = 0;   // stages this warp has consumed (slot g % ST_NST, phase (g / ST_NST) & 1)
-    for (int it = blockIdx.x * ST_WARPS + warp; it < items; it += nwarps) {
+    uint32_t blk = 0;   // row blocks this warp has consumed: every slot is used once per block
+    // this lane's 8 columns: lanes 0-15 in box 0 (strip columns -4..131), 16-31 in box 1 (124..259)
+    const float *lane_base = ring_smem + (lane < 16 ? 0 : Cfg::BOX_FLOATS) + 4 + 8 * (lane & 15);
+    const float *halo_base = lane == 0 ? ring_smem : (lane == 31 ? ring_smem + Cfg::BOX_FLOATS + 132 : lane_base);
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(&a.ctr[0], 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= items) break;
         const int strip = it % a.strips, chunk = it / a.strips;
-        const int col0 = strip * 128;
+        const int col0 = strip * ST_COLS;
         const int oA = chunk * a.rw;                          // band-relative output rows [oA, oB)
         const int oB = min(a.band_rows, oA + a.rw);
         const int rA = a.r0 + oA;                             // full-grid row of output oA
-        const int nstaged = (oB - oA) + 2 * H;                // staged rows rA - H .. rB - 1 + H
-        const int nst = (nstaged + ST_RS - 1) / ST_RS;
-        auto issue = [&](int t) {                             // local stage t -> slot (g + t) % ST_NST
-            const uint32_t slot = (g + t) % ST_NST;
-            mbar_expect_tx(&bar[slot], ST_STAGE_BYTES);
-            tma_load_3d(ring_smem + slot * ST_STAGE_FLOATS, &tm, &bar[slot], col0 - 4,
-                        rA - H + t * ST_RS - a.r_lo, 0);
+        const int nblk = ((oB - oA) + 2 * H + U - 1) / U;     // staged rows rA - H ..., padded
+        auto issue = [&](int b, int s) {                      // block b, stage s -> slot s
+            mbar_expect_tx(&bar[s], Cfg::STAGE_BYTES);
+            const int trow = rA - H + b * U + s * RS - a.r_lo;
+            tma_load_3d(ring_smem + s * Cfg::STAGE_FLOATS, &tm, &bar[s], col0 - 4, trow, 0);
+            tma_load_3d(ring_smem + s * Cfg::STAGE_FLOATS + Cfg::BOX_FLOATS, &tm, &bar[s], col0 + 124, trow, 0);
         };
         if (lane == 0)
-            for (int t = 0; t < min(nst, ST_NST); ++t) issue(t);
-        const int c0 = col0 + 4 * lane;
-        int nc[4];
+            for (int s = 0; s < NST; ++s) issue(0, s);
+        const int c0 = col0 + 8 * lane;
+        // column clip counts and the interior-row reciprocals 1 / (W nc)
+        float ncf[8];
+        f32x2 inv_in[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) nc[j] = min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1;
-        const bool cols_live = c0 < a.C;
-        const bool full4 = c0 + 3 < a.C && (a.C & 3) == 0;
-        float ring[2][W][4];
-        for (int ib = 0; ib < nstaged; ib += W) {
+        for (int j = 0; j < 8; ++j) ncf[j] = (float)(min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1);
 #pragma unroll
-            for (int u = 0; u < W; ++u) {
-                const int i = ib + u;                         // staged row (ring slot u = i % W)
-                if (i < nstaged) {
-                    const int t = i / ST_RS, rr = i - t * ST_RS;
-                    const uint32_t slot = (g + t) % ST_NST;
-                    if (rr == 0) mbar_wait(&bar[slot], ((g + t) / ST_NST) & 1u);
-                    const float *stage = ring_smem + slot * ST_STAGE_FLOATS;
+        for (int q = 0; q < 4; ++q) inv_in[q] = pk2(1.0f / ((float)W * ncf[2 * q]), 1.0f / ((float)W * ncf[2 * q + 1]));
+        const bool full8 = c0 + 7 < a.C && (a.C & 7) == 0;
+        uint8_t *lab_item = a.lab + (size_t)oA * a.C + c0;
+        f32x2 ring[W][4];                                     // d = h_occ - h_emp, column pairs
+        f32x2 V[4];                                           // running vertical sums of d
 #pragma unroll
-                    for (int cls = 0; cls < 2; ++cls) {
-                        const float *rp = stage + (cls * ST_RS + rr) * ST_W;
-                        const float4 v = *reinterpret_cast<const float4 *>(rp + 4 + 4 * lane);
-                        float4 L, Rt;
-                        L.x = __shfl_up_sync(0xffffffffu, v.x, 1);
-                        L.y = __shfl_up_sync(0xffffffffu, v.y, 1);
-                        L.z = __shfl_up_sync(0xffffffffu, v.z, 1);
-                        L.w = __shfl_up_sync(0xffffffffu, v.w, 1);
-                        Rt.x = __shfl_down_sync(0xffffffffu, v.x, 1);
-                        Rt.y = __shfl_down_sync(0xffffffffu, v.y, 1);
-                        Rt.z = __shfl_down_sync(0xffffffffu, v.z, 1);
-                        Rt.w = __shfl_down_sync(0xffffffffu, v.w, 1);
-                        if (lane == 0) L = *reinterpret_cast<const float4 *>(rp);
-                        if (lane == 31) Rt = *reinterpret_cast<const float4 *>(rp + 132);
-                        const float x[12] = {L.x, L.y, L.z, L.w, v.x, v.y, v.z, v.w, Rt.x, Rt.y, Rt.z, Rt.w};
+        for (int q = 0; q < 4; ++q) V[q] = pk2(0.f, 0.f);
+        for (int b = 0; b < nblk; ++b, ++blk) {
+            const uint32_t par = blk & 1u;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            float sh = 0.f;
+            for (int uu = 0; uu < U; ++uu) {
+                const int s = uu / RS, rr = uu % RS, u = uu % W;
+                if (rr == 0) mbar_wait(&bar[s], par);
+                const int soff = s * Cfg::STAGE_FLOATS + rr * ST_W;
+                f32x2 hcls[2][4];
 #pragma unroll
-                            for (int dv = -H; dv <= H; ++dv) sh += x[4 + j + dv];
-                            ring[cls][u][j] = sh;
-                        }
+                for (int cls = 0; cls < 2; ++cls) {
+                    const float *rp = lane_base + soff + cls * RS * ST_W;
+                    const float4 va = *reinterpret_cast<const float4 *>(rp);
+                    const float4 vb = *reinterpret_cast<const float4 *>(rp + 4);
+                    const float4 hv = *reinterpret_cast<const float4 *>(halo_base + soff + cls * RS * ST_W);
+                    float x[16];                              // columns c0-4 .. c0+11
+                    x[4] = va.x; x[5] = va.y; x[6] = va.z; x[7] = va.w;
+                    x[8] = vb.x; x[9] = vb.y; x[10] = vb.z; x[11] = vb.w;
+                    {
+                        const float t0 = __shfl_up_sync(0xffffffffu, vb.w, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, va.x, 1);
+                        x[3] = lane == 0 ? hv.w : t0;
+                        x[12] = lane == 31 ? hv.x : t1;
                     }
-                    if (rr == ST_RS - 1 || i == nstaged - 1) {   // stage consumed: refill its slot
-                        __syncwarp();
-                        if (lane == 0 && t + ST_NST < nst) {
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            issue(t + ST_NST);
-                        }
+                    if (H >= 2) {
+                        const float t0 = __shfl_up_sync(0xffffffffu, vb.z, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, va.y, 1);
+                        x[2] = lane == 0 ? hv.z : t0;
+                        x[13] = lane == 31 ? hv.y : t1;
                     }
-                    if (i >= 2 * H && cols_live) {
-                        const int o = oA + i - 2 * H;             // band-relative output row
-                        const int row = a.r0 + o;
+                    if (H >= 3) {
+                        const float t0 = __shfl_up_sync(0xffffffffu, vb.y, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, va.z, 1);
+                        x[1] = lane == 0 ? hv.y : t0;
+                        x[14] = lane == 31 ? hv.z : t1;
+                    }
+                    if (H >= 4) {
+                        const float t0 = __shfl_up_sync(0xffffffffu, vb.x, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, va.w, 1);
+                        x[0] = lane == 0 ? hv.x : t0;
+                        x[15] = lane == 31 ? hv.w : t1;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {            // columns (2q, 2q+1)
+                        f32x2 sh = pk2(x[4 + 2 * q - H], x[5 + 2 * q - H]);
+#pragma unroll
+                        for (int dv = -H + 1; dv <= H; ++dv) sh = add2(sh, pk2(x[4 + 2 * q + dv], x[5 + 2 * q + dv]));
+                        hcls[cls][q] = sh;
+                    }
+                }
+                if (rr == RS - 1) {                           // stage s consumed: refill for block b+1
+                    __syncwarp();
+                    if (lane == 0 && b + 1 < nblk) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue(b + 1, s);
+                    }
+                }
+                const int i = b * U + uu;                     // staged row
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const f32x2 d = add2(hcls[1][q], mul2(hcls[0][q], bc2(-1.f)));   // h_occ - h_emp
+                    V[q] = add2(V[q], d);
+                    if (i >= W) V[q] = add2(V[q], mul2(ring[u][q], bc2(-1.f)));       // drop row i - W
+                    ring[u][q] = d;
+                }
+                const int o = oA + i - 2 * H;                 // band-relative output row
+                if (i >= 2 * H && o < oB) {                   // warp-uniform
+                    const int row = a.r0 + o;
+                    f32x2 g2[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) g2[q] = mul2(V[q], inv_in[q]);
+                    if (row < H || row >= a.R - H) {          // clipped rows (grid top / bottom)
                         const float cntr = (float)(min(row + H, a.R - 1) - max(row - H, 0) + 1);
-                        float g4[4], s14[4], s04[4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            float sc[2];
-#pragma unroll
-                            for (int cls = 0; cls < 2; ++cls) {
-                                float sv = 0.f;
-#pragma unroll
-                                for (int du = 0; du < W; ++du) sv += ring[cls][(u + 1 + du) % W][j];
-                                sc[cls] = sv;
-                            }
-                            const float inv = 1.0f / (cntr * (float)nc[j]);
-                            s14[j] = sc[1] * inv;
-                            s04[j] = sc[0] * inv;
-                            g4[j] = s14[j] - s04[j];
-                        }
-                        const size_t off = (size_t)o * a.C + c0;
-                        if (a.lab) {
-                            uint8_t l4[4];
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) l4[j] = g4[j] >= a.rho_occ ? 1 : (g4[j] < a.rho_emp ? 0 : 2);
-                            if (full4) *reinterpret_cast<uchar4 *>(a.lab + off) = make_uchar4(l4[0], l4[1], l4[2], l4[3]);
-                            else
-                                for (int j = 0; j < 4 && c0 + j < a.C; ++j) a.lab[off + j] = l4[j];
-                        }
-                        if (a.S) {
-                            float *S1 = a.S + off, *S0 = a.S + (size_t)a.band_rows * a.C + off,
-                                  *SG = a.S + (size_t)2 * a.band_rows * a.C + off;
-                            if (full4) {
-                                *reinterpret_cast<float4 *>(S1) = make_float4(s14[0], s14[1], s14[2], s14[3]);
-                                *reinterpret_cast<float4 *>(S0) = make_float4(s04[0], s04[1], s04[2], s04[3]);
-                                *reinterpret_cast<float4 *>(SG) = make_float4(g4[0], g4[1], g4[2], g4[3]);
-                            } else {
-                                for (int j = 0; j < 4 && c0 + j < a.C; ++j) {
-                                    S1[j] = s14[j];
-                                    S0[j] = s04[j];
-                                    SG[j] = g4[j];
-                                }
-                            }
-                        }
+                        for (int q = 0; q < 4; ++q)
+                            g2[q] = mul2(V[q], pk2(1.0f / (cntr * ncf[2 * q]), 1.0f / (cntr * ncf[2 * q + 1])));
                     }
+                    uint32_t l[2] = {0u, 0u};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float ga, gb;
+                        upk2(g2[q], ga, gb);
+                        l[q >> 1] |= (label_of(ga, a.rho_occ, a.rho_emp) | label_of(gb, a.rho_occ, a.rho_emp) << 8)
+                                     << (16 * (q & 1));
+                    }
+                    uint8_t *lp = lab_item + (size_t)(o - oA) * a.C;
+                    if (full8) *reinterpret_cast<uint2 *>(lp) = make_uint2(l[0], l[1]);
+                    else
+                        for (int j = 0; j < 8 && c0 + j < a.C; ++j) lp[j] = (uint8_t)(l[j >> 2] >> (8 * (j & 3)));
                 }
             }
         }
-        g += nst;
+    }
+    // the last warp to finish resets the queue for the next launch
+    if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(&a.ctr[1], 1) == (int)(gridDim.x * ST_WARPS) - 1) {
+            a.ctr[0] = 0;
+            a.ctr[1] = 0;
+        }
     }
 }
 
@@ -300,10 +342,11 @@ __global__ void __launch_bounds__(ENT_THREADS) k_entropy(const float *__restrict
                 }
                 cnt = (float)n;
             }
-            Sc[cls] = s * (1.0f / cnt);   // as the streamed kernel: bit-identical box results
+            Sc[cls] = __fmul_rn(s, 1.0f / cnt);   // as the streamed kernel (no contraction): bit-identical
+
         }
         if (col < C) {
-            const float g = Sc[1] - Sc[0];
+            const float g = __fsub_rn(Sc[1], Sc[0]);
             const size_t o = (size_t)br * C + col;
             if (S) {
                 S[o] = Sc[1];
@@ -401,6 +444,22 @@ __global__ void __launch_bounds__(HT) k_entropy_hist(const uint8_t *__restrict__
     }
 }
 
+template <int H>
+int launch_stream(vsaogm_ctx *c, const CUtensorMap &tm, StreamArgs sa, int band, cudaEvent_t *ev)
+{
+    using Cfg = StCfg<H>;
+    // items of rw output rows (default 16: the 2H halo rows stay a modest fraction of the
+    // staged rows), taken dynamically by all resident warps
+    sa.rw = c->entropy_rw > 0 ? c->entropy_rw : 16;
+    sa.chunks = (band + sa.rw - 1) / sa.rw;
+    sa.ctr = c->d_ent_ctr;
+    const int blocks = c->num_sms * Cfg::BLOCKS_PER_SM;
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_stream<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BLOCK_SMEM));
+    vsa_prof_begin(c, VSAOGM_K_ENTROPY, ev);
+    k_entropy_stream<H><<<blocks, ST_WARPS * 32, Cfg::BLOCK_SMEM, c->stream>>>(tm, sa);
+    return VSAOGM_OK;
+}
+
 }  // namespace
 
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab)
@@ -426,7 +485,8 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
     const int band = c->g_r1 - c->g_r0;
     const int ldh = (c->g_cols + 7) / 8 * 8;
     cudaEvent_t ev;
-    const bool stream_k = p->half_occ == p->half_emp && !p->disk && H <= 4 && c->entropy_kernel != 1;
+    const bool stream_k =
+        p->half_occ == p->half_emp && !p->disk && H <= 4 && lab && !S && c->entropy_kernel != 1;
     if (stream_k) {
         // tensor map over the decoded H_b rows: dims {cols, r_ext, 2 classes}; out-of-bounds
         // boxes are zero-filled (the window clipping)
@@ -435,7 +495,7 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
         CUtensorMap tm;
         cuuint64_t dims[3] = {(cuuint64_t)c->g_cols, (cuuint64_t)c->g_rext, 2};
         cuuint64_t strides[2] = {(cuuint64_t)ldh * 4, (cuuint64_t)c->g_rext * ldh * 4};
-        cuuint32_t box[3] = {(cuuint32_t)ST_W, (cuuint32_t)ST_RS, 2};
+        cuuint32_t box[3] = {(cuuint32_t)ST_W, 1 /* StCfg<H>::RS */, 2};
         cuuint32_t estr[3] = {1, 1, 1};
         if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->d_hb, dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -447,33 +507,18 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
         sa.r_lo = c->g_rlo;
         sa.r0 = c->g_r0;
         sa.band_rows = band;
-        sa.strips = (c->g_cols + 127) / 128;
-        // one wave of work items over the resident warps; at least 16 output rows per item so
-        // that the 2H halo rows stay a small fraction of the staged rows
-        const int warps = c->num_sms * ST_BLOCKS_PER_SM * ST_WARPS;
-        sa.rw = std::max(16, (int)(((int64_t)band * sa.strips + warps - 1) / warps));
-        if (c->entropy_rw > 0) sa.rw = c->entropy_rw;
-        sa.chunks = (band + sa.rw - 1) / sa.rw;
+        sa.strips = (c->g_cols + ST_COLS - 1) / ST_COLS;
         sa.rho_occ = p->rho_occ;
         sa.rho_emp = p->rho_emp;
-        sa.S = S;
         sa.lab = lab;
-        const int items = sa.strips * sa.chunks;
-        const int blocks = std::min((items + ST_WARPS - 1) / ST_WARPS, c->num_sms * ST_BLOCKS_PER_SM);
-        vsa_prof_begin(c, VSAOGM_K_ENTROPY, &ev);
+        int rc = VSAOGM_OK;
         switch (H) {
-#define VSA_ST(HH)                                                                                                 \
-    case HH:                                                                                                       \
-        VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_stream<HH>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                          (int)ST_SMEM));                                                          \
-        k_entropy_stream<HH><<<blocks, ST_WARPS * 32, ST_SMEM, c->stream>>>(tm, sa);                               \
-        break;
-            VSA_ST(1)
-            VSA_ST(2)
-            VSA_ST(3)
-            VSA_ST(4)
-#undef VSA_ST
+        case 1: rc = launch_stream<1>(c, tm, sa, band, &ev); break;
+        case 2: rc = launch_stream<2>(c, tm, sa, band, &ev); break;
+        case 3: rc = launch_stream<3>(c, tm, sa, band, &ev); break;
+        default: rc = launch_stream<4>(c, tm, sa, band, &ev); break;
         }
+        if (rc) return rc;
     } else {
         const int TW = TC + 2 * H, TH = TR + 2 * H;
         const size_t smem = sizeof(float) * (2 * (size_t)TH * TW + 2 * (size_t)TH * TC);

@@ -119,9 +119,12 @@ def test_delta1_create_quadrants_equals_create():
 
 @pytest.mark.parametrize("delta", [1, 2])
 def test_encode_paths_agree(monkeypatch, delta):
-    """The three encode paths (0: counting sort by slot + equal runs, the default; 1: label-split
-    blocks for delta = 1 / slot-filtered for delta > 1; 2: slot-filtered blocks) give the same
-    memories up to fp32 chunk summation order, and the same counts."""
+    """The three encode paths (0: counting sort by slot + equal runs, the default for delta > 1;
+    1: label-split blocks for delta = 1 / slot-filtered for delta > 1; 2: slot-filtered blocks)
+    give the same memories up to fp32 rounding, and the same counts.  The pair (half-angle)
+    kernels pair consecutive points of a slot within their tile or run, so different paths
+    pair some points differently and round those terms differently: each path is within
+    ~1.5e-5 of the fp64 oracle, two paths within 5e-5 of each other."""
     from paper_2408_09066_b200 import Mapper
     sc = Scenario("C2")
     xy, lab = sc.all_points()
@@ -136,20 +139,21 @@ def test_encode_paths_agree(monkeypatch, delta):
         assert list(mems[0][1]) == list(other[1])
         for s in range(2 * delta * delta):
             if mems[0][1][s]:
-                assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 1e-5 * np.linalg.norm(mems[0][0][s])
+                assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 5e-5 * np.linalg.norm(mems[0][0][s])
 
 
 @pytest.mark.parametrize("delta", [1, 2])
 def test_encode_packed_variants_agree(monkeypatch, delta):
-    """The packed fp32x2 encode kernels (VSAOGM_ENC_X2 = 1: uniform 4-warp blocks; 2: all-MUFU
-    warps beside 4-polynomial warps, the default; 3: 1- beside 5-polynomial warps) agree with
-    the scalar kernel (0) up to fp32 rounding: the polynomial phasors (sincos_fma2_lite, max
-    error 1e-6) and the chunking differ, the counts are exact."""
+    """The packed fp32x2 encode kernels (enc_x2 = 1: uniform 4-warp blocks; 2: all-MUFU warps
+    beside 4-polynomial warps; 3: 1- beside 5-polynomial warps; 4: the pair (half-angle)
+    kernels, the default) agree with the scalar kernel (0) up to fp32 rounding: the
+    polynomial phasors (sincos_fma2_lite, max error 1e-6), the pairing and the chunking
+    differ (each within ~1.5e-5 of the oracle), the counts are exact."""
     from paper_2408_09066_b200 import Mapper
     sc = Scenario("C2")
     xy, lab = sc.all_points()
     mems = []
-    for knob in ("0", "1", "2", "3"):
+    for knob in ("0", "1", "2", "3", "4"):
         mp = Mapper(4096, 3, 0.25, sc.bounds, delta=delta)
         mp.set_tuning("enc_x2", int(knob))
         mp.encode_bundle(*_cuda(xy, lab))
@@ -159,4 +163,4 @@ def test_encode_packed_variants_agree(monkeypatch, delta):
         assert list(mems[0][1]) == list(other[1])
         for s in range(2 * delta * delta):
             if mems[0][1][s]:
-                assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 1e-5 * np.linalg.norm(mems[0][0][s])
+                assert np.linalg.norm(mems[0][0][s] - other[0][s]) <= 5e-5 * np.linalg.norm(mems[0][0][s])
