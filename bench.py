@@ -383,6 +383,9 @@ def run_native(args):
                 "peak_basis": enc_roof["basis"], "mufu_only_peak": round(enc_roof["mufu_only"] / 1e9, 2),
                 "frac_of_mufu_only": round(enc_rate / enc_roof["mufu_only"], 4),
                 "frac_of_mufu_only_single_point": round(enc_rate / enc_roof["mufu_only_single"], 4),
+                "measured_loop_ceiling": (round(enc_roof["measured"]["value"] / 1e9, 2) if enc_roof["measured"] else None),
+                "frac_of_measured_loop_ceiling": (round(enc_rate / enc_roof["measured"]["value"], 4)
+                                                  if enc_roof["measured"] else None),
                 "frac_at_measured_clock": (round(enc_rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
                                            if clocks.get("sm_mhz") else None)}
     roofline = enc_line if dominant == "encode" else gemm_roof
@@ -440,7 +443,18 @@ def encode_ceiling(sm_mhz):
     phasor)."""
     m = 16 / 1.5
     per_clk = m + (128 - 4 * m) / 13
-    return {"combined": 148 * per_clk * sm_mhz * 1e6, "mufu_only": 148 * m * sm_mhz * 1e6,
+    measured = None
+    path = os.path.join(ROOT, "profiles", "ubench_pairs.jsonl")
+    if os.path.exists(path):
+        recs = [json.loads(x) for x in open(path) if x.strip().startswith("{")]
+        key = [k for k in recs[0] if k.startswith("phasors_per_clk_per_sm")][0] if recs else None
+        if key:
+            best = max(recs, key=lambda r: r[key])
+            measured = {"per_clk_per_sm": best[key], "npoly_role_b": best["npoly_role_b"],
+                        "value": 148 * best[key] * sm_mhz * 1e6,
+                        "basis": "tools/ubench_pairs.cu: the kernel's bundle loop alone (no staging, no tail), "
+                                 "best warp-role split; profiles/ubench_pairs.jsonl"}
+    return {"combined": 148 * per_clk * sm_mhz * 1e6, "mufu_only": 148 * m * sm_mhz * 1e6, "measured": measured,
             "mufu_only_single": 148 * 8 * sm_mhz * 1e6,
             "basis": f"combined MUFU+FMA-pipe ceiling of the pair encode {per_clk:.2f} phasors/clk/SM x 148 SM x "
                      f"{sm_mhz:.0f} MHz (guide unit counts: 16 MUFU + 128 FMA lanes/clk/SM; DESIGN.md sec. 6)"}

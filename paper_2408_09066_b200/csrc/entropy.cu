@@ -39,35 +39,34 @@ __device__ __forceinline__ int isqrt_floor(int t)
 // Box window, equal radii h1 = h0 = H <= 4 (every BASELINE config: 3x3 / 5x5 / 7x7), labels
 // only (the streaming step's output; a request for the S maps takes the generic kernel).
 // HBM-bound: 8 B read + 1 B written per cell.  Persistent warps take work items from a device
-// queue; an item is one 256-column strip x `rw` output rows of the band, streamed top to
+// queue; an item is one 128-column strip x `rw` output rows of the band, streamed top to
 // bottom:
-//   * lane 0 keeps a private ring of NST = 2H+1 TMA stages of RS rows in flight, each two
-//     cp.async.bulk.tensor.3d boxes of 136 columns x RS rows x both classes (columns -4..131
-//     and 124..259 of the strip: 4 halo columns on each side; a box is at most 256 wide); the
-//     tensor map's bounds are the decoded rows x grid columns, so the TMA zero-fill IS the
-//     window clipping of DESIGN.md L13; per-stage mbarriers, no block barriers, every warp
-//     independent;
-//   * rows go in blocks of U = RS NST rows, U a multiple of W = 2H+1, so the stage slot, the
+//   * lane 0 keeps a private ring of NST = 2H+1 TMA stages of RS = 2 rows in flight
+//     (cp.async.bulk.tensor.3d, box 136 columns x 2 rows x both classes, 4 halo columns on
+//     each side; the tensor map's bounds are the decoded rows x grid columns, so the TMA
+//     zero-fill IS the window clipping of DESIGN.md L13) on per-stage mbarriers -- no block
+//     barriers, every warp independent;
+//   * rows go in blocks of U = RS NST rows (a multiple of W = 2H+1), so the stage slot, the
 //     row inside the stage and the register-ring slot of every row are compile-time;
-//   * each lane owns 8 adjacent columns: per staged row and class it reads its two float4s,
-//     gets the H neighbour columns on each side by warp shuffles (edge lanes: the staged
-//     halo), forms the horizontal (2H+1)-sums as packed fp32x2 sums, and the class difference
+//   * each lane owns 4 adjacent columns: per staged row and class it reads its float4, gets
+//     the H neighbour columns on each side by warp shuffles (edge lanes: the staged halo),
+//     forms the horizontal (2H+1)-sums as packed fp32x2 sums and the class difference
 //     d = h_occ - h_emp; a running vertical sum V += d_new - d_old (the last W differences in
-//     registers) gives S = S_occ - S_emp = V / count for the row W-1 above, then the label.
-// Against the fp64 definition the fp32 rounding of these sums is <= 2e-6 in S.
+//     registers) gives S = S_occ - S_emp = V / count for the row 2H above, then the label.
+// Against the fp64 definition the fp32 rounding of these sums is <= 2e-6 in S (DESIGN.md
+// section 7).
 constexpr int ST_WARPS = 4;                       // warps per block
-constexpr int ST_COLS = 256;                      // output columns per strip (8 per lane)
-constexpr int ST_W = 136;                         // staged floats per box row (4 + 128 + 4)
+constexpr int ST_COLS = 128;                      // output columns per strip (4 per lane)
+constexpr int ST_W = ST_COLS + 8;                 // staged floats per row (4 + 128 + 4)
 
 template <int H>
 struct StCfg {
     static constexpr int W = 2 * H + 1;
-    static constexpr int RS = 1;                              // rows per stage
+    static constexpr int RS = 2;                              // rows per stage
     static constexpr int NST = W;                             // stages per ring
     static constexpr int U = RS * NST;                        // rows per block (multiple of W)
-    static constexpr int BOX_FLOATS = (2 * RS * ST_W + 31) / 32 * 32;     // [class][row][col], 128 B aligned
-    static constexpr int STAGE_FLOATS = 2 * BOX_FLOATS;       // two boxes: strip columns -4.. and 124..
-    static constexpr int STAGE_BYTES = 2 * 2 * RS * ST_W * 4; // TMA bytes per stage
+    static constexpr int STAGE_FLOATS = (2 * RS * ST_W + 31) / 32 * 32;   // [class][row][col], 128 B aligned
+    static constexpr int STAGE_BYTES = 2 * RS * ST_W * 4;     // TMA box bytes
     static constexpr int WARP_BYTES = NST * STAGE_FLOATS * 4;
     static constexpr int BLOCK_SMEM = ST_WARPS * WARP_BYTES;
     static constexpr int BLOCKS_PER_SM = 200 * 1024 / BLOCK_SMEM < 4 ? 200 * 1024 / BLOCK_SMEM : 4;
@@ -117,9 +116,10 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
     __syncwarp();
     const int items = a.strips * a.chunks;
     uint32_t blk = 0;   // row blocks this warp has consumed: every slot is used once per block
-    // this lane's 8 columns: lanes 0-15 in box 0 (strip columns -4..131), 16-31 in box 1 (124..259)
-    const float *lane_base = ring_smem + (lane < 16 ? 0 : Cfg::BOX_FLOATS) + 4 + 8 * (lane & 15);
-    const float *halo_base = lane == 0 ? ring_smem : (lane == 31 ? ring_smem + Cfg::BOX_FLOATS + 132 : lane_base);
+    const float *lane_base = ring_smem + 4 + 4 * lane;        // this lane's 4 columns
+    // one float4 per lane holding its outer halo: lane 0 the 4 columns left of the strip,
+    // lane 31 the 4 columns right of it (other lanes re-read their own, unused)
+    const float *halo_base = ring_smem + (lane == 0 ? 0 : (lane == 31 ? 4 + ST_COLS : 4 + 4 * lane));
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(&a.ctr[0], 1);
@@ -133,26 +133,23 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
         const int nblk = ((oB - oA) + 2 * H + U - 1) / U;     // staged rows rA - H ..., padded
         auto issue = [&](int b, int s) {                      // block b, stage s -> slot s
             mbar_expect_tx(&bar[s], Cfg::STAGE_BYTES);
-            const int trow = rA - H + b * U + s * RS - a.r_lo;
-            tma_load_3d(ring_smem + s * Cfg::STAGE_FLOATS, &tm, &bar[s], col0 - 4, trow, 0);
-            tma_load_3d(ring_smem + s * Cfg::STAGE_FLOATS + Cfg::BOX_FLOATS, &tm, &bar[s], col0 + 124, trow, 0);
+            tma_load_3d(ring_smem + s * Cfg::STAGE_FLOATS, &tm, &bar[s], col0 - 4,
+                        rA - H + b * U + s * RS - a.r_lo, 0);
         };
         if (lane == 0)
             for (int s = 0; s < NST; ++s) issue(0, s);
-        const int c0 = col0 + 8 * lane;
+        const int c0 = col0 + 4 * lane;
         // column clip counts and the interior-row reciprocals 1 / (W nc)
-        float ncf[8];
-        f32x2 inv_in[4];
+        float ncf[4];
+        f32x2 inv_in[2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) ncf[j] = (float)(min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1);
+        for (int j = 0; j < 4; ++j) ncf[j] = (float)(min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) inv_in[q] = pk2(1.0f / ((float)W * ncf[2 * q]), 1.0f / ((float)W * ncf[2 * q + 1]));
-        const bool full8 = c0 + 7 < a.C && (a.C & 7) == 0;
+        for (int q = 0; q < 2; ++q) inv_in[q] = pk2(1.0f / ((float)W * ncf[2 * q]), 1.0f / ((float)W * ncf[2 * q + 1]));
+        const bool full4 = c0 + 3 < a.C && (a.C & 3) == 0;
         uint8_t *lab_item = a.lab + (size_t)oA * a.C + c0;
-        f32x2 ring[W][4];                                     // d = h_occ - h_emp, column pairs
-        f32x2 V[4];                                           // running vertical sums of d
-#pragma unroll
-        for (int q = 0; q < 4; ++q) V[q] = pk2(0.f, 0.f);
+        f32x2 ring[W][2];                                     // d = h_occ - h_emp, column pairs
+        f32x2 V[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};         // running vertical sums of d
         for (int b = 0; b < nblk; ++b, ++blk) {
             const uint32_t par = blk & 1u;
 #pragma unroll
@@ -160,42 +157,39 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
                 const int s = uu / RS, rr = uu % RS, u = uu % W;
                 if (rr == 0) mbar_wait(&bar[s], par);
                 const int soff = s * Cfg::STAGE_FLOATS + rr * ST_W;
-                f32x2 hcls[2][4];
+                f32x2 hcls[2][2];
 #pragma unroll
                 for (int cls = 0; cls < 2; ++cls) {
-                    const float *rp = lane_base + soff + cls * RS * ST_W;
-                    const float4 va = *reinterpret_cast<const float4 *>(rp);
-                    const float4 vb = *reinterpret_cast<const float4 *>(rp + 4);
+                    const float4 v = *reinterpret_cast<const float4 *>(lane_base + soff + cls * RS * ST_W);
                     const float4 hv = *reinterpret_cast<const float4 *>(halo_base + soff + cls * RS * ST_W);
-                    float x[16];                              // columns c0-4 .. c0+11
-                    x[4] = va.x; x[5] = va.y; x[6] = va.z; x[7] = va.w;
-                    x[8] = vb.x; x[9] = vb.y; x[10] = vb.z; x[11] = vb.w;
+                    float x[12];                              // columns c0-4 .. c0+7
+                    x[4] = v.x; x[5] = v.y; x[6] = v.z; x[7] = v.w;
                     {
-                        const float t0 = __shfl_up_sync(0xffffffffu, vb.w, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, va.x, 1);
+                        const float t0 = __shfl_up_sync(0xffffffffu, v.w, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, v.x, 1);
                         x[3] = lane == 0 ? hv.w : t0;
-                        x[12] = lane == 31 ? hv.x : t1;
+                        x[8] = lane == 31 ? hv.x : t1;
                     }
                     if (H >= 2) {
-                        const float t0 = __shfl_up_sync(0xffffffffu, vb.z, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, va.y, 1);
+                        const float t0 = __shfl_up_sync(0xffffffffu, v.z, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, v.y, 1);
                         x[2] = lane == 0 ? hv.z : t0;
-                        x[13] = lane == 31 ? hv.y : t1;
+                        x[9] = lane == 31 ? hv.y : t1;
                     }
                     if (H >= 3) {
-                        const float t0 = __shfl_up_sync(0xffffffffu, vb.y, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, va.z, 1);
+                        const float t0 = __shfl_up_sync(0xffffffffu, v.y, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, v.z, 1);
                         x[1] = lane == 0 ? hv.y : t0;
-                        x[14] = lane == 31 ? hv.z : t1;
+                        x[10] = lane == 31 ? hv.z : t1;
                     }
                     if (H >= 4) {
-                        const float t0 = __shfl_up_sync(0xffffffffu, vb.x, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, va.w, 1);
+                        const float t0 = __shfl_up_sync(0xffffffffu, v.x, 1);
+                        const float t1 = __shfl_down_sync(0xffffffffu, v.w, 1);
                         x[0] = lane == 0 ? hv.x : t0;
-                        x[15] = lane == 31 ? hv.w : t1;
+                        x[11] = lane == 31 ? hv.w : t1;
                     }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {            // columns (2q, 2q+1)
+                    for (int q = 0; q < 2; ++q) {            // columns (2q, 2q+1)
                         f32x2 sh = pk2(x[4 + 2 * q - H], x[5 + 2 * q - H]);
 #pragma unroll
                         for (int dv = -H + 1; dv <= H; ++dv) sh = add2(sh, pk2(x[4 + 2 * q + dv], x[5 + 2 * q + dv]));
@@ -211,36 +205,32 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
                 }
                 const int i = b * U + uu;                     // staged row
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const f32x2 d = add2(hcls[1][q], mul2(hcls[0][q], bc2(-1.f)));   // h_occ - h_emp
+                for (int q = 0; q < 2; ++q) {
+                    const f32x2 d = fma2(hcls[0][q], bc2(-1.f), hcls[1][q]);          // h_occ - h_emp
                     V[q] = add2(V[q], d);
-                    if (i >= W) V[q] = add2(V[q], mul2(ring[u][q], bc2(-1.f)));       // drop row i - W
+                    if (i >= W) V[q] = fma2(ring[u][q], bc2(-1.f), V[q]);            // drop row i - W
                     ring[u][q] = d;
                 }
                 const int o = oA + i - 2 * H;                 // band-relative output row
                 if (i >= 2 * H && o < oB) {                   // warp-uniform
                     const int row = a.r0 + o;
-                    f32x2 g2[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) g2[q] = mul2(V[q], inv_in[q]);
+                    f32x2 g2[2] = {mul2(V[0], inv_in[0]), mul2(V[1], inv_in[1])};
                     if (row < H || row >= a.R - H) {          // clipped rows (grid top / bottom)
                         const float cntr = (float)(min(row + H, a.R - 1) - max(row - H, 0) + 1);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < 2; ++q)
                             g2[q] = mul2(V[q], pk2(1.0f / (cntr * ncf[2 * q]), 1.0f / (cntr * ncf[2 * q + 1])));
                     }
-                    uint32_t l[2] = {0u, 0u};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        float ga, gb;
-                        upk2(g2[q], ga, gb);
-                        l[q >> 1] |= (label_of(ga, a.rho_occ, a.rho_emp) | label_of(gb, a.rho_occ, a.rho_emp) << 8)
-                                     << (16 * (q & 1));
-                    }
+                    float g4[4];
+                    upk2(g2[0], g4[0], g4[1]);
+                    upk2(g2[1], g4[2], g4[3]);
+                    const uint32_t l4 = label_of(g4[0], a.rho_occ, a.rho_emp) | label_of(g4[1], a.rho_occ, a.rho_emp) << 8 |
+                                        label_of(g4[2], a.rho_occ, a.rho_emp) << 16 |
+                                        label_of(g4[3], a.rho_occ, a.rho_emp) << 24;
                     uint8_t *lp = lab_item + (size_t)(o - oA) * a.C;
-                    if (full8) *reinterpret_cast<uint2 *>(lp) = make_uint2(l[0], l[1]);
+                    if (full4) *reinterpret_cast<uint32_t *>(lp) = l4;
                     else
-                        for (int j = 0; j < 8 && c0 + j < a.C; ++j) lp[j] = (uint8_t)(l[j >> 2] >> (8 * (j & 3)));
+                        for (int j = 0; j < 4 && c0 + j < a.C; ++j) lp[j] = (uint8_t)(l4 >> (8 * j));
                 }
             }
         }
@@ -495,7 +485,7 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
         CUtensorMap tm;
         cuuint64_t dims[3] = {(cuuint64_t)c->g_cols, (cuuint64_t)c->g_rext, 2};
         cuuint64_t strides[2] = {(cuuint64_t)ldh * 4, (cuuint64_t)c->g_rext * ldh * 4};
-        cuuint32_t box[3] = {(cuuint32_t)ST_W, 1 /* StCfg<H>::RS */, 2};
+        cuuint32_t box[3] = {(cuuint32_t)ST_W, 2 /* StCfg<H>::RS */, 2};
         cuuint32_t estr[3] = {1, 1, 1};
         if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->d_hb, dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
