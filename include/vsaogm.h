@@ -177,7 +177,7 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
  * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
  * CTA pair, 1 single CTA), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,
- * else the split-K factor), "gemm_l2_hints" (1 default: A evict-first / B evict-last TMA loads), "pipe_early" (0/1), "entropy_kernel"
+ * else the split-K factor), "gemm_l2_hints" (0 none, the default; 1 A evict-first + B evict-last; 2 B evict-last), "pipe_early" (0/1), "entropy_kernel"
  * (0 auto, 1 the generic staged kernel), "entropy_rw" (0 auto, else output rows per
  * work item of the streamed entropy kernel).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
 int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);

@@ -583,7 +583,7 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
         {"gemm_variant", &c->gemm_variant, -1, 1},
         {"gemm_bn", &c->gemm_bn, 0, 256},
         {"gemm_splits", &c->gemm_splits, 0, 64},
-        {"gemm_l2_hints", &c->gemm_l2_hints, 0, 1},
+        {"gemm_l2_hints", &c->gemm_l2_hints, 0, 2},
         {"pipe_early", &c->pipe_early, 0, 1},
         {"entropy_kernel", &c->entropy_kernel, 0, 1},
         {"entropy_rw", &c->entropy_rw, 0, 1 << 20},

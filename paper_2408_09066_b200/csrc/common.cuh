@@ -106,7 +106,7 @@ struct vsaogm_ctx {
     int gemm_variant = -1;  // -1 auto (CTA pair), 0 CTA pair, 1 single CTA (one group only)
     int gemm_bn = 0;        // 0 auto, else the CTA-pair tile width (128..256, multiple of 32)
     int gemm_splits = 0;    // 0 auto, else the split-K factor
-    int gemm_l2_hints = 1;  // TMA L2 eviction hints in the decode GEMM (A evict-first, B evict-last)
+    int gemm_l2_hints = 0;  // TMA L2 eviction hints in the decode GEMM: 0 none (default: no measured gain), 1 A first + B last, 2 B last
     int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
     int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
     int entropy_rw = 0;     // 0 auto, else output rows per streamed work item (test hook)

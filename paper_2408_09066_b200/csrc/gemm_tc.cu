@@ -72,7 +72,7 @@ struct Epi {
     float *ws;         // split-K partials ws[(s * ws_rows + a_row) * ws_cols + col]
     int ws_rows, ws_cols;
     int splits, kb_per;
-    int l2_hints;      // TMA loads with L2 eviction hints (A evict-first, B evict-last)
+    int l2_hints;      // TMA L2 eviction hints: 0 none, 1 A evict-first + B evict-last, 2 B evict-last
 };
 
 __device__ __forceinline__ float hb_of_p(float p)
@@ -359,9 +359,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
-                    if (epi.l2_hints) {
-                        // A (each panel read by one wave) evict-first; B (every panel re-read by
-                        // the next wave, 66 MB at C4 < 126 MB L2) evict-last: B is read from DRAM once
+                    if (epi.l2_hints == 2) {
+                        // B (every panel re-read by the next wave, 66 MB at C4 < 126 MB L2)
+                        // evict-last; A normal (an A panel is shared by the concurrent tiles of its
+                        // m-block row: n-fastest order)
+                        tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow);
+                        tma_load_2d_2sm_hint(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow,
+                                             VSA_L2_EVICT_LAST);
+                    } else if (epi.l2_hints == 1) {   // A evict-first as well (measured: A re-read)
                         tma_load_2d_2sm_hint(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow,
                                              VSA_L2_EVICT_FIRST);
                         tma_load_2d_2sm_hint(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow,
@@ -536,11 +541,14 @@ int launch2_bn(const void *A, const void *B, int a_rows, int b_rows, int K, int 
     return VSAOGM_OK;
 }
 
-// BN minimising (waves x BN): the MMA time of a tile is proportional to BN.
+// BN minimising (waves x BN): the MMA time of a tile is proportional to BN.  When the widest
+// tile already fits one wave, it is kept: narrower tiles would fill more pairs but move more
+// operand bytes per flop from L2 (measured at C3: BN 256 59 us, BN 128 68 us).
 int pick_bn(const Groups &G, int num_sms)
 {
     static const int cands[] = {256, 224, 192, 160, 128};
     const int pairs = num_sms / 2;
+    if (group_tiles(G, 256) <= pairs) return 256;
     int best = 256;
     long best_cost = -1;
     for (int bn : cands) {

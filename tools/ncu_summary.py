@@ -29,7 +29,8 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
-SHORT = {"k_encode_bundle": "encode", "k_decode_gemm": "decode_gemm", "k_entropy": "entropy",
+SHORT = {"k_encode_pairs": "encode", "k_encode_bundle": "encode", "k_decode_gemm": "decode_gemm",
+         "k_entropy": "entropy",
          "k_table<__half2, 1>": "table_A", "k_table<__nv_bfloat162, 1>": "table_A",
          "k_table<__half2, 0>": "table_B", "k_table<__nv_bfloat162, 0>": "table_B",
          "k_reduce_partials": "reduce", "k_commit_norms": "norms", "k_commit": "commit"}
