@@ -91,7 +91,7 @@ def main(tag):
     # quadrant memories (NEXT #1): the C4 step with delta = 2 and 4
     for dl in (2, 4):
         res.append(bench_config("C4", 10, pk, points=Scenario("C4").batch(0), delta=dl))
-    path = os.path.join(ROOT, "profiles", f"{tag}_configs.json")
+    path = os.path.join(ROOT, "gpurun_out", f"{tag}_configs.json")   # copied to profiles/ by hand
     json.dump(res, open(path, "w"), indent=1)
     print(path)
 
