@@ -206,6 +206,9 @@ def run_native(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     mp = Mapper(D, 0, l, sc.bounds)
+    for kv in [x for x in args.tuning.split(",") if x]:   # measurement variants (vsaogm_set_tuning)
+        k, v = kv.split("=")
+        mp.set_tuning(k, int(v))
     ar_ms = []                                   # all-reduce durations (serial loop, world > 1)
 
     def step(b, precision=F16, ar_timer=None):
@@ -397,7 +400,7 @@ def run_native(args):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "f16 MMA operands, fp32 accumulate (decode); fp32 (encode phases / sincos / sums)",
-        "data": "synthetic", "config": workload_config(sc, n_mean, world),
+        "data": "synthetic", "config": dict(workload_config(sc, n_mean, world), **({"tuning": args.tuning} if args.tuning else {})),
         "points_bundled_per_s": round(n_mean / (ms_per_step * 1e-3), 1),
         "decode_cells_per_s_gemm_only": round(cells / (gemm_ms * 1e-3), 1),
         "decode_pct_tensor_peak": round(100 * gemm_tf / pk["bf16_tflops"], 2),
@@ -667,6 +670,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--c5-steps", type=int, default=3)
+    ap.add_argument("--tuning", default="", help="comma-separated key=value library tuning variants (measurement only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -533,12 +533,15 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     const bool early = c->pipe_early != 0;   // tuning variant
     if (early && (rc = vsa_mark_main(c))) return rc;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
-    if ((rc = vsa_launch_table_A(c, G, g->y0, g->res, r_lo, prec, slot0))) return rc;
+    // table A, unless the GEMM generates its A tiles on the fly (gemm_agen)
+    if (!c->gemm_agen && (rc = vsa_launch_table_A(c, G, g->y0, g->res, r_lo, prec, slot0))) return rc;
     // the next encode (encode stream) may start now: pending is committed and the scaled
-    // memories are consumed; it then shares the SMs with this decode's GEMM
+    // memories are consumed (by table A, or read by the GEMM: the next norms kernel, which
+    // rewrites them, is queued after this GEMM on this stream); it then shares the SMs with
+    // this decode's GEMM
     if (!early && (rc = vsa_mark_main(c))) return rc;
     if ((rc = vsa_launch_decode_gemm(c, G, a_rows, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,
-                                     r_lo - g->row_begin, g->row_end - g->row_begin)))
+                                     r_lo - g->row_begin, g->row_end - g->row_begin, slot0, g->y0, g->res, r_lo)))
         return rc;
     c->decoded = true;
     c->g_estimator = c->estimator;
@@ -584,6 +587,7 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
         {"gemm_bn", &c->gemm_bn, 0, 256},
         {"gemm_splits", &c->gemm_splits, 0, 64},
         {"gemm_l2_hints", &c->gemm_l2_hints, 0, 2},
+        {"gemm_agen", &c->gemm_agen, 0, 1},
         {"pipe_early", &c->pipe_early, 0, 1},
         {"entropy_kernel", &c->entropy_kernel, 0, 1},
         {"entropy_rw", &c->entropy_rw, 0, 1 << 20},

@@ -106,6 +106,7 @@ struct vsaogm_ctx {
     int gemm_variant = -1;  // -1 auto (CTA pair), 0 CTA pair, 1 single CTA (one group only)
     int gemm_bn = 0;        // 0 auto, else the CTA-pair tile width (128..256, multiple of 32)
     int gemm_splits = 0;    // 0 auto, else the split-K factor
+    int gemm_agen = 0;      // 1: A phasor tiles generated in the GEMM (no table A)
     int gemm_l2_hints = 0;  // TMA L2 eviction hints in the decode GEMM: 0 none (default: no measured gain), 1 A first + B last, 2 B last
     int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
     int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
@@ -203,7 +204,8 @@ int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int p
 int vsa_launch_table_A(vsaogm_ctx *c, const Groups &G, double y0, double res, int32_t r_lo, int prec,
                        const int *slot0);
 int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32_t N, int prec, float inv_scale,
-                           float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows);
+                           float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows, const int *slot0,
+                           double y0, double res, int32_t r_lo);
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab);
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
                  cudaStream_t s, int num_sms, int variant, int bn = 0, int splits = 0);

@@ -31,6 +31,8 @@
 // k_decode_gemm (1-CTA, M=128 x N=256, single group): the first version, kept as
 //   a measured comparison point (VSAOGM_GEMM=1cta) and for the test hook.
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <stdlib.h>
 #include <string.h>
@@ -73,6 +75,13 @@ struct Epi {
     int ws_rows, ws_cols;
     int splits, kb_per;
     int l2_hints;      // TMA L2 eviction hints: 0 none, 1 A evict-first + B evict-last, 2 B evict-last
+    // A tiles generated on the fly (AGEN kernels): a = s_c Ey_k(y) conj(m_ck), stored as
+    // conj(a) = e^{-i 2 pi ty_k y} mhat_ck = (Re a, -Im a)  (tables.cu layout, no table A)
+    const double *ag_ty;     // theta_y / (2 pi l), turns per metre [Dp]
+    const float2 *ag_mhat;   // sqrt(D) m / ||m|| per slot [S][Dp]
+    double ag_y0, ag_res;    // first grid row's lower edge minus the phase origin c_y; cell size
+    int ag_rlo, ag_Dp, ag_bf16;
+    int ag_slot0[VSA_MAX_GROUPS];   // memory slot of class 0 per group
 };
 
 __device__ __forceinline__ float hb_of_p(float p)
@@ -269,6 +278,117 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
 }
 
+// ------------------------------------------------------------------ phasor tiles on the fly
+// One k-block (32 phasor dimensions = 64 K elements) of this CTA's 128 A rows, written straight
+// into the stage's SWIZZLE_128B K-major tile (the layout the TMA would produce: 16-byte chunk
+// index XOR row % 8 inside 1024-byte atoms).  128 threads (4 warps); thread t: dimension pair
+// kp = t % 16, and two row sequences r = b + 16 i (i = 0..7), b = o + 8 s (s = 0, 1),
+// o = {0, 4, 1, 5, 2, 6, 3, 7}[t / 16] (the two half-warps of a warp write rows 4 apart:
+// disjoint bank halves).  Along a sequence the row phasor advances by a rotation,
+// c(y + 16 res) = c(y) e^{-i 2 pi ty 16 res}; the start of each sequence (and a class change
+// inside it) is evaluated directly from the fp64 turn count, as tables.cu does (7 rotation steps
+// at most: ~1e-6 relative, far below 16-bit rounding).  The per-dimension inputs (turn rates,
+// scaled memories of both classes) are loaded one k-block ahead (AgenIn).
+struct AgenIn {
+    double ty0, ty1;
+    float2 m[2][2];   // [class][dimension k0, k0 + 1]
+};
+
+// prefetch a later k-block's inputs into L1 (no register dependence: the generator never waits on it)
+__device__ __forceinline__ void agen_prefetch(int kb, int t, int g, const Epi &e)
+{
+    const int k0 = kb * 32 + 2 * (t & 15);
+    if (k0 >= e.ag_Dp) return;
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.ag_ty + k0));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.ag_mhat + (size_t)e.ag_slot0[g] * e.ag_Dp + k0));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(e.ag_mhat + (size_t)(e.ag_slot0[g] + 1) * e.ag_Dp + k0));
+}
+
+__device__ __forceinline__ AgenIn agen_load(int kb, int t, int g, const Epi &e)
+{
+    const int k0 = kb * 32 + 2 * (t & 15);
+    AgenIn in;
+    in.ty0 = k0 < e.ag_Dp ? e.ag_ty[k0] : 0.0;
+    in.ty1 = k0 + 1 < e.ag_Dp ? e.ag_ty[k0 + 1] : 0.0;
+#pragma unroll
+    for (int cls = 0; cls < 2; ++cls) {
+        const float2 *mh = e.ag_mhat + (size_t)(e.ag_slot0[g] + cls) * e.ag_Dp;
+        in.m[cls][0] = k0 < e.ag_Dp ? mh[k0] : make_float2(0.f, 0.f);
+        in.m[cls][1] = k0 + 1 < e.ag_Dp ? mh[k0 + 1] : make_float2(0.f, 0.f);
+    }
+    return in;
+}
+
+template <bool BF>
+__device__ __forceinline__ uint32_t agen_pack(float a, float b)
+{
+    if (BF) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__device__ __forceinline__ float2 agen_expm(double turns_per_m, double coord)
+{
+    // e^{-i 2 pi f}, f = turns - rint(turns) in [-1/2, 1/2]
+    const double t = turns_per_m * coord;
+    const double r = __dsub_rn(__dadd_rn(t, 6755399441055744.0), 6755399441055744.0);
+    float sv, cv;
+    __sincosf(6.28318530717958648f * (float)__dsub_rn(t, r), &sv, &cv);
+    return make_float2(cv, -sv);
+}
+
+template <bool BF>
+__device__ __forceinline__ void agen_kblock(uint8_t *tile, int t, const AgenIn &in, const Groups &G, int g,
+                                            int m_base, const Epi &e)
+{
+    const int kp = t & 15;
+    const int q = t >> 4;
+    const int o = (q >> 1) + 4 * (q & 1);
+    const float2 rot0 = agen_expm(in.ty0, 16.0 * e.ag_res), rot1 = agen_expm(in.ty1, 16.0 * e.ag_res);
+    const int nr = G.nrows[g], mrows = G.mrows[g];
+    const uint32_t col_re = (uint32_t)(kp >> 2), col_im = 4u + (uint32_t)(kp >> 2);   // logical 16-byte chunks
+    const uint32_t inchunk = (uint32_t)(kp & 3) * 4u;
+    const double ybase = e.ag_y0 + ((double)(e.ag_rlo + G.row0[g]) + 0.5) * e.ag_res;
+#pragma unroll
+    for (int sq = 0; sq < 2; ++sq) {
+        const int b = o + 8 * sq;                       // first row of the sequence (tile-local)
+        float cr0 = 0.f, ci0 = 0.f, cr1 = 0.f, ci1 = 0.f;
+        int cls_prev = -1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int r = b + 16 * i;
+            const int m_l = m_base + r;                 // group-local A row
+            uint32_t pre = 0u, pim = 0u;
+            if (m_l < mrows) {
+                const int cls = m_l >= nr;
+                if (cls != cls_prev) {                  // sequence start or class change: direct
+                    const double y = ybase + (double)(m_l - cls * nr) * e.ag_res;
+                    const float2 p0 = agen_expm(in.ty0, y), p1 = agen_expm(in.ty1, y);
+                    const float2 m0 = in.m[cls][0], m1 = in.m[cls][1];
+                    cr0 = p0.x * m0.x - p0.y * m0.y;
+                    ci0 = p0.x * m0.y + p0.y * m0.x;
+                    cr1 = p1.x * m1.x - p1.y * m1.y;
+                    ci1 = p1.x * m1.y + p1.y * m1.x;
+                    cls_prev = cls;
+                } else {                                // advance by 16 rows
+                    const float a0 = cr0 * rot0.x - ci0 * rot0.y, b0 = cr0 * rot0.y + ci0 * rot0.x;
+                    const float a1 = cr1 * rot1.x - ci1 * rot1.y, b1 = cr1 * rot1.y + ci1 * rot1.x;
+                    cr0 = a0; ci0 = b0; cr1 = a1; ci1 = b1;
+                }
+                pre = agen_pack<BF>(cr0, cr1);
+                pim = agen_pack<BF>(ci0, ci1);
+            }
+            uint8_t *row = tile + (uint32_t)r * 128u;
+            const uint32_t sw = (uint32_t)(r & 7);
+            *reinterpret_cast<uint32_t *>(row + (((col_re ^ sw) << 4) | inchunk)) = pre;
+            *reinterpret_cast<uint32_t *>(row + (((col_im ^ sw) << 4) | inchunk)) = pim;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ 2-CTA kernel (grouped, split-K)
 // work unit u -> (tile t = u / S, split sk = u % S); tile t -> group g (prefix of the
 // groups' tile counts) -> n-fastest (mb, nb) inside the group.
@@ -284,8 +404,11 @@ __device__ __forceinline__ void unit_coords(int tile, const int *s_pref, const i
 
 // register cap: <= 80 per thread (15 K per CTA) so that a GEMM CTA and three 8-warp encode
 // blocks fit one SM's register file when the streaming pipeline overlaps them (bench: §10)
-template <int MODE, int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
+// AGEN: the A tiles are generated in shared memory by four extra warps per CTA (agen_kblock) instead
+// of TMA-loaded from table A (north_star: "phasor tiles generated on the fly"); the full barrier then
+// counts the B bytes plus the eight generator warps' arrivals of the pair.
+template <int MODE, int BN, bool AGEN = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS + 128 : GEMM_THREADS, AGEN ? 2 : 4)
     k_decode_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ Groups G, int K, uint32_t idesc, Epi epi)
 {
@@ -322,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
         }
         s_pref[ng] = t;
         for (int s = 0; s < STAGES2; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], AGEN ? 9 : 1);   // AGEN: + 4 generator warps x 2 CTAs
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -358,6 +481,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
                 const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    if (AGEN) {
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * BH_BYTES);
+                        tma_load_2d_2sm(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow);
+                        if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (rank == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
                     if (epi.l2_hints == 2) {
                         // B (every panel re-read by the next wave, 66 MB at C4 < 126 MB L2)
@@ -389,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
                 tc_fence_after();
                 const uint32_t d = tmem_base + as * 256;
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    mbar_wait(&full[stage], phase);   // (AGEN: + the generators' release.cluster arrivals)
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b0 = smem_u32(sB + stage * BH_BYTES);
@@ -402,6 +531,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 4)
                 }
                 tc_commit2_mc(&tfull[as]);
                 if (++as == 2) { as = 0; aphase ^= 1; }
+            }
+        }
+    } else if (AGEN && warp >= 6) {
+        // phasor-tile generators: this CTA's 128 A rows of every k-block of every unit; the
+        // inputs of the next k-block are loaded while this one is generated
+        const int t = (warp - 6) * 32 + lane;
+        uint32_t stage = 0, phase = 0;
+        for (int u = pair; u < num_units; u += num_pairs) {
+            const int tile = u / S, sk = u - tile * S;
+            int g, mb, nb;
+            unit_coords(tile, s_pref, s_tn, ng, g, mb, nb);
+            const int m_base = mb * 256 + (int)rank * 128;
+            const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
+            for (int j = 1; j <= 3 && kb0 + j < kb1; ++j) agen_prefetch(kb0 + j, t, g, epi);
+            AgenIn cur = agen_load(kb0, t, g, epi);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                if (kb + 4 < kb1) agen_prefetch(kb + 4, t, g, epi);
+                const AgenIn nxt = agen_load(kb + 1 < kb1 ? kb + 1 : kb, t, g, epi);   // L1 hit
+                // slot free: one lane polls (the arrival is the MMA's commit; a CTA-scope acquire
+                // suffices for the write-after-read, and a cluster-scope acquire per thread would
+                // invalidate L1 on every poll)
+                if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
+                __syncwarp();
+                if (epi.ag_bf16) agen_kblock<true>(sA + stage * A_BYTES, t, cur, G, g, m_base, epi);
+                else agen_kblock<false>(sA + stage * A_BYTES, t, cur, G, g, m_base, epi);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> UMMA reads
+                __syncwarp();
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive(&full[stage]);
+                    else mbar_arrive_cluster(&full[stage], 0);
+                }
+                if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                cur = nxt;
             }
         }
     } else {
@@ -517,21 +679,28 @@ long group_tiles(const Groups &G, int bn)
 
 template <int MODE, int BN>
 int launch2_bn(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, Epi epi,
-               cudaStream_t s, int num_sms)
+               cudaStream_t s, int num_sms, bool agen)
 {
     CUtensorMap ta, tb;
-    int rc = make_map(&ta, A, a_rows, K, 128, prec);
+    int rc = make_map(&tb, B, b_rows, K, BN / 2, prec);
     if (rc) return rc;
-    rc = make_map(&tb, B, b_rows, K, BN / 2, prec);
-    if (rc) return rc;
+    if (agen) ta = tb;   // unused: the A tiles are generated in shared memory
+    else if ((rc = make_map(&ta, A, a_rows, K, 128, prec))) return rc;
     const size_t smem = 1024 + (size_t)STAGES2 * (128 + BN / 2) * VSA_BK * 2 + 256;
-    VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long units = group_tiles(G, BN) * epi.splits;
     const int pairs = num_sms / 2;
     const int grid = 2 * (int)(units < pairs ? units : pairs);
     if (grid == 0) return VSAOGM_OK;
     const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, 256, BN);
-    k_decode_gemm2<MODE, BN><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, G, K, idesc, epi);
+    if (agen) {
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        k_decode_gemm2<MODE, BN, true><<<grid, GEMM_THREADS + 128, smem, s>>>(ta, tb, G, K, idesc, epi);
+    } else {
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        k_decode_gemm2<MODE, BN><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, G, K, idesc, epi);
+    }
     VSA_CUDA_TRY(cudaGetLastError());
     if (epi.splits > 1) {
         const size_t RC = (size_t)epi.ws_rows * epi.ws_cols;
@@ -581,14 +750,14 @@ int pick_splits(const Groups &G, int ws_rows, int ws_cols, int K, int bn, int nu
 
 template <int MODE>
 int launch2(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, const Epi &epi,
-            cudaStream_t s, int num_sms, int bn)
+            cudaStream_t s, int num_sms, int bn, bool agen)
 {
     switch (bn) {
-    case 224: return launch2_bn<MODE, 224>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
-    case 192: return launch2_bn<MODE, 192>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
-    case 160: return launch2_bn<MODE, 160>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
-    case 128: return launch2_bn<MODE, 128>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
-    default: return launch2_bn<MODE, 256>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    case 224: return launch2_bn<MODE, 224>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
+    case 192: return launch2_bn<MODE, 192>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
+    case 160: return launch2_bn<MODE, 160>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
+    case 128: return launch2_bn<MODE, 128>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
+    default: return launch2_bn<MODE, 256>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
     }
 }
 
@@ -598,9 +767,9 @@ int launch2(const void *A, const void *B, int a_rows, int b_rows, int K, int pre
 template <int MODE>
 int launch(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, Epi epi,
            cudaStream_t s, int num_sms, int variant, float **ws, size_t *ws_cap, int bn_force = 0,
-           int splits_force = 0)
+           int splits_force = 0, bool agen = false)
 {
-    if (variant == 1 && G.n == 1) return launch1<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
+    if (variant == 1 && G.n == 1 && !agen) return launch1<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms);
     int bn = pick_bn(G, num_sms);
     if (bn_force > 0) bn = bn_force;
     epi.ws_rows = a_rows;
@@ -622,13 +791,14 @@ int launch(const void *A, const void *B, int a_rows, int b_rows, int K, int prec
         }
         epi.ws = *ws;
     }
-    return launch2<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, bn);
+    return launch2<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, bn, agen);
 }
 
 }  // namespace
 
 int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32_t N, int prec, float inv_scale,
-                           float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows)
+                           float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows, const int *slot0,
+                           double y0, double res, int32_t r_lo)
 {
     Epi e{};
     e.inv_scale = inv_scale;
@@ -643,10 +813,21 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
     e.splits = 1;
     e.kb_per = c->Kp / VSA_BK;
     e.l2_hints = c->gemm_l2_hints;
+    const bool agen = c->gemm_agen != 0;
+    if (agen) {
+        e.ag_ty = c->d_ty_turns;
+        e.ag_mhat = c->d_mhat;
+        e.ag_y0 = y0 - c->cy;
+        e.ag_res = res;
+        e.ag_rlo = r_lo;
+        e.ag_Dp = c->Dp;
+        e.ag_bf16 = prec == VSAOGM_BF16;
+        for (int g = 0; g < G.n; ++g) e.ag_slot0[g] = slot0[g];
+    }
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_DECODE_GEMM, &ev);
     int rc = launch<1>(c->d_A, c->d_B, a_rows, N, c->Kp, prec, G, e, c->stream, c->num_sms, c->gemm_variant, &c->d_ws,
-                       &c->ws_cap, c->gemm_bn, c->gemm_splits);
+                       &c->ws_cap, c->gemm_bn, c->gemm_splits, agen);
     if (rc) return rc;
     vsa_prof_end(c, VSAOGM_K_DECODE_GEMM, ev);
     c->launches++;

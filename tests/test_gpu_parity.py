@@ -558,3 +558,42 @@ def test_encode_stream_pipeline_matches_serial():
     assert torch.equal(a[2], b[2])
     assert torch.equal(a[3], b[3])
     assert np.array_equal(a[4][0], b[4][0]) and list(a[4][1]) == list(b[4][1])
+
+
+@pytest.mark.parametrize("delta,prec", [(1, 0), (1, 1), (2, 0)])
+def test_gemm_phasor_tiles_on_the_fly(delta, prec):
+    """gemm_agen = 1: the decode GEMM generates its A phasor tiles in shared memory (row
+    recurrence, no table A).  q equals the table-A decode within the 16-bit operand rounding
+    (1e-3 of peak fp16, 2e-2 bf16) and the oracle within the north_star bounds, on a full grid
+    with a class boundary inside an A tile, on a row band with halo rows (split-K), and with
+    quadrant memories (grouped GEMM); labels agree."""
+    from paper_2408_09066_b200 import Mapper
+    sc = Scenario("C2")
+    xy, lab = sc.all_points()
+    cfg = sc.cfg
+    D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], 333, cfg["res"]
+    tau = label_tau(D)
+    mp = Mapper(D, 0, l, sc.bounds, delta=delta)
+    mp.encode_bundle(*_cuda(xy, lab))
+    outs = {}
+    for agen in (0, 1):
+        mp.set_tuning("gemm_agen", agen)
+        for (r0, r1) in ((0, R), (150, 250)):
+            q = torch.empty((2, r1 - r0, C), dtype=torch.float32, device="cuda")
+            mp.decode(0.0, 0.0, res, R, C, r0, r1, h, precision=prec, q_out=q)
+            L = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
+            mp.entropy(h, h, tau, -tau, 0, None, L)
+            outs[(agen, r0)] = (q.cpu().numpy().astype(np.float64), L.cpu().numpy())
+    assert mp.sync() == 0
+    mp.close()
+    tol = Q_TOL[prec]
+    for r0 in (0, 150):
+        qa, La = outs[(0, r0)]
+        qb, Lb = outs[(1, r0)]
+        assert _qerr(qb, qa) <= tol, _qerr(qb, qa)
+        assert (La == Lb).mean() >= 0.999
+    if delta == 1:
+        tx, ty = oracle.theta(0, D)
+        mo, _, _ = oracle.encode(tx, ty, l, xy, lab)
+        qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, 0, R, 0, C)
+        assert _qerr(outs[(1, 0)][0], qo) <= tol

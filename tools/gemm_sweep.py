@@ -45,7 +45,8 @@ def main():
         tf = flops / (ms * 1e-3) / 1e12
         print(json.dumps({"cfg": sc.name, "spec": spec, "gemm_us": round(1e3 * ms, 2), "tflops": round(tf, 1),
                           "frac_burst": round(tf / pk["bf16_tflops"], 4),
-                          "table_A_us": round(1e3 * prof["table_A"][0] / prof["table_A"][1], 2)}), flush=True)
+                          "table_A_us": round(1e3 * prof["table_A"][0] / prof["table_A"][1], 2) if prof["table_A"][1] else 0.0}),
+              flush=True)
         for kv in [x for x in spec.split(",") if x]:
             mp.set_tuning(kv.split("=")[0], 0 if kv.split("=")[0] != "gemm_l2_hints" else 1)
     mp.close()
