@@ -48,9 +48,10 @@ __device__ __forceinline__ int isqrt_floor(int t)
 //     barriers, every warp independent;
 //   * rows go in blocks of U = RS NST rows (a multiple of W = 2H+1), so the stage slot, the
 //     row inside the stage and the register-ring slot of every row are compile-time;
-//   * each lane owns 4 adjacent columns: per staged row and class it reads its float4, gets
-//     the H neighbour columns on each side by warp shuffles (edge lanes: the staged halo),
-//     forms the horizontal (2H+1)-sums as packed fp32x2 sums and the class difference
+//   * each lane owns 4 adjacent columns: per staged row and class it reads its float4 and the
+//     H neighbour columns on each side straight from the staged row (no shuffles: shared
+//     memory has the bandwidth, the issue slots are the limit), forms the first horizontal
+//     (2H+1)-sum in order and the next three by sliding, and the class difference
 //     d = h_occ - h_emp; a running vertical sum V += d_new - d_old (the last W differences in
 //     registers) gives S = S_occ - S_emp = V / count for the row 2H above, then the label.
 // Against the fp64 definition the fp32 rounding of these sums is <= 2e-6 in S (DESIGN.md
@@ -117,9 +118,6 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
     const int items = a.strips * a.chunks;
     uint32_t blk = 0;   // row blocks this warp has consumed: every slot is used once per block
     const float *lane_base = ring_smem + 4 + 4 * lane;        // this lane's 4 columns
-    // one float4 per lane holding its outer halo: lane 0 the 4 columns left of the strip,
-    // lane 31 the 4 columns right of it (other lanes re-read their own, unused)
-    const float *halo_base = ring_smem + (lane == 0 ? 0 : (lane == 31 ? 4 + ST_COLS : 4 + 4 * lane));
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(&a.ctr[0], 1);
@@ -140,16 +138,17 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
             for (int s = 0; s < NST; ++s) issue(0, s);
         const int c0 = col0 + 4 * lane;
         // column clip counts and the interior-row reciprocals 1 / (W nc)
-        float ncf[4];
-        f32x2 inv_in[2];
+        float ncf[4], inv_in[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ncf[j] = (float)(min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) inv_in[q] = pk2(1.0f / ((float)W * ncf[2 * q]), 1.0f / ((float)W * ncf[2 * q + 1]));
+        for (int j = 0; j < 4; ++j) {
+            ncf[j] = (float)(min(c0 + j + H, a.C - 1) - max(c0 + j - H, 0) + 1);
+            inv_in[j] = 1.0f / ((float)W * ncf[j]);
+        }
         const bool full4 = c0 + 3 < a.C && (a.C & 3) == 0;
         uint8_t *lab_item = a.lab + (size_t)oA * a.C + c0;
-        f32x2 ring[W][2];                                     // d = h_occ - h_emp, column pairs
-        f32x2 V[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};         // running vertical sums of d
+        float ring[W][4];                                     // d = h_occ - h_emp of the last W rows
+        float V[4] = {0.f, 0.f, 0.f, 0.f};                    // running vertical sums of d
+        uint8_t *lp = lab_item - (size_t)2 * H * a.C;         // label row of staged row i: lp + i C
         for (int b = 0; b < nblk; ++b, ++blk) {
             const uint32_t par = blk & 1u;
 #pragma unroll
@@ -157,80 +156,64 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
                 const int s = uu / RS, rr = uu % RS, u = uu % W;
                 if (rr == 0) mbar_wait(&bar[s], par);
                 const int soff = s * Cfg::STAGE_FLOATS + rr * ST_W;
-                f32x2 hcls[2][2];
+                float hs[2][4];
 #pragma unroll
                 for (int cls = 0; cls < 2; ++cls) {
-                    const float4 v = *reinterpret_cast<const float4 *>(lane_base + soff + cls * RS * ST_W);
-                    const float4 hv = *reinterpret_cast<const float4 *>(halo_base + soff + cls * RS * ST_W);
-                    float x[12];                              // columns c0-4 .. c0+7
+                    // columns c0-H .. c0+3+H straight from the staged row (halo included: no shuffles)
+                    const float *rp = lane_base + soff + cls * RS * ST_W;
+                    float x[12];                              // x[4 + j] = column c0 + j
+                    const float4 v = *reinterpret_cast<const float4 *>(rp);
                     x[4] = v.x; x[5] = v.y; x[6] = v.z; x[7] = v.w;
-                    {
-                        const float t0 = __shfl_up_sync(0xffffffffu, v.w, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, v.x, 1);
-                        x[3] = lane == 0 ? hv.w : t0;
-                        x[8] = lane == 31 ? hv.x : t1;
+                    if (H <= 2) {
+                        const float2 l2 = *reinterpret_cast<const float2 *>(rp - 2);
+                        const float2 r2 = *reinterpret_cast<const float2 *>(rp + 4);
+                        x[2] = l2.x; x[3] = l2.y; x[8] = r2.x; x[9] = r2.y;
+                    } else {
+                        const float4 l4 = *reinterpret_cast<const float4 *>(rp - 4);
+                        const float4 r4 = *reinterpret_cast<const float4 *>(rp + 4);
+                        x[0] = l4.x; x[1] = l4.y; x[2] = l4.z; x[3] = l4.w;
+                        x[8] = r4.x; x[9] = r4.y; x[10] = r4.z; x[11] = r4.w;
                     }
-                    if (H >= 2) {
-                        const float t0 = __shfl_up_sync(0xffffffffu, v.z, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, v.y, 1);
-                        x[2] = lane == 0 ? hv.z : t0;
-                        x[9] = lane == 31 ? hv.y : t1;
-                    }
-                    if (H >= 3) {
-                        const float t0 = __shfl_up_sync(0xffffffffu, v.y, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, v.z, 1);
-                        x[1] = lane == 0 ? hv.y : t0;
-                        x[10] = lane == 31 ? hv.z : t1;
-                    }
-                    if (H >= 4) {
-                        const float t0 = __shfl_up_sync(0xffffffffu, v.x, 1);
-                        const float t1 = __shfl_down_sync(0xffffffffu, v.w, 1);
-                        x[0] = lane == 0 ? hv.x : t0;
-                        x[11] = lane == 31 ? hv.w : t1;
-                    }
+                    // horizontal (2H+1)-sums: the first in order, the next three sliding
+                    float h0 = x[4 - H];
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {            // columns (2q, 2q+1)
-                        f32x2 sh = pk2(x[4 + 2 * q - H], x[5 + 2 * q - H]);
+                    for (int dv = -H + 1; dv <= H; ++dv) h0 += x[4 + dv];
+                    hs[cls][0] = h0;
 #pragma unroll
-                        for (int dv = -H + 1; dv <= H; ++dv) sh = add2(sh, pk2(x[4 + 2 * q + dv], x[5 + 2 * q + dv]));
-                        hcls[cls][q] = sh;
-                    }
+                    for (int j = 1; j < 4; ++j) hs[cls][j] = (hs[cls][j - 1] - x[3 + j - H]) + x[4 + j + H];
                 }
                 if (rr == RS - 1) {                           // stage s consumed: refill for block b+1
+                    // every lane's reads of the stage have completed (their values were consumed
+                    // by the sums above), so the TMA may overwrite it once the warp reconverges
                     __syncwarp();
-                    if (lane == 0 && b + 1 < nblk) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        issue(b + 1, s);
-                    }
+                    if (lane == 0 && b + 1 < nblk) issue(b + 1, s);
                 }
                 const int i = b * U + uu;                     // staged row
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const f32x2 d = fma2(hcls[0][q], bc2(-1.f), hcls[1][q]);          // h_occ - h_emp
-                    V[q] = add2(V[q], d);
-                    if (i >= W) V[q] = fma2(ring[u][q], bc2(-1.f), V[q]);            // drop row i - W
-                    ring[u][q] = d;
+                for (int j = 0; j < 4; ++j) {
+                    const float d = hs[1][j] - hs[0][j];     // h_occ - h_emp
+                    V[j] += d;
+                    if (i >= W) V[j] -= ring[u][j];           // drop row i - W
+                    ring[u][j] = d;
                 }
                 const int o = oA + i - 2 * H;                 // band-relative output row
                 if (i >= 2 * H && o < oB) {                   // warp-uniform
                     const int row = a.r0 + o;
-                    f32x2 g2[2] = {mul2(V[0], inv_in[0]), mul2(V[1], inv_in[1])};
+                    float g4[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) g4[j] = V[j] * inv_in[j];
                     if (row < H || row >= a.R - H) {          // clipped rows (grid top / bottom)
                         const float cntr = (float)(min(row + H, a.R - 1) - max(row - H, 0) + 1);
 #pragma unroll
-                        for (int q = 0; q < 2; ++q)
-                            g2[q] = mul2(V[q], pk2(1.0f / (cntr * ncf[2 * q]), 1.0f / (cntr * ncf[2 * q + 1])));
+                        for (int j = 0; j < 4; ++j) g4[j] = V[j] * (1.0f / (cntr * ncf[j]));
                     }
-                    float g4[4];
-                    upk2(g2[0], g4[0], g4[1]);
-                    upk2(g2[1], g4[2], g4[3]);
                     const uint32_t l4 = label_of(g4[0], a.rho_occ, a.rho_emp) | label_of(g4[1], a.rho_occ, a.rho_emp) << 8 |
                                         label_of(g4[2], a.rho_occ, a.rho_emp) << 16 |
                                         label_of(g4[3], a.rho_occ, a.rho_emp) << 24;
-                    uint8_t *lp = lab_item + (size_t)(o - oA) * a.C;
-                    if (full4) *reinterpret_cast<uint32_t *>(lp) = l4;
+                    uint8_t *lrow = lp + (size_t)i * a.C;
+                    if (full4) *reinterpret_cast<uint32_t *>(lrow) = l4;
                     else
-                        for (int j = 0; j < 4 && c0 + j < a.C; ++j) lp[j] = (uint8_t)(l4 >> (8 * j));
+                        for (int j = 0; j < 4 && c0 + j < a.C; ++j) lrow[j] = (uint8_t)(l4 >> (8 * j));
                 }
             }
         }
