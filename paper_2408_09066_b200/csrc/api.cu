@@ -223,7 +223,9 @@ void vsaogm_destroy(vsaogm_ctx *c)
     void *ptrs[] = {c->d_wx, c->d_wy, c->d_tx_turns, c->d_ty_turns, c->d_m, c->d_pending, c->d_counts,
                     c->d_norm2, c->d_mhat, c->d_normpart, c->d_err, c->d_ent_ctr, c->d_part, c->d_part_cnt, c->d_stage_xy, c->d_stage_lab, c->d_A,
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
-                    c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code};
+                    c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code, c->d_nu_grid, c->d_nu_f1, c->d_nu_G,
+                    c->d_nu_psi, c->d_nu_tw, c->d_nu_ph, c->d_nu_out, c->d_nu_bins,
+                    c->d_nu_key, c->d_nu_sorted, c->d_nu_units};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -575,6 +577,7 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
         {"enc_pairs_npoly", &c->enc_pairs_npoly, 0, 8},
         {"enc_pairs_minb", &c->enc_pairs_minb, 3, 4},
         {"enc_pairs_split", &c->enc_pairs_split, 0, 1},
+        {"enc_method", &c->enc_method, 0, 1},
         {"enc_x2_minb", &c->enc_x2_minb, 3, 4},
         {"enc_x2_waves", &c->enc_x2_waves, 1, 64},
         {"enc_npoly", &c->enc_npoly, 0, 4},

@@ -97,7 +97,19 @@ struct vsaogm_ctx {
     int enc_x2 = 4;
     int enc_pairs_npoly = 4;  // FMA-pipe dimensions of 8 in the pair kernel's second warp role
     int enc_pairs_minb = 3;   // resident pair-kernel blocks per SM (3: 80 registers, no spills)
-    int enc_pairs_split = 1;  // 1 (default): one class per block (k_encode_pairs1, 64 registers, 4 per SM)
+    int enc_pairs_split = 1;
+    // encode method: 0 direct (pair kernels), 1 type-3 NUFFT (nufft.cu; delta = 1, D >= 2048)
+    int enc_method = 0;
+    bool nu_ready = false;
+    double nu_h = 0, nu_tau = 0, nu_tau2 = 0, nu_lo = 0;
+    int nu_n1 = 0, nu_logn = 0, nu_ntx = 0;
+    void *d_nu_grid = nullptr, *d_nu_f1 = nullptr, *d_nu_G = nullptr;   // int64 tile windows, f32x2 [2][N][n1], [2][N][N]
+    int *d_nu_bins = nullptr;   // bin counts [nb], offsets [nb + 1], unit offsets [nb + 1], unit count [1]
+    int *d_nu_units = nullptr;  // unit -> bin, unit -> first point
+    void *d_nu_key = nullptr, *d_nu_sorted = nullptr; size_t nu_pts_cap = 0;   // per-point (bin, slot); binned points
+    float *d_nu_psi = nullptr;                                         // 1 / psi^(l - n1/2)
+    void *d_nu_tw = nullptr, *d_nu_ph = nullptr;                       // twiddles, centring phases
+    int *d_nu_out = nullptr; size_t nu_out_cap = 0;                    // outliers per chunk  // 1 (default): one class per block (k_encode_pairs1, 64 registers, 4 per SM)
     int enc_x2_npoly = 4;   // polynomial dimensions of 8 in the second warp role
     int enc_x2_waves = 4;   // waves of packed encode blocks (dynamic SM balance vs partials)
     int enc_x2_minb = 4;    // resident 8-warp blocks per SM (4: 64 registers, the default; 3: 80)
@@ -198,6 +210,10 @@ void vsa_prof_end(vsaogm_ctx *c, int kid, cudaEvent_t a);
 // ---- launchers implemented in the kernel translation units -----------------
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
 int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
+int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
+                            int chunks);
+int vsa_launch_nufft_outliers(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
+                              int chunks);
 int vsa_launch_commit(vsaogm_ctx *c);
 int vsa_launch_norms(vsaogm_ctx *c, int do_commit);   // [commit +] norms + scaled memory mhat
 int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec);

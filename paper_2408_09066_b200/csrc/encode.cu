@@ -406,12 +406,24 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs(
 // registers lighter (64 registers, 4 blocks per SM without spills, so that three blocks fit
 // beside a decode-GEMM CTA in the pipelined schedule).  Every block stages the whole tile and
 // keeps its class's points (in order), so the per-dimension sums are those of k_encode_pairs.
-template <int THREADS, int NPA, int NPB, int MINB>
+// OUTL (NUFFT fallback, nufft.cu): only the points outside the NUFFT grid are bundled, a chunk
+// without such points exits at once, and the block's sums are added to the pending memories
+// directly (fp64 atomics: the order of the chunks' additions is not fixed, L16).
+struct NuOutl {
+    double lo, inv_h;
+    int n1;
+    const int *out_cnt;
+    double *pending;
+    int D;
+};
+
+template <int THREADS, int NPA, int NPB, int MINB, bool OUTL = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs1(
     const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n, int64_t chunk_pts,
     const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
-    float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err)
+    float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err, NuOutl nu = NuOutl{})
 {
+    if (OUTL && nu.out_cnt[blockIdx.y] == 0) return;   // block-uniform
     constexpr int KT = 8;
     constexpr int NW = THREADS / 32;
     constexpr int TILE = THREADS;
@@ -455,6 +467,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs1(
                 if (!(isfinite(v.x) && isfinite(v.y))) { code = 2; my_err |= VSA_ERRBIT_NONFINITE; }
                 mine = code == cls;
                 rec = make_double2((double)v.x - cx, (double)v.y - cy);
+                if (OUTL && mine) {   // the same fp64 expression as k_nu_spread's grid test
+                    const int ix = (int)floor((rec.x - nu.lo) * nu.inv_h), iy = (int)floor((rec.y - nu.lo) * nu.inv_h);
+                    mine = ix - 6 < 0 || iy - 6 < 0 || ix + 7 >= nu.n1 || iy + 7 >= nu.n1;
+                }
             }
             const unsigned b = __ballot_sync(0xffffffffu, mine);
             if (lane == 0) s_g[warp] = __popc(b);
@@ -485,16 +501,25 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs1(
 #pragma unroll
         for (int j = 0; j < KT; ++j) {
             const int k = kbase + j * THREADS;
-            if (k < Dp) part[((size_t)chunk * 2 + cls) * Dp + k] = acc.get(j);
+            if (OUTL) {
+                if (k < nu.D) {
+                    const float2 v = acc.get(j);
+                    atomicAdd(nu.pending + 2 * ((size_t)cls * Dp + k), (double)v.x);
+                    atomicAdd(nu.pending + 2 * ((size_t)cls * Dp + k) + 1, (double)v.y);
+                }
+            } else if (k < Dp) {
+                part[((size_t)chunk * 2 + cls) * Dp + k] = acc.get(j);
+            }
         }
     };
     if (role_b) run(PairAcc<KT, NPB>{});
     else run(PairAcc<KT, NPA>{});
-    if (kb == 0) {
+    if (!OUTL && kb == 0) {
         if (my_err && cls == 0) atomicOr(err, my_err);
         if (tid == 0) part_cnt[chunk * 2 + cls] = cn;
     }
 }
+
 
 // Quadrant routing (delta > 1; Alg. 1): slot = 2 beta + psi with
 // beta the nearest quadrant centre in fp64 squared distance, ties to the lowest
@@ -760,12 +785,38 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
 
 }  // namespace
 
+int vsa_launch_nufft_outliers(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
+                              int chunks)
+{
+    NuOutl nu{c->nu_lo, 1.0 / c->nu_h, c->nu_n1, c->d_nu_out, c->d_pending, c->D};
+    const int kblocks = (c->Dp + 2047) / 2048;
+    k_encode_pairs1<256, 0, 4, 4, true><<<dim3(kblocks, chunks, 2), 256, 0, c->stream>>>(
+        (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, nullptr, nullptr, c->d_err, nu);
+    VSA_CUDA_TRY(cudaGetLastError());
+    c->launches++;
+    return VSAOGM_OK;
+}
+
 int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n)
 {
     // default (enc_path 0): counting sort by slot + equal runs (encode_sorted.cu).
     // Measured alternatives kept as tuning variants: enc_path 1 = label-split blocks
     // (delta = 1) / slot-filtered blocks (delta > 1); enc_path 2 = slot-filtered always.
     if (c->enc_path == 0 || (c->enc_path < 0 && c->nslots > 2)) return vsa_launch_encode_sorted(c, xy, lab, n);
+    if (c->enc_method == 1 && c->nslots == 2 && c->Dp >= 2048) {
+        // type-3 NUFFT (nufft.cu) + direct fallback for the points outside its grid; the chunks
+        // are those of the direct kernel (4 waves of 4 blocks per SM over the k-blocks)
+        const int kblocks = (c->Dp + 2047) / 2048;
+        int64_t chunks = std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 4 * 4 / (2 * kblocks), (n + 63) / 64));
+        const int64_t chunk_pts = (n + chunks - 1) / chunks;
+        chunks = (n + chunk_pts - 1) / chunk_pts;
+        cudaEvent_t ev;
+        vsa_prof_begin(c, VSAOGM_K_ENCODE, &ev);
+        int rc = vsa_launch_encode_nufft(c, xy, lab, n, chunk_pts, (int)chunks);
+        if (!rc) rc = vsa_launch_nufft_outliers(c, xy, lab, n, chunk_pts, (int)chunks);
+        vsa_prof_end(c, VSAOGM_K_ENCODE, ev);
+        return rc;
+    }
     const bool slots_path = c->nslots > 2 || c->enc_path == 2;
     const int KT = (!slots_path && c->enc_kt == 16 && c->Dp >= 2048) ? 16 : (c->Dp >= 1024 ? 8 : 4);
     // packed kernel: 128 threads (enc_x2 = 1) or 8-warp role variants (2, 3: 2048 dims per block)

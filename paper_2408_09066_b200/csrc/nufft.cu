@@ -1,0 +1,502 @@
+// nufft.cu -- the encode (K2, Eq. 9 + Eq. 5, Alg. 1 with delta = 1) as a type-3 non-uniform FFT.
+//
+//   pending_{c,k} += sum_{i : psi_i = c} exp(i (w^x_k x_i + w^y_k y_i)),  w = theta / l,
+//   (x_i, y_i) centred on the bounds centre (PAPER.md:252-258 Eq. 9, :216-219 Eq. 5).
+//
+// The direct encode evaluates N x D phasors (k_encode_pairs1: 1.5 MUFU ops each).  The same sums
+// are a 2-D type-3 NUFFT: points x_i (in the world box) to frequencies s_k = w_k (|s| <= pi / l).
+// Following the gridding formulation (Dutt & Rokhlin; Greengard & Lee 2004; Lee & Greengard 2005):
+//   1. spread: b(g) = sum_i phi(g h - x_i) on a fine grid of spacing h = pi / (sigma S) = l / 2
+//      (sigma = 2, S = pi / l), Gaussian phi(u) = exp(-|u|^2 / (4 tau)), 14 x 14 cells per point,
+//      accumulated in 32.32 fixed point (int64 atomics: exact, so the result does not depend on
+//      the order of the additions -- the L16 reproducibility of the fp64 reductions);
+//   2. B(s) = h^2 sum_g b(g) e^{i s.g h} is a type-2 NUFFT at the targets t_k = s_k h in
+//      [-pi/2, pi/2]^2: pre-correct b by 1 / psi^(l) (the Gaussian psi of the interpolation),
+//      zero-pad to n2 = 2^p >= 2 n1 and take a 2-D FFT (own radix-2 Stockham kernels, rows then
+//      columns), then interpolate at t_k over 13 x 13 grid points;
+//   3. pending += B(s_k) / Phi(s_k), Phi = 4 pi tau exp(-|s|^2 tau) (the FT of phi).
+// Accuracy (Gaussian gridding, msp = 6 both steps): ~1e-6 relative in l2 over k, below the fp32
+// direct encode's ~1.5e-5.
+// Points outside the grid (world bounds + margin) are bundled by the direct pair kernel
+// (k_encode_nufft_outliers), chunk by chunk.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int NU_MSP = 6;               // spreading half-width: cells ix-6 .. ix+7 (14)
+constexpr int NU_W = 2 * NU_MSP + 2;    // 14
+constexpr int NU_MSP2 = 6;              // interpolation half-width: m0-6 .. m0+6 (13)
+constexpr double NU_FIX = 4294967296.0; // 2^32: fixed-point scale of the spread grid
+
+// ---- 1. spreading --------------------------------------------------------------------------
+// The fine grid is cut into NU_TS x NU_TS tiles; a point belongs to the tile of its cell and
+// spreads into the tile's window (the tile plus 6 cells before and 7 after, per axis).
+// (a) k_nu_bin: class / validity, cell, tile; per-(class, tile) counts (the atomic's return
+//     value is the point's slot inside its bin, warp-aggregated); outliers (support off the grid) counted per
+//     chunk for the direct fallback; valid points counted per class (integer sums: exact).
+// (b) k_nu_scan: exclusive prefix of the bin counts (one block).
+// (c) k_nu_place: each point to its bin's range (the order inside a bin is arbitrary -- the
+//     accumulation below is in integers, so the result is not).
+// (d) k_nu_spread_tiles: block = (tile, class), one warp per point: the 196 weights of a point
+//     (14 x 14 separable Gaussian) go to 196 distinct cells, so each warp adds into its own
+//     private copy of the window without atomics, in integer fixed point; the 8 copies are then
+//     summed (exact) and written to the tile's scratch slot as 32.32 fixed point.  The row FFT
+//     sums the (<= 4) windows covering each cell.
+constexpr int NU_TS = 16;                      // tile side (cells)
+constexpr int NU_WIN = NU_TS + NU_W - 1;       // 45: window side
+constexpr int NU_WOFF = NU_MSP;                // window starts 6 cells before the tile
+
+__global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n,
+                                                double cx, double cy, double lo, double inv_h, int n1, int ntx,
+                                                int *__restrict__ bin_cnt, int2 *__restrict__ pkey, int64_t chunk_pts,
+                                                int *__restrict__ out_cnt, double *__restrict__ pcount,
+                                                int *__restrict__ err)
+{
+    __shared__ int s_cnt[2];
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int my_err = 0;
+    int2 key = make_int2(-1, 0);
+    if (i < n) {
+        const float2 v = xy[i];
+        const int L = lab[i];
+        if (L > 1) my_err |= VSA_ERRBIT_LABEL;
+        else if (!(isfinite(v.x) && isfinite(v.y))) my_err |= VSA_ERRBIT_NONFINITE;
+        else {
+            atomicAdd(&s_cnt[L], 1);
+            const int ix = (int)floor(((double)v.x - cx - lo) * inv_h), iy = (int)floor(((double)v.y - cy - lo) * inv_h);
+            if (ix - NU_MSP < 0 || iy - NU_MSP < 0 || ix + NU_MSP + 1 >= n1 || iy + NU_MSP + 1 >= n1)
+                atomicAdd(&out_cnt[i / chunk_pts], 1);       // outlier: direct fallback
+            else
+                key.x = (L * ntx + iy / NU_TS) * ntx + ix / NU_TS;
+        }
+    }
+    // warp-aggregated slot allocation: one atomic per distinct bin in the warp (neighbouring
+    // points of a scan share bins; a hot bin would otherwise serialise thousands of atomics)
+    const unsigned peers = __match_any_sync(0xffffffffu, key.x);
+    if (key.x >= 0) {
+        const int leader = __ffs(peers) - 1;
+        const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+        int base = 0;
+        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&bin_cnt[key.x], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        key.y = base + rank;
+    }
+    if (i < n) pkey[i] = key;
+    if (my_err) atomicOr(err, my_err);
+    __syncthreads();
+    if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&pcount[threadIdx.x], (double)s_cnt[threadIdx.x]);
+}
+
+// exclusive prefix of the bin counts and of the bins' work units (NU_UNIT points each): unit u
+// covers points [unit_first[u], +NU_UNIT) of bin unit_bin[u]; *n_units = the total
+constexpr int NU_UNIT = 256;
+__global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cnt, int nbins, int *__restrict__ bin_off,
+                                                  int *__restrict__ unit_off, int *__restrict__ unit_bin,
+                                                  int *__restrict__ unit_first, int *__restrict__ n_units)
+{
+    __shared__ int s_part[1024], s_upart[1024];
+    const int per = (nbins + 1023) / 1024;
+    const int b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
+    int sum = 0, usum = 0;
+    for (int b = b0; b < b1; ++b) {
+        sum += bin_cnt[b];
+        usum += (bin_cnt[b] + NU_UNIT - 1) / NU_UNIT;
+    }
+    s_part[threadIdx.x] = sum;
+    s_upart[threadIdx.x] = usum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {   // inclusive Hillis-Steele scans
+        const int v = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0;
+        const int uv = threadIdx.x >= o ? s_upart[threadIdx.x - o] : 0;
+        __syncthreads();
+        s_part[threadIdx.x] += v;
+        s_upart[threadIdx.x] += uv;
+        __syncthreads();
+    }
+    int run = s_part[threadIdx.x] - sum, urun = s_upart[threadIdx.x] - usum;
+    for (int b = b0; b < b1; ++b) {
+        bin_off[b] = run;
+        unit_off[b] = urun;
+        const int nu = (bin_cnt[b] + NU_UNIT - 1) / NU_UNIT;
+        for (int q = 0; q < nu; ++q) {
+            unit_bin[urun + q] = b;
+            unit_first[urun + q] = run + q * NU_UNIT;
+        }
+        run += bin_cnt[b];
+        urun += nu;
+    }
+    if (threadIdx.x == 1023) {
+        bin_off[nbins] = s_part[1023];
+        unit_off[nbins] = s_upart[1023];
+        *n_units = s_upart[1023];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_nu_place(const float2 *__restrict__ xy, int64_t n, const int2 *__restrict__ pkey,
+                                                  const int *__restrict__ bin_off, float2 *__restrict__ sorted)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int2 key = pkey[i];
+    if (key.x < 0) return;
+    // the raw coordinates: k_nu_spread_tiles recomputes the cell with k_nu_bin's fp64 expression
+    sorted[bin_off[key.x] + key.y] = xy[i];
+}
+
+__global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restrict__ sorted, const int *__restrict__ bin_off,
+                                                         const int *__restrict__ unit_bin,
+                                                         const int *__restrict__ unit_first,
+                                                         const int *__restrict__ n_units, int ntx, double cx, double cy,
+                                                         double lo, double h, double inv_h, double tau,
+                                                         unsigned long long *__restrict__ scratch)
+{
+    constexpr int NWIN = NU_WIN * NU_WIN;
+    __shared__ unsigned int s_win[8][NWIN];            // one window per warp
+    const int unit = blockIdx.x;
+    if (unit >= *n_units) return;                     // block-uniform (the grid is an upper bound)
+    const int bin = unit_bin[unit];                   // (class, tile_y, tile_x)
+    const int first = unit_first[unit];
+    const int cnt = min(NU_UNIT, bin_off[bin + 1] - first);
+    // fixed point 2^20 per unit weight (a cell sums at most NU_UNIT weights <= 1: no 32-bit
+    // overflow even after the 8 copies are added); written as 32.32 fixed point (an exact shift)
+    constexpr int sh = 20;                            // <= NU_UNIT points: no 32-bit overflow
+    const float qscale = (float)(1u << sh);
+    for (int q = threadIdx.x; q < 8 * NWIN; q += blockDim.x) (&s_win[0][0])[q] = 0u;
+    __syncthreads();
+    const int t = bin % (ntx * ntx);
+    const int tx = t % ntx, ty = t / ntx;
+    const int gx0 = tx * NU_TS - NU_WOFF, gy0 = ty * NU_TS - NU_WOFF;   // window origin (cells)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned int *win = s_win[warp];
+    const float inv4t = (float)(1.0 / (4.0 * tau));
+    const float2 *pts = sorted + first;
+    // the warp's points (p = warp + 8 j) loaded at once, one per lane, then broadcast
+    const int nmine = (cnt - warp + 7) / 8;
+    for (int j0 = 0; j0 < nmine; j0 += 32) {
+      const float2 mine = j0 + lane < nmine ? pts[warp + 8 * (j0 + lane)] : make_float2(0.f, 0.f);
+      const int jn = min(32, nmine - j0);
+      for (int jj = 0; jj < jn; ++jj) {
+        const float2 raw = make_float2(__shfl_sync(0xffffffffu, mine.x, jj), __shfl_sync(0xffffffffu, mine.y, jj));
+        const double px = (double)raw.x - cx, py = (double)raw.y - cy;   // as k_nu_bin
+        const int ix = (int)floor((px - lo) * inv_h), iy = (int)floor((py - lo) * inv_h);
+        // lanes 0..13: x weights, 16..29: y weights of this point's 14 x 14 support
+        const int d = lane & 15;
+        const double gcoord = (double)((lane < 16 ? ix : iy) - NU_MSP + d) * h + lo;
+        const float u = (float)(gcoord - (lane < 16 ? px : py));
+        const float w = d < NU_W ? __expf(-u * u * inv4t) : 0.f;
+        const int base = (iy - NU_MSP - gy0) * NU_WIN + (ix - NU_MSP - gx0);   // support origin in the window
+#pragma unroll
+        for (int r = 0; r < 7; ++r) {                  // cell = lane + 32 r: distinct within a round
+            const int cidx = lane + 32 * r;
+            const int dx = cidx % NU_W, dy = cidx / NU_W;
+            const float wx = __shfl_sync(0xffffffffu, w, dx);
+            const float wy = __shfl_sync(0xffffffffu, w, 16 + (dy < NU_W ? dy : 0));
+            if (cidx < NU_W * NU_W) win[base + dy * NU_WIN + dx] += __float2uint_rn(wx * wy * qscale);
+            __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    unsigned long long *dst = scratch + (size_t)unit * NWIN;
+    for (int q = threadIdx.x; q < NWIN; q += blockDim.x) {
+        unsigned long long acc = 0;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8) acc += s_win[w8][q];
+        dst[q] = acc << (32 - sh);
+    }
+}
+
+// ---- 2. FFTs ------------------------------------------------------------------------------
+// Radix-2 Stockham (self-sorting) transform of N = 2^LOGN complex values in shared memory with
+// the positive exponent, G_m = sum_j a_j e^{+2 pi i j m / N}; tw[q] = e^{+2 pi i q / N}, q < N/2.
+template <int LOGN, int T>
+__device__ __forceinline__ float2 *stockham(float2 *a, float2 *b, const float2 *__restrict__ tw)
+{
+    constexpr int N = 1 << LOGN;
+#pragma unroll
+    for (int s = 0; s < LOGN; ++s) {
+        const int p = 1 << s;                          // compile-time after unrolling
+        __syncthreads();
+#pragma unroll
+        for (int jj = 0; jj < N / 2; jj += T) {
+            const int j = jj + threadIdx.x;
+            const int k = j & (p - 1);
+            const float2 x0 = a[j], x1 = a[j + N / 2];
+            const float2 w = tw[k << (LOGN - 1 - s)];
+            const float2 t = make_float2(w.x * x1.x - w.y * x1.y, w.x * x1.y + w.y * x1.x);
+            const int o = ((j - k) << 1) + k;
+            b[o] = make_float2(x0.x + t.x, x0.y + t.y);
+            b[o + p] = make_float2(x0.x - t.x, x0.y - t.y);
+        }
+        float2 *c = a;
+        a = b;
+        b = c;
+    }
+    __syncthreads();
+    return a;
+}
+
+// row pass: block = one grid row gy of one class.  Sums the (<= 4) tile windows covering each
+// cell of the row (fixed point, exact), pre-corrects (psi_inv[gx] psi_inv[gy]), zero-pads to N,
+// transforms along x, and writes the column-major intermediate F1T[c][mx][gy] (mx < N, gy < n1).
+template <int LOGN, int T>
+__global__ void __launch_bounds__(T) k_nu_rowfft(const unsigned long long *__restrict__ scratch,
+                                                 const int *__restrict__ unit_off, int ntx, int n1,
+                                                 const float *__restrict__ psi_inv, const float2 *__restrict__ tw,
+                                                 float2 *__restrict__ f1t)
+{
+    constexpr int N = 1 << LOGN;
+    extern __shared__ float2 sm_fft[];
+    float2 *a = sm_fft, *b = sm_fft + N, *stw = sm_fft + 2 * N;
+    for (int q = threadIdx.x; q < N / 2; q += T) stw[q] = tw[q];
+    const int gy = blockIdx.x, c = blockIdx.y;
+    // tile rows whose windows cover gy: ty with ty*TS - WOFF <= gy < ty*TS - WOFF + WIN
+    const int ty_hi = min(ntx - 1, (gy + NU_WOFF) / NU_TS);
+    const int ty_num = gy + NU_WOFF - NU_WIN;                 // floor division for negatives
+    const int ty_lo = ty_num < 0 ? 0 : ty_num / NU_TS + 1;
+    const float py = psi_inv[gy];
+    for (int j = threadIdx.x; j < N; j += T) {
+        float v = 0.f;
+        if (j < n1) {
+            const int tx_hi = min(ntx - 1, (j + NU_WOFF) / NU_TS);
+            const int tx_num = j + NU_WOFF - NU_WIN;
+            const int tx_lo = tx_num < 0 ? 0 : tx_num / NU_TS + 1;
+            long long acc = 0;
+            for (int ty = ty_lo; ty <= ty_hi; ++ty)
+                for (int tx = tx_lo; tx <= tx_hi; ++tx) {
+                    const int bin = (c * ntx + ty) * ntx + tx;
+                    const int wy = gy - (ty * NU_TS - NU_WOFF), wx = j - (tx * NU_TS - NU_WOFF);
+                    for (int u = unit_off[bin]; u < unit_off[bin + 1]; ++u)   // the bin's work units
+                        acc += (long long)scratch[((size_t)u * NU_WIN + wy) * NU_WIN + wx];
+                }
+            v = (float)((double)acc * (1.0 / NU_FIX)) * psi_inv[j] * py;
+        }
+        a[j] = make_float2(v, 0.f);
+    }
+    float2 *r = stockham<LOGN, T>(a, b, stw);
+    // only the frequencies the interpolation reads: |m| < K2 = N/4 + 8 (|t| <= pi/2 plus the
+    // 6-point reach), stored compactly at m + K2
+    constexpr int K2 = N / 4 + 8;
+    float2 *out = f1t + (size_t)c * 2 * K2 * n1;
+    for (int cc = threadIdx.x; cc < 2 * K2; cc += T) {
+        const int m = cc - K2;
+        out[(size_t)cc * n1 + gy] = r[m & (N - 1)];
+    }
+}
+
+// column pass: block = one (compact) x-frequency of one class; transforms along y and writes
+// the compact G[c][mx + K2][my + K2] (|mx|, |my| < K2).
+template <int LOGN, int T>
+__global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t, int n1, const float2 *__restrict__ tw,
+                                                 float2 *__restrict__ G)
+{
+    constexpr int N = 1 << LOGN;
+    extern __shared__ float2 sm_fft[];
+    float2 *a = sm_fft, *b = sm_fft + N, *stw = sm_fft + 2 * N;
+    for (int q = threadIdx.x; q < N / 2; q += T) stw[q] = tw[q];
+    constexpr int K2 = N / 4 + 8;
+    const int cx = blockIdx.x, c = blockIdx.y;          // compact x-frequency, class
+    const float2 *in = f1t + ((size_t)c * 2 * K2 + cx) * n1;
+    for (int j = threadIdx.x; j < N; j += T) a[j] = j < n1 ? in[j] : make_float2(0.f, 0.f);
+    float2 *r = stockham<LOGN, T>(a, b, stw);
+    float2 *out = G + ((size_t)c * 2 * K2 + cx) * 2 * K2;
+    for (int cc = threadIdx.x; cc < 2 * K2; cc += T) out[cc] = r[(cc - K2) & (N - 1)];
+}
+
+// ---- 3. interpolation + deconvolution ------------------------------------------------------
+// one warp per (dimension k, class c): g(t) = hs^2 sum_{m near t} psi(t - t_m) G(t_m) e^{-i n1/2 t_m}
+// over the 13 x 13 grid points nearest t (the grid index l runs from 0 while the coefficients are
+// centred at n1/2); lanes take the points in a fixed order and the warp sums them in a fixed
+// tree (deterministic); then pending += h^2 g / Phi(s).
+__global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G, int logn, int n1, int D, int Dp,
+                                                   const double *__restrict__ tx_turns, const double *__restrict__ ty_turns,
+                                                   double h, double tau, double tau2, const float2 *__restrict__ ph,
+                                                   double *__restrict__ pending)
+{
+    constexpr int NP = 2 * NU_MSP2 + 1;   // 13
+    const int lane = threadIdx.x & 31;
+    const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int c = blockIdx.y;
+    if (k >= D) return;   // warp-uniform
+    const int N = 1 << logn;
+    const double hs = 2.0 * 3.14159265358979323846 / N;
+    const double sx = 2.0 * 3.14159265358979323846 * tx_turns[k], sy = 2.0 * 3.14159265358979323846 * ty_turns[k];
+    const double tx = sx * h, ty = sy * h;   // fp64 frequencies w = theta / l
+    const int m0x = (int)rint(tx / hs), m0y = (int)rint(ty / hs);
+    const float inv4t2 = (float)(1.0 / (4.0 * tau2));
+    const int K2 = N / 4 + 8;                // compact frequency range (k_nu_colfft)
+    const float2 *Gc = G + (size_t)c * 4 * K2 * K2;
+    float ar = 0.f, ai = 0.f;
+    for (int idx = lane; idx < NP * NP; idx += 32) {
+        const int dx = idx / NP, dy = idx - dx * NP;
+        const int mx = m0x - NU_MSP2 + dx, my = m0y - NU_MSP2 + dy;
+        const float ux = (float)(tx - (double)mx * hs), uy = (float)(ty - (double)my * hs);
+        const float w = __expf(-(ux * ux + uy * uy) * inv4t2);
+        const float2 px = ph[mx & (N - 1)], py = ph[my & (N - 1)];
+        const float2 p = make_float2(w * (px.x * py.x - px.y * py.y), w * (px.x * py.y + px.y * py.x));
+        const float2 g = Gc[(size_t)(mx + K2) * 2 * K2 + (my + K2)];
+        ar += g.x * p.x - g.y * p.y;
+        ai += g.x * p.y + g.y * p.x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+    }
+    if (lane == 0) {
+        const double s2 = sx * sx + sy * sy;
+        const double scale = h * h * hs * hs / (4.0 * 3.14159265358979323846 * tau * exp(-s2 * tau));
+        double *pd = pending + 2 * ((size_t)c * Dp + k);
+        pd[0] += scale * ar;
+        pd[1] += scale * ai;
+    }
+}
+
+}  // namespace
+
+// ---- plan and launch -----------------------------------------------------------------------
+int vsa_nufft_plan(vsaogm_ctx *c)
+{
+    if (c->nu_ready) return VSAOGM_OK;
+    const double S = 3.14159265358979323846 / c->l;   // |w| <= pi / l
+    const double sigma = 2.0;
+    const double h = 3.14159265358979323846 / (sigma * S);
+    const double W = c->bounds.x_max - c->bounds.x_min, Hh = c->bounds.y_max - c->bounds.y_min;
+    const double margin = 1.0 + 0.05 * std::max(W, Hh);   // metres beyond the bounds on the grid
+    const double X = 0.5 * std::max(W, Hh) + margin;       // half-width of the covered square (centred)
+    int n1 = 2 * (int)ceil((X + (NU_MSP + 2) * h) / h);
+    int logn = 1;
+    while ((1 << logn) < 2 * n1) ++logn;
+    if (logn > 13) return VSAOGM_EINVAL_ARG;             // n2 <= 8192 (shared-memory transform)
+    const int N = 1 << logn;
+    const double R = (double)N / n1;
+    c->nu_h = h;
+    c->nu_tau = NU_MSP * h * h / (3.14159265358979323846 * sigma * (sigma - 0.5));
+    c->nu_tau2 = 3.14159265358979323846 * NU_MSP2 / ((double)n1 * n1 * R * (R - 0.5));
+    c->nu_n1 = n1;
+    c->nu_logn = logn;
+    c->nu_lo = -(n1 / 2) * h;
+    std::vector<float> psi(n1);
+    for (int l = 0; l < n1; ++l) {
+        const double lc = l - n1 / 2;
+        psi[l] = (float)(1.0 / (sqrt(4.0 * 3.14159265358979323846 * c->nu_tau2) * exp(-lc * lc * c->nu_tau2)));
+    }
+    std::vector<float2> tw(N / 2), ph(N);
+    for (int q = 0; q < N / 2; ++q) {
+        const double a = 2.0 * 3.14159265358979323846 * q / N;
+        tw[q] = make_float2((float)cos(a), (float)sin(a));
+    }
+    for (int m = 0; m < N; ++m) {
+        const double a = -2.0 * 3.14159265358979323846 * (double)(n1 / 2) * m / N;
+        ph[m] = make_float2((float)cos(a), (float)sin(a));
+    }
+    const int ntx = (n1 + NU_TS - 1) / NU_TS;
+    c->nu_ntx = ntx;
+    const int nbins = 2 * ntx * ntx;
+    const size_t K2 = N / 4 + 8;
+    const size_t grid_bytes = 0, f1_bytes = 2 * 2 * K2 * n1 * 8, g_bytes = 2 * 4 * K2 * K2 * 8;
+    if (cudaMalloc(&c->d_nu_bins, (3 * (size_t)nbins + 3) * sizeof(int)) != cudaSuccess) return VSAOGM_ENOMEM;
+    VSA_CUDA_TRY(cudaMemset(c->d_nu_bins, 0, (3 * (size_t)nbins + 3) * sizeof(int)));
+    (void)grid_bytes;   // the unit windows are sized per encode (vsa_launch_encode_nufft)
+    if (cudaMalloc(&c->d_nu_f1, f1_bytes) != cudaSuccess ||
+        cudaMalloc(&c->d_nu_G, g_bytes) != cudaSuccess || cudaMalloc(&c->d_nu_psi, n1 * 4) != cudaSuccess ||
+        cudaMalloc(&c->d_nu_tw, (N / 2) * 8) != cudaSuccess || cudaMalloc(&c->d_nu_ph, N * 8) != cudaSuccess)
+        return VSAOGM_ENOMEM;
+    VSA_CUDA_TRY(cudaMemcpy(c->d_nu_psi, psi.data(), n1 * 4, cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(c->d_nu_tw, tw.data(), (N / 2) * 8, cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(c->d_nu_ph, ph.data(), N * 8, cudaMemcpyHostToDevice));
+    c->nu_ready = true;
+    return VSAOGM_OK;
+}
+
+namespace {
+template <int LOGN>
+int launch_ffts(vsaogm_ctx *c)
+{
+    constexpr int T = 512;
+    const int N = 1 << LOGN;
+    const size_t smem = (2 * (size_t)N + N / 2) * sizeof(float2);
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_rowfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_colfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_nu_rowfft<LOGN, T><<<dim3(c->nu_n1, 2), T, smem, c->stream>>>(
+        (const unsigned long long *)c->d_nu_grid, c->d_nu_bins + 2 * (2 * c->nu_ntx * c->nu_ntx) + 1, c->nu_ntx,
+        c->nu_n1, c->d_nu_psi,
+        (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_f1);
+    k_nu_colfft<LOGN, T><<<dim3(2 * (N / 4 + 8), 2), T, smem, c->stream>>>((const float2 *)c->d_nu_f1, c->nu_n1,
+                                                              (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_G);
+    return VSAOGM_OK;
+}
+}  // namespace
+
+int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
+                            int chunks)
+{
+    int rc;
+    if ((rc = vsa_nufft_plan(c))) return rc;
+    if ((size_t)chunks > c->nu_out_cap) {
+        if (c->d_nu_out) cudaFree(c->d_nu_out);
+        if (cudaMalloc(&c->d_nu_out, chunks * sizeof(int)) != cudaSuccess) { c->d_nu_out = nullptr; c->nu_out_cap = 0; return VSAOGM_ENOMEM; }
+        c->nu_out_cap = chunks;
+    }
+    const int ntx = c->nu_ntx, nbins = 2 * ntx * ntx;
+    const size_t max_units = (size_t)n / NU_UNIT + nbins;   // sum over bins of ceil(cnt / NU_UNIT)
+    if ((size_t)n > c->nu_pts_cap) {
+        if (c->d_nu_key) cudaFree(c->d_nu_key);
+        if (c->d_nu_sorted) cudaFree(c->d_nu_sorted);
+        if (c->d_nu_grid) cudaFree(c->d_nu_grid);
+        if (c->d_nu_units) cudaFree(c->d_nu_units);
+        c->d_nu_key = c->d_nu_sorted = c->d_nu_grid = nullptr;
+        c->d_nu_units = nullptr;
+        c->nu_pts_cap = 0;
+        const size_t cap = (size_t)n + (size_t)n / 4;   // headroom: batch sizes vary
+        const size_t ucap = cap / NU_UNIT + nbins;
+        if (cudaMalloc(&c->d_nu_key, cap * sizeof(int2)) != cudaSuccess ||
+            cudaMalloc(&c->d_nu_sorted, cap * sizeof(float2)) != cudaSuccess ||
+            cudaMalloc(&c->d_nu_grid, ucap * NU_WIN * NU_WIN * sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMalloc(&c->d_nu_units, 2 * ucap * sizeof(int)) != cudaSuccess)
+            return VSAOGM_ENOMEM;
+        c->nu_pts_cap = cap;
+    }
+    int *bin_cnt = c->d_nu_bins, *bin_off = c->d_nu_bins + nbins, *unit_off = c->d_nu_bins + 2 * nbins + 1;
+    int *n_units = c->d_nu_bins + 3 * nbins + 2;
+    int *unit_bin = c->d_nu_units, *unit_first = c->d_nu_units + (c->nu_pts_cap / NU_UNIT + nbins);
+    VSA_CUDA_TRY(cudaMemsetAsync(c->d_nu_out, 0, chunks * sizeof(int), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(bin_cnt, 0, nbins * sizeof(int), c->stream));
+    const unsigned pblocks = (unsigned)((n + 255) / 256);
+    const double inv_h = 1.0 / c->nu_h;
+    k_nu_bin<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, lab, n, c->cx, c->cy, c->nu_lo, inv_h, c->nu_n1, ntx,
+                                             bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out, c->d_pcounts,
+                                             c->d_err);
+    k_nu_scan<<<1, 1024, 0, c->stream>>>(bin_cnt, nbins, bin_off, unit_off, unit_bin, unit_first, n_units);
+    k_nu_place<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, n, (const int2 *)c->d_nu_key, bin_off,
+                                               (float2 *)c->d_nu_sorted);
+    k_nu_spread_tiles<<<(unsigned)max_units, 256, 0, c->stream>>>(
+        (const float2 *)c->d_nu_sorted, bin_off, unit_bin, unit_first, n_units, ntx, c->cx, c->cy, c->nu_lo, c->nu_h,
+        inv_h, c->nu_tau, (unsigned long long *)c->d_nu_grid);
+    VSA_CUDA_TRY(cudaGetLastError());
+    switch (c->nu_logn) {
+    case 8: rc = launch_ffts<8>(c); break;
+    case 9: rc = launch_ffts<9>(c); break;
+    case 10: rc = launch_ffts<10>(c); break;
+    case 11: rc = launch_ffts<11>(c); break;
+    case 12: rc = launch_ffts<12>(c); break;
+    case 13: rc = launch_ffts<13>(c); break;
+    default: rc = launch_ffts<7>(c); break;
+    }
+    if (rc) return rc;
+    VSA_CUDA_TRY(cudaGetLastError());
+    k_nu_interp<<<dim3((c->D + 7) / 8, 2), 256, 0, c->stream>>>((const float2 *)c->d_nu_G, c->nu_logn, c->nu_n1,
+                                                                      c->D, c->Dp, c->d_tx_turns, c->d_ty_turns, c->nu_h,
+                                                                      c->nu_tau, c->nu_tau2, (const float2 *)c->d_nu_ph,
+                                                                      c->d_pending);
+    VSA_CUDA_TRY(cudaGetLastError());
+    c->launches += 7;
+    return VSAOGM_OK;
+}
