@@ -99,7 +99,7 @@ struct vsaogm_ctx {
     int enc_pairs_minb = 3;   // resident pair-kernel blocks per SM (3: 80 registers, no spills)
     int enc_pairs_split = 1;
     // encode method: 0 direct (pair kernels), 1 type-3 NUFFT (nufft.cu; delta = 1, D >= 2048)
-    int enc_method = 0;
+    int enc_method = 1;
     bool nu_ready = false;
     double nu_h = 0, nu_tau = 0, nu_tau2 = 0, nu_lo = 0;
     int nu_n1 = 0, nu_logn = 0, nu_ntx = 0;

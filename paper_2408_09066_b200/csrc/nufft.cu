@@ -177,31 +177,39 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
     unsigned int *win = s_win[warp];
     const float inv4t = (float)(1.0 / (4.0 * tau));
     const float2 *pts = sorted + first;
+    // this lane's 7 support cells (cell = lane + 32 r of the 14 x 14 support), fixed per lane
+    int dxr[7], dyr[7], offr[7];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+        const int cidx = lane + 32 * r;
+        dxr[r] = cidx % NU_W;
+        dyr[r] = cidx < NU_W * NU_W ? cidx / NU_W : 0;
+        offr[r] = dyr[r] * NU_WIN + dxr[r];
+    }
+    const bool last_ok = lane + 32 * 6 < NU_W * NU_W;   // rounds 0..5 always valid (196 = 6 * 32 + 4)
     // the warp's points (p = warp + 8 j) loaded at once, one per lane, then broadcast
     const int nmine = (cnt - warp + 7) / 8;
     for (int j0 = 0; j0 < nmine; j0 += 32) {
-      const float2 mine = j0 + lane < nmine ? pts[warp + 8 * (j0 + lane)] : make_float2(0.f, 0.f);
-      const int jn = min(32, nmine - j0);
-      for (int jj = 0; jj < jn; ++jj) {
-        const float2 raw = make_float2(__shfl_sync(0xffffffffu, mine.x, jj), __shfl_sync(0xffffffffu, mine.y, jj));
-        const double px = (double)raw.x - cx, py = (double)raw.y - cy;   // as k_nu_bin
-        const int ix = (int)floor((px - lo) * inv_h), iy = (int)floor((py - lo) * inv_h);
-        // lanes 0..13: x weights, 16..29: y weights of this point's 14 x 14 support
-        const int d = lane & 15;
-        const double gcoord = (double)((lane < 16 ? ix : iy) - NU_MSP + d) * h + lo;
-        const float u = (float)(gcoord - (lane < 16 ? px : py));
-        const float w = d < NU_W ? __expf(-u * u * inv4t) : 0.f;
-        const int base = (iy - NU_MSP - gy0) * NU_WIN + (ix - NU_MSP - gx0);   // support origin in the window
+        const float2 mine = j0 + lane < nmine ? pts[warp + 8 * (j0 + lane)] : make_float2(0.f, 0.f);
+        const int jn = min(32, nmine - j0);
+        for (int jj = 0; jj < jn; ++jj) {
+            const float2 raw = make_float2(__shfl_sync(0xffffffffu, mine.x, jj), __shfl_sync(0xffffffffu, mine.y, jj));
+            const double px = (double)raw.x - cx, py = (double)raw.y - cy;   // as k_nu_bin
+            const int ix = (int)floor((px - lo) * inv_h), iy = (int)floor((py - lo) * inv_h);
+            // lanes 0..13: x weights, 16..29: y weights of this point's 14 x 14 support
+            const int d = lane & 15;
+            const double gcoord = (double)((lane < 16 ? ix : iy) - NU_MSP + d) * h + lo;
+            const float u = (float)(gcoord - (lane < 16 ? px : py));
+            const float w = d < NU_W ? __expf(-u * u * inv4t) * (lane < 16 ? qscale : 1.f) : 0.f;   // x weights carry the scale
+            unsigned int *wb = win + (iy - NU_MSP - gy0) * NU_WIN + (ix - NU_MSP - gx0);   // support origin
 #pragma unroll
-        for (int r = 0; r < 7; ++r) {                  // cell = lane + 32 r: distinct within a round
-            const int cidx = lane + 32 * r;
-            const int dx = cidx % NU_W, dy = cidx / NU_W;
-            const float wx = __shfl_sync(0xffffffffu, w, dx);
-            const float wy = __shfl_sync(0xffffffffu, w, 16 + (dy < NU_W ? dy : 0));
-            if (cidx < NU_W * NU_W) win[base + dy * NU_WIN + dx] += __float2uint_rn(wx * wy * qscale);
+            for (int r = 0; r < 7; ++r) {              // distinct cells within a round
+                const float wx = __shfl_sync(0xffffffffu, w, dxr[r]);
+                const float wy = __shfl_sync(0xffffffffu, w, 16 + dyr[r]);
+                if (r < 6 || last_ok) wb[offr[r]] += __float2uint_rn(wx * wy);
+            }
             __syncwarp();
         }
-      }
     }
     __syncthreads();
     unsigned long long *dst = scratch + (size_t)unit * NWIN;
@@ -215,7 +223,8 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
 
 // ---- 2. FFTs ------------------------------------------------------------------------------
 // Radix-2 Stockham (self-sorting) transform of N = 2^LOGN complex values in shared memory with
-// the positive exponent, G_m = sum_j a_j e^{+2 pi i j m / N}; tw[q] = e^{+2 pi i q / N}, q < N/2.
+// the positive exponent, G_m = sum_j a_j e^{+2 pi i j m / N}; per-stage twiddle tables
+// tw[p - 1 + k] = e^{+2 pi i k / (2p)}, k < p, p = 1, 2, 4, ... N/2 (N - 1 entries).
 template <int LOGN, int T>
 __device__ __forceinline__ float2 *stockham(float2 *a, float2 *b, const float2 *__restrict__ tw)
 {
@@ -229,7 +238,7 @@ __device__ __forceinline__ float2 *stockham(float2 *a, float2 *b, const float2 *
             const int j = jj + threadIdx.x;
             const int k = j & (p - 1);
             const float2 x0 = a[j], x1 = a[j + N / 2];
-            const float2 w = tw[k << (LOGN - 1 - s)];
+            const float2 w = tw[(p - 1) + k];          // stage table: consecutive k, no bank conflicts
             const float2 t = make_float2(w.x * x1.x - w.y * x1.y, w.x * x1.y + w.y * x1.x);
             const int o = ((j - k) << 1) + k;
             b[o] = make_float2(x0.x + t.x, x0.y + t.y);
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(const unsigned long long *__res
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
     float2 *a = sm_fft, *b = sm_fft + N, *stw = sm_fft + 2 * N;
-    for (int q = threadIdx.x; q < N / 2; q += T) stw[q] = tw[q];
+    for (int q = threadIdx.x; q < N - 1; q += T) stw[q] = tw[q];
     const int gy = blockIdx.x, c = blockIdx.y;
     // tile rows whose windows cover gy: ty with ty*TS - WOFF <= gy < ty*TS - WOFF + WIN
     const int ty_hi = min(ntx - 1, (gy + NU_WOFF) / NU_TS);
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t,
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
     float2 *a = sm_fft, *b = sm_fft + N, *stw = sm_fft + 2 * N;
-    for (int q = threadIdx.x; q < N / 2; q += T) stw[q] = tw[q];
+    for (int q = threadIdx.x; q < N - 1; q += T) stw[q] = tw[q];
     constexpr int K2 = N / 4 + 8;
     const int cx = blockIdx.x, c = blockIdx.y;          // compact x-frequency, class
     const float2 *in = f1t + ((size_t)c * 2 * K2 + cx) * n1;
@@ -388,11 +397,12 @@ int vsa_nufft_plan(vsaogm_ctx *c)
         const double lc = l - n1 / 2;
         psi[l] = (float)(1.0 / (sqrt(4.0 * 3.14159265358979323846 * c->nu_tau2) * exp(-lc * lc * c->nu_tau2)));
     }
-    std::vector<float2> tw(N / 2), ph(N);
-    for (int q = 0; q < N / 2; ++q) {
-        const double a = 2.0 * 3.14159265358979323846 * q / N;
-        tw[q] = make_float2((float)cos(a), (float)sin(a));
-    }
+    std::vector<float2> tw(N), ph(N);
+    for (int p = 1; p < N; p <<= 1)
+        for (int k = 0; k < p; ++k) {
+            const double a = 3.14159265358979323846 * k / p;   // 2 pi k / (2p)
+            tw[p - 1 + k] = make_float2((float)cos(a), (float)sin(a));
+        }
     for (int m = 0; m < N; ++m) {
         const double a = -2.0 * 3.14159265358979323846 * (double)(n1 / 2) * m / N;
         ph[m] = make_float2((float)cos(a), (float)sin(a));
@@ -407,10 +417,10 @@ int vsa_nufft_plan(vsaogm_ctx *c)
     (void)grid_bytes;   // the unit windows are sized per encode (vsa_launch_encode_nufft)
     if (cudaMalloc(&c->d_nu_f1, f1_bytes) != cudaSuccess ||
         cudaMalloc(&c->d_nu_G, g_bytes) != cudaSuccess || cudaMalloc(&c->d_nu_psi, n1 * 4) != cudaSuccess ||
-        cudaMalloc(&c->d_nu_tw, (N / 2) * 8) != cudaSuccess || cudaMalloc(&c->d_nu_ph, N * 8) != cudaSuccess)
+        cudaMalloc(&c->d_nu_tw, N * 8) != cudaSuccess || cudaMalloc(&c->d_nu_ph, N * 8) != cudaSuccess)
         return VSAOGM_ENOMEM;
     VSA_CUDA_TRY(cudaMemcpy(c->d_nu_psi, psi.data(), n1 * 4, cudaMemcpyHostToDevice));
-    VSA_CUDA_TRY(cudaMemcpy(c->d_nu_tw, tw.data(), (N / 2) * 8, cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(c->d_nu_tw, tw.data(), N * 8, cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(c->d_nu_ph, ph.data(), N * 8, cudaMemcpyHostToDevice));
     c->nu_ready = true;
     return VSAOGM_OK;
@@ -422,7 +432,7 @@ int launch_ffts(vsaogm_ctx *c)
 {
     constexpr int T = 512;
     const int N = 1 << LOGN;
-    const size_t smem = (2 * (size_t)N + N / 2) * sizeof(float2);
+    const size_t smem = (3 * (size_t)N) * sizeof(float2);
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_rowfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_colfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_nu_rowfft<LOGN, T><<<dim3(c->nu_n1, 2), T, smem, c->stream>>>(
