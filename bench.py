@@ -209,6 +209,7 @@ def run_native(args):
     for kv in [x for x in args.tuning.split(",") if x]:   # measurement variants (vsaogm_set_tuning)
         k, v = kv.split("=")
         mp.set_tuning(k, int(v))
+    nufft = mp.get_tuning("enc_method") == 1
     ar_ms = []                                   # all-reduce durations (serial loop, world > 1)
 
     def step(b, precision=F16, ar_timer=None):
@@ -391,6 +392,19 @@ def run_native(args):
                                                   if enc_roof["measured"] else None),
                 "frac_at_measured_clock": (round(enc_rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
                                            if clocks.get("sm_mhz") else None)}
+    if nufft:
+        # the type-3 NUFFT encode is several short memory/latency-bound kernels, none an ALU
+        # roofline: report its rate in phasor-equivalents (N x D / time) against the direct
+        # method's ceilings; the dominant single kernel is the decode GEMM
+        enc_line = {"kernel": "type-3 NUFFT (k_nu_bin, k_nu_scan, k_nu_place, k_nu_spread_tiles, k_nu_rowfft, "
+                              "k_nu_colfft, k_nu_interp, k_encode_pairs1<outliers>)",
+                    "bound": "latency / shared memory (no ALU roofline applies)", "ms": round(enc_ms, 4),
+                    "phasor_equivalents_per_s": round(enc_rate, 1),
+                    "x_direct_pair_lp_ceiling": round(enc_rate / enc_roof["combined"], 3),
+                    "x_direct_measured_loop_ceiling": (round(enc_rate / enc_roof["measured"]["value"], 3)
+                                                       if enc_roof["measured"] else None),
+                    "x_mufu_only_single_point": round(enc_rate / enc_roof["mufu_only_single"], 3)}
+        dominant = "decode_gemm"
     roofline = enc_line if dominant == "encode" else gemm_roof
     gemm_bf16_ms = avg(prof_bf16, "decode_gemm")
     gemm_bf16_tf = flops / (gemm_bf16_ms * 1e-3) / 1e12
@@ -399,7 +413,8 @@ def run_native(args):
         "metric": METRIC, "value": round(value, 1), "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "f16 MMA operands, fp32 accumulate (decode); fp32 (encode phases / sincos / sums)",
+        "dtype": "f16 MMA operands, fp32 accumulate (decode); encode: " + (
+            "type-3 NUFFT (fp32 FFT, 32.32 fixed-point spreading, fp64 phases)" if nufft else "fp32 phases / sincos / sums"),
         "data": "synthetic", "config": dict(workload_config(sc, n_mean, world), **({"tuning": args.tuning} if args.tuning else {})),
         "points_bundled_per_s": round(n_mean / (ms_per_step * 1e-3), 1),
         "decode_cells_per_s_gemm_only": round(cells / (gemm_ms * 1e-3), 1),

@@ -172,7 +172,8 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
 
 /* Tuning variants (measurement and test hook; the defaults are the measured best and no
  * environment variable changes them).  Sets the integer knob `key` of this context for
- * later calls: "enc_x2" (encode kernel family; 4 = the pair kernel, the default),
+ * later calls: "enc_method" (0 direct pair kernels, 1 the type-3 NUFFT: the default for delta = 1 and
+ * D >= 2048), "enc_x2" (direct encode kernel family; 4 = the pair kernel, the default),
  * "enc_pairs_npoly", "enc_pairs_minb", "enc_pairs_split", "enc_x2_npoly", "enc_x2_minb",
  * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
@@ -181,6 +182,9 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
  * (0 auto, 1 the generic staged kernel), "entropy_rw" (0 auto, else output rows per
  * work item of the streamed entropy kernel).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
 int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);
+
+/* Read a tuning knob of this context into *value (the same keys).  Errors: EINVAL_ARG. */
+int vsaogm_get_tuning(vsaogm_ctx *ctx, const char *key, int64_t *value);
 
 /* Local entropy (Alg. 2), global entropy S = S_occ - S_emp, 3-way labels
  * (Eq. 12 + L14) over the band of the last vsaogm_decode.  s_dev: NULL or

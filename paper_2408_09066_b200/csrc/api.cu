@@ -564,7 +564,17 @@ int vsaogm_set_estimator(vsaogm_ctx *c, int32_t estimator)
     return VSAOGM_OK;
 }
 
-int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
+static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *get);
+
+int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value) { return tuning_knob(c, key, value, nullptr); }
+
+int vsaogm_get_tuning(vsaogm_ctx *c, const char *key, int64_t *value)
+{
+    if (!value) return VSAOGM_EINVAL_ARG;
+    return tuning_knob(c, key, 0, value);
+}
+
+static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *get)
 {
     if (!c || !key) return VSAOGM_EINVAL_ARG;
     struct Knob {
@@ -597,6 +607,10 @@ int vsaogm_set_tuning(vsaogm_ctx *c, const char *key, int64_t value)
     };
     for (const Knob &k : knobs)
         if (strcmp(k.name, key) == 0) {
+            if (get) {
+                *get = *k.field;
+                return VSAOGM_OK;
+            }
             if (value < k.lo || value > k.hi) return VSAOGM_EINVAL_ARG;
             *k.field = (int)value;
             return VSAOGM_OK;

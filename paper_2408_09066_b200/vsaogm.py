@@ -26,7 +26,7 @@ EXPORTS = (
     "vsaogm_entropy_host", "vsaogm_sync", "vsaogm_get_memory", "vsaogm_get_phases", "vsaogm_profile_enable",
     "vsaogm_profile_read", "vsaogm_launch_count", "vsaogm_test_gemm", "vsaogm_strerror", "vsaogm_export",
     "vsaogm_import", "vsaogm_set_estimator", "vsaogm_encode_bundle_host_async", "vsaogm_entropy_host_async",
-    "vsaogm_wait", "vsaogm_set_encode_stream", "vsaogm_set_tuning",
+    "vsaogm_wait", "vsaogm_set_encode_stream", "vsaogm_set_tuning", "vsaogm_get_tuning",
 )
 EPRECOND = -9
 
@@ -94,6 +94,7 @@ def load() -> ctypes.CDLL:
         "vsaogm_wait": ([P, i64], ctypes.c_int),
         "vsaogm_set_encode_stream": ([P, P], ctypes.c_int),
         "vsaogm_set_tuning": ([P, ctypes.c_char_p, i64], ctypes.c_int),
+        "vsaogm_get_tuning": ([P, ctypes.c_char_p, ctypes.POINTER(i64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -284,6 +285,11 @@ class Mapper:
     def set_tuning(self, key: str, value: int):
         """Set a tuning variant of this context (vsaogm.h: vsaogm_set_tuning)."""
         _check(self._lib.vsaogm_set_tuning(self._ctx, key.encode(), int(value)), f"vsaogm_set_tuning({key})")
+
+    def get_tuning(self, key: str) -> int:
+        v = ctypes.c_int64()
+        _check(self._lib.vsaogm_get_tuning(self._ctx, key.encode(), ctypes.byref(v)), f"vsaogm_get_tuning({key})")
+        return int(v.value)
 
     def set_estimator(self, estimator: int):
         """0: window mean of H_b(p) (default); 1: 8-bit grey-level histogram entropy (decode again after)."""
