@@ -172,8 +172,8 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
 
 /* Tuning variants (measurement and test hook; the defaults are the measured best and no
  * environment variable changes them).  Sets the integer knob `key` of this context for
- * later calls: "enc_method" (0 direct pair kernels, 1 the type-3 NUFFT: the default for delta = 1 and
- * D >= 2048), "enc_x2" (direct encode kernel family; 4 = the pair kernel, the default),
+ * later calls: "enc_method" (-1 auto, the default: the type-3 NUFFT for delta = 1 and D >= 2048 when its
+ * modelled time is below the direct kernel's; 0 direct pair kernels; 1 NUFFT), "enc_x2" (direct encode kernel family; 4 = the pair kernel, the default),
  * "enc_pairs_npoly", "enc_pairs_minb", "enc_pairs_split", "enc_x2_npoly", "enc_x2_minb",
  * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0

@@ -587,7 +587,7 @@ static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *g
         {"enc_pairs_npoly", &c->enc_pairs_npoly, 0, 8},
         {"enc_pairs_minb", &c->enc_pairs_minb, 3, 4},
         {"enc_pairs_split", &c->enc_pairs_split, 0, 1},
-        {"enc_method", &c->enc_method, 0, 1},
+        {"enc_method", &c->enc_method, -1, 1},
         {"enc_x2_minb", &c->enc_x2_minb, 3, 4},
         {"enc_x2_waves", &c->enc_x2_waves, 1, 64},
         {"enc_npoly", &c->enc_npoly, 0, 4},

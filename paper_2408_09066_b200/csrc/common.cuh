@@ -98,8 +98,9 @@ struct vsaogm_ctx {
     int enc_pairs_npoly = 4;  // FMA-pipe dimensions of 8 in the pair kernel's second warp role
     int enc_pairs_minb = 3;   // resident pair-kernel blocks per SM (3: 80 registers, no spills)
     int enc_pairs_split = 1;
-    // encode method: 0 direct (pair kernels), 1 type-3 NUFFT (nufft.cu; delta = 1, D >= 2048)
-    int enc_method = 1;
+    // encode method: -1 auto (the NUFFT where its modelled time is lower), 0 direct (pair kernels),
+    // 1 type-3 NUFFT (nufft.cu; delta = 1, D >= 2048)
+    int enc_method = -1;
     bool nu_ready = false;
     double nu_h = 0, nu_tau = 0, nu_tau2 = 0, nu_lo = 0;
     int nu_n1 = 0, nu_logn = 0, nu_ntx = 0;
@@ -214,6 +215,7 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
                             int chunks);
 int vsa_launch_nufft_outliers(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
                               int chunks);
+bool vsa_nufft_wanted(vsaogm_ctx *c, int64_t n);
 int vsa_launch_commit(vsaogm_ctx *c);
 int vsa_launch_norms(vsaogm_ctx *c, int do_commit);   // [commit +] norms + scaled memory mhat
 int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int prec);

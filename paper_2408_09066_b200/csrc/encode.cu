@@ -803,7 +803,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
     // Measured alternatives kept as tuning variants: enc_path 1 = label-split blocks
     // (delta = 1) / slot-filtered blocks (delta > 1); enc_path 2 = slot-filtered always.
     if (c->enc_path == 0 || (c->enc_path < 0 && c->nslots > 2)) return vsa_launch_encode_sorted(c, xy, lab, n);
-    if (c->enc_method == 1 && c->nslots == 2 && c->Dp >= 2048) {
+    if (vsa_nufft_wanted(c, n)) {
         // type-3 NUFFT (nufft.cu) + direct fallback for the points outside its grid; the chunks
         // are those of the direct kernel (4 waves of 4 blocks per SM over the k-blocks)
         const int kblocks = (c->Dp + 2047) / 2048;

@@ -371,27 +371,54 @@ __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G,
 }  // namespace
 
 // ---- plan and launch -----------------------------------------------------------------------
-int vsa_nufft_plan(vsaogm_ctx *c)
+// grid geometry only (host): h, tau, n1, N = 2^logn; no allocation
+int vsa_nufft_geometry(vsaogm_ctx *c)
 {
-    if (c->nu_ready) return VSAOGM_OK;
+    if (c->nu_n1) return VSAOGM_OK;
     const double S = 3.14159265358979323846 / c->l;   // |w| <= pi / l
     const double sigma = 2.0;
     const double h = 3.14159265358979323846 / (sigma * S);
     const double W = c->bounds.x_max - c->bounds.x_min, Hh = c->bounds.y_max - c->bounds.y_min;
     const double margin = 1.0 + 0.05 * std::max(W, Hh);   // metres beyond the bounds on the grid
     const double X = 0.5 * std::max(W, Hh) + margin;       // half-width of the covered square (centred)
-    int n1 = 2 * (int)ceil((X + (NU_MSP + 2) * h) / h);
+    const double n1d = 2.0 * ceil((X + (NU_MSP + 2) * h) / h);
+    if (!(n1d <= 4096.0)) return VSAOGM_EINVAL_ARG;        // N <= 8192 (shared-memory transform)
+    int n1 = (int)n1d;
     int logn = 1;
     while ((1 << logn) < 2 * n1) ++logn;
-    if (logn > 13) return VSAOGM_EINVAL_ARG;             // n2 <= 8192 (shared-memory transform)
-    const int N = 1 << logn;
-    const double R = (double)N / n1;
     c->nu_h = h;
-    c->nu_tau = NU_MSP * h * h / (3.14159265358979323846 * sigma * (sigma - 0.5));
-    c->nu_tau2 = 3.14159265358979323846 * NU_MSP2 / ((double)n1 * n1 * R * (R - 0.5));
     c->nu_n1 = n1;
     c->nu_logn = logn;
     c->nu_lo = -(n1 / 2) * h;
+    return VSAOGM_OK;
+}
+
+// encode method for a batch of n points (vsa_launch_encode): the NUFFT when its modelled time
+// is below the direct pair kernel's (measured at C2 / C4 / C5: FFTs ~90 us at N = 2048 scaling
+// with N^2, spreading ~60 us per 204k points, ~20 us of launches; direct ~N D / 3.5e12 s)
+bool vsa_nufft_wanted(vsaogm_ctx *c, int64_t n)
+{
+    if (c->nslots != 2 || c->Dp < 2048 || c->enc_method == 0) return false;
+    if (vsa_nufft_geometry(c)) return false;
+    if (c->enc_method == 1) return true;
+    const double N = (double)(1 << c->nu_logn);
+    const double t_nufft = 90e-6 * (N / 2048.0) * (N / 2048.0) + 60e-6 * (double)n / 204000.0 + 20e-6;
+    const double t_direct = (double)n * c->D / 3.5e12;
+    return t_nufft < t_direct;
+}
+
+int vsa_nufft_plan(vsaogm_ctx *c)
+{
+    if (c->nu_ready) return VSAOGM_OK;
+    int rc;
+    if ((rc = vsa_nufft_geometry(c))) return rc;
+    const double sigma = 2.0;
+    const double h = c->nu_h;
+    const int n1 = c->nu_n1, logn = c->nu_logn;
+    const int N = 1 << logn;
+    const double R = (double)N / n1;
+    c->nu_tau = NU_MSP * h * h / (3.14159265358979323846 * sigma * (sigma - 0.5));
+    c->nu_tau2 = 3.14159265358979323846 * NU_MSP2 / ((double)n1 * n1 * R * (R - 0.5));
     std::vector<float> psi(n1);
     for (int l = 0; l < n1; ++l) {
         const double lc = l - n1 / 2;

@@ -597,3 +597,58 @@ def test_gemm_phasor_tiles_on_the_fly(delta, prec):
         mo, _, _ = oracle.encode(tx, ty, l, xy, lab)
         qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, 0, R, 0, C)
         assert _qerr(outs[(1, 0)][0], qo) <= tol
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4"])
+def test_encode_methods_agree_and_nufft_reproducible(cfg):
+    """The type-3 NUFFT encode (enc_method 1) and the direct pair kernel (0) give the same
+    memories within their fp32 error (each is within ~1.5e-5 of the fp64 oracle, the NUFFT within
+    ~1e-6), the same counts; two NUFFT encodes of the same points are bit-identical (fixed-point
+    spreading, fixed-order reductions)."""
+    from paper_2408_09066_b200 import Mapper
+    sc = Scenario(cfg)
+    xy, lab = sc.batch(0) if sc.cfg["batch_scans"] else sc.all_points()
+    D, l = sc.cfg["D"], sc.cfg["l"]
+    mems = {}
+    for method in (0, 1):
+        mp = Mapper(D, 0, l, sc.bounds)
+        mp.set_tuning("enc_method", method)
+        mp.encode_bundle(*_cuda(xy, lab))
+        mems[method] = mp.get_memory()
+        if method == 1:
+            mp.reset()
+            mp.encode_bundle(*_cuda(xy, lab))
+            again = mp.get_memory()
+            assert np.array_equal(again[0], mems[1][0]) and list(again[1]) == list(mems[1][1])
+        mp.close()
+    assert list(mems[0][1]) == list(mems[1][1])
+    assert _mem_err(mems[1][0], mems[0][0]) <= 5e-5
+    tx, ty = oracle.theta(0, D)
+    mo, co, _ = oracle.encode(tx, ty, l, xy, lab)
+    assert _mem_err(mems[1][0], mo) <= 1e-5
+
+
+def test_nufft_outliers_and_single_class():
+    """Points off the NUFFT grid (far outside the world bounds: the direct fallback) and a batch
+    with one class only: memories equal the oracle's, the empty class stays exactly zero."""
+    from paper_2408_09066_b200 import Mapper
+    rng = np.random.default_rng(7)
+    D, l, W = 4096, 0.3, 40.0
+    xy = rng.uniform(0, W, size=(60000, 2)).astype(np.float32)
+    xy[:500] = rng.uniform(-3 * W, 4 * W, size=(500, 2)).astype(np.float32)   # outliers
+    lab = (rng.random(60000) < 0.3).astype(np.uint8)
+    tx, ty = oracle.theta(0, D)
+    for labels in (lab, np.ones_like(lab)):
+        mp = Mapper(D, 0, l, (0.0, 0.0, W, W))
+        mp.set_tuning("enc_method", 1)
+        mp.encode_bundle(*_cuda(xy, labels))
+        assert mp.sync() == 0
+        mg, cg = mp.get_memory()
+        mp.close()
+        mo, co, _ = oracle.encode(tx, ty, l, xy, labels)
+        assert list(cg) == list(co)
+        for c in (0, 1):
+            if co[c]:
+                assert np.linalg.norm(mg[c] - mo[c]) <= 1e-5 * np.linalg.norm(mo[c])
+            else:
+                assert not np.any(mg[c])
