@@ -238,7 +238,7 @@ __device__ __forceinline__ float2 *stockham(float2 *a, float2 *b, const float2 *
             const int j = jj + threadIdx.x;
             const int k = j & (p - 1);
             const float2 x0 = a[j], x1 = a[j + N / 2];
-            const float2 w = tw[(p - 1) + k];          // stage table: consecutive k, no bank conflicts
+            const float2 w = __ldg(tw + (p - 1) + k);   // stage table: consecutive k
             const float2 t = make_float2(w.x * x1.x - w.y * x1.y, w.x * x1.y + w.y * x1.x);
             const int o = ((j - k) << 1) + k;
             b[o] = make_float2(x0.x + t.x, x0.y + t.y);
@@ -263,8 +263,7 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(const unsigned long long *__res
 {
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
-    float2 *a = sm_fft, *b = sm_fft + N, *stw = sm_fft + 2 * N;
-    for (int q = threadIdx.x; q < N - 1; q += T) stw[q] = tw[q];
+    float2 *a = sm_fft, *b = sm_fft + N;
     const int gy = blockIdx.x, c = blockIdx.y;
     // tile rows whose windows cover gy: ty with ty*TS - WOFF <= gy < ty*TS - WOFF + WIN
     const int ty_hi = min(ntx - 1, (gy + NU_WOFF) / NU_TS);
@@ -289,7 +288,7 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(const unsigned long long *__res
         }
         a[j] = make_float2(v, 0.f);
     }
-    float2 *r = stockham<LOGN, T>(a, b, stw);
+    float2 *r = stockham<LOGN, T>(a, b, tw);
     // only the frequencies the interpolation reads: |m| < K2 = N/4 + 8 (|t| <= pi/2 plus the
     // 6-point reach), stored compactly at m + K2
     constexpr int K2 = N / 4 + 8;
@@ -308,13 +307,12 @@ __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t,
 {
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
-    float2 *a = sm_fft, *b = sm_fft + N, *stw = sm_fft + 2 * N;
-    for (int q = threadIdx.x; q < N - 1; q += T) stw[q] = tw[q];
+    float2 *a = sm_fft, *b = sm_fft + N;
     constexpr int K2 = N / 4 + 8;
     const int cx = blockIdx.x, c = blockIdx.y;          // compact x-frequency, class
     const float2 *in = f1t + ((size_t)c * 2 * K2 + cx) * n1;
     for (int j = threadIdx.x; j < N; j += T) a[j] = j < n1 ? in[j] : make_float2(0.f, 0.f);
-    float2 *r = stockham<LOGN, T>(a, b, stw);
+    float2 *r = stockham<LOGN, T>(a, b, tw);
     float2 *out = G + ((size_t)c * 2 * K2 + cx) * 2 * K2;
     for (int cc = threadIdx.x; cc < 2 * K2; cc += T) out[cc] = r[(cc - K2) & (N - 1)];
 }
@@ -459,7 +457,9 @@ int launch_ffts(vsaogm_ctx *c)
 {
     constexpr int T = 512;
     const int N = 1 << LOGN;
-    const size_t smem = (3 * (size_t)N) * sizeof(float2);
+    // 2 N complex values (32 KB at N = 2048): fits beside a decode-GEMM CTA in the pipelined
+    // schedule; the per-stage twiddles are read from global memory (coalesced, L1-resident)
+    const size_t smem = (2 * (size_t)N) * sizeof(float2);
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_rowfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_colfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_nu_rowfft<LOGN, T><<<dim3(c->nu_n1, 2), T, smem, c->stream>>>(
