@@ -252,6 +252,63 @@ __device__ __forceinline__ float2 *stockham(float2 *a, float2 *b, const float2 *
     return a;
 }
 
+// Mixed radix-4 / radix-2 Stockham transform (same result as stockham<>): an odd LOGN starts with
+// one radix-2 stage, then radix-4 stages (sub-transform size Ns x4 per stage): half the barriers
+// and shared-memory passes of radix 2.  Radix-4 twiddles e^{+2 pi i k / (4 Ns)} are the radix-2
+// table's stage 2 Ns entries (tw[2 Ns - 1 + k]); w^2, w^3 by products.
+template <int LOGN, int T>
+__device__ __forceinline__ float2 *stockham4(float2 *a, float2 *b, const float2 *__restrict__ tw)
+{
+    constexpr int N = 1 << LOGN;
+    int ns = 1;
+    if (LOGN & 1) {   // radix-2 stage, Ns = 1 (twiddle 1)
+        __syncthreads();
+#pragma unroll
+        for (int jj = 0; jj < N / 2; jj += T) {
+            const int j = jj + threadIdx.x;
+            const float2 x0 = a[j], x1 = a[j + N / 2];
+            b[2 * j] = make_float2(x0.x + x1.x, x0.y + x1.y);
+            b[2 * j + 1] = make_float2(x0.x - x1.x, x0.y - x1.y);
+        }
+        float2 *c = a;
+        a = b;
+        b = c;
+        ns = 2;
+    }
+#pragma unroll
+    for (int st = 0; st < LOGN / 2; ++st) {
+        __syncthreads();
+#pragma unroll
+        for (int jj = 0; jj < N / 4; jj += T) {
+            const int j = jj + threadIdx.x;
+            const int k = j & (ns - 1);
+            float2 x0 = a[j], x1 = a[j + N / 4], x2 = a[j + N / 2], x3 = a[j + 3 * N / 4];
+            if (ns > 1) {
+                const float2 w1 = __ldg(tw + 2 * ns - 1 + k);
+                const float2 w2 = make_float2(w1.x * w1.x - w1.y * w1.y, 2.f * w1.x * w1.y);
+                const float2 w3 = make_float2(w2.x * w1.x - w2.y * w1.y, w2.x * w1.y + w2.y * w1.x);
+                x1 = make_float2(w1.x * x1.x - w1.y * x1.y, w1.x * x1.y + w1.y * x1.x);
+                x2 = make_float2(w2.x * x2.x - w2.y * x2.y, w2.x * x2.y + w2.y * x2.x);
+                x3 = make_float2(w3.x * x3.x - w3.y * x3.y, w3.x * x3.y + w3.y * x3.x);
+            }
+            // 4-point DFT with the + sign: i^q
+            const float2 s02 = make_float2(x0.x + x2.x, x0.y + x2.y), d02 = make_float2(x0.x - x2.x, x0.y - x2.y);
+            const float2 s13 = make_float2(x1.x + x3.x, x1.y + x3.y), d13 = make_float2(x1.x - x3.x, x1.y - x3.y);
+            const int o = ((j - k) << 2) + k;
+            b[o] = make_float2(s02.x + s13.x, s02.y + s13.y);
+            b[o + ns] = make_float2(d02.x - d13.y, d02.y + d13.x);           // + i d13
+            b[o + 2 * ns] = make_float2(s02.x - s13.x, s02.y - s13.y);
+            b[o + 3 * ns] = make_float2(d02.x + d13.y, d02.y - d13.x);       // - i d13
+        }
+        float2 *c = a;
+        a = b;
+        b = c;
+        ns <<= 2;
+    }
+    __syncthreads();
+    return a;
+}
+
 // row pass: block = one grid row gy of one class.  Sums the (<= 4) tile windows covering each
 // cell of the row (fixed point, exact), pre-corrects (psi_inv[gx] psi_inv[gy]), zero-pads to N,
 // transforms along x, and writes the column-major intermediate F1T[c][mx][gy] (mx < N, gy < n1).
@@ -288,7 +345,7 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(const unsigned long long *__res
         }
         a[j] = make_float2(v, 0.f);
     }
-    float2 *r = stockham<LOGN, T>(a, b, tw);
+    float2 *r = stockham4<LOGN, T>(a, b, tw);
     // only the frequencies the interpolation reads: |m| < K2 = N/4 + 8 (|t| <= pi/2 plus the
     // 6-point reach), stored compactly at m + K2
     constexpr int K2 = N / 4 + 8;
@@ -312,7 +369,7 @@ __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t,
     const int cx = blockIdx.x, c = blockIdx.y;          // compact x-frequency, class
     const float2 *in = f1t + ((size_t)c * 2 * K2 + cx) * n1;
     for (int j = threadIdx.x; j < N; j += T) a[j] = j < n1 ? in[j] : make_float2(0.f, 0.f);
-    float2 *r = stockham<LOGN, T>(a, b, tw);
+    float2 *r = stockham4<LOGN, T>(a, b, tw);
     float2 *out = G + ((size_t)c * 2 * K2 + cx) * 2 * K2;
     for (int cc = threadIdx.x; cc < 2 * K2; cc += T) out[cc] = r[(cc - K2) & (N - 1)];
 }
