@@ -12,8 +12,9 @@
 //      the order of the additions -- the L16 reproducibility of the fp64 reductions);
 //   2. B(s) = h^2 sum_g b(g) e^{i s.g h} is a type-2 NUFFT at the targets t_k = s_k h in
 //      [-pi/2, pi/2]^2: pre-correct b by 1 / psi^(l) (the Gaussian psi of the interpolation),
-//      zero-pad to n2 = 2^p >= 2 n1 and take a 2-D FFT (own radix-2 Stockham kernels, rows then
-//      columns), then interpolate at t_k over 13 x 13 grid points;
+//      zero-pad to n2 = 2^p >= 2 n1 and take a 2-D FFT (own mixed radix-4 Stockham kernels, rows
+//      then columns, both classes in one complex transform), then interpolate at t_k over 13 x 13
+//      grid points;
 //   3. pending += B(s_k) / Phi(s_k), Phi = 4 pi tau exp(-|s|^2 tau) (the FT of phi).
 // Accuracy (Gaussian gridding, msp = 6 both steps): ~1e-6 relative in l2 over k, below the fp32
 // direct encode's ~1.5e-5.
@@ -45,20 +46,20 @@ constexpr double NU_FIX = 4294967296.0; // 2^32: fixed-point scale of the spread
 // (d) k_nu_spread_tiles: block = (tile, class), one warp per point: the 196 weights of a point
 //     (14 x 14 separable Gaussian) go to 196 distinct cells, so each warp adds into its own
 //     private copy of the window without atomics, in integer fixed point; the 8 copies are then
-//     summed (exact) and written to the tile's scratch slot as 32.32 fixed point.  The row FFT
-//     sums the (<= 4) windows covering each cell.
+//     summed (exact) and the nonzero cells added into the class's dense 32.32 fixed-point grid
+//     with 64-bit integer atomics (exact: order-independent).  The row FFT reads and re-zeroes it.
 constexpr int NU_TS = 16;                      // tile side (cells)
-constexpr int NU_WIN = NU_TS + NU_W - 1;       // 45: window side
+constexpr int NU_WIN = NU_TS + NU_W - 1;       // 29: window side
 constexpr int NU_WOFF = NU_MSP;                // window starts 6 cells before the tile
 
 __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n,
                                                 double cx, double cy, double lo, double inv_h, int n1, int ntx,
                                                 int *__restrict__ bin_cnt, int2 *__restrict__ pkey, int64_t chunk_pts,
                                                 int *__restrict__ out_cnt, double *__restrict__ pcount,
-                                                int *__restrict__ err)
+                                                int *__restrict__ bcnt, int *__restrict__ err)
 {
-    __shared__ int s_cnt[2];
-    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __shared__ int s_cnt[4];   // class counts: all valid points, grid points
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int my_err = 0;
@@ -73,8 +74,10 @@ __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, c
             const int ix = (int)floor(((double)v.x - cx - lo) * inv_h), iy = (int)floor(((double)v.y - cy - lo) * inv_h);
             if (ix - NU_MSP < 0 || iy - NU_MSP < 0 || ix + NU_MSP + 1 >= n1 || iy + NU_MSP + 1 >= n1)
                 atomicAdd(&out_cnt[i / chunk_pts], 1);       // outlier: direct fallback
-            else
+            else {
                 key.x = (L * ntx + iy / NU_TS) * ntx + ix / NU_TS;
+                atomicAdd(&s_cnt[2 + L], 1);
+            }
         }
     }
     // warp-aggregated slot allocation: one atomic per distinct bin in the warp (neighbouring
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, c
     if (my_err) atomicOr(err, my_err);
     __syncthreads();
     if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&pcount[threadIdx.x], (double)s_cnt[threadIdx.x]);
+    if (threadIdx.x >= 2 && threadIdx.x < 4 && s_cnt[threadIdx.x]) atomicAdd(&bcnt[threadIdx.x - 2], s_cnt[threadIdx.x]);
 }
 
 // exclusive prefix of the bin counts and of the bins' work units (NU_UNIT points each): unit u
@@ -153,9 +157,9 @@ __global__ void __launch_bounds__(256) k_nu_place(const float2 *__restrict__ xy,
 __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restrict__ sorted, const int *__restrict__ bin_off,
                                                          const int *__restrict__ unit_bin,
                                                          const int *__restrict__ unit_first,
-                                                         const int *__restrict__ n_units, int ntx, double cx, double cy,
-                                                         double lo, double h, double inv_h, double tau,
-                                                         unsigned long long *__restrict__ scratch)
+                                                         const int *__restrict__ n_units, int ntx, int n1, double cx,
+                                                         double cy, double lo, double h, double inv_h, double tau,
+                                                         unsigned long long *__restrict__ grid)
 {
     constexpr int NWIN = NU_WIN * NU_WIN;
     __shared__ unsigned int s_win[8][NWIN];            // one window per warp
@@ -212,85 +216,81 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
         }
     }
     __syncthreads();
-    unsigned long long *dst = scratch + (size_t)unit * NWIN;
+    // the nonzero cells (all inside the grid: a point's whole support is) into the class's
+    // dense 32.32 grid: integer atomics, so the sum does not depend on the order of the units
+    unsigned long long *gc = grid + (size_t)(bin / (ntx * ntx)) * n1 * n1;
     for (int q = threadIdx.x; q < NWIN; q += blockDim.x) {
         unsigned long long acc = 0;
 #pragma unroll
         for (int w8 = 0; w8 < 8; ++w8) acc += s_win[w8][q];
-        dst[q] = acc << (32 - sh);
+        if (acc) {
+            const int wy = q / NU_WIN, wx = q - wy * NU_WIN;
+            atomicAdd(gc + (size_t)(gy0 + wy) * n1 + (gx0 + wx), acc << (32 - sh));
+        }
     }
 }
 
 // ---- 2. FFTs ------------------------------------------------------------------------------
-// Radix-2 Stockham (self-sorting) transform of N = 2^LOGN complex values in shared memory with
-// the positive exponent, G_m = sum_j a_j e^{+2 pi i j m / N}; per-stage twiddle tables
-// tw[p - 1 + k] = e^{+2 pi i k / (2p)}, k < p, p = 1, 2, 4, ... N/2 (N - 1 entries).
-template <int LOGN, int T>
-__device__ __forceinline__ float2 *stockham(float2 *a, float2 *b, const float2 *__restrict__ tw)
+// Both classes go through ONE complex transform: Z = b_0 + i alpha b_1 (the grids are real), and
+// the interpolation separates them by the conjugate symmetry of real transforms,
+//   B_0(m) = (Z^(m) + conj Z^(-m)) / 2,   B_1(m) = (Z^(m) - conj Z^(-m)) / (2 i alpha),
+// which halves the FFT work.  alpha = 2^e (exact) balances the classes' magnitudes (the fp32
+// transform error is relative to |Z|): e = round(log2(n_0 / n_1)) over this batch's grid points.
+__device__ __forceinline__ float nu_alpha(const int *__restrict__ bcnt)
 {
-    constexpr int N = 1 << LOGN;
-#pragma unroll
-    for (int s = 0; s < LOGN; ++s) {
-        const int p = 1 << s;                          // compile-time after unrolling
-        __syncthreads();
-#pragma unroll
-        for (int jj = 0; jj < N / 2; jj += T) {
-            const int j = jj + threadIdx.x;
-            const int k = j & (p - 1);
-            const float2 x0 = a[j], x1 = a[j + N / 2];
-            const float2 w = __ldg(tw + (p - 1) + k);   // stage table: consecutive k
-            const float2 t = make_float2(w.x * x1.x - w.y * x1.y, w.x * x1.y + w.y * x1.x);
-            const int o = ((j - k) << 1) + k;
-            b[o] = make_float2(x0.x + t.x, x0.y + t.y);
-            b[o + p] = make_float2(x0.x - t.x, x0.y - t.y);
-        }
-        float2 *c = a;
-        a = b;
-        b = c;
-    }
-    __syncthreads();
-    return a;
+    const int n0 = bcnt[0], n1 = bcnt[1];
+    if (n0 <= 0 || n1 <= 0) return 1.f;
+    const int e = max(-12, min(12, (int)rintf(log2f((float)n0 / (float)n1))));
+    return ldexpf(1.f, e);
 }
 
-// Mixed radix-4 / radix-2 Stockham transform (same result as stockham<>): an odd LOGN starts with
-// one radix-2 stage, then radix-4 stages (sub-transform size Ns x4 per stage): half the barriers
-// and shared-memory passes of radix 2.  Radix-4 twiddles e^{+2 pi i k / (4 Ns)} are the radix-2
-// table's stage 2 Ns entries (tw[2 Ns - 1 + k]); w^2, w^3 by products.
-template <int LOGN, int T>
-__device__ __forceinline__ float2 *stockham4(float2 *a, float2 *b, const float2 *__restrict__ tw)
+// Mixed radix Stockham (self-sorting) transform of N = 2^LOGN complex values in shared memory
+// with the positive exponent, G_m = sum_j x_j e^{+2 pi i j m / N}, of an input whose upper half
+// is zero (the zero padding: n1 <= N / 2): the first stage is folded into the load -- x_j =
+// load(j), j < N / 2 -- (radix 2 for odd LOGN: (x_j, x_j); radix 4 for even LOGN: the 4-point
+// DFT of (x_j, x_{j + N/4}, 0, 0)), then radix-4 stages (sub-transform size Ns x4 per stage).
+// Radix-4 twiddles e^{+2 pi i k / (4 Ns)}, k < Ns: tw[2 Ns - 1 + k] of the per-stage table
+// tw[p - 1 + k] = e^{+2 pi i k / (2p)}, k < p, p = 1, 2, 4, ... N/2; w^2, w^3 by products.
+template <int LOGN, int T, class Load>
+__device__ __forceinline__ float2 *stockham_zp(float2 *a, float2 *b, const float2 *__restrict__ tw, Load load)
 {
     constexpr int N = 1 << LOGN;
-    int ns = 1;
-    if (LOGN & 1) {   // radix-2 stage, Ns = 1 (twiddle 1)
-        __syncthreads();
+    int ns;
+    if (LOGN & 1) {
 #pragma unroll
         for (int jj = 0; jj < N / 2; jj += T) {
             const int j = jj + threadIdx.x;
-            const float2 x0 = a[j], x1 = a[j + N / 2];
-            b[2 * j] = make_float2(x0.x + x1.x, x0.y + x1.y);
-            b[2 * j + 1] = make_float2(x0.x - x1.x, x0.y - x1.y);
+            if (N / 2 < T && j >= N / 2) break;   // small transforms: fewer values than threads
+            const float2 v = load(j);
+            *reinterpret_cast<float4 *>(a + 2 * j) = make_float4(v.x, v.y, v.x, v.y);
         }
-        float2 *c = a;
-        a = b;
-        b = c;
         ns = 2;
+    } else {
+#pragma unroll
+        for (int jj = 0; jj < N / 4; jj += T) {
+            const int j = jj + threadIdx.x;
+            if (N / 4 < T && j >= N / 4) break;
+            const float2 x0 = load(j), x1 = load(j + N / 4);
+            *reinterpret_cast<float4 *>(a + 4 * j) = make_float4(x0.x + x1.x, x0.y + x1.y, x0.x - x1.y, x0.y + x1.x);
+            *reinterpret_cast<float4 *>(a + 4 * j + 2) = make_float4(x0.x - x1.x, x0.y - x1.y, x0.x + x1.y, x0.y - x1.x);
+        }
+        ns = 4;
     }
 #pragma unroll
-    for (int st = 0; st < LOGN / 2; ++st) {
+    for (int st = 0; st < (LOGN - 1) / 2; ++st) {
         __syncthreads();
 #pragma unroll
         for (int jj = 0; jj < N / 4; jj += T) {
             const int j = jj + threadIdx.x;
+            if (N / 4 < T && j >= N / 4) break;
             const int k = j & (ns - 1);
             float2 x0 = a[j], x1 = a[j + N / 4], x2 = a[j + N / 2], x3 = a[j + 3 * N / 4];
-            if (ns > 1) {
-                const float2 w1 = __ldg(tw + 2 * ns - 1 + k);
-                const float2 w2 = make_float2(w1.x * w1.x - w1.y * w1.y, 2.f * w1.x * w1.y);
-                const float2 w3 = make_float2(w2.x * w1.x - w2.y * w1.y, w2.x * w1.y + w2.y * w1.x);
-                x1 = make_float2(w1.x * x1.x - w1.y * x1.y, w1.x * x1.y + w1.y * x1.x);
-                x2 = make_float2(w2.x * x2.x - w2.y * x2.y, w2.x * x2.y + w2.y * x2.x);
-                x3 = make_float2(w3.x * x3.x - w3.y * x3.y, w3.x * x3.y + w3.y * x3.x);
-            }
+            const float2 w1 = __ldg(tw + 2 * ns - 1 + k);
+            const float2 w2 = make_float2(w1.x * w1.x - w1.y * w1.y, 2.f * w1.x * w1.y);
+            const float2 w3 = make_float2(w2.x * w1.x - w2.y * w1.y, w2.x * w1.y + w2.y * w1.x);
+            x1 = make_float2(w1.x * x1.x - w1.y * x1.y, w1.x * x1.y + w1.y * x1.x);
+            x2 = make_float2(w2.x * x2.x - w2.y * x2.y, w2.x * x2.y + w2.y * x2.x);
+            x3 = make_float2(w3.x * x3.x - w3.y * x3.y, w3.x * x3.y + w3.y * x3.x);
             // 4-point DFT with the + sign: i^q
             const float2 s02 = make_float2(x0.x + x2.x, x0.y + x2.y), d02 = make_float2(x0.x - x2.x, x0.y - x2.y);
             const float2 s13 = make_float2(x1.x + x3.x, x1.y + x3.y), d13 = make_float2(x1.x - x3.x, x1.y - x3.y);
@@ -309,85 +309,65 @@ __device__ __forceinline__ float2 *stockham4(float2 *a, float2 *b, const float2 
     return a;
 }
 
-// row pass: block = one grid row gy of one class.  Sums the (<= 4) tile windows covering each
-// cell of the row (fixed point, exact), pre-corrects (psi_inv[gx] psi_inv[gy]), zero-pads to N,
-// transforms along x, and writes the column-major intermediate F1T[c][mx][gy] (mx < N, gy < n1).
+// row pass: block = one grid row gy.  Reads the row of both classes' fixed-point grids (and
+// zeroes what it read: the grid is clean for the next encode), pre-corrects (psi_inv[gx]
+// psi_inv[gy]), packs Z = b_0 + i alpha b_1, zero-pads to N, transforms along x, and writes the
+// column-major intermediate F1T[mx][gy] (compact mx, gy < n1).
 template <int LOGN, int T>
-__global__ void __launch_bounds__(T) k_nu_rowfft(const unsigned long long *__restrict__ scratch,
-                                                 const int *__restrict__ unit_off, int ntx, int n1,
-                                                 const float *__restrict__ psi_inv, const float2 *__restrict__ tw,
-                                                 float2 *__restrict__ f1t)
+__global__ void __launch_bounds__(T) k_nu_rowfft(unsigned long long *__restrict__ grid, int n1,
+                                                 const int *__restrict__ bcnt, const float *__restrict__ psi_inv,
+                                                 const float2 *__restrict__ tw, float2 *__restrict__ f1t)
 {
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
-    float2 *a = sm_fft, *b = sm_fft + N;
-    const int gy = blockIdx.x, c = blockIdx.y;
-    // tile rows whose windows cover gy: ty with ty*TS - WOFF <= gy < ty*TS - WOFF + WIN
-    const int ty_hi = min(ntx - 1, (gy + NU_WOFF) / NU_TS);
-    const int ty_num = gy + NU_WOFF - NU_WIN;                 // floor division for negatives
-    const int ty_lo = ty_num < 0 ? 0 : ty_num / NU_TS + 1;
-    const float py = psi_inv[gy];
-    for (int j = threadIdx.x; j < N; j += T) {
-        float v = 0.f;
-        if (j < n1) {
-            const int tx_hi = min(ntx - 1, (j + NU_WOFF) / NU_TS);
-            const int tx_num = j + NU_WOFF - NU_WIN;
-            const int tx_lo = tx_num < 0 ? 0 : tx_num / NU_TS + 1;
-            long long acc = 0;
-            for (int ty = ty_lo; ty <= ty_hi; ++ty)
-                for (int tx = tx_lo; tx <= tx_hi; ++tx) {
-                    const int bin = (c * ntx + ty) * ntx + tx;
-                    const int wy = gy - (ty * NU_TS - NU_WOFF), wx = j - (tx * NU_TS - NU_WOFF);
-                    for (int u = unit_off[bin]; u < unit_off[bin + 1]; ++u)   // the bin's work units
-                        acc += (long long)scratch[((size_t)u * NU_WIN + wy) * NU_WIN + wx];
-                }
-            v = (float)((double)acc * (1.0 / NU_FIX)) * psi_inv[j] * py;
-        }
-        a[j] = make_float2(v, 0.f);
-    }
-    float2 *r = stockham4<LOGN, T>(a, b, tw);
+    const int gy = blockIdx.x;
+    const float py = psi_inv[gy], alpha = nu_alpha(bcnt);
+    unsigned long long *row0 = grid + (size_t)gy * n1, *row1 = grid + ((size_t)n1 + gy) * n1;
+    float2 *r = stockham_zp<LOGN, T>(sm_fft, sm_fft + N, tw, [&](int j) {
+        if (j >= n1) return make_float2(0.f, 0.f);
+        const unsigned long long v0 = row0[j], v1 = row1[j];
+        if (v0) row0[j] = 0ull;
+        if (v1) row1[j] = 0ull;
+        const float s = psi_inv[j] * py;
+        return make_float2((float)((double)v0 * (1.0 / NU_FIX)) * s, (float)((double)v1 * (1.0 / NU_FIX)) * s * alpha);
+    });
     // only the frequencies the interpolation reads: |m| < K2 = N/4 + 8 (|t| <= pi/2 plus the
     // 6-point reach), stored compactly at m + K2
     constexpr int K2 = N / 4 + 8;
-    float2 *out = f1t + (size_t)c * 2 * K2 * n1;
-    for (int cc = threadIdx.x; cc < 2 * K2; cc += T) {
-        const int m = cc - K2;
-        out[(size_t)cc * n1 + gy] = r[m & (N - 1)];
-    }
+    for (int cc = threadIdx.x; cc < 2 * K2; cc += T) f1t[(size_t)cc * n1 + gy] = r[(cc - K2) & (N - 1)];
 }
 
-// column pass: block = one (compact) x-frequency of one class; transforms along y and writes
-// the compact G[c][mx + K2][my + K2] (|mx|, |my| < K2).
+// column pass: block = one (compact) x-frequency; transforms along y and writes the compact
+// Z^[mx + K2][my + K2] (|mx|, |my| < K2).
 template <int LOGN, int T>
 __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t, int n1, const float2 *__restrict__ tw,
                                                  float2 *__restrict__ G)
 {
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
-    float2 *a = sm_fft, *b = sm_fft + N;
     constexpr int K2 = N / 4 + 8;
-    const int cx = blockIdx.x, c = blockIdx.y;          // compact x-frequency, class
-    const float2 *in = f1t + ((size_t)c * 2 * K2 + cx) * n1;
-    for (int j = threadIdx.x; j < N; j += T) a[j] = j < n1 ? in[j] : make_float2(0.f, 0.f);
-    float2 *r = stockham4<LOGN, T>(a, b, tw);
-    float2 *out = G + ((size_t)c * 2 * K2 + cx) * 2 * K2;
+    const int cx = blockIdx.x;
+    const float2 *in = f1t + (size_t)cx * n1;
+    float2 *r = stockham_zp<LOGN, T>(sm_fft, sm_fft + N, tw,
+                                     [&](int j) { return j < n1 ? in[j] : make_float2(0.f, 0.f); });
+    float2 *out = G + (size_t)cx * 2 * K2;
     for (int cc = threadIdx.x; cc < 2 * K2; cc += T) out[cc] = r[(cc - K2) & (N - 1)];
 }
 
 // ---- 3. interpolation + deconvolution ------------------------------------------------------
-// one warp per (dimension k, class c): g(t) = hs^2 sum_{m near t} psi(t - t_m) G(t_m) e^{-i n1/2 t_m}
+// one warp per dimension k: g_c(t) = hs^2 sum_{m near t} psi(t - t_m) B_c(t_m) e^{-i n1/2 t_m}
 // over the 13 x 13 grid points nearest t (the grid index l runs from 0 while the coefficients are
-// centred at n1/2); lanes take the points in a fixed order and the warp sums them in a fixed
-// tree (deterministic); then pending += h^2 g / Phi(s).
+// centred at n1/2), B_c separated from Z^(m), Z^(-m) (above); lanes take the points in a fixed
+// order and the warp sums them in a fixed tree (deterministic); then pending_c += h^2 g_c / Phi(s)
+// for each class with grid points in this batch (an empty class stays exactly zero).
 __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G, int logn, int n1, int D, int Dp,
                                                    const double *__restrict__ tx_turns, const double *__restrict__ ty_turns,
                                                    double h, double tau, double tau2, const float2 *__restrict__ ph,
-                                                   double *__restrict__ pending)
+                                                   const int *__restrict__ bcnt, double *__restrict__ pending)
 {
     constexpr int NP = 2 * NU_MSP2 + 1;   // 13
     const int lane = threadIdx.x & 31;
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int c = blockIdx.y;
     if (k >= D) return;   // warp-uniform
     const int N = 1 << logn;
     const double hs = 2.0 * 3.14159265358979323846 / N;
@@ -395,9 +375,9 @@ __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G,
     const double tx = sx * h, ty = sy * h;   // fp64 frequencies w = theta / l
     const int m0x = (int)rint(tx / hs), m0y = (int)rint(ty / hs);
     const float inv4t2 = (float)(1.0 / (4.0 * tau2));
-    const int K2 = N / 4 + 8;                // compact frequency range (k_nu_colfft)
-    const float2 *Gc = G + (size_t)c * 4 * K2 * K2;
-    float ar = 0.f, ai = 0.f;
+    const float inv2a = 0.5f / nu_alpha(bcnt);
+    const int K2 = N / 4 + 8;                // compact frequency range (k_nu_colfft); |m| <= N/4 + 7
+    float a0r = 0.f, a0i = 0.f, a1r = 0.f, a1i = 0.f;
     for (int idx = lane; idx < NP * NP; idx += 32) {
         const int dx = idx / NP, dy = idx - dx * NP;
         const int mx = m0x - NU_MSP2 + dx, my = m0y - NU_MSP2 + dy;
@@ -405,21 +385,35 @@ __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G,
         const float w = __expf(-(ux * ux + uy * uy) * inv4t2);
         const float2 px = ph[mx & (N - 1)], py = ph[my & (N - 1)];
         const float2 p = make_float2(w * (px.x * py.x - px.y * py.y), w * (px.x * py.y + px.y * py.x));
-        const float2 g = Gc[(size_t)(mx + K2) * 2 * K2 + (my + K2)];
-        ar += g.x * p.x - g.y * p.y;
-        ai += g.x * p.y + g.y * p.x;
+        const float2 g = G[(size_t)(mx + K2) * 2 * K2 + (my + K2)];
+        const float2 gm = G[(size_t)(K2 - mx) * 2 * K2 + (K2 - my)];
+        const float2 b0 = make_float2(0.5f * (g.x + gm.x), 0.5f * (g.y - gm.y));
+        const float2 b1 = make_float2(inv2a * (g.y + gm.y), -inv2a * (g.x - gm.x));
+        a0r += b0.x * p.x - b0.y * p.y;
+        a0i += b0.x * p.y + b0.y * p.x;
+        a1r += b1.x * p.x - b1.y * p.y;
+        a1i += b1.x * p.y + b1.y * p.x;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        ar += __shfl_xor_sync(0xffffffffu, ar, o);
-        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+        a0r += __shfl_xor_sync(0xffffffffu, a0r, o);
+        a0i += __shfl_xor_sync(0xffffffffu, a0i, o);
+        a1r += __shfl_xor_sync(0xffffffffu, a1r, o);
+        a1i += __shfl_xor_sync(0xffffffffu, a1i, o);
     }
     if (lane == 0) {
         const double s2 = sx * sx + sy * sy;
         const double scale = h * h * hs * hs / (4.0 * 3.14159265358979323846 * tau * exp(-s2 * tau));
-        double *pd = pending + 2 * ((size_t)c * Dp + k);
-        pd[0] += scale * ar;
-        pd[1] += scale * ai;
+        if (bcnt[0] > 0) {
+            double *pd = pending + 2 * (size_t)k;
+            pd[0] += scale * a0r;
+            pd[1] += scale * a0i;
+        }
+        if (bcnt[1] > 0) {
+            double *pd = pending + 2 * ((size_t)Dp + k);
+            pd[0] += scale * a1r;
+            pd[1] += scale * a1i;
+        }
     }
 }
 
@@ -493,10 +487,13 @@ int vsa_nufft_plan(vsaogm_ctx *c)
     c->nu_ntx = ntx;
     const int nbins = 2 * ntx * ntx;
     const size_t K2 = N / 4 + 8;
-    const size_t grid_bytes = 0, f1_bytes = 2 * 2 * K2 * n1 * 8, g_bytes = 2 * 4 * K2 * K2 * 8;
-    if (cudaMalloc(&c->d_nu_bins, (3 * (size_t)nbins + 3) * sizeof(int)) != cudaSuccess) return VSAOGM_ENOMEM;
-    VSA_CUDA_TRY(cudaMemset(c->d_nu_bins, 0, (3 * (size_t)nbins + 3) * sizeof(int)));
-    (void)grid_bytes;   // the unit windows are sized per encode (vsa_launch_encode_nufft)
+    // dense fixed-point grids of both classes (zeroed once; the row FFT re-zeroes what it reads),
+    // the packed transform's intermediate and compact output
+    const size_t grid_bytes = 2 * (size_t)n1 * n1 * 8, f1_bytes = 2 * K2 * n1 * 8, g_bytes = 4 * K2 * K2 * 8;
+    if (cudaMalloc(&c->d_nu_bins, (3 * (size_t)nbins + 5) * sizeof(int)) != cudaSuccess) return VSAOGM_ENOMEM;
+    VSA_CUDA_TRY(cudaMemset(c->d_nu_bins, 0, (3 * (size_t)nbins + 5) * sizeof(int)));
+    if (cudaMalloc(&c->d_nu_grid, grid_bytes) != cudaSuccess) return VSAOGM_ENOMEM;
+    VSA_CUDA_TRY(cudaMemset(c->d_nu_grid, 0, grid_bytes));
     if (cudaMalloc(&c->d_nu_f1, f1_bytes) != cudaSuccess ||
         cudaMalloc(&c->d_nu_G, g_bytes) != cudaSuccess || cudaMalloc(&c->d_nu_psi, n1 * 4) != cudaSuccess ||
         cudaMalloc(&c->d_nu_tw, N * 8) != cudaSuccess || cudaMalloc(&c->d_nu_ph, N * 8) != cudaSuccess)
@@ -510,7 +507,7 @@ int vsa_nufft_plan(vsaogm_ctx *c)
 
 namespace {
 template <int LOGN>
-int launch_ffts(vsaogm_ctx *c)
+int launch_ffts(vsaogm_ctx *c, const int *bcnt)
 {
     constexpr int T = 512;
     const int N = 1 << LOGN;
@@ -519,11 +516,10 @@ int launch_ffts(vsaogm_ctx *c)
     const size_t smem = (2 * (size_t)N) * sizeof(float2);
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_rowfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_colfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_nu_rowfft<LOGN, T><<<dim3(c->nu_n1, 2), T, smem, c->stream>>>(
-        (const unsigned long long *)c->d_nu_grid, c->d_nu_bins + 2 * (2 * c->nu_ntx * c->nu_ntx) + 1, c->nu_ntx,
-        c->nu_n1, c->d_nu_psi,
-        (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_f1);
-    k_nu_colfft<LOGN, T><<<dim3(2 * (N / 4 + 8), 2), T, smem, c->stream>>>((const float2 *)c->d_nu_f1, c->nu_n1,
+    k_nu_rowfft<LOGN, T><<<c->nu_n1, T, smem, c->stream>>>((unsigned long long *)c->d_nu_grid, c->nu_n1, bcnt,
+                                                           c->d_nu_psi, (const float2 *)c->d_nu_tw,
+                                                           (float2 *)c->d_nu_f1);
+    k_nu_colfft<LOGN, T><<<2 * (N / 4 + 8), T, smem, c->stream>>>((const float2 *)c->d_nu_f1, c->nu_n1,
                                                               (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_G);
     return VSAOGM_OK;
 }
@@ -544,52 +540,52 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     if ((size_t)n > c->nu_pts_cap) {
         if (c->d_nu_key) cudaFree(c->d_nu_key);
         if (c->d_nu_sorted) cudaFree(c->d_nu_sorted);
-        if (c->d_nu_grid) cudaFree(c->d_nu_grid);
         if (c->d_nu_units) cudaFree(c->d_nu_units);
-        c->d_nu_key = c->d_nu_sorted = c->d_nu_grid = nullptr;
+        c->d_nu_key = c->d_nu_sorted = nullptr;
         c->d_nu_units = nullptr;
         c->nu_pts_cap = 0;
         const size_t cap = (size_t)n + (size_t)n / 4;   // headroom: batch sizes vary
         const size_t ucap = cap / NU_UNIT + nbins;
         if (cudaMalloc(&c->d_nu_key, cap * sizeof(int2)) != cudaSuccess ||
             cudaMalloc(&c->d_nu_sorted, cap * sizeof(float2)) != cudaSuccess ||
-            cudaMalloc(&c->d_nu_grid, ucap * NU_WIN * NU_WIN * sizeof(unsigned long long)) != cudaSuccess ||
             cudaMalloc(&c->d_nu_units, 2 * ucap * sizeof(int)) != cudaSuccess)
             return VSAOGM_ENOMEM;
         c->nu_pts_cap = cap;
     }
-    int *bin_cnt = c->d_nu_bins, *bin_off = c->d_nu_bins + nbins, *unit_off = c->d_nu_bins + 2 * nbins + 1;
-    int *n_units = c->d_nu_bins + 3 * nbins + 2;
+    // d_nu_bins: bin counts [nbins], grid-point class counts [2], bin offsets [nbins + 1], unit
+    // offsets [nbins + 1], unit count
+    int *bin_cnt = c->d_nu_bins, *bcnt = c->d_nu_bins + nbins, *bin_off = bcnt + 2, *unit_off = bin_off + nbins + 1;
+    int *n_units = unit_off + nbins + 1;
     int *unit_bin = c->d_nu_units, *unit_first = c->d_nu_units + (c->nu_pts_cap / NU_UNIT + nbins);
     VSA_CUDA_TRY(cudaMemsetAsync(c->d_nu_out, 0, chunks * sizeof(int), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(bin_cnt, 0, nbins * sizeof(int), c->stream));
+    VSA_CUDA_TRY(cudaMemsetAsync(bin_cnt, 0, (nbins + 2) * sizeof(int), c->stream));
     const unsigned pblocks = (unsigned)((n + 255) / 256);
     const double inv_h = 1.0 / c->nu_h;
     k_nu_bin<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, lab, n, c->cx, c->cy, c->nu_lo, inv_h, c->nu_n1, ntx,
                                              bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out, c->d_pcounts,
-                                             c->d_err);
+                                             bcnt, c->d_err);
     k_nu_scan<<<1, 1024, 0, c->stream>>>(bin_cnt, nbins, bin_off, unit_off, unit_bin, unit_first, n_units);
     k_nu_place<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, n, (const int2 *)c->d_nu_key, bin_off,
                                                (float2 *)c->d_nu_sorted);
     k_nu_spread_tiles<<<(unsigned)max_units, 256, 0, c->stream>>>(
-        (const float2 *)c->d_nu_sorted, bin_off, unit_bin, unit_first, n_units, ntx, c->cx, c->cy, c->nu_lo, c->nu_h,
+        (const float2 *)c->d_nu_sorted, bin_off, unit_bin, unit_first, n_units, ntx, c->nu_n1, c->cx, c->cy, c->nu_lo, c->nu_h,
         inv_h, c->nu_tau, (unsigned long long *)c->d_nu_grid);
     VSA_CUDA_TRY(cudaGetLastError());
     switch (c->nu_logn) {
-    case 8: rc = launch_ffts<8>(c); break;
-    case 9: rc = launch_ffts<9>(c); break;
-    case 10: rc = launch_ffts<10>(c); break;
-    case 11: rc = launch_ffts<11>(c); break;
-    case 12: rc = launch_ffts<12>(c); break;
-    case 13: rc = launch_ffts<13>(c); break;
-    default: rc = launch_ffts<7>(c); break;
+    case 8: rc = launch_ffts<8>(c, bcnt); break;
+    case 9: rc = launch_ffts<9>(c, bcnt); break;
+    case 10: rc = launch_ffts<10>(c, bcnt); break;
+    case 11: rc = launch_ffts<11>(c, bcnt); break;
+    case 12: rc = launch_ffts<12>(c, bcnt); break;
+    case 13: rc = launch_ffts<13>(c, bcnt); break;
+    default: rc = launch_ffts<7>(c, bcnt); break;
     }
     if (rc) return rc;
     VSA_CUDA_TRY(cudaGetLastError());
-    k_nu_interp<<<dim3((c->D + 7) / 8, 2), 256, 0, c->stream>>>((const float2 *)c->d_nu_G, c->nu_logn, c->nu_n1,
+    k_nu_interp<<<(c->D + 7) / 8, 256, 0, c->stream>>>((const float2 *)c->d_nu_G, c->nu_logn, c->nu_n1,
                                                                       c->D, c->Dp, c->d_tx_turns, c->d_ty_turns, c->nu_h,
                                                                       c->nu_tau, c->nu_tau2, (const float2 *)c->d_nu_ph,
-                                                                      c->d_pending);
+                                                                      bcnt, c->d_pending);
     VSA_CUDA_TRY(cudaGetLastError());
     c->launches += 7;
     return VSAOGM_OK;

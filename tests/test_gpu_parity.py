@@ -652,3 +652,27 @@ def test_nufft_outliers_and_single_class():
                 assert np.linalg.norm(mg[c] - mo[c]) <= 1e-5 * np.linalg.norm(mo[c])
             else:
                 assert not np.any(mg[c])
+
+
+@pytest.mark.parametrize("W", [9.6, 23.0, 50.0, 105.0, 215.0, 432.0])
+def test_nufft_transform_sizes(W):
+    """The NUFFT encode at every transform size (l = 0.3: N = 256 ... 8192 as the world grows,
+    odd and even log2 N, fewer values than threads per stage at the small end) equals the oracle
+    within 1e-5; the counts are exact."""
+    from paper_2408_09066_b200 import Mapper
+    rng = np.random.default_rng(int(W * 10))
+    D, l = 2048, 0.3
+    xy = rng.uniform(0, W, size=(20000, 2)).astype(np.float32)
+    lab = (rng.random(20000) < 0.25).astype(np.uint8)
+    mp = Mapper(D, 0, l, (0.0, 0.0, W, W))
+    mp.set_tuning("enc_method", 1)
+    for _ in range(2):   # the second encode checks that the row pass left the grid clean
+        mp.reset()
+        mp.encode_bundle(*_cuda(xy, lab))
+        assert mp.sync() == 0
+        mg, cg = mp.get_memory()
+    mp.close()
+    tx, ty = oracle.theta(0, D)
+    mo, co, _ = oracle.encode(tx, ty, l, xy, lab)
+    assert list(cg) == list(co)
+    assert _mem_err(mg, mo) <= 1e-5
