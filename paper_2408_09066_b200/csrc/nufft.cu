@@ -43,13 +43,14 @@ constexpr double NU_FIX = 4294967296.0; // 2^32: fixed-point scale of the spread
 // (b) k_nu_scan: exclusive prefix of the bin counts (one block).
 // (c) k_nu_place: each point to its bin's range (the order inside a bin is arbitrary -- the
 //     accumulation below is in integers, so the result is not).
-// (d) k_nu_spread_tiles: block = (tile, class), one warp per point: the 196 weights of a point
-//     (14 x 14 separable Gaussian) go to 196 distinct cells, so each warp adds into its own
-//     private copy of the window without atomics, in integer fixed point; the 8 copies are then
-//     summed (exact) and the nonzero cells added into the class's dense 32.32 fixed-point grid
-//     with 64-bit integer atomics (exact: order-independent).  The row FFT reads and re-zeroes it.
+// (d) k_nu_spread_tiles: block = (tile, class) work unit, one warp per point: the 196 weights of
+//     a point (14 x 14 separable Gaussian) are added into the block's shared window with 32-bit
+//     shared-memory atomics in integer fixed point (exact), then the window's nonzero cells into
+//     the class's dense 32.32 fixed-point grid with 64-bit integer atomics (exact: the result does
+//     not depend on the order).  The row FFT reads and re-zeroes the grid.
 constexpr int NU_TS = 16;                      // tile side (cells)
 constexpr int NU_WIN = NU_TS + NU_W - 1;       // 29: window side
+constexpr int NU_WST = 30;                     // window row stride (words): 7 rows apart = 18 banks
 constexpr int NU_WOFF = NU_MSP;                // window starts 6 cells before the tile
 
 __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n,
@@ -105,41 +106,75 @@ __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cn
                                                   int *__restrict__ unit_off, int *__restrict__ unit_bin,
                                                   int *__restrict__ unit_first, int *__restrict__ n_units)
 {
-    __shared__ int s_part[1024], s_upart[1024];
+    // thread t: bins [t per, (t + 1) per), read 8 at a time (independent loads); block scan by
+    // warp shuffles (two barriers)
+    constexpr int U = 8;
+    __shared__ int s_w[32], s_uw[32];
     const int per = (nbins + 1023) / 1024;
-    const int b0 = threadIdx.x * per, b1 = min(nbins, b0 + per);
+    const int b0 = min(nbins, (int)threadIdx.x * per), b1 = min(nbins, b0 + per);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int sum = 0, usum = 0;
-    for (int b = b0; b < b1; ++b) {
-        sum += bin_cnt[b];
-        usum += (bin_cnt[b] + NU_UNIT - 1) / NU_UNIT;
-    }
-    s_part[threadIdx.x] = sum;
-    s_upart[threadIdx.x] = usum;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {   // inclusive Hillis-Steele scans
-        const int v = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0;
-        const int uv = threadIdx.x >= o ? s_upart[threadIdx.x - o] : 0;
-        __syncthreads();
-        s_part[threadIdx.x] += v;
-        s_upart[threadIdx.x] += uv;
-        __syncthreads();
-    }
-    int run = s_part[threadIdx.x] - sum, urun = s_upart[threadIdx.x] - usum;
-    for (int b = b0; b < b1; ++b) {
-        bin_off[b] = run;
-        unit_off[b] = urun;
-        const int nu = (bin_cnt[b] + NU_UNIT - 1) / NU_UNIT;
-        for (int q = 0; q < nu; ++q) {
-            unit_bin[urun + q] = b;
-            unit_first[urun + q] = run + q * NU_UNIT;
+    for (int b = b0; b < b1; b += U) {
+        int v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = b + u < b1 ? __ldcg(bin_cnt + b + u) : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            sum += v[u];
+            usum += (v[u] + NU_UNIT - 1) / NU_UNIT;
         }
-        run += bin_cnt[b];
-        urun += nu;
+    }
+    int inc = sum, uinc = usum;   // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o), ut = __shfl_up_sync(0xffffffffu, uinc, o);
+        if (lane >= o) {
+            inc += t;
+            uinc += ut;
+        }
+    }
+    if (lane == 31) {
+        s_w[warp] = inc;
+        s_uw[warp] = uinc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int wi = s_w[lane], uwi = s_uw[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wi, o), ut = __shfl_up_sync(0xffffffffu, uwi, o);
+            if (lane >= o) {
+                wi += t;
+                uwi += ut;
+            }
+        }
+        s_w[lane] = wi;
+        s_uw[lane] = uwi;
+    }
+    __syncthreads();
+    int run = inc - sum + (warp ? s_w[warp - 1] : 0), urun = uinc - usum + (warp ? s_uw[warp - 1] : 0);
+    for (int b = b0; b < b1; b += U) {
+        int v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = b + u < b1 ? __ldcg(bin_cnt + b + u) : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (b + u >= b1) break;
+            bin_off[b + u] = run;
+            unit_off[b + u] = urun;
+            const int nu = (v[u] + NU_UNIT - 1) / NU_UNIT;
+            for (int q = 0; q < nu; ++q) {
+                unit_bin[urun + q] = b + u;
+                unit_first[urun + q] = run + q * NU_UNIT;
+            }
+            run += v[u];
+            urun += nu;
+        }
     }
     if (threadIdx.x == 1023) {
-        bin_off[nbins] = s_part[1023];
-        unit_off[nbins] = s_upart[1023];
-        *n_units = s_upart[1023];
+        bin_off[nbins] = s_w[31];
+        unit_off[nbins] = s_uw[31];
+        *n_units = s_uw[31];
     }
 }
 
@@ -161,71 +196,71 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
                                                          double cy, double lo, double h, double inv_h, double tau,
                                                          unsigned long long *__restrict__ grid)
 {
-    constexpr int NWIN = NU_WIN * NU_WIN;
-    __shared__ unsigned int s_win[8][NWIN];            // one window per warp
+    __shared__ unsigned int s_win[NU_WIN * NU_WST];   // the block's window (row stride NU_WST)
     const int unit = blockIdx.x;
     if (unit >= *n_units) return;                     // block-uniform (the grid is an upper bound)
     const int bin = unit_bin[unit];                   // (class, tile_y, tile_x)
     const int first = unit_first[unit];
     const int cnt = min(NU_UNIT, bin_off[bin + 1] - first);
-    // fixed point 2^20 per unit weight (a cell sums at most NU_UNIT weights <= 1: no 32-bit
-    // overflow even after the 8 copies are added); written as 32.32 fixed point (an exact shift)
-    constexpr int sh = 20;                            // <= NU_UNIT points: no 32-bit overflow
+    // fixed point 2^20 per unit weight: a cell sums at most NU_UNIT weights <= 1 (< 2^28, no 32-bit
+    // overflow); written as 32.32 fixed point (an exact shift)
+    constexpr int sh = 20;
     const float qscale = (float)(1u << sh);
-    for (int q = threadIdx.x; q < 8 * NWIN; q += blockDim.x) (&s_win[0][0])[q] = 0u;
+    for (int q = threadIdx.x; q < NU_WIN * NU_WST; q += blockDim.x) s_win[q] = 0u;
     __syncthreads();
     const int t = bin % (ntx * ntx);
     const int tx = t % ntx, ty = t / ntx;
     const int gx0 = tx * NU_TS - NU_WOFF, gy0 = ty * NU_TS - NU_WOFF;   // window origin (cells)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned int *win = s_win[warp];
-    const float inv4t = (float)(1.0 / (4.0 * tau));
+    // Gaussian in cell units: phi = exp(-c u^2), c = h^2 / (4 tau), u = support index - 6 - offset.
+    // Lane = support column dx (lanes 14, 15 of each half idle), half-warp = rows 7 half .. +6;
+    // the row weights by the recurrence exp(-c (u+1)^2) = exp(-c u^2) r, r = exp(-c (2u + 1)),
+    // r <- r exp(-2c) (Greengard & Lee's fast Gaussian gridding): 3 exponentials per lane and point.
+    const float c2 = (float)(h * h / (4.0 * tau));
+    const float e2 = __expf(-2.f * c2);
+    const int dx = lane & 15, half = lane >> 4;
+    const bool col_ok = dx < NU_W;
     const float2 *pts = sorted + first;
-    // this lane's 7 support cells (cell = lane + 32 r of the 14 x 14 support), fixed per lane
-    int dxr[7], dyr[7], offr[7];
-#pragma unroll
-    for (int r = 0; r < 7; ++r) {
-        const int cidx = lane + 32 * r;
-        dxr[r] = cidx % NU_W;
-        dyr[r] = cidx < NU_W * NU_W ? cidx / NU_W : 0;
-        offr[r] = dyr[r] * NU_WIN + dxr[r];
-    }
-    const bool last_ok = lane + 32 * 6 < NU_W * NU_W;   // rounds 0..5 always valid (196 = 6 * 32 + 4)
-    // the warp's points (p = warp + 8 j) loaded at once, one per lane, then broadcast
+    // the warp's points (p = warp + 8 j): 32 at a time, one per lane, which computes the point's
+    // cell with k_nu_bin's fp64 expression and its fractional offset in the cell; broadcast
     const int nmine = (cnt - warp + 7) / 8;
     for (int j0 = 0; j0 < nmine; j0 += 32) {
-        const float2 mine = j0 + lane < nmine ? pts[warp + 8 * (j0 + lane)] : make_float2(0.f, 0.f);
+        const float2 raw = j0 + lane < nmine ? pts[warp + 8 * (j0 + lane)] : make_float2(0.f, 0.f);
+        const double gxd = ((double)raw.x - cx - lo) * inv_h, gyd = ((double)raw.y - cy - lo) * inv_h;
+        const double flx = floor(gxd), fly = floor(gyd);
+        const int mcell = ((int)fly << 16) | (int)flx;       // 0 <= ix, iy < n1 <= 4096
+        const float mfx = (float)(gxd - flx), mfy = (float)(gyd - fly);
         const int jn = min(32, nmine - j0);
         for (int jj = 0; jj < jn; ++jj) {
-            const float2 raw = make_float2(__shfl_sync(0xffffffffu, mine.x, jj), __shfl_sync(0xffffffffu, mine.y, jj));
-            const double px = (double)raw.x - cx, py = (double)raw.y - cy;   // as k_nu_bin
-            const int ix = (int)floor((px - lo) * inv_h), iy = (int)floor((py - lo) * inv_h);
-            // lanes 0..13: x weights, 16..29: y weights of this point's 14 x 14 support
-            const int d = lane & 15;
-            const double gcoord = (double)((lane < 16 ? ix : iy) - NU_MSP + d) * h + lo;
-            const float u = (float)(gcoord - (lane < 16 ? px : py));
-            const float w = d < NU_W ? __expf(-u * u * inv4t) * (lane < 16 ? qscale : 1.f) : 0.f;   // x weights carry the scale
-            unsigned int *wb = win + (iy - NU_MSP - gy0) * NU_WIN + (ix - NU_MSP - gx0);   // support origin
+            const int cell = __shfl_sync(0xffffffffu, mcell, jj);
+            const float fx = __shfl_sync(0xffffffffu, mfx, jj), fy = __shfl_sync(0xffffffffu, mfy, jj);
+            const int ix = cell & 0xffff, iy = cell >> 16;
+            const float ux = (float)(dx - NU_MSP) - fx, uy = (float)(7 * half - NU_MSP) - fy;
+            const float wx = __expf(-c2 * ux * ux) * qscale;   // the x weight carries the scale
+            float wy = __expf(-c2 * uy * uy), r = __expf(-c2 * (2.f * uy + 1.f));
+            unsigned int *wb = s_win + (iy - NU_MSP - gy0 + 7 * half) * NU_WST + (ix - NU_MSP - gx0 + dx);
+            if (col_ok) {
 #pragma unroll
-            for (int r = 0; r < 7; ++r) {              // distinct cells within a round
-                const float wx = __shfl_sync(0xffffffffu, w, dxr[r]);
-                const float wy = __shfl_sync(0xffffffffu, w, 16 + dyr[r]);
-                if (r < 6 || last_ok) wb[offr[r]] += __float2uint_rn(wx * wy);
+                for (int k = 0; k < 7; ++k) {
+                    // round to the nearest integer by the 1.5 * 2^23 bias (wx wy <= 2^20 < 2^22):
+                    // ALU ops instead of a conversion on the XU pipe
+                    const unsigned int q = __float_as_uint(fmaf(wx, wy, 12582912.f)) - 0x4B400000u;
+                    atomicAdd(wb + k * NU_WST, q);   // shared-memory integer atomics: exact
+                    wy *= r;
+                    r *= e2;
+                }
             }
-            __syncwarp();
         }
     }
     __syncthreads();
     // the nonzero cells (all inside the grid: a point's whole support is) into the class's
     // dense 32.32 grid: integer atomics, so the sum does not depend on the order of the units
     unsigned long long *gc = grid + (size_t)(bin / (ntx * ntx)) * n1 * n1;
-    for (int q = threadIdx.x; q < NWIN; q += blockDim.x) {
-        unsigned long long acc = 0;
-#pragma unroll
-        for (int w8 = 0; w8 < 8; ++w8) acc += s_win[w8][q];
-        if (acc) {
-            const int wy = q / NU_WIN, wx = q - wy * NU_WIN;
-            atomicAdd(gc + (size_t)(gy0 + wy) * n1 + (gx0 + wx), acc << (32 - sh));
+    for (int q = threadIdx.x; q < NU_WIN * NU_WST; q += blockDim.x) {
+        const unsigned int v = s_win[q];
+        if (v) {
+            const int wy = q / NU_WST, wx = q - wy * NU_WST;
+            atomicAdd(gc + (size_t)(gy0 + wy) * n1 + (gx0 + wx), (unsigned long long)v << (32 - sh));
         }
     }
 }
@@ -374,14 +409,19 @@ __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G,
     const double sx = 2.0 * 3.14159265358979323846 * tx_turns[k], sy = 2.0 * 3.14159265358979323846 * ty_turns[k];
     const double tx = sx * h, ty = sy * h;   // fp64 frequencies w = theta / l
     const int m0x = (int)rint(tx / hs), m0y = (int)rint(ty / hs);
+    const float ftx = (float)(tx / hs - m0x), fty = (float)(ty / hs - m0y);   // in [-1/2, 1/2]
+    const float hsf = (float)hs;
     const float inv4t2 = (float)(1.0 / (4.0 * tau2));
     const float inv2a = 0.5f / nu_alpha(bcnt);
     const int K2 = N / 4 + 8;                // compact frequency range (k_nu_colfft); |m| <= N/4 + 7
     float a0r = 0.f, a0i = 0.f, a1r = 0.f, a1i = 0.f;
-    for (int idx = lane; idx < NP * NP; idx += 32) {
+#pragma unroll
+    for (int it = 0; it < (NP * NP + 31) / 32; ++it) {   // all loads of the warp's points in flight
+        const int idx = lane + 32 * it;
+        if (idx >= NP * NP) break;
         const int dx = idx / NP, dy = idx - dx * NP;
         const int mx = m0x - NU_MSP2 + dx, my = m0y - NU_MSP2 + dy;
-        const float ux = (float)(tx - (double)mx * hs), uy = (float)(ty - (double)my * hs);
+        const float ux = (ftx - (float)(dx - NU_MSP2)) * hsf, uy = (fty - (float)(dy - NU_MSP2)) * hsf;
         const float w = __expf(-(ux * ux + uy * uy) * inv4t2);
         const float2 px = ph[mx & (N - 1)], py = ph[my & (N - 1)];
         const float2 p = make_float2(w * (px.x * py.x - px.y * py.y), w * (px.x * py.y + px.y * py.x));
