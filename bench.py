@@ -280,6 +280,25 @@ def run_native(args):
         prof_bf16 = mp.profile_read()
         mp.profile_enable(False)
 
+        # the direct (sincos-and-reduce) pair encode of the same batches, timed alone: its ALU
+        # roofline is the north_star's encode evidence even where the NUFFT is the default
+        enc_direct_ms = None
+        if nufft:
+            md = Mapper(D, 0, l, sc.bounds)
+            md.set_tuning("enc_method", 0)
+            for b in range(2):
+                md.encode_bundle(*dev_batches[b % nb])
+            barrier()
+            md.profile_read()
+            md.profile_enable(True)
+            for k in range(kb):
+                md.encode_bundle(*dev_batches[(args.warmup + k) % nb])
+            barrier()
+            pd = md.profile_read()
+            md.close()
+            enc_direct_ms = pd["encode"][0] / max(1, pd["encode"][1])
+            direct_pts = float(np.mean([len(host_batches[(args.warmup + k) % nb][1]) for k in range(kb)]))
+
         hi, lo = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0)
         with torch.cuda.stream(hi):
             mp.set_encode_stream(lo)
@@ -368,6 +387,19 @@ def run_native(args):
     enc_roof = encode_ceiling(sm_max)
     enc_rate = phasors / (enc_ms * 1e-3)
     clocks = clk.summary()
+
+    def alu_line(rate):
+        return {"kernel": "k_encode_pairs", "bound": "alu", "achieved": round(rate / 1e9, 2),
+                "peak": round(enc_roof["combined"] / 1e9, 2), "unit": "Gphasor/s",
+                "frac": round(rate / enc_roof["combined"], 4), "traffic": traffic.get("encode"),
+                "peak_basis": enc_roof["basis"], "mufu_only_peak": round(enc_roof["mufu_only"] / 1e9, 2),
+                "frac_of_mufu_only": round(rate / enc_roof["mufu_only"], 4),
+                "frac_of_mufu_only_single_point": round(rate / enc_roof["mufu_only_single"], 4),
+                "measured_loop_ceiling": (round(enc_roof["measured"]["value"] / 1e9, 2) if enc_roof["measured"] else None),
+                "frac_of_measured_loop_ceiling": (round(rate / enc_roof["measured"]["value"], 4)
+                                                  if enc_roof["measured"] else None),
+                "frac_at_measured_clock": (round(rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
+                                           if clocks.get("sm_mhz") else None)}
     # decode GEMM: 2 M N K flops with M = 2 (band + halo rows), N = C, K = 2 Dp
     ra, rb = decoded_rows(R, r0, r1, h)
     Dp = (D + 31) // 32 * 32
@@ -382,17 +414,8 @@ def run_native(args):
                  "frac_of_sustained": round(gemm_tf / pk["bf16_tflops_sustained"], 4),
                  "traffic": traffic.get("decode_gemm"),
                  "peak_basis": f"MEASURED_PEAKS.json ({pk_kind}) bf16 burst (fp16 dense = bf16 dense)"}
-    enc_line = {"kernel": "k_encode_pairs", "bound": "alu", "achieved": round(enc_rate / 1e9, 2),
-                "peak": round(enc_roof["combined"] / 1e9, 2), "unit": "Gphasor/s",
-                "frac": round(enc_rate / enc_roof["combined"], 4), "traffic": traffic.get("encode"),
-                "peak_basis": enc_roof["basis"], "mufu_only_peak": round(enc_roof["mufu_only"] / 1e9, 2),
-                "frac_of_mufu_only": round(enc_rate / enc_roof["mufu_only"], 4),
-                "frac_of_mufu_only_single_point": round(enc_rate / enc_roof["mufu_only_single"], 4),
-                "measured_loop_ceiling": (round(enc_roof["measured"]["value"] / 1e9, 2) if enc_roof["measured"] else None),
-                "frac_of_measured_loop_ceiling": (round(enc_rate / enc_roof["measured"]["value"], 4)
-                                                  if enc_roof["measured"] else None),
-                "frac_at_measured_clock": (round(enc_rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
-                                           if clocks.get("sm_mhz") else None)}
+    enc_line = alu_line(enc_rate)
+    enc_direct = None
     if nufft:
         # the type-3 NUFFT encode is several short memory/latency-bound kernels, none an ALU
         # roofline: report its rate in phasor-equivalents (N x D / time) against the direct
@@ -406,6 +429,8 @@ def run_native(args):
                                                        if enc_roof["measured"] else None),
                     "x_mufu_only_single_point": round(enc_rate / enc_roof["mufu_only_single"], 3)}
         dominant = "decode_gemm"
+        enc_direct = dict(alu_line(direct_pts * D / (enc_direct_ms * 1e-3)), ms=round(enc_direct_ms, 4),
+                          note="direct pair encode (enc_method 0) of the same batches, serial, timed alone")
     roofline = enc_line if dominant == "encode" else gemm_roof
     gemm_bf16_ms = avg(prof_bf16, "decode_gemm")
     gemm_bf16_tf = flops / (gemm_bf16_ms * 1e-3) / 1e12
@@ -421,6 +446,7 @@ def run_native(args):
         "decode_cells_per_s_gemm_only": round(cells / (gemm_ms * 1e-3), 1),
         "decode_pct_tensor_peak": round(100 * gemm_tf / pk["bf16_tflops"], 2),
         "roofline": roofline, "decode_roofline": gemm_roof, "encode_roofline": enc_line,
+        "encode_direct_roofline": enc_direct,
         "schedule": "pipelined: encode of batch k+1 (low-priority stream) overlaps the GEMM + entropy of batch k",
         "serial": {"ms_per_step": round(serial_ms_per_step, 4), "value": round(cells / (serial_ms_per_step * 1e-3), 1),
                    "note": "one stream, L2 flushed between steps; kernel_ms_per_step and the rooflines are from here"},

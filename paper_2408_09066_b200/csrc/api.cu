@@ -182,9 +182,9 @@ int vsaogm_create_quadrants(int32_t D, uint64_t seed, double length_scale, vsaog
         if ((rc = dev_alloc_zero(&c->d_pending, 2 * (size_t)c->nslots * c->Dp + c->nslots))) break;
         c->d_pcounts = c->d_pending + 2 * (size_t)c->nslots * c->Dp;
         if ((rc = dev_alloc_zero(&c->d_counts, c->nslots))) break;
-        if ((rc = dev_alloc_zero(&c->d_norm2, c->nslots))) break;
+        if ((rc = dev_alloc_zero(&c->d_norm2, 2 * (size_t)c->nslots))) break;
         if ((rc = dev_alloc_zero(&c->d_mhat, (size_t)c->nslots * c->Dp))) break;
-        if ((rc = dev_alloc_zero(&c->d_normpart, (size_t)c->nslots * 16))) break;
+        if ((rc = dev_alloc_zero(&c->d_normpart, (size_t)c->nslots * 17))) break;
         if ((rc = dev_alloc_zero(&c->d_qc, 2 * (size_t)c->nq))) break;
         {
             std::vector<double> qc(2 * c->nq);

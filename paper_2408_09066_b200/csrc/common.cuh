@@ -137,9 +137,9 @@ struct vsaogm_ctx {
     double *d_pending = nullptr;
     long long *d_counts = nullptr;                 // [S]
     double *d_pcounts = nullptr;                   // = d_pending + 2 S Dp (not a separate allocation)
-    double *d_norm2 = nullptr;                     // ||m_c||^2 [2]
+    double *d_norm2 = nullptr;                     // ||m_c||^2 [S], then sqrt(D) / ||m_c|| [S]
     float2 *d_mhat = nullptr;                      // sqrt(D) m_c / ||m_c||, fp32 [S][Dp]
-    double *d_normpart = nullptr;                  // per-block partial ||m_c||^2 [S][16]
+    double *d_normpart = nullptr;                  // per-block partial ||m_c||^2 [S][16], then S u32 tickets
     int *d_err = nullptr;                          // deferred error bits
     int *d_ent_ctr = nullptr;                      // streamed entropy work queue [2]: next item, warps done
     float2 *d_part = nullptr;                      // encode chunk partials
@@ -213,6 +213,7 @@ int vsa_launch_encode(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_
 int vsa_launch_encode_sorted(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n);
 int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
                             int chunks);
+int vsa_launch_mhat(vsaogm_ctx *c);
 int vsa_launch_nufft_outliers(vsaogm_ctx *c, const float *xy, const uint8_t *lab, int64_t n, int64_t chunk_pts,
                               int chunks);
 bool vsa_nufft_wanted(vsaogm_ctx *c, int64_t n);

@@ -728,20 +728,21 @@ __global__ void k_commit(double *__restrict__ m, double *__restrict__ pending, l
     }
 }
 
-// Optional commit (m += pending, pending = 0), then ||m_c||^2 per memory slot (Eq. 10) and
-// the scaled conjugate-ready memory mhat_c = sqrt(D) m_c / ||m_c|| (0 for an empty class, L8)
-// in fp32 for the table-A kernel.  Cooperative grid (slot, nb <= NORM_BLOCKS k-ranges; nb
-// shrinks with the slot count so that the grid stays co-resident): each block
-// reduces its range with a fixed tree into normpart[slot][b]; after a grid-wide barrier every
-// block adds its slot's NORM_BLOCKS partials in index order (deterministic, identical in all
-// blocks) and scales its own range.
+// Optional commit (m += pending, pending = 0), then ||m_c||^2 per memory slot (Eq. 10): grid
+// (slot, nb <= NORM_BLOCKS k-ranges, nb fixed per Dp); each block commits its range and reduces
+// it with a fixed tree into normpart[slot][b]; the last block of a slot to finish (atomic
+// ticket) adds the slot's nb partials in a fixed order (deterministic) into norm2 -- an ordinary
+// launch, no grid barrier.  The table-A kernel scales m by sqrt(D) / ||m|| itself (k_mhat
+// writes the scaled fp32 copy only for the on-the-fly phasor-tile GEMM, gemm_agen).
 constexpr int NORM_THREADS = 256, NORM_BLOCKS = 16;
 __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restrict__ m, double *__restrict__ pending,
                                                                long long *__restrict__ cnt, double *__restrict__ pcnt,
                                                                int do_commit, int Dp, int D, double *__restrict__ normpart,
-                                                               double *__restrict__ norm2, float2 *__restrict__ mhat)
+                                                               unsigned int *__restrict__ ticket,
+                                                               double *__restrict__ norm2)
 {
     __shared__ double s[NORM_THREADS];
+    __shared__ bool s_last;
     const int c = blockIdx.x, b = blockIdx.y, nb = gridDim.y;
     const int per = (Dp + nb - 1) / nb;
     const int k1 = min(Dp, (b + 1) * per);
@@ -765,22 +766,48 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
         if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) normpart[c * NORM_BLOCKS + b] = s[0];
-    cg::this_grid().sync();
-    double n2 = 0.0;
-    for (int i = 0; i < nb; ++i) n2 += normpart[c * NORM_BLOCKS + i];
-    const double sc = n2 > 0.0 ? sqrt((double)D / n2) : 0.0;
-    for (int k = b * per + threadIdx.x; k < k1; k += NORM_THREADS) {
-        const size_t o = 2 * ((size_t)c * Dp + k);
-        mhat[(size_t)c * Dp + k] = make_float2((float)(m[o] * sc), (float)(m[o + 1] * sc));
+    if (threadIdx.x == 0) {
+        normpart[c * NORM_BLOCKS + b] = s[0];
+        __threadfence();   // the partial and this block's m are visible before the ticket
+        s_last = atomicAdd(ticket + c, 1u) == (unsigned)nb - 1;
     }
-    if (b == 0 && threadIdx.x == 0) {
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    __shared__ double s_n2;
+    if (threadIdx.x < 32) {   // fixed order: lane-strided, then a butterfly
+        double v = 0.0;
+        for (int i = threadIdx.x; i < nb; i += 32) v += __ldcg(normpart + c * NORM_BLOCKS + i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) {
+            s_n2 = v;
+            ticket[c] = 0u;   // ready for the next launch (stream-ordered)
+        }
+    }
+    __syncthreads();
+    const double n2 = s_n2;
+    if (threadIdx.x == 0) {
         norm2[c] = n2;
+        norm2[gridDim.x + c] = n2 > 0.0 ? sqrt((double)D / n2) : 0.0;   // the table-A scale
         if (do_commit) {
             cnt[c] += (long long)pcnt[c];
             pcnt[c] = 0.0;
         }
     }
+}
+
+// mhat_c = sqrt(D) m_c / ||m_c|| (0 for an empty class, L8) in fp32: the same expression as the
+// table-A kernel's
+__global__ void __launch_bounds__(256) k_mhat(const double2 *__restrict__ m, const double *__restrict__ norm2, int D,
+                                              int Dp, int n, float2 *__restrict__ mhat)
+{
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    const double n2 = norm2[i / Dp];
+    const double sc = n2 > 0.0 ? sqrt((double)D / n2) : 0.0;
+    const double2 v = m[i];
+    mhat[i] = make_float2((float)(v.x * sc), (float)(v.y * sc));
 }
 
 }  // namespace
@@ -1014,15 +1041,26 @@ int vsa_launch_norms(vsaogm_ctx *c, int do_commit)
         double *m = c->d_m, *pend = c->d_pending, *np = c->d_normpart, *n2 = c->d_norm2;
         long long *cnt = c->d_counts;
         double *pcnt = c->d_pcounts;
-        int dc = do_commit, Dp = c->Dp, D = c->D;
-        float2 *mh = c->d_mhat;
-        void *args[] = {&m, &pend, &cnt, &pcnt, &dc, &Dp, &D, &np, &n2, &mh};
-        const int nb = std::max(1, std::min(NORM_BLOCKS, c->num_sms * 4 / c->nslots));
-        VSA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_commit_norms, dim3(c->nslots, nb),
-                                                 dim3(NORM_THREADS), args, 0, c->stream));
+        // nb fixed per Dp (so the norm's summation order is too); tickets after the partials
+        const int nb = std::max(1, std::min(NORM_BLOCKS, (c->Dp + 2 * NORM_THREADS - 1) / (2 * NORM_THREADS)));
+        k_commit_norms<<<dim3(c->nslots, nb), NORM_THREADS, 0, c->stream>>>(
+            m, pend, cnt, pcnt, do_commit, c->Dp, c->D, np, reinterpret_cast<unsigned int *>(np + (size_t)c->nslots * NORM_BLOCKS),
+            n2);
+
     }
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_NORMS, ev);
+    c->launches++;
+    return VSAOGM_OK;
+}
+
+// the scaled fp32 memories for the on-the-fly phasor-tile GEMM (gemm_agen), from the committed
+// memories and the norms of the last vsa_launch_norms
+int vsa_launch_mhat(vsaogm_ctx *c)
+{
+    const int n = c->nslots * c->Dp;
+    k_mhat<<<(n + 255) / 256, 256, 0, c->stream>>>((const double2 *)c->d_m, c->d_norm2, c->D, c->Dp, n, c->d_mhat);
+    VSA_CUDA_TRY(cudaGetLastError());
     c->launches++;
     return VSAOGM_OK;
 }

@@ -815,6 +815,8 @@ int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32
     e.l2_hints = c->gemm_l2_hints;
     const bool agen = c->gemm_agen != 0;
     if (agen) {
+        int rc0 = vsa_launch_mhat(c);
+        if (rc0) return rc0;
         e.ag_ty = c->d_ty_turns;
         e.ag_mhat = c->d_mhat;
         e.ag_y0 = y0 - c->cy;

@@ -106,75 +106,66 @@ __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cn
                                                   int *__restrict__ unit_off, int *__restrict__ unit_bin,
                                                   int *__restrict__ unit_first, int *__restrict__ n_units)
 {
-    // thread t: bins [t per, (t + 1) per), read 8 at a time (independent loads); block scan by
-    // warp shuffles (two barriers)
-    constexpr int U = 8;
-    __shared__ int s_w[32], s_uw[32];
-    const int per = (nbins + 1023) / 1024;
-    const int b0 = min(nbins, (int)threadIdx.x * per), b1 = min(nbins, b0 + per);
+    // chunks of 1024 bins, one per thread (coalesced); up to CH chunks' counts loaded at once;
+    // each chunk scanned by warp shuffles (two barriers) on top of the running carry
+    constexpr int CH = 8;
+    __shared__ int s_w[2][32], s_uw[2][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int sum = 0, usum = 0;
-    for (int b = b0; b < b1; b += U) {
-        int v[U];
+    int carry = 0, ucarry = 0;
+    for (int base = 0; base < nbins; base += CH * 1024) {
+        int v[CH];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = b + u < b1 ? __ldcg(bin_cnt + b + u) : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            sum += v[u];
-            usum += (v[u] + NU_UNIT - 1) / NU_UNIT;
+        for (int q = 0; q < CH; ++q) {
+            const int b = base + q * 1024 + threadIdx.x;
+            v[q] = b < nbins ? __ldcg(bin_cnt + b) : 0;
         }
-    }
-    int inc = sum, uinc = usum;   // inclusive warp scans
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, inc, o), ut = __shfl_up_sync(0xffffffffu, uinc, o);
-        if (lane >= o) {
-            inc += t;
-            uinc += ut;
-        }
-    }
-    if (lane == 31) {
-        s_w[warp] = inc;
-        s_uw[warp] = uinc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        int wi = s_w[lane], uwi = s_uw[lane];
+        for (int q = 0; q < CH; ++q) {
+            if (base + q * 1024 >= nbins) break;   // block-uniform
+            const int b = base + q * 1024 + threadIdx.x;
+            const int nu = (v[q] + NU_UNIT - 1) / NU_UNIT;
+            int inc = v[q], uinc = nu;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, wi, o), ut = __shfl_up_sync(0xffffffffu, uwi, o);
-            if (lane >= o) {
-                wi += t;
-                uwi += ut;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o), ut = __shfl_up_sync(0xffffffffu, uinc, o);
+                if (lane >= o) {
+                    inc += t;
+                    uinc += ut;
+                }
             }
-        }
-        s_w[lane] = wi;
-        s_uw[lane] = uwi;
-    }
-    __syncthreads();
-    int run = inc - sum + (warp ? s_w[warp - 1] : 0), urun = uinc - usum + (warp ? s_uw[warp - 1] : 0);
-    for (int b = b0; b < b1; b += U) {
-        int v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = b + u < b1 ? __ldcg(bin_cnt + b + u) : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (b + u >= b1) break;
-            bin_off[b + u] = run;
-            unit_off[b + u] = urun;
-            const int nu = (v[u] + NU_UNIT - 1) / NU_UNIT;
-            for (int q = 0; q < nu; ++q) {
-                unit_bin[urun + q] = b + u;
-                unit_first[urun + q] = run + q * NU_UNIT;
+            const int pb = q & 1;   // double-buffered warp totals: one barrier per chunk suffices
+            if (lane == 31) {
+                s_w[pb][warp] = inc;
+                s_uw[pb][warp] = uinc;
             }
-            run += v[u];
-            urun += nu;
+            __syncthreads();
+            int wi = s_w[pb][lane], uwi = s_uw[pb][lane];   // every warp scans the 32 totals
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, wi, o), ut = __shfl_up_sync(0xffffffffu, uwi, o);
+                if (lane >= o) {
+                    wi += t;
+                    uwi += ut;
+                }
+            }
+            const int wpre = __shfl_sync(0xffffffffu, wi, (warp + 31) & 31), uwpre = __shfl_sync(0xffffffffu, uwi, (warp + 31) & 31);
+            const int run = carry + inc - v[q] + (warp ? wpre : 0), urun = ucarry + uinc - nu + (warp ? uwpre : 0);
+            if (b < nbins) {
+                bin_off[b] = run;
+                unit_off[b] = urun;
+                for (int u = 0; u < nu; ++u) {
+                    unit_bin[urun + u] = b;
+                    unit_first[urun + u] = run + u * NU_UNIT;
+                }
+            }
+            carry += __shfl_sync(0xffffffffu, wi, 31);
+            ucarry += __shfl_sync(0xffffffffu, uwi, 31);
         }
     }
-    if (threadIdx.x == 1023) {
-        bin_off[nbins] = s_w[31];
-        unit_off[nbins] = s_uw[31];
-        *n_units = s_uw[31];
+    if (threadIdx.x == 0) {
+        bin_off[nbins] = carry;
+        unit_off[nbins] = ucarry;
+        *n_units = ucarry;
     }
 }
 

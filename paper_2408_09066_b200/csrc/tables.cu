@@ -59,7 +59,8 @@ __device__ __forceinline__ void phasor_turns(double tau, double coord, float *s,
 template <typename T2, bool IS_A>
 __global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, int rows, int Dp, int D, int Kp,
                                                        const double *__restrict__ tau, double base, double res,
-                                                       int row0, const float2 *__restrict__ mhat)
+                                                       int row0, const double2 *__restrict__ m,
+                                                       const double *__restrict__ mscale)
 {
     const int kq = blockIdx.x * TAB_THREADS + threadIdx.x;
     const int k0 = kq * TAB_KT;
@@ -72,11 +73,12 @@ __global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, 
     if (IS_A) {
 #pragma unroll
         for (int cls = 0; cls < 2; ++cls) {
+            const double sc = mscale[cls];   // sqrt(D) / ||m_c||, 0 for an empty class (k_commit_norms)
 #pragma unroll
             for (int e = 0; e < TAB_KT; ++e) {
-                const float2 v = mhat[(size_t)cls * Dp + k0 + e];   // sqrt(D) m / ||m|| (k_commit_norms)
-                mr[cls][e] = v.x;
-                mi[cls][e] = v.y;
+                const double2 v = m[(size_t)cls * Dp + k0 + e];   // sqrt(D) m / ||m||, rounded to fp32
+                mr[cls][e] = (float)(v.x * sc);
+                mi[cls][e] = (float)(v.y * sc);
             }
         }
     }
@@ -128,15 +130,15 @@ int grow(void **p, size_t *cap, size_t need)
 
 template <bool IS_A>
 void launch_table(vsaogm_ctx *c, void *out, int rows, const double *tau, double base, double res, int row0, int prec,
-                  const float2 *mhat)
+                  const double2 *m, const double *mscale)
 {
     dim3 grid((c->Dp / TAB_KT + TAB_THREADS - 1) / TAB_THREADS, (rows + TAB_ROWS - 1) / TAB_ROWS);
     if (prec == VSAOGM_BF16)
         k_table<__nv_bfloat162, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp,
-                                                                            tau, base, res, row0, mhat);
+                                                                            tau, base, res, row0, m, mscale);
     else
         k_table<__half2, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp, tau,
-                                                                     base, res, row0, mhat);
+                                                                     base, res, row0, m, mscale);
 }
 
 }  // namespace
@@ -150,7 +152,7 @@ int vsa_launch_table_B(vsaogm_ctx *c, double x0, double res, int32_t cols, int p
     if (rc) return rc;
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_TABLE_B, &ev);
-    launch_table<false>(c, c->d_B, cols, c->d_tx_turns, x0 - c->cx, res, 0, prec, nullptr);
+    launch_table<false>(c, c->d_B, cols, c->d_tx_turns, x0 - c->cx, res, 0, prec, nullptr, nullptr);
     VSA_CUDA_TRY(cudaGetLastError());
     vsa_prof_end(c, VSAOGM_K_TABLE_B, ev);
     c->launches++;
@@ -173,7 +175,8 @@ int vsa_launch_table_A(vsaogm_ctx *c, const Groups &G, double y0, double res, in
     vsa_prof_begin(c, VSAOGM_K_TABLE_A, &ev);
     for (int g = 0; g < G.n; ++g) {
         launch_table<true>(c, (uint8_t *)c->d_A + (size_t)G.a_row0[g] * c->Kp * 2, G.nrows[g], c->d_ty_turns,
-                           y0 - c->cy, res, r_lo + G.row0[g], prec, c->d_mhat + (size_t)slot0[g] * c->Dp);
+                           y0 - c->cy, res, r_lo + G.row0[g], prec,
+                           (const double2 *)c->d_m + (size_t)slot0[g] * c->Dp, c->d_norm2 + c->nslots + slot0[g]);
         c->launches++;
     }
     VSA_CUDA_TRY(cudaGetLastError());
