@@ -177,10 +177,11 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
  * "enc_pairs_npoly", "enc_pairs_minb", "enc_pairs_split", "enc_x2_npoly", "enc_x2_minb",
  * "enc_x2_waves", "enc_npoly", "enc_minb", "enc_kt", "enc_path", "enc_waves",
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
- * CTA pair, 1 single CTA), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,
+ * CTA pair, 1 single CTA, 2 two CTA pairs per cluster with B multicast), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,
  * else the split-K factor), "gemm_l2_hints" (0 none, the default; 1 A evict-first + B evict-last; 2 B evict-last), "pipe_early" (0/1), "entropy_kernel"
  * (0 auto, 1 the generic staged kernel), "entropy_rw" (0 auto, else output rows per
- * work item of the streamed entropy kernel).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
+ * work item of the streamed entropy kernel), "table_rows" (1..256, default 32: phasor-table
+ * rows per thread of the table kernels).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
 int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);
 
 /* Read a tuning knob of this context into *value (the same keys).  Errors: EINVAL_ARG. */
@@ -279,7 +280,8 @@ int64_t vsaogm_launch_count(const vsaogm_ctx *ctx);
 /* Test hook: the decode GEMM kernel alone.  C[M][N] (float32, row-major) =
  * A[M][K] . B[N][K]^T with A, B 16-bit (precision) K-major device arrays,
  * K a multiple of 64, 1 <= M, N.  kernel: -1 library default, 0 the CTA-pair
- * (cta_group::2) kernel, 1 the single-CTA kernel; bn (0 auto, else 128..256 in
+ * (cta_group::2) kernel, 1 the single-CTA kernel, 2 the CTA-pair kernel in clusters
+ * of two pairs with B multicast; bn (0 auto, else 128..256 in
  * steps of 32) and splits (0 auto, else the split-K factor) pin the CTA-pair
  * kernel's tile width and split-K.  Runs on `stream` and synchronises it. */
 int vsaogm_test_gemm(const void *A_dev, const void *B_dev, int32_t M, int32_t N, int32_t K,

@@ -596,7 +596,7 @@ static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *g
         {"enc_path", &c->enc_path, -1, 2},
         {"enc_waves", &c->enc_waves, 1, 64},
         {"enc_runs_waves", &c->enc_runs_waves, 1, 64},
-        {"gemm_variant", &c->gemm_variant, -1, 1},
+        {"gemm_variant", &c->gemm_variant, -1, 2},
         {"gemm_bn", &c->gemm_bn, 0, 256},
         {"gemm_splits", &c->gemm_splits, 0, 64},
         {"gemm_l2_hints", &c->gemm_l2_hints, 0, 2},
@@ -604,6 +604,7 @@ static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *g
         {"pipe_early", &c->pipe_early, 0, 1},
         {"entropy_kernel", &c->entropy_kernel, 0, 1},
         {"entropy_rw", &c->entropy_rw, 0, 1 << 20},
+        {"table_rows", &c->table_rows, 1, 256},
     };
     for (const Knob &k : knobs)
         if (strcmp(k.name, key) == 0) {
@@ -784,7 +785,7 @@ int64_t vsaogm_launch_count(const vsaogm_ctx *c) { return c ? c->launches : 0; }
 int vsaogm_test_gemm(const void *A, const void *B, int32_t M, int32_t N, int32_t K, vsaogm_precision prec,
                      int32_t kernel, int32_t bn, int32_t splits, float *C, void *stream)
 {
-    if (!A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 != 0 || kernel < -1 || kernel > 1)
+    if (!A || !B || !C || M < 1 || N < 1 || K < 64 || K % 64 != 0 || kernel < -1 || kernel > 2)
         return VSAOGM_EINVAL_ARG;
     if (bn != 0 && (bn < 128 || bn > 256 || bn % 32 != 0)) return VSAOGM_EINVAL_ARG;
     if (splits < 0) return VSAOGM_EINVAL_ARG;

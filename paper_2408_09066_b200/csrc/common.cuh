@@ -124,6 +124,7 @@ struct vsaogm_ctx {
     int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
     int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
     int entropy_rw = 0;     // 0 auto, else output rows per streamed work item (test hook)
+    int table_rows = 32;    // table rows per thread of k_table (setup amortised over them)
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta
@@ -687,6 +688,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *ma
         : "memory");
 }
 
+// as tma_load_2d_2sm, multicast: the box lands at the same offset in every CTA of ctaMask, and
+// each destination's bytes are counted on the barrier of its own pair's CTA 0
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                                   uint16_t mask)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask)
+        : "memory");
+}
+
 // as tma_load_2d_2sm with an L2 eviction-priority hint (64-bit cache policy: the encodings of
 // createpolicy.fractional evict_first / evict_last with fraction 1.0)
 constexpr uint64_t VSA_L2_EVICT_FIRST = 0x12F0000000000000ull;
@@ -713,11 +726,11 @@ __device__ __forceinline__ void tc_mma2_f16(uint32_t tmem_d, uint64_t adesc, uin
 }
 
 // commit the issuing thread's prior tcgen05 ops to the barrier at this offset in both CTAs
-__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar)
+__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar, uint16_t mask = 3)
 {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"((uint16_t)3)
+        "h"(mask)
         : "memory");
 }

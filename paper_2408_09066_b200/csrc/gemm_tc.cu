@@ -407,11 +407,21 @@ __device__ __forceinline__ void unit_coords(int tile, const int *s_pref, const i
 // AGEN: the A tiles are generated in shared memory by four extra warps per CTA (agen_kblock) instead
 // of TMA-loaded from table A (north_star: "phasor tiles generated on the fly"); the full barrier then
 // counts the B bytes plus the eight generator warps' arrivals of the pair.
-template <int MODE, int BN, bool AGEN = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS + 128 : GEMM_THREADS, AGEN ? 2 : 4)
+// Pipeline waits poll with CTA-scope acquire (mbar_wait), as CUTLASS's cluster pipelines do: the
+// arrivals are tcgen05.commit completions (async proxy, ordered by the tcgen05 fences) and the
+// epilogue's remote release arrivals after tcgen05.wait::ld; a cluster-scope acquire on every
+// poll compiled to an L1 invalidation (CCTL.IVALL) per iteration -- 3.2 M per launch at C4.
+// CL = 4: clusters of two CTA pairs; the pairs take m-blocks 2 mp and 2 mp + 1 of the same
+// n-block, so both need the same B rows: each CTA TMA-loads half of its B half (BN/4 rows) and
+// multicasts it to itself and the same-rank CTA of the other pair -- 23 % fewer L2 -> SM bytes
+// per flop at BN = 224.  A slot is then written by two CTAs' producers, so "slot free" needs both
+// pairs' MMA commits (count 2, commits multicast to all four CTAs).
+template <int MODE, int BN, bool AGEN = false, int CL = 2>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS + 128 : GEMM_THREADS, AGEN ? 2 : 4)
     k_decode_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ Groups G, int K, uint32_t idesc, Epi epi)
 {
+    static_assert(CL == 2 || (CL == 4 && !AGEN), "4-CTA clusters: TMA-loaded A only");
     constexpr uint32_t A_BYTES = 128 * VSA_BK * 2;          // this CTA's 128 rows of A
     constexpr uint32_t BH_BYTES = (BN / 2) * VSA_BK * 2;    // this CTA's half of B
     constexpr uint32_t ST_BYTES = A_BYTES + BH_BYTES;
@@ -431,7 +441,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
-    const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+    const uint32_t rp = rank & 1, pr = rank >> 1;   // rank in the CTA pair, pair in the cluster
+    const int wid = blockIdx.x / CL, num_w = gridDim.x / CL;   // cluster = work-unit owner
+    constexpr uint16_t ALL_MASK = CL == 4 ? 0xF : 0x3;
+    const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
     const int num_kb = K / VSA_BK;
     const int S = epi.splits;                 // split-K factor (1 = none)
     const int ng = G.n;
@@ -441,12 +454,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
         for (int g = 0; g < ng; ++g) {
             s_pref[g] = t;
             s_tn[g] = (G.ncols[g] + BN - 1) / BN;
-            t += ((G.mrows[g] + 255) / 256) * s_tn[g];
+            t += (((G.mrows[g] + 255) / 256 + CL / 2 - 1) / (CL / 2)) * s_tn[g];
         }
         s_pref[ng] = t;
         for (int s = 0; s < STAGES2; ++s) {
             mbar_init(&full[s], AGEN ? 9 : 1);   // AGEN: + 4 generator warps x 2 CTAs
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CL / 2);   // CL = 4: both pairs' MMAs read this CTA's B rows
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
@@ -472,23 +485,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
             uint32_t stage = 0, phase = 0;
-            for (int u = pair; u < num_units; u += num_pairs) {
+            for (int u = wid; u < num_units; u += num_w) {
                 const int tile = u / S, sk = u - tile * S;
                 int g, mb, nb;
                 unit_coords(tile, s_pref, s_tn, ng, g, mb, nb);
-                const int arow = G.a_row0[g] + mb * 256 + (int)rank * 128;
-                const int brow = G.col0[g] + nb * BN + (int)rank * (BN / 2);
+                if (CL == 4) mb = 2 * mb + (int)pr;
+                const int arow = G.a_row0[g] + mb * 256 + (int)rp * 128;
+                const int brow = G.col0[g] + nb * BN + (int)rp * (BN / 2);
                 const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    mbar_wait(&empty[stage], phase ^ 1);
                     if (AGEN) {
-                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * BH_BYTES);
+                        if (rp == 0) mbar_expect_tx(&full[stage], 2 * BH_BYTES);
                         tma_load_2d_2sm(sB + stage * BH_BYTES, &tmB, &full[stage], kb * VSA_BK, brow);
                         if (++stage == STAGES2) { stage = 0; phase ^= 1; }
                         continue;
                     }
-                    if (rank == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
-                    if (epi.l2_hints == 2) {
+                    if (rp == 0) mbar_expect_tx(&full[stage], 2 * ST_BYTES);
+                    if (CL == 4) {
+                        tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * VSA_BK, arow);
+                        tma_load_2d_2sm_mc(sB + stage * BH_BYTES + pr * (BN / 4) * 128, &tmB, &full[stage], kb * VSA_BK,
+                                           brow + (int)pr * (BN / 4), (uint16_t)((1u << rank) | (1u << (rank ^ 2))));
+                    } else if (epi.l2_hints == 2) {
                         // B (every panel re-read by the next wave, 66 MB at C4 < 126 MB L2)
                         // evict-last; A normal (an A panel is shared by the concurrent tiles of its
                         // m-block row: n-fastest order)
@@ -509,12 +527,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
             }
         }
     } else if (warp == 1) {
-        if (rank == 0 && lane == 0) {
+        if (rp == 0 && lane == 0) {
             uint32_t stage = 0, phase = 0, as = 0, aphase = 0;
-            for (int u = pair; u < num_units; u += num_pairs) {
+            for (int u = wid; u < num_units; u += num_w) {
                 const int sk = u % S;
                 const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
-                mbar_wait_cluster(&tempty[as], aphase ^ 1);
+                mbar_wait(&tempty[as], aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + as * 256;
                 for (int kb = kb0; kb < kb1; ++kb) {
@@ -526,10 +544,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
                     for (int k = 0; k < VSA_BK / 16; ++k)
                         tc_mma2_f16(d, sw128_kmajor_desc(a0 + 32 * k), sw128_kmajor_desc(b0 + 32 * k), idesc,
                                     (kb != kb0) || (k != 0));
-                    tc_commit2_mc(&empty[stage]);
+                    tc_commit2_mc(&empty[stage], ALL_MASK);
                     if (++stage == STAGES2) { stage = 0; phase ^= 1; }
                 }
-                tc_commit2_mc(&tfull[as]);
+                tc_commit2_mc(&tfull[as], pair_mask);
                 if (++as == 2) { as = 0; aphase ^= 1; }
             }
         }
@@ -538,11 +556,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
         // inputs of the next k-block are loaded while this one is generated
         const int t = (warp - 6) * 32 + lane;
         uint32_t stage = 0, phase = 0;
-        for (int u = pair; u < num_units; u += num_pairs) {
+        for (int u = wid; u < num_units; u += num_w) {
             const int tile = u / S, sk = u - tile * S;
             int g, mb, nb;
             unit_coords(tile, s_pref, s_tn, ng, g, mb, nb);
-            const int m_base = mb * 256 + (int)rank * 128;
+            const int m_base = mb * 256 + (int)rp * 128;
             const int kb0 = sk * epi.kb_per, kb1 = min(num_kb, kb0 + epi.kb_per);
             for (int j = 1; j <= 3 && kb0 + j < kb1; ++j) agen_prefetch(kb0 + j, t, g, epi);
             AgenIn cur = agen_load(kb0, t, g, epi);
@@ -559,7 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> UMMA reads
                 __syncwarp();
                 if (lane == 0) {
-                    if (rank == 0) mbar_arrive(&full[stage]);
+                    if (rp == 0) mbar_arrive(&full[stage]);
                     else mbar_arrive_cluster(&full[stage], 0);
                 }
                 if (++stage == STAGES2) { stage = 0; phase ^= 1; }
@@ -568,13 +586,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
         }
     } else {
         const int quarter = warp & 3;
-        const int row_in_tile = (int)rank * 128 + quarter * 32 + lane;
+        const int row_in_tile = (int)rp * 128 + quarter * 32 + lane;
         uint32_t as = 0, aphase = 0;
-        for (int u = pair; u < num_units; u += num_pairs) {
+        for (int u = wid; u < num_units; u += num_w) {
             const int tile = u / S, sk = u - tile * S;
             int g, mb, nb;
             unit_coords(tile, s_pref, s_tn, ng, g, mb, nb);
-            mbar_wait_cluster(&tfull[as], aphase);
+            if (CL == 4) mb = 2 * mb + (int)pr;
+            mbar_wait(&tfull[as], aphase);
             tc_fence_after();
             const int m_l = mb * 256 + row_in_tile;
 #pragma unroll 1
@@ -588,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(AGEN ? GEMM_THREADS 
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&tempty[as], 0);
+            if (lane == 0) mbar_arrive_cluster(&tempty[as], rank & ~1u);
             if (++as == 2) { as = 0; aphase ^= 1; }
         }
     }
@@ -670,18 +689,60 @@ int launch1(const void *A, const void *B, int a_rows, int b_rows, int K, int pre
     return VSAOGM_OK;
 }
 
-long group_tiles(const Groups &G, int bn)
+long group_tiles(const Groups &G, int bn, int cl = 2)
 {
     long t = 0;
-    for (int g = 0; g < G.n; ++g) t += (long)((G.mrows[g] + 255) / 256) * ((G.ncols[g] + bn - 1) / bn);
+    for (int g = 0; g < G.n; ++g)
+        t += (long)(((G.mrows[g] + 255) / 256 + cl / 2 - 1) / (cl / 2)) * ((G.ncols[g] + bn - 1) / bn);
     return t;
+}
+
+// co-resident 4-CTA clusters of k_decode_gemm2<MODE, BN, false, 4> (a cluster must fit one GPC)
+template <int MODE, int BN>
+int max_clusters4(size_t smem, int num_sms)
+{
+    static int cached[2] = {0, 0};
+    int &n = cached[MODE ? 1 : 0];
+    if (n) return n;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4 * (num_sms / 4));
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    int q = 0;
+    if (cudaOccupancyMaxActiveClusters(&q, (void *)k_decode_gemm2<MODE, BN, false, 4>, &cfg) != cudaSuccess || q <= 0) {
+        cudaGetLastError();
+        q = num_sms / 4 - 2;   // conservative: GPC sizes need not be multiples of 4
+    }
+    n = q;
+    return n;
 }
 
 template <int MODE, int BN>
 int launch2_bn(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, Epi epi,
-               cudaStream_t s, int num_sms, bool agen)
+               cudaStream_t s, int num_sms, bool agen, int cl)
 {
     CUtensorMap ta, tb;
+    if (cl == 4 && !agen) {   // two CTA pairs per cluster, B multicast
+        int rc = make_map(&tb, B, b_rows, K, BN / 4, prec);
+        if (rc) return rc;
+        if ((rc = make_map(&ta, A, a_rows, K, 128, prec))) return rc;
+        const size_t smem = 1024 + (size_t)STAGES2 * (128 + BN / 2) * VSA_BK * 2 + 256;
+        VSA_CUDA_TRY(cudaFuncSetAttribute(k_decode_gemm2<MODE, BN, false, 4>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const long units = group_tiles(G, BN, 4) * epi.splits;
+        const int ncl = max_clusters4<MODE, BN>(smem, num_sms);
+        const int grid = 4 * (int)(units < ncl ? units : ncl);
+        if (grid == 0) return VSAOGM_OK;
+        const uint32_t idesc = make_idesc_f16(prec == VSAOGM_BF16, 256, BN);
+        k_decode_gemm2<MODE, BN, false, 4><<<grid, GEMM_THREADS, smem, s>>>(ta, tb, G, K, idesc, epi);
+        VSA_CUDA_TRY(cudaGetLastError());
+        if (epi.splits > 1) {
+            const size_t RC = (size_t)epi.ws_rows * epi.ws_cols;
+            k_splitk_reduce<MODE><<<(unsigned)((RC + 255) / 256), 256, 0, s>>>(G, epi);
+            VSA_CUDA_TRY(cudaGetLastError());
+        }
+        return VSAOGM_OK;
+    }
     int rc = make_map(&tb, B, b_rows, K, BN / 2, prec);
     if (rc) return rc;
     if (agen) ta = tb;   // unused: the A tiles are generated in shared memory
@@ -750,18 +811,19 @@ int pick_splits(const Groups &G, int ws_rows, int ws_cols, int K, int bn, int nu
 
 template <int MODE>
 int launch2(const void *A, const void *B, int a_rows, int b_rows, int K, int prec, const Groups &G, const Epi &epi,
-            cudaStream_t s, int num_sms, int bn, bool agen)
+            cudaStream_t s, int num_sms, int bn, bool agen, int cl)
 {
     switch (bn) {
-    case 224: return launch2_bn<MODE, 224>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
-    case 192: return launch2_bn<MODE, 192>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
-    case 160: return launch2_bn<MODE, 160>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
-    case 128: return launch2_bn<MODE, 128>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
-    default: return launch2_bn<MODE, 256>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen);
+    case 224: return launch2_bn<MODE, 224>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen, cl);
+    case 192: return launch2_bn<MODE, 192>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen, cl);
+    case 160: return launch2_bn<MODE, 160>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen, cl);
+    case 128: return launch2_bn<MODE, 128>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen, cl);
+    default: return launch2_bn<MODE, 256>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, agen, cl);
     }
 }
 
-// variant: -1 / 0 = 2-CTA (default), 1 = 1-CTA (single group only); bn_force > 0 pins the
+// variant: -1 / 0 = 2-CTA (default), 1 = 1-CTA (single group only), 2 = 4-CTA clusters (two
+// pairs, B multicast); bn_force > 0 pins the
 // 2-CTA tile width, splits_force > 0 the split-K factor (vsaogm_set_tuning).  *ws / *ws_cap:
 // a caller-owned growable workspace for split-K partials.
 template <int MODE>
@@ -791,7 +853,7 @@ int launch(const void *A, const void *B, int a_rows, int b_rows, int K, int prec
         }
         epi.ws = *ws;
     }
-    return launch2<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, bn, agen);
+    return launch2<MODE>(A, B, a_rows, b_rows, K, prec, G, epi, s, num_sms, bn, agen, variant == 2 ? 4 : 2);
 }
 
 }  // namespace

@@ -17,7 +17,7 @@
 // so that sum_j A[m][j] B[n][j] = s_c H_c = D q_c: the GEMM epilogue multiplies by 1/D.
 // The sqrt(D) keeps |A| ~ 1 on average (16-bit operands stay normal numbers).
 //
-// One thread owns 8 consecutive k (16-byte stores) and walks TAB_ROWS rows,
+// One thread owns 8 consecutive k (16-byte stores) and walks table_rows rows,
 // so theta and the scaled memory are loaded once per thread.  Phases are
 // reduced in fp64 (turns = tau_k * coordinate, minus the nearest integer) and
 // evaluated with MUFU sin/cos on the reduced argument |2 pi f| <= pi.
@@ -30,7 +30,6 @@ namespace {
 
 constexpr int TAB_THREADS = 128;
 constexpr int TAB_KT = 8;
-constexpr int TAB_ROWS = 8;
 
 template <typename T2>
 __device__ __forceinline__ T2 pack2(float a, float b);
@@ -59,7 +58,7 @@ __device__ __forceinline__ void phasor_turns(double tau, double coord, float *s,
 template <typename T2, bool IS_A>
 __global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, int rows, int Dp, int D, int Kp,
                                                        const double *__restrict__ tau, double base, double res,
-                                                       int row0, const double2 *__restrict__ m,
+                                                       int row0, int tab_rows, const double2 *__restrict__ m,
                                                        const double *__restrict__ mscale)
 {
     const int kq = blockIdx.x * TAB_THREADS + threadIdx.x;
@@ -82,8 +81,8 @@ __global__ void __launch_bounds__(TAB_THREADS) k_table(uint4 *__restrict__ out, 
             }
         }
     }
-    const int i0 = blockIdx.y * TAB_ROWS;
-    const int i1 = min(rows, i0 + TAB_ROWS);
+    const int i0 = blockIdx.y * tab_rows;
+    const int i1 = min(rows, i0 + tab_rows);
     // element offsets (in 16-byte units) of this thread's Re and Im octets within a row
     const size_t re_off = (size_t)(64 * g + w) / 8, im_off = (size_t)(64 * g + 32 + w) / 8;
     const size_t row_u4 = (size_t)Kp / 8;
@@ -132,13 +131,13 @@ template <bool IS_A>
 void launch_table(vsaogm_ctx *c, void *out, int rows, const double *tau, double base, double res, int row0, int prec,
                   const double2 *m, const double *mscale)
 {
-    dim3 grid((c->Dp / TAB_KT + TAB_THREADS - 1) / TAB_THREADS, (rows + TAB_ROWS - 1) / TAB_ROWS);
+    dim3 grid((c->Dp / TAB_KT + TAB_THREADS - 1) / TAB_THREADS, (rows + c->table_rows - 1) / c->table_rows);
     if (prec == VSAOGM_BF16)
         k_table<__nv_bfloat162, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp,
-                                                                            tau, base, res, row0, m, mscale);
+                                                                            tau, base, res, row0, c->table_rows, m, mscale);
     else
         k_table<__half2, IS_A><<<grid, TAB_THREADS, 0, c->stream>>>((uint4 *)out, rows, c->Dp, c->D, c->Kp, tau,
-                                                                     base, res, row0, m, mscale);
+                                                                     base, res, row0, c->table_rows, m, mscale);
 }
 
 }  // namespace

@@ -338,7 +338,8 @@ class Mapper:
 
 def test_gemm(A: torch.Tensor, B: torch.Tensor, precision=F16, kernel: int = -1, bn: int = 0,
               splits: int = 0) -> torch.Tensor:
-    """C = A @ B^T through the decode GEMM kernel (raw epilogue); kernel 0 = CTA pair, 1 = single CTA;
+    """C = A @ B^T through the decode GEMM kernel (raw epilogue); kernel 0 = CTA pair, 1 = single CTA,
+    2 = two CTA pairs per cluster (B multicast);
     bn / splits pin the CTA-pair tile width / split-K factor (0 = auto)."""
     lib = load()
     M, K = A.shape

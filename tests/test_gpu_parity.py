@@ -62,7 +62,7 @@ def test_theta_bit_exact():
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 128), (1000, 777, 640), (4000, 2000, 1024),
                                    (257, 33, 192)])
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("kernel", [0, 1, 2])
 def test_gemm_vs_torch_fp32(M, N, K, prec, kernel):
     from paper_2408_09066_b200 import test_gemm
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
@@ -77,12 +77,13 @@ def test_gemm_vs_torch_fp32(M, N, K, prec, kernel):
 
 @pytest.mark.parametrize("splits", [2, 3, 7])
 @pytest.mark.parametrize("M,N,K", [(300, 500, 1024), (508, 2000, 4096)])
-def test_gemm_split_k(splits, M, N, K):
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_gemm_split_k(splits, M, N, K, kernel):
     from paper_2408_09066_b200 import test_gemm
     g = torch.Generator(device="cuda").manual_seed(splits + M)
     A = torch.randn(M, K, device="cuda", generator=g).half()
     B = torch.randn(N, K, device="cuda", generator=g).half()
-    C = test_gemm(A, B, 0, 0, splits=splits)
+    C = test_gemm(A, B, 0, kernel, splits=splits)
     ref = A.float() @ B.float().T
     assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-4
 
@@ -111,12 +112,13 @@ def test_decode_band_split_k_matches_unsplit():
 
 
 @pytest.mark.parametrize("bn", [256, 224, 192, 160, 128])
-def test_gemm_pair_tile_widths(bn):
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_gemm_pair_tile_widths(bn, kernel):
     from paper_2408_09066_b200 import test_gemm
     g = torch.Generator(device="cuda").manual_seed(bn)
     A = torch.randn(600, 320, device="cuda", generator=g).half()
     B = torch.randn(1000, 320, device="cuda", generator=g).half()
-    C = test_gemm(A, B, 0, 0, bn=bn)
+    C = test_gemm(A, B, 0, kernel, bn=bn)
     ref = A.float() @ B.float().T
     assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-4
 

@@ -28,8 +28,10 @@ def main():
     Dp = (D + 31) // 32 * 32
     flops = 2.0 * 2 * R * C * 2 * Dp
     for spec in sys.argv[1:] or [""]:
+        saved = {}
         for kv in [x for x in spec.split(",") if x]:
             k, v = kv.split("=")
+            saved[k] = mp.get_tuning(k)
             mp.set_tuning(k, int(v))
         for _ in range(3):
             mp.decode(0.0, 0.0, res, R, C, 0, R, h)
@@ -47,8 +49,8 @@ def main():
                           "frac_burst": round(tf / pk["bf16_tflops"], 4),
                           "table_A_us": round(1e3 * prof["table_A"][0] / prof["table_A"][1], 2) if prof["table_A"][1] else 0.0}),
               flush=True)
-        for kv in [x for x in spec.split(",") if x]:
-            mp.set_tuning(kv.split("=")[0], 0 if kv.split("=")[0] != "gemm_l2_hints" else 1)
+        for k, v in saved.items():
+            mp.set_tuning(k, v)
     mp.close()
 
 
