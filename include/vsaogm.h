@@ -151,9 +151,14 @@ int vsaogm_commit(vsaogm_ctx *ctx);
 int vsaogm_reset(vsaogm_ctx *ctx);
 
 /* Decode every cell of this rank's band (plus halo rows) into signed
- * similarities (Eq. 10 normalisation, Eq. 11 query) on the tensor cores, and
+ * similarities (Eq. 10 normalisation, Eq. 11 query), and
  * the per-cell binary entropy H_b(q^2) kept in the context for
- * vsaogm_entropy.  q_dev: NULL, or float32 [2][row_end-row_begin][cols]
+ * vsaogm_entropy.  Two methods compute the same sums (tuning key
+ * "dec_method"): a dense tcgen05 GEMM over separable phasor tables (precision
+ * selects its 16-bit operand type; fp32 accumulation), and a type-1 NUFFT
+ * (fp32 Gaussian gridding + FFTs, nudecode.cu; delta = 1, grid spacing below
+ * l / 2, `precision` unused).  The default picks the NUFFT where it applies
+ * and its modelled time is lower.  q_dev: NULL, or float32 [2][row_end-row_begin][cols]
  * (class 0 empty, 1 occupied) receiving q for the band's own rows.  In
  * single-rank mode pending memories are committed first.
  * Errors: EINVAL_ARG (grid), ESTATE (multi-rank mode with uncommitted
@@ -181,7 +186,8 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
  * else the split-K factor), "gemm_l2_hints" (0 none, the default; 1 A evict-first + B evict-last; 2 B evict-last), "pipe_early" (0/1), "entropy_kernel"
  * (0 auto, 1 the generic staged kernel), "entropy_rw" (0 auto, else output rows per
  * work item of the streamed entropy kernel), "table_rows" (1..256, default 32: phasor-table
- * rows per thread of the table kernels).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
+ * rows per thread of the table kernels), "dec_method" (-1 auto, the default; 0 the tcgen05 GEMM;
+ * 1 the NUFFT where it applies, else the GEMM).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
 int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);
 
 /* Read a tuning knob of this context into *value (the same keys).  Errors: EINVAL_ARG. */
@@ -270,7 +276,8 @@ int vsaogm_get_phases(vsaogm_ctx *ctx, double *host);
 #define VSAOGM_K_TABLE_A 5
 #define VSAOGM_K_DECODE_GEMM 6
 #define VSAOGM_K_ENTROPY 7
-#define VSAOGM_NKERNELS 8
+#define VSAOGM_K_DECODE_NUFFT 8   /* the NUFFT decode: spread + two transforms (nudecode.cu) */
+#define VSAOGM_NKERNELS 9
 int vsaogm_profile_enable(vsaogm_ctx *ctx, int enable);
 int vsaogm_profile_read(vsaogm_ctx *ctx, double *ms, int64_t *launches);
 

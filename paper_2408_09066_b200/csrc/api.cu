@@ -228,6 +228,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
                     c->d_nu_key, c->d_nu_sorted, c->d_nu_units};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    vsa_nudecode_free(c);
     for (auto &r : c->prof_live) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->up) {
@@ -532,6 +533,12 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     if ((rc = vsa_join_encode(c))) return rc;
     if ((rc = vsa_launch_norms(c, do_commit))) return rc;
     c->dirty = false;
+    if (c->delta == 1 && vsa_nudecode_applies(c, g->x0, g->y0, g->res, g->cols, r_lo, r_ext)) {
+        // the type-1 NUFFT decode (nudecode.cu): no phasor tables; fp32 throughout (prec unused)
+        if ((rc = vsa_launch_decode_nufft(c, g->x0, g->y0, g->res, g->cols, r_lo, r_ext, c->d_hb, c->d_code, ldh,
+                                          q, r_lo - g->row_begin, g->row_end - g->row_begin, true)))
+            return rc;
+    } else {
     const bool early = c->pipe_early != 0;   // tuning variant
     if (early && (rc = vsa_mark_main(c))) return rc;
     if ((rc = vsa_launch_table_B(c, g->x0, g->res, g->cols, prec))) return rc;
@@ -545,6 +552,7 @@ int vsaogm_decode(vsaogm_ctx *c, const vsaogm_grid *g, vsaogm_precision prec, fl
     if ((rc = vsa_launch_decode_gemm(c, G, a_rows, g->cols, prec, 1.0f / (float)c->D, c->d_hb, q, r_ext,
                                      r_lo - g->row_begin, g->row_end - g->row_begin, slot0, g->y0, g->res, r_lo)))
         return rc;
+    }
     c->decoded = true;
     c->g_estimator = c->estimator;
     c->g_rows = g->rows;
@@ -605,6 +613,7 @@ static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *g
         {"entropy_kernel", &c->entropy_kernel, 0, 1},
         {"entropy_rw", &c->entropy_rw, 0, 1 << 20},
         {"table_rows", &c->table_rows, 1, 256},
+        {"dec_method", &c->dec_method, -1, 1},
     };
     for (const Knob &k : knobs)
         if (strcmp(k.name, key) == 0) {

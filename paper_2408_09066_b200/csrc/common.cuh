@@ -48,6 +48,7 @@ void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, in
 // staging / output slots of the pipelined host I/O (vsaogm_*_host_async): three of each; a slot
 // is reused VSA_IO_SLOTS calls later, so the host may keep VSA_IO_SLOTS - 1 steps in flight
 #define VSA_IO_SLOTS 3
+#define VSA_ND_PLANS 4   // cached NUFFT-decode plans (decode geometries)
 
 // Decode GEMM problem groups (one per quadrant with decoded cells; delta = 1: one group).
 // Group g: A-table rows [a_row0, a_row0 + mrows) = class 0 then class 1 blocks of nrows grid
@@ -125,6 +126,16 @@ struct vsaogm_ctx {
     int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
     int entropy_rw = 0;     // 0 auto, else output rows per streamed work item (test hook)
     int table_rows = 32;    // table rows per thread of k_table (setup amortised over them)
+    // decode method: -1 auto (the type-1 NUFFT of nudecode.cu where it applies and its modelled
+    // time is lower), 0 the tcgen05 GEMM over phasor tables, 1 the NUFFT (delta = 1)
+    int dec_method = -1;
+    void *nd_plans[VSA_ND_PLANS] = {};   // cached NUFFT-decode plans (nudecode.cu), one per geometry
+    int nd_nplans = 0;
+    int64_t nd_tick = 0;
+    void *d_nd_tw = nullptr;                          // twiddles for transforms up to 8192 points
+    void *d_nd_G = nullptr; size_t nd_G_cap = 0;      // compact spread grid [Wx][Wy] complex fp32
+    void *d_nd_T = nullptr; size_t nd_T_cap = 0;      // column-transformed band [Wx][ldt] complex fp32
+    void *d_nd_st = nullptr; size_t nd_st_cap = 0;    // point strengths in bin order [2 D] complex fp32
     vsaogm_bounds bounds{};
     double cx = 0, cy = 0;            // phase origin = bounds centre
     std::vector<double> thx, thy;     // host fp64 theta
@@ -226,6 +237,11 @@ int vsa_launch_table_A(vsaogm_ctx *c, const Groups &G, double y0, double res, in
 int vsa_launch_decode_gemm(vsaogm_ctx *c, const Groups &G, int32_t a_rows, int32_t N, int prec, float inv_scale,
                            float *hb, float *q, int32_t r_ext, int32_t q_off, int32_t band_rows, const int *slot0,
                            double y0, double res, int32_t r_lo);
+bool vsa_nudecode_applies(vsaogm_ctx *c, double x0, double y0, double res, int32_t cols, int32_t r_lo, int32_t r_ext);
+int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int32_t cols, int32_t r_lo, int32_t r_ext,
+                            float *hb, uint8_t *code, size_t ldh, float *q, int32_t q_off, int32_t band_rows,
+                            bool mark_main);
+void vsa_nudecode_free(vsaogm_ctx *c);
 int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, uint8_t *lab);
 int vsa_gemm_raw(const void *A, const void *B, int32_t M, int32_t N, int32_t K, int prec, float *C,
                  cudaStream_t s, int num_sms, int variant, int bn = 0, int splits = 0);

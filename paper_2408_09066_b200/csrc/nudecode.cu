@@ -1,0 +1,624 @@
+// nudecode.cu -- the decode (Eq. 11 + Born rule + H_b) as a type-1 NUFFT.
+//
+//   q_c(x, y) = Re sum_k conj(m_ck) exp(2 pi i (tx_k (x - cx) + ty_k (y - cy))) / (sqrt(D) ||m_c||)
+//
+// (Eq. 11 after the Eq. 10 normalisation; t = theta / (2 pi l) turns per
+// metre; the phase origin (cx, cy) is the bounds centre, a rotation that cancels in q).  On the cells
+// of a regular grid, x_j = x0 + (j + 1/2) res, this is a 2-D trigonometric sum with D off-grid
+// frequencies: the decode GEMM (gemm_tc.cu) evaluates it densely (8 R C D flops); here it is a
+// type-1 non-uniform FFT (Dutt & Rokhlin 1993; Greengard & Lee 2004, Gaussian gridding):
+//
+//   0. with centred output indices j' = j - jc, r' = r - rc (jc = C / 2, rc = R_ext / 2) and the
+//      shift folded into the strengths, s_ck = a_ck e^{2 pi i (tx_k U0 + ty_k V0)}, a_ck =
+//      conj(m_ck) / (sqrt(D) ||m_c||) (0 for an empty class, L8), U0 = x_jc - cx, V0 = y_rc - cy,
+//      f_c(r', j') = sum_k s_ck e^{i (xi^x_k j' + xi^y_k r')},  xi = 2 pi t res  (radians per cell);
+//   1. both classes in ONE complex sum whose real and imaginary parts are q_0 and q_1 (q_c = Re f_c):
+//      q_0 + i q_1 = sum_k [ c_k e^{+i xi_k . (j', r')} + d_k e^{-i xi_k . (j', r')} ],
+//      c_k = (s_0k + i s_1k) / 2,  d_k = (conj s_0k + i conj s_1k) / 2  (2 D points at +-xi_k);
+//   2. spread: G(m) = sum_p st_p g_x(m_x h_x - xi^x_p) g_y(m_y h_y - xi^y_p) on the periodic fine
+//      grid of M_x x M_y points (h = 2 pi / M, M = 2^p >= 2 x outputs: oversampling sigma >= 2),
+//      Gaussian g(u) = exp(-u^2 / (4 tau)), tau = pi msp / (n^2 sigma (sigma - 1/2)), msp = 5;
+//      only the band |m| <= B = ceil(max |xi| / h) + 6 is nonzero (xi <= pi res / l: B ~ M res / 2l);
+//   3. F(t) = (1 / M_x M_y) sum_m G(m) e^{+2 pi i m . t / M}: a pruned 2-D FFT -- along y for each of
+//      the W_x = 2 B_x + 1 band columns (zero-padded: the band is shifted to the start, the shift's
+//      phase e^{-2 pi i B t / M} folded into the output factor), then along x for each decoded row;
+//      only the outputs |t| < M / 4 (the centred rows / columns) are formed in the fused last stage;
+//   4. deconvolve: f(r', j') = (pi / tau) e^{j'^2 tau_x + r'^2 tau_y} F(r', j'); q_0 = Re, q_1 = Im;
+//      the epilogue is the GEMM's: p = min(q^2, 1) (Born rule), H_b(p) for Alg. 2
+//      or the 8-bit p code of the histogram estimator, q for the band's own rows.
+// Accuracy: ~1e-6 of the peak |q| (Gaussian gridding with msp = 5, fp32 transforms), against the
+// fp16-operand GEMM's ~1e-4..1e-3.
+//
+// Kernels (one decode): k_nd_spread (block = 16 x 16 tile of the band grid; gathers the points of
+// the 3 x 3 neighbouring bins in a fixed host-sorted order: deterministic, no atomics),
+// k_nd_colfft (block = one band column), k_nd_rowfft (block = ND_RB decoded rows).  The binning
+// of the 2 D points depends only on theta and the grid geometry: it is built on the host once per
+// geometry (a plan) and cached.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace {
+
+constexpr int ND_TS = 16;          // spread tile side (cells)
+constexpr int ND_BS = 8;           // point bin side (cells)
+constexpr int ND_CH = 64;          // points staged per chunk in the spread kernel
+constexpr double ND_MSP = 5.0;     // Gaussian width parameter (accuracy ~1e-6)
+constexpr int ND_MARGIN = 6;       // band half-width beyond max |xi| / h (cells)
+constexpr int ND_RB = 4;           // decoded rows per row-transform block
+constexpr int ND_LOGN_MAX = 13;    // shared-memory transforms up to 8192 points
+constexpr double kPi = 3.14159265358979323846;
+
+struct NdPlan {
+    // geometry key
+    double x0 = 0, y0 = 0, res = 0;
+    int cols = 0, r_lo = 0, r_ext = 0;
+    // transform geometry
+    int logx = 0, logy = 0, Mx = 0, My = 0;
+    int Bx = 0, By = 0, Wx = 0, Wy = 0, nbx = 0, nby = 0, ntx = 0, nty = 0;
+    int jc = 0, rc = 0, ldt = 0;
+    double U0 = 0, V0 = 0;
+    float ax = 0, ay = 0;              // h^2 / (4 tau) per axis
+    int *d_kid = nullptr;              // point ids (k, or D + k for -xi_k) in bin order [2 D]
+    float2 *d_pos = nullptr;           // per slot: position relative to its bin's first cell (cells)
+    int *d_bin_off = nullptr;          // [nbx nby + 1]
+    float2 *d_Px = nullptr;            // output factors per column [cols]
+    float2 *d_Py = nullptr;            // output factors per decoded row [r_ext]
+    int64_t used = 0;                  // LRU tick
+};
+
+// per decode: the strength of every point, in bin order (slot s holds point kid[s]: k, or D + k
+// for the mirrored point at -xi_k)
+__global__ void __launch_bounds__(256) k_nd_strength(const int *__restrict__ kid, int npts, int D, int Dp,
+                                                     const double2 *__restrict__ m, const double *__restrict__ mscale,
+                                                     double inv_D, const double *__restrict__ tx_t,
+                                                     const double *__restrict__ ty_t, double U0, double V0,
+                                                     float2 *__restrict__ st)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= npts) return;
+    const int pt = kid[s];
+    const bool neg = pt >= D;
+    const int k = neg ? pt - D : pt;
+    const double t = tx_t[k] * U0 + ty_t[k] * V0;   // turns of the centring shift
+    const float f = (float)(t - rint(t));            // in [-1/2, 1/2]
+    float sn, cs;
+    sincospif(2.f * f, &sn, &cs);
+    const double sc0 = mscale[0] * inv_D, sc1 = mscale[1] * inv_D;   // 1 / (sqrt(D) ||m_c||), 0 if empty
+    const double2 m0 = m[k], m1 = m[Dp + k];
+    // a_c = conj(m_c) sc_c; s_c = a_c e^{i phi}
+    const float a0r = (float)(m0.x * sc0), a0i = (float)(-m0.y * sc0);
+    const float a1r = (float)(m1.x * sc1), a1i = (float)(-m1.y * sc1);
+    const float s0r = a0r * cs - a0i * sn, s0i = a0r * sn + a0i * cs;
+    const float s1r = a1r * cs - a1i * sn, s1i = a1r * sn + a1i * cs;
+    // c = (s0 + i s1) / 2 at +xi; d = (conj s0 + i conj s1) / 2 at -xi
+    st[s] = neg ? make_float2(0.5f * (s0r + s1i), 0.5f * (s1r - s0i)) : make_float2(0.5f * (s0r - s1i), 0.5f * (s0i + s1r));
+}
+
+struct NdSpread {
+    const float2 *st;        // strengths per slot
+    const float2 *pos;       // position per slot relative to its bin's first cell (cells, fp32)
+    const int *bin_off;      // [nbx nby + 1]
+    int Wx, Wy, nbx, nby;
+    float ax, ay;            // h^2 / (4 tau)
+    float2 *Gt;              // compact band grid, x-major: Gt[ux][uy]
+};
+
+// block = one 16 x 16 tile of the band grid; gathers the points binned (8 x 8 bins) within 8 cells of
+// it -- the 4 x 4 bins covering [16 b - 8, 16 b + 24) per axis, four contiguous slot ranges (one per
+// bin row), where a point farther than 8 cells has weight < e^-31 --, up to 128 per pass.  One
+// thread per staged point computes its position relative to the tile; then all threads compute the
+// 16 x-weights g_x and the 16 strength-scaled y-weights h_y = g_y st of every staged point, and
+// every thread (one cell) sums g_x[q][x] h_y[q][y] over the points in slot order (deterministic).
+__global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ NdSpread p)
+{
+    constexpr int CH = 128;
+    __shared__ float2 s_st[CH];
+    __shared__ float2 s_u[CH];   // the point's position relative to this tile's first cell
+    __shared__ float s_gx[CH][ND_TS + 1];
+    __shared__ float2 s_hy[CH][ND_TS];
+    const int bx = blockIdx.x, by = blockIdx.y, tid = threadIdx.x;
+    const int cxl = tid >> 4, cyl = tid & 15;   // a warp = 2 band columns x 16 rows (contiguous stores)
+    const int xb0 = max(2 * bx - 1, 0), xb1 = min(2 * bx + 2, p.nbx - 1);
+    int beg[4], len[4], yb_of[4], nr = 0, total = 0;
+    for (int dy = -1; dy <= 2; ++dy) {
+        const int yb = 2 * by + dy;
+        if (yb < 0 || yb >= p.nby) continue;
+        beg[nr] = __ldg(p.bin_off + yb * p.nbx + xb0);
+        len[nr] = __ldg(p.bin_off + yb * p.nbx + xb1 + 1) - beg[nr];
+        yb_of[nr] = yb;
+        total += len[nr];
+        ++nr;
+    }
+    float accr = 0.f, acci = 0.f, accr2 = 0.f, acci2 = 0.f;
+    for (int c0 = 0; c0 < total; c0 += CH) {
+        const int nc = min(CH, total - c0);
+        if (c0) __syncthreads();   // the previous pass is consumed
+        if (tid < nc) {
+            int i = c0 + tid, r = 0;
+            while (i >= len[r]) { i -= len[r]; ++r; }
+            const int slot = beg[r] + i;
+            // the slot's bin column: the bins of this row range in order xb0 .. xb1
+            const int rowb = yb_of[r] * p.nbx;
+            int xbp = xb0;
+            while (xbp < xb1 && slot >= __ldg(p.bin_off + rowb + xbp + 1)) ++xbp;
+            const float2 ps = __ldg(p.pos + slot);
+            s_u[tid] = make_float2((float)(xbp * ND_BS - bx * ND_TS) + ps.x, (float)(yb_of[r] * ND_BS - by * ND_TS) + ps.y);
+            s_st[tid] = __ldg(p.st + slot);
+        }
+        __syncthreads();
+        for (int e = tid; e < nc * 2 * ND_TS; e += 256) {
+            const int q = e >> 5, r = e & 31;
+            const float2 u = s_u[q];
+            if (r < ND_TS) {
+                const float d = (float)r - u.x;
+                s_gx[q][r] = __expf(-d * d * p.ax);
+            } else {
+                const float d = (float)(r - ND_TS) - u.y;
+                const float g = __expf(-d * d * p.ay);
+                const float2 st = s_st[q];
+                s_hy[q][r - ND_TS] = make_float2(g * st.x, g * st.y);
+            }
+        }
+        __syncthreads();
+        int q = 0;
+#pragma unroll 4
+        for (; q + 1 < nc; q += 2) {   // two independent accumulator pairs (summed in a fixed order)
+            const float g = s_gx[q][cxl], g2 = s_gx[q + 1][cxl];
+            const float2 hy = s_hy[q][cyl], hy2 = s_hy[q + 1][cyl];
+            accr = fmaf(g, hy.x, accr);
+            acci = fmaf(g, hy.y, acci);
+            accr2 = fmaf(g2, hy2.x, accr2);
+            acci2 = fmaf(g2, hy2.y, acci2);
+        }
+        if (q < nc) {
+            const float g = s_gx[q][cxl];
+            const float2 hy = s_hy[q][cyl];
+            accr = fmaf(g, hy.x, accr);
+            acci = fmaf(g, hy.y, acci);
+        }
+    }
+    accr += accr2;
+    acci += acci2;
+    const int ux = bx * ND_TS + cxl, uy = by * ND_TS + cyl;
+    if (ux < p.Wx && uy < p.Wy) p.Gt[(size_t)ux * p.Wy + uy] = make_float2(accr, acci);
+}
+
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b)
+{
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// transform along y of band column ux (fftr::fft: register radix-16 passes); output rows r in
+// [0, r_ext) (r' = r - rc, the centred modes |r'| < M / 4), times Py[r]
+template <int LOGN, int T, int NZ>
+__global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(const float2 *__restrict__ Gt, int Wy, const float2 *__restrict__ tw,
+                                                 const float2 *__restrict__ Py, int r_ext, int rc, int ldt,
+                                                 float2 *__restrict__ Tt)
+{
+    constexpr int N = 1 << LOGN;
+    extern __shared__ float2 sm_fft[];
+    const int ux = blockIdx.x;
+    const float2 *in = Gt + (size_t)ux * Wy;
+    float2 *out = Tt + (size_t)ux * ldt;
+    fftr::fft<LOGN, T, NZ, true>(
+        sm_fft, tw, [&](int j) { return j < Wy ? __ldg(in + j) : make_float2(0.f, 0.f); },
+        [&](int m, float2 v) {
+            const int r = rc + (m < N / 2 ? m : m - N);
+            if (r >= 0 && r < r_ext) out[r] = cmulf(__ldg(Py + r), v);
+        });
+}
+
+struct NdEpi {
+    const double *mscale;   // sqrt(D) / ||m_c|| [2]: 0 for an empty class
+    float *hb;        // hb[(c * r_ext + row) * ldh + col]
+    uint8_t *code;    // histogram estimator: 8-bit p code at the same index (hb unused)
+    int ldh, r_ext;
+    float *q;         // q[(c * band_rows + row + q_off) * cols + col] for band rows, or null
+    int q_off, band_rows, cols;
+};
+
+__device__ __forceinline__ float nd_hb_of_p(float p)
+{
+    // binary entropy in bits, 0 log 0 = 0, with MUFU log2: -p log2 p - (1 - p) log2(1 - p).  For
+    // p < 1/16, log(1 - p) = -(p + p^2/2 + ... + p^6/6) (truncation < 1e-8 relative): 1 - p in
+    // fp32 would lose log2(1/p) bits of p, the cancellation log1pf avoids in the GEMM epilogue.
+    float h = 0.f;
+    if (p > 0.f) h = -p * __log2f(p);
+    if (p < 0.0625f) {
+        const float s = p * (1.f + p * (0.5f + p * (0.33333333f + p * (0.25f + p * (0.2f + p * 0.16666667f)))));
+        h += (1.f - p) * s * 1.44269504088896341f;
+    } else if (p < 1.f) {
+        h -= (1.f - p) * __log2f(1.f - p);
+    }
+    return h;
+}
+
+__device__ __forceinline__ uint8_t nd_code8(float p)
+{
+    const int c = __float2int_rd(__fadd_rn(__fmul_rn(p, 255.0f), 0.5f));
+    return (uint8_t)min(255, max(0, c));
+}
+
+__device__ __forceinline__ void nd_store(const NdEpi &e, int row, int col, float2 g, bool live0, bool live1)
+{
+    // an empty class decodes to exactly 0 (L8), not to the other class's transform rounding
+    const float qv[2] = {live0 ? g.x : 0.f, live1 ? g.y : 0.f};
+    const int br = row + e.q_off;
+#pragma unroll
+    for (int cls = 0; cls < 2; ++cls) {
+        const float pr = fminf(qv[cls] * qv[cls], 1.f);
+        const size_t o = ((size_t)cls * e.r_ext + row) * e.ldh + col;
+        if (e.code) e.code[o] = nd_code8(pr);
+        else e.hb[o] = nd_hb_of_p(pr);
+        if (e.q && br >= 0 && br < e.band_rows) e.q[((size_t)cls * e.band_rows + br) * e.cols + col] = qv[cls];
+    }
+}
+
+// transform along x of ND_RB decoded rows (staged from the column-transformed Tt[ux][r]);
+// outputs j in [0, cols) (j' = j - jc), times Px[j], then the epilogue
+template <int LOGN, int T, int NZ>
+__global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(const float2 *__restrict__ Tt, int ldt, int Wx,
+                                                 const float2 *__restrict__ tw, const float2 *__restrict__ Px,
+                                                 int cols, int jc, const NdEpi e)
+{
+    constexpr int N = 1 << LOGN;
+    extern __shared__ float2 sm_fft[];
+    float2 *stage = sm_fft + N + N / 16;   // [ND_RB][Wx]
+    const int r0 = blockIdx.x * ND_RB;
+    const int nr = min(ND_RB, e.r_ext - r0);
+    const bool live0 = e.mscale[0] != 0.0, live1 = e.mscale[1] != 0.0;
+    for (int ux = threadIdx.x; ux < Wx; ux += T) {
+        const float4 *src = reinterpret_cast<const float4 *>(Tt + (size_t)ux * ldt + r0);   // ldt, r0: multiples of 4
+        const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
+        stage[ux] = make_float2(v0.x, v0.y);
+        stage[Wx + ux] = make_float2(v0.z, v0.w);
+        stage[2 * Wx + ux] = make_float2(v1.x, v1.y);
+        stage[3 * Wx + ux] = make_float2(v1.z, v1.w);
+    }
+    for (int rr = 0; rr < nr; ++rr) {
+        __syncthreads();   // staging done / the previous row's transform consumed
+        const float2 *srow = stage + rr * Wx;
+        const int row = r0 + rr;
+        fftr::fft<LOGN, T, NZ, true>(
+            sm_fft, tw, [&](int j) { return j < Wx ? srow[j] : make_float2(0.f, 0.f); },
+            [&](int m, float2 v) {
+                const int col = jc + (m < N / 2 ? m : m - N);
+                if (col >= 0 && col < cols) nd_store(e, row, col, cmulf(__ldg(Px + col), v), live0, live1);
+            });
+    }
+}
+
+int nd_grow(void **p, size_t *cap, size_t need)
+{
+    if (need <= *cap) return VSAOGM_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    if (cudaMalloc(p, need) != cudaSuccess) { *p = nullptr; return VSAOGM_ENOMEM; }
+    *cap = need;
+    return VSAOGM_OK;
+}
+
+int ilog2_ceil(int64_t v)
+{
+    int l = 0;
+    while (((int64_t)1 << l) < v) ++l;
+    return l;
+}
+
+void free_plan(NdPlan *p)
+{
+    if (!p) return;
+    void *ptrs[] = {p->d_kid, p->d_pos, p->d_bin_off, p->d_Px, p->d_Py};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    delete p;
+}
+
+// the geometry of a decode (no allocation); false if the NUFFT does not apply
+bool nd_geometry(const vsaogm_ctx *c, double x0, double y0, double res, int cols, int r_lo, int r_ext, NdPlan &P)
+{
+    if (c->nslots != 2 || cols < 1 || r_ext < 1) return false;
+    P.x0 = x0;
+    P.y0 = y0;
+    P.res = res;
+    P.cols = cols;
+    P.r_lo = r_lo;
+    P.r_ext = r_ext;
+    P.logx = std::max(8, ilog2_ceil(2 * (int64_t)cols));
+    P.logy = std::max(8, ilog2_ceil(2 * (int64_t)r_ext));
+    if (P.logx > ND_LOGN_MAX || P.logy > ND_LOGN_MAX) return false;
+    P.Mx = 1 << P.logx;
+    P.My = 1 << P.logy;
+    double amx = 0.0, amy = 0.0;   // max |turns per metre|
+    for (int k = 0; k < c->D; ++k) {
+        amx = std::max(amx, fabs(c->thx[k] / (2.0 * kPi * c->l)));
+        amy = std::max(amy, fabs(c->thy[k] / (2.0 * kPi * c->l)));
+    }
+    P.Bx = (int)ceil(amx * res * P.Mx) + ND_MARGIN;
+    P.By = (int)ceil(amy * res * P.My) + ND_MARGIN;
+    P.Wx = 2 * P.Bx + 1;
+    P.Wy = 2 * P.By + 1;
+    if (P.Wx > P.Mx / 2 || P.Wy > P.My / 2) return false;   // band wider than the zero-padded half
+    if (((size_t)P.Mx + P.Mx / 16 + (size_t)ND_RB * P.Wx) * sizeof(float2) > 227 * 1024) return false;   // row-transform smem
+    P.nbx = (P.Wx + ND_BS - 1) / ND_BS;   // point bins
+    P.nby = (P.Wy + ND_BS - 1) / ND_BS;
+    P.ntx = (P.Wx + ND_TS - 1) / ND_TS;   // spread tiles
+    P.nty = (P.Wy + ND_TS - 1) / ND_TS;
+    P.jc = cols / 2;
+    P.rc = r_ext / 2;
+    P.ldt = (r_ext + 3) / 4 * 4;
+    P.U0 = x0 + ((double)P.jc + 0.5) * res - c->cx;
+    P.V0 = y0 + ((double)(r_lo + P.rc) + 0.5) * res - c->cy;
+    return true;
+}
+
+double nd_tau(int n, int M) { const double s = (double)M / n; return kPi * ND_MSP / ((double)n * n * s * (s - 0.5)); }
+
+int nd_build(vsaogm_ctx *c, NdPlan &P)
+{
+    const int D = c->D;
+    const double sx = P.res * P.Mx, sy = P.res * P.My;
+    const int nb = P.nbx * P.nby;
+    std::vector<int> bin(2 * (size_t)D), cnt(nb + 1, 0);
+    std::vector<double> fxa(2 * (size_t)D), fya(2 * (size_t)D);
+    for (int pt = 0; pt < 2 * D; ++pt) {
+        const int k = pt % D;
+        const double sg = pt < D ? 1.0 : -1.0;
+        // fine-grid position in cells from the band's first cell (the device's turns per metre,
+        // computed the same way as in vsaogm_create)
+        const double fx = sg * (c->thx[k] / (2.0 * kPi * c->l)) * sx + P.Bx, fy = sg * (c->thy[k] / (2.0 * kPi * c->l)) * sy + P.By;
+        fxa[pt] = fx;
+        fya[pt] = fy;
+        const int ux = std::min(P.Wx - 1, std::max(0, (int)floor(fx)));
+        const int uy = std::min(P.Wy - 1, std::max(0, (int)floor(fy)));
+        bin[pt] = (uy / ND_BS) * P.nbx + ux / ND_BS;
+        cnt[bin[pt] + 1]++;
+    }
+    for (int b = 0; b < nb; ++b) cnt[b + 1] += cnt[b];
+    std::vector<int> off(cnt.begin(), cnt.end()), kid(2 * (size_t)D);
+    std::vector<float2> pos(2 * (size_t)D);
+    for (int pt = 0; pt < 2 * D; ++pt) {   // stable: ascending point id per bin
+        const int s = off[bin[pt]]++;
+        kid[s] = pt;
+        const int bxp = bin[pt] % P.nbx, byp = bin[pt] / P.nbx;
+        pos[s] = make_float2((float)(fxa[pt] - ND_BS * bxp), (float)(fya[pt] - ND_BS * byp));
+    }
+    const double tx_ = nd_tau(P.cols, P.Mx), ty_ = nd_tau(P.r_ext, P.My);
+    const double hx = 2.0 * kPi / P.Mx, hy = 2.0 * kPi / P.My;
+    P.ax = (float)(hx * hx / (4.0 * tx_));
+    P.ay = (float)(hy * hy / (4.0 * ty_));
+    std::vector<float2> px(P.cols), py(P.r_ext);
+    for (int j = 0; j < P.cols; ++j) {
+        const double jp = j - P.jc;
+        const double mag = sqrt(kPi / tx_) * exp(jp * jp * tx_) / P.Mx;
+        // e^{-2 pi i B j' / M} with the integer product reduced exactly
+        const double turns = (double)(((int64_t)P.Bx * (int64_t)(j - P.jc)) % P.Mx) / P.Mx;
+        px[j] = make_float2((float)(mag * cos(-2.0 * kPi * turns)), (float)(mag * sin(-2.0 * kPi * turns)));
+    }
+    for (int r = 0; r < P.r_ext; ++r) {
+        const double rp = r - P.rc;
+        const double mag = sqrt(kPi / ty_) * exp(rp * rp * ty_) / P.My;
+        const double turns = (double)(((int64_t)P.By * (int64_t)(r - P.rc)) % P.My) / P.My;
+        py[r] = make_float2((float)(mag * cos(-2.0 * kPi * turns)), (float)(mag * sin(-2.0 * kPi * turns)));
+    }
+    if (cudaMalloc(&P.d_kid, kid.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&P.d_pos, pos.size() * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&P.d_bin_off, cnt.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&P.d_Px, px.size() * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&P.d_Py, py.size() * sizeof(float2)) != cudaSuccess)
+        return VSAOGM_ENOMEM;
+    VSA_CUDA_TRY(cudaMemcpy(P.d_kid, kid.data(), kid.size() * sizeof(int), cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(P.d_pos, pos.data(), pos.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(P.d_bin_off, cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(P.d_Px, px.data(), px.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(P.d_Py, py.data(), py.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    return VSAOGM_OK;
+}
+
+// the cached plan of this geometry (at most VSA_ND_PLANS; the least recently used is replaced)
+int nd_plan(vsaogm_ctx *c, double x0, double y0, double res, int cols, int r_lo, int r_ext, NdPlan **out)
+{
+    ++c->nd_tick;
+    for (int i = 0; i < c->nd_nplans; ++i) {
+        NdPlan *p = static_cast<NdPlan *>(c->nd_plans[i]);
+        if (p->x0 == x0 && p->y0 == y0 && p->res == res && p->cols == cols && p->r_lo == r_lo && p->r_ext == r_ext) {
+            p->used = c->nd_tick;
+            *out = p;
+            return VSAOGM_OK;
+        }
+    }
+    NdPlan G;
+    if (!nd_geometry(c, x0, y0, res, cols, r_lo, r_ext, G)) return VSAOGM_EINVAL_ARG;
+    if (!c->d_nd_tw) {   // universal twiddle table (fft.cuh): tw[p - 1 + k] = e^{i pi k / p}
+        const int n = 1 << ND_LOGN_MAX;
+        std::vector<float2> tw(n);
+        for (int p = 1; p < n; p <<= 1)
+            for (int k = 0; k < p; ++k) {
+                const double a = kPi * k / p;
+                tw[p - 1 + k] = make_float2((float)cos(a), (float)sin(a));
+            }
+        if (cudaMalloc(&c->d_nd_tw, n * sizeof(float2)) != cudaSuccess) { c->d_nd_tw = nullptr; return VSAOGM_ENOMEM; }
+        VSA_CUDA_TRY(cudaMemcpy(c->d_nd_tw, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+    int slot = c->nd_nplans;
+    if (slot == VSA_ND_PLANS) {   // evict the least recently used plan (its buffers may be in flight)
+        slot = 0;
+        for (int i = 1; i < VSA_ND_PLANS; ++i)
+            if (static_cast<NdPlan *>(c->nd_plans[i])->used < static_cast<NdPlan *>(c->nd_plans[slot])->used) slot = i;
+        VSA_CUDA_TRY(cudaDeviceSynchronize());
+        free_plan(static_cast<NdPlan *>(c->nd_plans[slot]));
+        c->nd_plans[slot] = nullptr;
+    } else {
+        ++c->nd_nplans;
+    }
+    NdPlan *p = new NdPlan(G);
+    c->nd_plans[slot] = p;
+    int rc = nd_build(c, *p);
+    if (rc) {
+        free_plan(p);
+        c->nd_plans[slot] = c->nd_plans[--c->nd_nplans];
+        c->nd_plans[c->nd_nplans] = nullptr;
+        return rc;
+    }
+    p->used = c->nd_tick;
+    *out = p;
+    return VSAOGM_OK;
+}
+
+// nonzero input groups of N / 16 values (the first radix-16 pass skips the others), rounded up
+// to an instantiated count (transforms whose first pass is radix 16: LOGN = 8, 12)
+int nz_of(int W, int logn)
+{
+    if ((logn & 3) != 0) return 16;
+    const int g = (W + (1 << logn) / 16 - 1) / ((1 << logn) / 16);
+    return g <= 3 ? 3 : g <= 4 ? 4 : 8;
+}
+
+template <int LOGN, int NZ>
+int launch_colfft_nz(vsaogm_ctx *c, const NdPlan &P)
+{
+    constexpr int N = 1 << LOGN;
+    constexpr int T = N / 16 < 32 ? 32 : N / 16;
+    const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_nd_colfft<LOGN, T, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_nd_colfft<LOGN, T, NZ><<<P.Wx, T, smem, c->stream>>>((const float2 *)c->d_nd_G, P.Wy, (const float2 *)c->d_nd_tw,
+                                                           P.d_Py, P.r_ext, P.rc, P.ldt, (float2 *)c->d_nd_T);
+    return VSAOGM_OK;
+}
+
+template <int LOGN, int NZ>
+int launch_rowfft_nz(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
+{
+    constexpr int N = 1 << LOGN;
+    constexpr int T = N / 16 < 32 ? 32 : N / 16;
+    const size_t smem = ((size_t)(N + N / 16) + (size_t)ND_RB * P.Wx) * sizeof(float2);
+    VSA_CUDA_TRY(cudaFuncSetAttribute(k_nd_rowfft<LOGN, T, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_nd_rowfft<LOGN, T, NZ><<<(P.r_ext + ND_RB - 1) / ND_RB, T, smem, c->stream>>>(
+        (const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw, P.d_Px, P.cols, P.jc, e);
+    return VSAOGM_OK;
+}
+
+template <int LOGN>
+int launch_colfft(vsaogm_ctx *c, const NdPlan &P)
+{
+    if constexpr ((LOGN & 3) == 0) {
+        switch (nz_of(P.Wy, LOGN)) {
+        case 3: return launch_colfft_nz<LOGN, 3>(c, P);
+        case 4: return launch_colfft_nz<LOGN, 4>(c, P);
+        default: return launch_colfft_nz<LOGN, 8>(c, P);
+        }
+    }
+    return launch_colfft_nz<LOGN, 16>(c, P);
+}
+
+template <int LOGN>
+int launch_rowfft(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
+{
+    if constexpr ((LOGN & 3) == 0) {
+        switch (nz_of(P.Wx, LOGN)) {
+        case 3: return launch_rowfft_nz<LOGN, 3>(c, P, e);
+        case 4: return launch_rowfft_nz<LOGN, 4>(c, P, e);
+        default: return launch_rowfft_nz<LOGN, 8>(c, P, e);
+        }
+    }
+    return launch_rowfft_nz<LOGN, 16>(c, P, e);
+}
+
+}  // namespace
+
+bool vsa_nudecode_applies(vsaogm_ctx *c, double x0, double y0, double res, int32_t cols, int32_t r_lo, int32_t r_ext)
+{
+    if (c->dec_method == 0 || c->nslots != 2) return false;
+    NdPlan G;
+    if (!nd_geometry(c, x0, y0, res, cols, r_lo, r_ext, G)) return false;
+    if (c->dec_method == 1) return true;
+    // auto: modelled times.  GEMM: 8 R C D flops at ~1.1 PF/s plus the
+    // tables; NUFFT: transform work (point-stages) at the measured FFT rate plus launches.
+    const double t_gemm = 8.0 * r_ext * (double)cols * c->D / 1.1e15 + 2.0 * (r_ext + 0.5 * cols) * (double)c->Dp * 2.0 / 4e12 + 8e-6;
+    const double work = (double)G.Wx * G.My * G.logy + (double)r_ext * G.Mx * G.logx;
+    const double t_nufft = work * 0.55e-12 * 1.5 + 2.0 * c->D * 1e-10 + 12e-6;
+    return t_nufft < t_gemm;
+}
+
+int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int32_t cols, int32_t r_lo, int32_t r_ext,
+                            float *hb, uint8_t *code, size_t ldh, float *q, int32_t q_off, int32_t band_rows,
+                            bool mark_main)
+{
+    NdPlan *P = nullptr;
+    int rc;
+    if ((rc = nd_plan(c, x0, y0, res, cols, r_lo, r_ext, &P))) return rc;
+    if ((rc = nd_grow(&c->d_nd_G, &c->nd_G_cap, (size_t)P->Wx * P->Wy * sizeof(float2)))) return rc;
+    if ((rc = nd_grow(&c->d_nd_T, &c->nd_T_cap, (size_t)P->Wx * P->ldt * sizeof(float2)))) return rc;
+    if ((rc = nd_grow(&c->d_nd_st, &c->nd_st_cap, 2 * (size_t)c->D * sizeof(float2)))) return rc;
+    cudaEvent_t ev;
+    vsa_prof_begin(c, VSAOGM_K_DECODE_NUFFT, &ev);
+    const int npts = 2 * c->D;
+    k_nd_strength<<<(npts + 255) / 256, 256, 0, c->stream>>>(P->d_kid, npts, c->D, c->Dp, (const double2 *)c->d_m,
+                                                            c->d_norm2 + c->nslots, 1.0 / c->D, c->d_tx_turns,
+                                                            c->d_ty_turns, P->U0, P->V0, (float2 *)c->d_nd_st);
+    // the memories are consumed: the next encode (encode stream) may start
+    if (mark_main && (rc = vsa_mark_main(c))) return rc;
+    NdSpread sp;
+    sp.st = (const float2 *)c->d_nd_st;
+    sp.pos = P->d_pos;
+    sp.bin_off = P->d_bin_off;
+    sp.Wx = P->Wx;
+    sp.Wy = P->Wy;
+    sp.nbx = P->nbx;
+    sp.nby = P->nby;
+    sp.ax = P->ax;
+    sp.ay = P->ay;
+    sp.Gt = (float2 *)c->d_nd_G;
+    k_nd_spread<<<dim3(P->ntx, P->nty), 256, 0, c->stream>>>(sp);
+    VSA_CUDA_TRY(cudaGetLastError());
+    switch (P->logy) {
+    case 8: rc = launch_colfft<8>(c, *P); break;
+    case 9: rc = launch_colfft<9>(c, *P); break;
+    case 10: rc = launch_colfft<10>(c, *P); break;
+    case 11: rc = launch_colfft<11>(c, *P); break;
+    case 12: rc = launch_colfft<12>(c, *P); break;
+    default: rc = launch_colfft<13>(c, *P); break;
+    }
+    if (rc) return rc;
+    VSA_CUDA_TRY(cudaGetLastError());
+    NdEpi e;
+    e.mscale = c->d_norm2 + c->nslots;
+    e.hb = hb;
+    e.code = code;
+    e.ldh = (int)ldh;
+    e.r_ext = r_ext;
+    e.q = q;
+    e.q_off = q_off;
+    e.band_rows = band_rows;
+    e.cols = cols;
+    switch (P->logx) {
+    case 8: rc = launch_rowfft<8>(c, *P, e); break;
+    case 9: rc = launch_rowfft<9>(c, *P, e); break;
+    case 10: rc = launch_rowfft<10>(c, *P, e); break;
+    case 11: rc = launch_rowfft<11>(c, *P, e); break;
+    case 12: rc = launch_rowfft<12>(c, *P, e); break;
+    default: rc = launch_rowfft<13>(c, *P, e); break;
+    }
+    if (rc) return rc;
+    VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_DECODE_NUFFT, ev);
+    c->launches += 4;
+    return VSAOGM_OK;
+}
+
+void vsa_nudecode_free(vsaogm_ctx *c)
+{
+    for (int i = 0; i < c->nd_nplans; ++i) free_plan(static_cast<NdPlan *>(c->nd_plans[i]));
+    c->nd_nplans = 0;
+    if (c->d_nd_tw) cudaFree(c->d_nd_tw);
+    if (c->d_nd_G) cudaFree(c->d_nd_G);
+    if (c->d_nd_T) cudaFree(c->d_nd_T);
+    if (c->d_nd_st) cudaFree(c->d_nd_st);
+    c->d_nd_tw = c->d_nd_G = c->d_nd_T = c->d_nd_st = nullptr;
+}

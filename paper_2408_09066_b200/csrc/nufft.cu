@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fft.cuh"
 
 namespace {
 
@@ -268,71 +269,6 @@ __device__ __forceinline__ float nu_alpha(const int *__restrict__ bcnt)
     if (n0 <= 0 || n1 <= 0) return 1.f;
     const int e = max(-12, min(12, (int)rintf(log2f((float)n0 / (float)n1))));
     return ldexpf(1.f, e);
-}
-
-// Mixed radix Stockham (self-sorting) transform of N = 2^LOGN complex values in shared memory
-// with the positive exponent, G_m = sum_j x_j e^{+2 pi i j m / N}, of an input whose upper half
-// is zero (the zero padding: n1 <= N / 2): the first stage is folded into the load -- x_j =
-// load(j), j < N / 2 -- (radix 2 for odd LOGN: (x_j, x_j); radix 4 for even LOGN: the 4-point
-// DFT of (x_j, x_{j + N/4}, 0, 0)), then radix-4 stages (sub-transform size Ns x4 per stage).
-// Radix-4 twiddles e^{+2 pi i k / (4 Ns)}, k < Ns: tw[2 Ns - 1 + k] of the per-stage table
-// tw[p - 1 + k] = e^{+2 pi i k / (2p)}, k < p, p = 1, 2, 4, ... N/2; w^2, w^3 by products.
-template <int LOGN, int T, class Load>
-__device__ __forceinline__ float2 *stockham_zp(float2 *a, float2 *b, const float2 *__restrict__ tw, Load load)
-{
-    constexpr int N = 1 << LOGN;
-    int ns;
-    if (LOGN & 1) {
-#pragma unroll
-        for (int jj = 0; jj < N / 2; jj += T) {
-            const int j = jj + threadIdx.x;
-            if (N / 2 < T && j >= N / 2) break;   // small transforms: fewer values than threads
-            const float2 v = load(j);
-            *reinterpret_cast<float4 *>(a + 2 * j) = make_float4(v.x, v.y, v.x, v.y);
-        }
-        ns = 2;
-    } else {
-#pragma unroll
-        for (int jj = 0; jj < N / 4; jj += T) {
-            const int j = jj + threadIdx.x;
-            if (N / 4 < T && j >= N / 4) break;
-            const float2 x0 = load(j), x1 = load(j + N / 4);
-            *reinterpret_cast<float4 *>(a + 4 * j) = make_float4(x0.x + x1.x, x0.y + x1.y, x0.x - x1.y, x0.y + x1.x);
-            *reinterpret_cast<float4 *>(a + 4 * j + 2) = make_float4(x0.x - x1.x, x0.y - x1.y, x0.x + x1.y, x0.y - x1.x);
-        }
-        ns = 4;
-    }
-#pragma unroll
-    for (int st = 0; st < (LOGN - 1) / 2; ++st) {
-        __syncthreads();
-#pragma unroll
-        for (int jj = 0; jj < N / 4; jj += T) {
-            const int j = jj + threadIdx.x;
-            if (N / 4 < T && j >= N / 4) break;
-            const int k = j & (ns - 1);
-            float2 x0 = a[j], x1 = a[j + N / 4], x2 = a[j + N / 2], x3 = a[j + 3 * N / 4];
-            const float2 w1 = __ldg(tw + 2 * ns - 1 + k);
-            const float2 w2 = make_float2(w1.x * w1.x - w1.y * w1.y, 2.f * w1.x * w1.y);
-            const float2 w3 = make_float2(w2.x * w1.x - w2.y * w1.y, w2.x * w1.y + w2.y * w1.x);
-            x1 = make_float2(w1.x * x1.x - w1.y * x1.y, w1.x * x1.y + w1.y * x1.x);
-            x2 = make_float2(w2.x * x2.x - w2.y * x2.y, w2.x * x2.y + w2.y * x2.x);
-            x3 = make_float2(w3.x * x3.x - w3.y * x3.y, w3.x * x3.y + w3.y * x3.x);
-            // 4-point DFT with the + sign: i^q
-            const float2 s02 = make_float2(x0.x + x2.x, x0.y + x2.y), d02 = make_float2(x0.x - x2.x, x0.y - x2.y);
-            const float2 s13 = make_float2(x1.x + x3.x, x1.y + x3.y), d13 = make_float2(x1.x - x3.x, x1.y - x3.y);
-            const int o = ((j - k) << 2) + k;
-            b[o] = make_float2(s02.x + s13.x, s02.y + s13.y);
-            b[o + ns] = make_float2(d02.x - d13.y, d02.y + d13.x);           // + i d13
-            b[o + 2 * ns] = make_float2(s02.x - s13.x, s02.y - s13.y);
-            b[o + 3 * ns] = make_float2(d02.x + d13.y, d02.y - d13.x);       // - i d13
-        }
-        float2 *c = a;
-        a = b;
-        b = c;
-        ns <<= 2;
-    }
-    __syncthreads();
-    return a;
 }
 
 // row pass: block = one grid row gy.  Reads the row of both classes' fixed-point grids (and
