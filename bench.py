@@ -40,7 +40,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "grid cells decoded/sec and points bundled/sec at D=8192; decode % tensor peak"
 CONFIG = "C4"
-N_DISTINCT_BATCHES = 8
+N_DISTINCT_BATCHES = 50   # every batch of C4 (5000 scans / 100): 92 MB of inputs on the device
 
 
 def label_tau(D: int) -> float:
@@ -145,13 +145,15 @@ def workload_config(sc, n_pts_mean, world):
     cfg = sc.cfg
     return {
         "workload": "C4 streaming step: bundle one 100-scan lidar batch into persistent D=8192 FHRR memories, "
-                    "decode the 2000x2000 grid (0.05 m) on tcgen05, 5x5 local entropy + 3-way labels",
+                    "decode the 2000x2000 grid (0.05 m), 5x5 local entropy + 3-way labels",
         "D": cfg["D"], "length_scale_m": cfg["l"], "grid": f"{cfg['rows']}x{cfg['cols']}@{cfg['res']}m",
         "points_per_step": int(round(n_pts_mean)), "cells_per_step": cfg["rows"] * cfg["cols"],
         "window": f"{2 * cfg['half'] + 1}x{2 * cfg['half'] + 1} box",
-        "decode_operands": "f16 (fp32 accumulate in TMEM); the bf16-operand decode is the `bf16` object",
-        "l2": "pipelined value and e2e: inputs larger than L2 (per-step working set: table A 131 MB written + "
-              "read, table B 65 MB, H_b 32 MB > 126 MB L2); serial sub-line: flushed between steps (256 MiB write)",
+        "decode": "type-1 NUFFT (fp32 Gaussian gridding + FFTs, the library's auto choice at C4); the tcgen05 "
+                  "GEMM decode (f16 / bf16 operands, fp32 accumulate) is the `gemm` object",
+        "l2": "pipelined value and e2e: inputs cycle through all 50 distinct C4 batches (92 MB) and every step "
+              "writes + reads ~60 MB (H_b 32 MB, labels, transform intermediates), so a batch is re-read "
+              "only after ~3 GB of other traffic; serial and gemm sub-lines: L2 flushed between steps (256 MiB write)",
         "parallelism": "single GPU" if world == 1 else f"points sharded x{world} + NCCL all-reduce of memories; "
                                                       f"grid row bands x{world} with halo",
         "distinct_batches": N_DISTINCT_BATCHES,
@@ -264,20 +266,28 @@ def run_native(args):
         barrier()
         prof = mp.profile_read()
 
-        # bf16-operand decode, same serial loop (fewer steps)
+        # the tcgen05 GEMM decode (dec_method 0), same serial loop (fewer steps), f16 then bf16
+        # operands: the north_star's "decode % tensor peak" (and the bf16 path reported separately)
         kb = max(3, min(args.steps, 20))
-        bevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kb)]
+        mp.set_tuning("dec_method", 0)
+        gemm_runs = {}
+        for name, prec in (("f16", F16), ("bf16", BF16)):
+            gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kb)]
+            for b in range(2):
+                step(b, precision=prec)
+            barrier()
+            mp.profile_read()
+            for k in range(kb):
+                flush.zero_()
+                gevs[k][0].record(stream)
+                step(args.warmup + k, precision=prec)
+                gevs[k][1].record(stream)
+            barrier()
+            gemm_runs[name] = (gevs, mp.profile_read())
+        mp.set_tuning("dec_method", -1)
         for b in range(2):
-            step(b, precision=BF16)
+            step(b)
         barrier()
-        mp.profile_read()
-        for k in range(kb):
-            flush.zero_()
-            bevs[k][0].record(stream)
-            step(args.warmup + k, precision=BF16)
-            bevs[k][1].record(stream)
-        barrier()
-        prof_bf16 = mp.profile_read()
         mp.profile_enable(False)
 
         # the direct (sincos-and-reduce) pair encode of the same batches, timed alone: its ALU
@@ -317,13 +327,15 @@ def run_native(args):
             barrier()
             launches = mp.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    bf16_ms = [a.elapsed_time(b) for a, b in bevs]
+    g16_ms = [a.elapsed_time(b) for a, b in gemm_runs["f16"][0]]
+    gbf_ms = [a.elapsed_time(b) for a, b in gemm_runs["bf16"][0]]
     ar_ms = [a.elapsed_time(b) for a, b in ar_evs] if world > 1 else []
-    serial_total, pipe_total, bf16_total, ar_median = max_over_ranks(
-        [sum(step_ms), p0.elapsed_time(p1), sum(bf16_ms), statistics.median(ar_ms) if ar_ms else 0.0])
+    serial_total, pipe_total, g16_total, gbf_total, ar_median = max_over_ranks(
+        [sum(step_ms), p0.elapsed_time(p1), sum(g16_ms), sum(gbf_ms), statistics.median(ar_ms) if ar_ms else 0.0])
     serial_ms_per_step = serial_total / args.steps
     ms_per_step = pipe_total / args.steps
-    bf16_ms_per_step = bf16_total / kb
+    g16_ms_per_step = g16_total / kb
+    bf16_ms_per_step = gbf_total / kb
 
     # end to end through the public pipelined host API: every step uploads its batch from pinned
     # host memory, bundles, decodes, and downloads the labels to pinned host memory; step k's
@@ -378,15 +390,17 @@ def run_native(args):
     def avg(p, name):
         ms, n = p[name]
         return ms / n if n else float("nan")
-    enc_ms, gemm_ms = avg(prof, "encode"), avg(prof, "decode_gemm")
+    prof_g16, prof_gbf = gemm_runs["f16"][1], gemm_runs["bf16"][1]
+    enc_ms = avg(prof, "encode")
+    gemm_ms, gemm_bf16_ms, tabA_ms = avg(prof_g16, "decode_gemm"), avg(prof_gbf, "decode_gemm"), avg(prof_g16, "table_A")
     shares = {k: round(v[0] / max(1e-12, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
-    # encode (dominant): ALU-bound; algorithmic work = D phasors per point
     my_pts = float(np.mean([len(host_batches[(args.warmup + k) % nb][1]) for k in range(args.steps)]))
     phasors = my_pts * D
     sm_max = pk.get("sm_max_mhz", 1965.0)
     enc_roof = encode_ceiling(sm_max)
     enc_rate = phasors / (enc_ms * 1e-3)
     clocks = clk.summary()
+    traffic = load_ncu_traffic()
 
     def alu_line(rate):
         return {"kernel": "k_encode_pairs", "bound": "alu", "achieved": round(rate / 1e9, 2),
@@ -400,60 +414,90 @@ def run_native(args):
                                                   if enc_roof["measured"] else None),
                 "frac_at_measured_clock": (round(rate / enc_roof["combined"] * sm_max / clocks["sm_mhz"], 4)
                                            if clocks.get("sm_mhz") else None)}
-    # decode GEMM: 2 M N K flops with M = 2 (band + halo rows), N = C, K = 2 Dp
+    # decode GEMM (`gemm` sub-line): 2 M N K flops with M = 2 (band + halo rows), N = C, K = 2 Dp; timed per
+    # launch (~0.2 ms) inside a short loop: its denominator is the BURST tensor peak (also vs sustained)
     ra, rb = decoded_rows(R, r0, r1, h)
     Dp = (D + 31) // 32 * 32
     flops = 2.0 * (2 * (rb - ra)) * C * (2 * Dp)
     gemm_tf = flops / (gemm_ms * 1e-3) / 1e12
-    traffic = load_ncu_traffic()
-    dominant = "encode" if shares.get("encode", 0) >= shares.get("decode_gemm", 0) else "decode_gemm"
-    # the GEMM is timed per launch (~0.2 ms) inside a short loop, not a seconds-long run:
-    # its denominator is the BURST tensor peak (also reported against sustained)
+    gemm_bf16_tf = flops / (gemm_bf16_ms * 1e-3) / 1e12
     gemm_roof = {"kernel": "k_decode_gemm2", "bound": "tensor", "achieved": round(gemm_tf, 1),
                  "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(gemm_tf / pk["bf16_tflops"], 4),
                  "frac_of_sustained": round(gemm_tf / pk["bf16_tflops_sustained"], 4),
                  "traffic": traffic.get("decode_gemm"),
                  "peak_basis": f"MEASURED_PEAKS.json ({pk_kind}) bf16 burst (fp16 dense = bf16 dense)"}
+    # NUFFT decode transforms: FFT work by the conventional 5 N log2 N flops per N-point transform
+    # (FFTW's accounting: the pruned first / last passes are counted as full), against the FP32 peak
+    # (148 SMs x 128 lanes x 2 flops (FMA) per clock at the max SM clock: DESIGN.md section 6b)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6
+    r_ext = rb - ra
+    logx = max(8, math.ceil(math.log2(2 * C)))
+    logy = max(8, math.ceil(math.log2(2 * r_ext)))
+    Wx = 2 * (math.ceil(res * (1 << logx) / (2 * l)) + 6) + 1
+
+    def fft_line(kernel, name, n_tr, logn):
+        ms = avg(prof, name)
+        fl = n_tr * 5.0 * (1 << logn) * logn
+        return {"kernel": kernel, "bound": "alu", "achieved": round(fl / (ms * 1e-3) / 1e12, 3),
+                "peak": round(fp32_peak / 1e12, 2), "unit": "TFLOP/s", "frac": round(fl / (ms * 1e-3) / fp32_peak, 4),
+                "traffic": traffic.get(name), "ms": round(ms, 5), "transforms": int(n_tr), "n": 1 << logn,
+                "peak_basis": "FP32 FMA peak: 148 SM x 128 lanes x 2 flop x max SM clock (guide unit counts); "
+                              "work = 5 N log2 N per transform (conventional FFT flop count)"}
+    nd_lines = {"nd_rowfft": fft_line("k_nd_rowfft (x transforms of the decoded rows + Born rule / H_b epilogue)",
+                                      "nd_rowfft", r_ext, logx),
+                "nd_colfft": fft_line("k_nd_colfft (y transforms of the band columns)", "nd_colfft", Wx, logy),
+                "nd_spread": {"kernel": "k_nd_strength + k_nd_spread", "ms": round(avg(prof, "nd_spread"), 5)}}
+    nufft_dec = prof["nd_rowfft"][1] > 0
     enc_line = alu_line(enc_rate)
     enc_direct = None
     if nufft:
         # the type-3 NUFFT encode is several short memory/latency-bound kernels, none an ALU
         # roofline: report its rate in phasor-equivalents (N x D / time) against the direct
-        # method's ceilings; the dominant single kernel is the decode GEMM
+        # method's ceilings
         enc_line = {"kernel": "type-3 NUFFT (k_nu_bin, k_nu_scan, k_nu_place, k_nu_spread_tiles, k_nu_rowfft, "
                               "k_nu_colfft, k_nu_interp, k_encode_pairs1<outliers>)",
-                    "bound": "latency / shared memory (no ALU roofline applies)", "ms": round(enc_ms, 4),
+                    "bound": "latency / shared memory (no single-kernel roofline)", "ms": round(enc_ms, 4),
                     "phasor_equivalents_per_s": round(enc_rate, 1),
                     "x_direct_pair_lp_ceiling": round(enc_rate / enc_roof["combined"], 3),
                     "x_direct_measured_loop_ceiling": (round(enc_rate / enc_roof["measured"]["value"], 3)
                                                        if enc_roof["measured"] else None),
                     "x_mufu_only_single_point": round(enc_rate / enc_roof["mufu_only_single"], 3)}
-        dominant = "decode_gemm"
         enc_direct = dict(alu_line(direct_pts * D / (enc_direct_ms * 1e-3)), ms=round(enc_direct_ms, 4),
                           note="direct pair encode (enc_method 0) of the same batches, serial, timed alone")
-    roofline = enc_line if dominant == "encode" else gemm_roof
-    gemm_bf16_ms = avg(prof_bf16, "decode_gemm")
-    gemm_bf16_tf = flops / (gemm_bf16_ms * 1e-3) / 1e12
+    # the dominant single kernel of the step (launch list, profiles/): the decode's row transform
+    # when the NUFFT decodes, else the GEMM; the direct encode when it is the encode method
+    if nufft_dec:
+        roofline = dict(nd_lines["nd_rowfft"], note="dominant single kernel of the step (ncu launch list, profiles/)")
+    else:
+        roofline = gemm_roof
+    if not nufft and enc_ms > max(avg(prof, "nd_rowfft") if nufft_dec else 0.0, gemm_ms if not nufft_dec else 0.0):
+        roofline = enc_line
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "f16 MMA operands, fp32 accumulate (decode); encode: " + (
-            "type-3 NUFFT (fp32 FFT, 32.32 fixed-point spreading, fp64 phases)" if nufft else "fp32 phases / sincos / sums"),
+        "dtype": ("f32 (decode: type-1 NUFFT, fp32 spreading + FFTs; encode: type-3 NUFFT, fp32 FFT, 32.32 "
+                  "fixed-point spreading, fp64 phases)" if nufft_dec else
+                  "f16 MMA operands, fp32 accumulate (decode); encode: fp32"),
         "data": "synthetic", "config": dict(workload_config(sc, n_mean, world), **({"tuning": args.tuning} if args.tuning else {})),
         "points_bundled_per_s": round(n_mean / (ms_per_step * 1e-3), 1),
         "decode_cells_per_s_gemm_only": round(cells / (gemm_ms * 1e-3), 1),
         "decode_pct_tensor_peak": round(100 * gemm_tf / pk["bf16_tflops"], 2),
-        "roofline": roofline, "decode_roofline": gemm_roof, "encode_roofline": enc_line,
-        "encode_direct_roofline": enc_direct,
-        "schedule": "pipelined: encode of batch k+1 (low-priority stream) overlaps the GEMM + entropy of batch k",
+        "roofline": roofline, "decode_roofline": gemm_roof, "decode_nufft_rooflines": nd_lines,
+        "encode_roofline": enc_line, "encode_direct_roofline": enc_direct,
+        "schedule": "pipelined: encode of batch k+1 (low-priority stream) overlaps the decode + entropy of batch k",
         "serial": {"ms_per_step": round(serial_ms_per_step, 4), "value": round(cells / (serial_ms_per_step * 1e-3), 1),
                    "note": "one stream, L2 flushed between steps; kernel_ms_per_step and the rooflines are from here"},
+        "gemm": {"ms_per_step": round(g16_ms_per_step, 4), "value": round(cells / (g16_ms_per_step * 1e-3), 1),
+                 "unit": "cells/s", "steps": kb, "decode_gemm_ms": round(gemm_ms, 5), "table_A_ms": round(tabA_ms, 5),
+                 "decode_tflops": round(gemm_tf, 1), "frac_of_burst": round(gemm_tf / pk["bf16_tflops"], 4),
+                 "note": "serial loop with the tcgen05 GEMM decode (dec_method 0, f16 operands, fp32 accumulate) "
+                         "in place of the NUFFT; parity bound 1e-3 (north_star)"},
         "bf16": {"ms_per_step": round(bf16_ms_per_step, 4), "value": round(cells / (bf16_ms_per_step * 1e-3), 1),
                  "unit": "cells/s", "steps": kb, "decode_gemm_ms": round(gemm_bf16_ms, 5),
                  "decode_tflops": round(gemm_bf16_tf, 1), "frac_of_burst": round(gemm_bf16_tf / pk["bf16_tflops"], 4),
-                 "note": "serial loop, bf16 decode operands (fp32 accumulate); parity bound 2e-2 (north_star)"},
+                 "note": "serial loop, GEMM decode with bf16 operands (fp32 accumulate); parity bound 2e-2 (north_star)"},
         "allreduce_us": round(1e3 * ar_median, 2) if world > 1 else None,
         "allreduce_bytes": (2 * 2 * Dp + 2) * 8,
         "kernel_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in prof.items()},
@@ -558,12 +602,14 @@ def run_c5(args, world, rank, dev, barrier, max_over_ranks):
     tot = sum(a.elapsed_time(b) for a, b in evs)
     ar_med = statistics.median([a.elapsed_time(b) for a, b in ar]) if world > 1 else 0.0
     enc_ms = (prof["encode"][0] + prof["reduce"][0]) / K
+    dec_ms = sum(prof[k][0] for k in ("norms", "table_B", "table_A", "decode_gemm", "nd_spread", "nd_colfft",
+                                      "nd_rowfft")) / K
     gemm_ms = prof["decode_gemm"][0] / K
-    tot, ar_med, enc_max, gemm_max = max_over_ranks([tot, ar_med, enc_ms, gemm_ms])
+    tot, ar_med, enc_max, dec_max = max_over_ranks([tot, ar_med, enc_ms, dec_ms])
     ms = tot / K
     ra, rb = decoded_rows(R, r0, r1, h)
     Dp = (D + 31) // 32 * 32
-    gemm_tf = 2.0 * (2 * (rb - ra)) * C * (2 * Dp) / (gemm_ms * 1e-3) / 1e12
+    gemm_tf = 2.0 * (2 * (rb - ra)) * C * (2 * Dp) / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     pk, _ = peaks()
     return {
         "workload": "C5: 10M labelled points (occupied:free ~ 1:2) bundled at D=16384 (points sharded), one "
@@ -571,12 +617,14 @@ def run_c5(args, world, rank, dev, barrier, max_over_ranks):
         "n_points": n, "cells": R * C, "steps": K, "ms_per_step": round(ms, 4),
         "value": round(R * C / (ms * 1e-3), 1), "unit": "cells/s",
         "points_bundled_per_s": round(n / (ms * 1e-3), 1),
-        "encode_ms": round(enc_max, 4), "decode_gemm_ms": round(gemm_max, 4),
-        "decode_tflops_rank0": round(gemm_tf, 1), "decode_frac_of_burst_rank0": round(gemm_tf / pk["bf16_tflops"], 4),
+        "encode_ms": round(enc_max, 4), "decode_ms": round(dec_max, 4),
+        "decode_method": "gemm" if gemm_ms > 0 else "nufft",
+        "decode_tflops_rank0": round(gemm_tf, 1) if gemm_tf else None,
+        "decode_frac_of_burst_rank0": round(gemm_tf / pk["bf16_tflops"], 4) if gemm_tf else None,
         "allreduce_us": round(1e3 * ar_med, 2) if world > 1 else None,
         "kernel_ms_per_step_rank0": {k: round(v[0] / K, 5) for k, v in prof.items()},
         "scaling": "strong", "timing": "CUDA events per step, max over ranks; no L2 flush (per-step working set "
-                                      "> 1 GB: table B 262 MB, table A 66-525 MB, H_b 16-128 MB, partials)",
+                                      "> 126 MB: the 10M points 90 MB, H_b 16-128 MB, transform intermediates)",
     }
 
 

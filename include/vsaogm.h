@@ -276,8 +276,10 @@ int vsaogm_get_phases(vsaogm_ctx *ctx, double *host);
 #define VSAOGM_K_TABLE_A 5
 #define VSAOGM_K_DECODE_GEMM 6
 #define VSAOGM_K_ENTROPY 7
-#define VSAOGM_K_DECODE_NUFFT 8   /* the NUFFT decode: spread + two transforms (nudecode.cu) */
-#define VSAOGM_NKERNELS 9
+#define VSAOGM_K_ND_SPREAD 8   /* NUFFT decode: point strengths + Gaussian gather (nudecode.cu) */
+#define VSAOGM_K_ND_COLFFT 9   /* NUFFT decode: transforms along y of the band columns */
+#define VSAOGM_K_ND_ROWFFT 10  /* NUFFT decode: transforms along x of the decoded rows + epilogue */
+#define VSAOGM_NKERNELS 11
 int vsaogm_profile_enable(vsaogm_ctx *ctx, int enable);
 int vsaogm_profile_read(vsaogm_ctx *ctx, double *ms, int64_t *launches);
 

@@ -116,7 +116,8 @@ __device__ __forceinline__ void fft_last_r4(const float2 *a, const float2 *__res
 // passes with the 16 values of a butterfly in registers (16 = 4 x 4, the quarter turns exact), a
 // first pass of radix 2^(LOGN mod 4) when LOGN is not a multiple of 4; the first pass reads its
 // inputs through load(j) (global memory, zero padding inside load), the last pass hands its
-// outputs to store(m, G_m) from registers, and the passes between exchange through ONE shared
+// outputs to store(i, m, G_m) from registers (i = the output's compile-time index within the thread's
+// last-pass outputs, b R + q, for per-thread tables the caller keeps in registers), and the passes between exchange through ONE shared
 // buffer of N + N/16 values (pad(i) = i + i/16 makes every pass's reads and writes conflict-free
 // for 8-byte values).  T = max(32, N / 16) threads: one radix-16 butterfly per thread and pass.
 // Twiddles e^{+2 pi i k / (R Ns)} from the universal table (tw[p - 1 + k] = e^{i pi k / p}), their
@@ -273,7 +274,7 @@ __device__ __forceinline__ void twiddle(float2 *x, float2 w)
 
 // one radix-R pass on sub-transforms of length NS: butterfly j < N / R, k = j mod NS,
 // x_r = in[j + r N / R] w^{r k} (w = e^{2 pi i / (R NS)}), y = DFT_R(x), out[(j - k) R + k + q NS] = y_q.
-// SRC 0: load(i); 1: shared buf.  DST 0: shared buf; 1: store(m, y).  NZ (first pass, R = 16): the
+// SRC 0: load(i); 1: shared buf.  DST 0: shared buf; 1: store(b R + q, m, y).  NZ (first pass, R = 16): the
 // inputs of groups r >= NZ are zero padding (not loaded).  ENDS (last pass, R = 16): only the
 // outputs q < 4 and q >= 12 (|m| < N / 4, the centred modes) are formed and stored.
 template <int LOGN, int R, int NS, int T, int SRC, int DST, int NZ, bool ENDS, class Load, class Store>
@@ -283,6 +284,10 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
     constexpr int NB = N / R;                         // butterflies
     constexpr int PER = (NB + T - 1) / T;            // per thread
     float2 x[PER][R];
+    float2 wb[PER];                                   // twiddle bases, loaded before the data (latency overlap)
+#pragma unroll
+    for (int b = 0; b < PER; ++b)
+        wb[b] = NS > 1 ? __ldg(tw + R * NS / 2 - 1 + ((threadIdx.x + b * T) & (NS - 1))) : make_float2(1.f, 0.f);
 #pragma unroll
     for (int b = 0; b < PER; ++b) {
         const int j = threadIdx.x + b * T;
@@ -299,7 +304,7 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
         const int j = threadIdx.x + b * T;
         if (NB % T == 0 || j < NB) {
             const int k = j & (NS - 1);
-            if (NS > 1) twiddle<R>(x[b], __ldg(tw + R * NS / 2 - 1 + k));
+            if (NS > 1) twiddle<R>(x[b], wb[b]);
             if constexpr (R == 16) dft_ab<4, 4, NZ, ENDS>(x[b]);
             else Dft<R>::run(x[b]);
             const int o = (j - k) * R + k;
@@ -307,7 +312,7 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
             for (int q = 0; q < R; ++q) {
                 if (ENDS && q >= 4 && q < 12) continue;
                 if (DST == 0) buf[pad(o + q * NS)] = x[b][q];
-                else store(o + q * NS, x[b][q]);
+                else store(b * R + q, o + q * NS, x[b][q]);
             }
         }
     }

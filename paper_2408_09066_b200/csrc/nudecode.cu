@@ -31,7 +31,7 @@
 //
 // Kernels (one decode): k_nd_spread (block = 16 x 16 tile of the band grid; gathers the points of
 // the 3 x 3 neighbouring bins in a fixed host-sorted order: deterministic, no atomics),
-// k_nd_colfft (block = one band column), k_nd_rowfft (block = ND_RB decoded rows).  The binning
+// k_nd_colfft (persistent over band columns), k_nd_rowfft (persistent over decoded rows).  The binning
 // of the 2 D points depends only on theta and the grid geometry: it is built on the host once per
 // geometry (a plan) and cached.
 #include <math.h>
@@ -49,7 +49,6 @@ constexpr int ND_BS = 8;           // point bin side (cells)
 constexpr int ND_CH = 64;          // points staged per chunk in the spread kernel
 constexpr double ND_MSP = 5.0;     // Gaussian width parameter (accuracy ~1e-6)
 constexpr int ND_MARGIN = 6;       // band half-width beyond max |xi| / h (cells)
-constexpr int ND_RB = 4;           // decoded rows per row-transform block
 constexpr int ND_LOGN_MAX = 13;    // shared-memory transforms up to 8192 points
 constexpr double kPi = 3.14159265358979323846;
 
@@ -193,24 +192,37 @@ __device__ __forceinline__ float2 cmulf(float2 a, float2 b)
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// transform along y of band column ux (fftr::fft: register radix-16 passes); output rows r in
-// [0, r_ext) (r' = r - rc, the centred modes |r'| < M / 4), times Py[r]
+// transforms along y of the band columns (fftr::fft: register radix-16 passes), persistent over
+// columns ux = blockIdx.x, += gridDim.x; output rows r in [0, r_ext) (r' = r - rc, the centred modes
+// |r'| < M / 4), times Py[r] (each thread's rows are fixed: their factors are loaded once)
 template <int LOGN, int T, int NZ>
-__global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(const float2 *__restrict__ Gt, int Wy, const float2 *__restrict__ tw,
-                                                 const float2 *__restrict__ Py, int r_ext, int rc, int ldt,
-                                                 float2 *__restrict__ Tt)
+__global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(const float2 *__restrict__ Gt, int Wx, int Wy,
+                                                                           const float2 *__restrict__ tw,
+                                                                           const float2 *__restrict__ Py, int r_ext, int rc,
+                                                                           int ldt, float2 *__restrict__ Tt)
 {
-    constexpr int N = 1 << LOGN;
+    constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
-    const int ux = blockIdx.x;
-    const float2 *in = Gt + (size_t)ux * Wy;
-    float2 *out = Tt + (size_t)ux * ldt;
-    fftr::fft<LOGN, T, NZ, true>(
-        sm_fft, tw, [&](int j) { return j < Wy ? __ldg(in + j) : make_float2(0.f, 0.f); },
-        [&](int m, float2 v) {
-            const int r = rc + (m < N / 2 ? m : m - N);
-            if (r >= 0 && r < r_ext) out[r] = cmulf(__ldg(Py + r), v);
-        });
+    const int j = threadIdx.x;
+    float2 py[16];
+    int rq[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int m = j + q * NS;
+        const int r = rc + (m < N / 2 ? m : m - N);
+        rq[q] = (j < NS && (q < 4 || q >= 12) && r >= 0 && r < r_ext) ? r : -1;
+        py[q] = rq[q] >= 0 ? __ldg(Py + r) : make_float2(0.f, 0.f);
+    }
+    for (int ux = blockIdx.x; ux < Wx; ux += gridDim.x) {
+        const float2 *in = Gt + (size_t)ux * Wy;
+        float2 *out = Tt + (size_t)ux * ldt;
+        __syncthreads();   // the previous column's transform consumed the buffer
+        fftr::fft<LOGN, T, NZ, true>(
+            sm_fft, tw, [&](int i) { return i < Wy ? __ldg(in + i) : make_float2(0.f, 0.f); },
+            [&](int q, int, float2 v) {
+                if (rq[q] >= 0) out[rq[q]] = cmulf(py[q], v);
+            });
+    }
 }
 
 struct NdEpi {
@@ -259,36 +271,35 @@ __device__ __forceinline__ void nd_store(const NdEpi &e, int row, int col, float
     }
 }
 
-// transform along x of ND_RB decoded rows (staged from the column-transformed Tt[ux][r]);
-// outputs j in [0, cols) (j' = j - jc), times Px[j], then the epilogue
+// transforms along x of the decoded rows, persistent over rows row = blockIdx.x, += gridDim.x; the
+// first pass reads the column-transformed Tt[ux][row] (strided: neighbouring rows, on other blocks,
+// share the sectors in L2); outputs j in [0, cols) (j' = j - jc), times Px[j] (each thread's
+// columns are fixed: their factors are loaded once), then the epilogue
 template <int LOGN, int T, int NZ>
 __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(const float2 *__restrict__ Tt, int ldt, int Wx,
-                                                 const float2 *__restrict__ tw, const float2 *__restrict__ Px,
-                                                 int cols, int jc, const NdEpi e)
+                                                                           const float2 *__restrict__ tw,
+                                                                           const float2 *__restrict__ Px, int cols, int jc,
+                                                                           const NdEpi e)
 {
-    constexpr int N = 1 << LOGN;
+    constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
-    float2 *stage = sm_fft + N + N / 16;   // [ND_RB][Wx]
-    const int r0 = blockIdx.x * ND_RB;
-    const int nr = min(ND_RB, e.r_ext - r0);
     const bool live0 = e.mscale[0] != 0.0, live1 = e.mscale[1] != 0.0;
-    for (int ux = threadIdx.x; ux < Wx; ux += T) {
-        const float4 *src = reinterpret_cast<const float4 *>(Tt + (size_t)ux * ldt + r0);   // ldt, r0: multiples of 4
-        const float4 v0 = __ldg(src), v1 = __ldg(src + 1);
-        stage[ux] = make_float2(v0.x, v0.y);
-        stage[Wx + ux] = make_float2(v0.z, v0.w);
-        stage[2 * Wx + ux] = make_float2(v1.x, v1.y);
-        stage[3 * Wx + ux] = make_float2(v1.z, v1.w);
+    const int j = threadIdx.x;
+    float2 px[16];
+    int cq[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int m = j + q * NS;
+        const int col = jc + (m < N / 2 ? m : m - N);
+        cq[q] = (j < NS && (q < 4 || q >= 12) && col >= 0 && col < cols) ? col : -1;
+        px[q] = cq[q] >= 0 ? __ldg(Px + col) : make_float2(0.f, 0.f);
     }
-    for (int rr = 0; rr < nr; ++rr) {
-        __syncthreads();   // staging done / the previous row's transform consumed
-        const float2 *srow = stage + rr * Wx;
-        const int row = r0 + rr;
+    for (int row = blockIdx.x; row < e.r_ext; row += gridDim.x) {
+        __syncthreads();   // the previous row's transform consumed the buffer
         fftr::fft<LOGN, T, NZ, true>(
-            sm_fft, tw, [&](int j) { return j < Wx ? srow[j] : make_float2(0.f, 0.f); },
-            [&](int m, float2 v) {
-                const int col = jc + (m < N / 2 ? m : m - N);
-                if (col >= 0 && col < cols) nd_store(e, row, col, cmulf(__ldg(Px + col), v), live0, live1);
+            sm_fft, tw, [&](int i) { return i < Wx ? __ldg(Tt + (size_t)i * ldt + row) : make_float2(0.f, 0.f); },
+            [&](int q, int, float2 v) {
+                if (cq[q] >= 0) nd_store(e, row, cq[q], cmulf(px[q], v), live0, live1);
             });
     }
 }
@@ -345,7 +356,6 @@ bool nd_geometry(const vsaogm_ctx *c, double x0, double y0, double res, int cols
     P.Wx = 2 * P.Bx + 1;
     P.Wy = 2 * P.By + 1;
     if (P.Wx > P.Mx / 2 || P.Wy > P.My / 2) return false;   // band wider than the zero-padded half
-    if (((size_t)P.Mx + P.Mx / 16 + (size_t)ND_RB * P.Wx) * sizeof(float2) > 227 * 1024) return false;   // row-transform smem
     P.nbx = (P.Wx + ND_BS - 1) / ND_BS;   // point bins
     P.nby = (P.Wy + ND_BS - 1) / ND_BS;
     P.ntx = (P.Wx + ND_TS - 1) / ND_TS;   // spread tiles
@@ -480,15 +490,25 @@ int nz_of(int W, int logn)
     return g <= 3 ? 3 : g <= 4 ? 4 : 8;
 }
 
+template <typename K>
+int persistent_grid(vsaogm_ctx *c, K kernel, int T, size_t smem, int work)
+{
+    int per_sm = 0;
+    VSA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, T, smem));
+    return std::max(1, std::min(work, c->num_sms * std::max(1, per_sm)));
+}
+
 template <int LOGN, int NZ>
 int launch_colfft_nz(vsaogm_ctx *c, const NdPlan &P)
 {
     constexpr int N = 1 << LOGN;
     constexpr int T = N / 16 < 32 ? 32 : N / 16;
     const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
-    VSA_CUDA_TRY(cudaFuncSetAttribute(k_nd_colfft<LOGN, T, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_nd_colfft<LOGN, T, NZ><<<P.Wx, T, smem, c->stream>>>((const float2 *)c->d_nd_G, P.Wy, (const float2 *)c->d_nd_tw,
-                                                           P.d_Py, P.r_ext, P.rc, P.ldt, (float2 *)c->d_nd_T);
+    auto kern = k_nd_colfft<LOGN, T, NZ>;
+    VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = persistent_grid(c, kern, T, smem, P.Wx);
+    kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_G, P.Wx, P.Wy, (const float2 *)c->d_nd_tw, P.d_Py,
+                                       P.r_ext, P.rc, P.ldt, (float2 *)c->d_nd_T);
     return VSAOGM_OK;
 }
 
@@ -497,10 +517,12 @@ int launch_rowfft_nz(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
 {
     constexpr int N = 1 << LOGN;
     constexpr int T = N / 16 < 32 ? 32 : N / 16;
-    const size_t smem = ((size_t)(N + N / 16) + (size_t)ND_RB * P.Wx) * sizeof(float2);
-    VSA_CUDA_TRY(cudaFuncSetAttribute(k_nd_rowfft<LOGN, T, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_nd_rowfft<LOGN, T, NZ><<<(P.r_ext + ND_RB - 1) / ND_RB, T, smem, c->stream>>>(
-        (const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw, P.d_Px, P.cols, P.jc, e);
+    const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
+    auto kern = k_nd_rowfft<LOGN, T, NZ>;
+    VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = persistent_grid(c, kern, T, smem, P.r_ext);
+    kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw, P.d_Px,
+                                       P.cols, P.jc, e);
     return VSAOGM_OK;
 }
 
@@ -557,7 +579,7 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     if ((rc = nd_grow(&c->d_nd_T, &c->nd_T_cap, (size_t)P->Wx * P->ldt * sizeof(float2)))) return rc;
     if ((rc = nd_grow(&c->d_nd_st, &c->nd_st_cap, 2 * (size_t)c->D * sizeof(float2)))) return rc;
     cudaEvent_t ev;
-    vsa_prof_begin(c, VSAOGM_K_DECODE_NUFFT, &ev);
+    vsa_prof_begin(c, VSAOGM_K_ND_SPREAD, &ev);
     const int npts = 2 * c->D;
     k_nd_strength<<<(npts + 255) / 256, 256, 0, c->stream>>>(P->d_kid, npts, c->D, c->Dp, (const double2 *)c->d_m,
                                                             c->d_norm2 + c->nslots, 1.0 / c->D, c->d_tx_turns,
@@ -577,6 +599,8 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     sp.Gt = (float2 *)c->d_nd_G;
     k_nd_spread<<<dim3(P->ntx, P->nty), 256, 0, c->stream>>>(sp);
     VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_ND_SPREAD, ev);
+    vsa_prof_begin(c, VSAOGM_K_ND_COLFFT, &ev);
     switch (P->logy) {
     case 8: rc = launch_colfft<8>(c, *P); break;
     case 9: rc = launch_colfft<9>(c, *P); break;
@@ -587,6 +611,8 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     }
     if (rc) return rc;
     VSA_CUDA_TRY(cudaGetLastError());
+    vsa_prof_end(c, VSAOGM_K_ND_COLFFT, ev);
+    vsa_prof_begin(c, VSAOGM_K_ND_ROWFFT, &ev);
     NdEpi e;
     e.mscale = c->d_norm2 + c->nslots;
     e.hb = hb;
@@ -607,7 +633,7 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     }
     if (rc) return rc;
     VSA_CUDA_TRY(cudaGetLastError());
-    vsa_prof_end(c, VSAOGM_K_DECODE_NUFFT, ev);
+    vsa_prof_end(c, VSAOGM_K_ND_ROWFFT, ev);
     c->launches += 4;
     return VSAOGM_OK;
 }

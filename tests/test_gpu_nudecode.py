@@ -58,7 +58,7 @@ def test_c2_full_grid_both_methods(method):
     mp = Mapper(D, 0, l, sc.bounds)
     mp.encode_bundle(_cuda(xy), _cuda(lab))
     qg, prof = _decode(mp, 0, 0, res, R, C, 0, R, 0, method)
-    ran = "decode_nufft" if method == 1 else "decode_gemm"
+    ran = "nd_rowfft" if method == 1 else "decode_gemm"
     assert prof[ran][1] >= 1
     S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
     L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
@@ -107,7 +107,7 @@ def test_nudecode_geometries(geom):
     mp = Mapper(D, 0, l, bounds)
     mp.encode_bundle(_cuda(xy), _cuda(lab))
     qg, prof = _decode(mp, x0, y0, res, R, C, r0, r1, halo, 1)
-    assert prof["decode_nufft"][1] >= 1
+    assert prof["nd_rowfft"][1] >= 1
     mp.close()
     tx, ty = oracle.theta(0, D)
     mo, _, _ = oracle.encode(tx, ty, l, xy, lab)
@@ -170,7 +170,7 @@ def test_nudecode_c1_falls_back_to_gemm():
     mp.encode_bundle(_cuda(xy), _cuda(lab))
     qg, prof = _decode(mp, 0, 0, res, R, C, 0, R, 0, 1)
     mp.close()
-    assert prof["decode_gemm"][1] >= 1 and prof["decode_nufft"][1] == 0
+    assert prof["decode_gemm"][1] >= 1 and prof["nd_rowfft"][1] == 0
     tx, ty = oracle.theta(0, D)
     mo, _, _ = oracle.encode(tx, ty, l, xy, lab)
     qo = oracle.decode_grid(tx, ty, l, mo, 0, 0, res, 0, R, 0, C)

@@ -95,6 +95,7 @@ def test_decode_band_split_k_matches_unsplit():
     xy, lab = sc.all_points()
     D, l, h, R, C, res = 2048, 0.25, 2, 2000, 2000, 0.02
     mp = _mapper(D, l, sc.bounds)
+    mp.set_tuning("dec_method", 0)   # the GEMM's split-K (the NUFFT decode has no split)
     mp.encode_bundle(*_cuda(xy, lab))
     out = []
     for s in (None, "1"):
@@ -576,6 +577,7 @@ def test_gemm_phasor_tiles_on_the_fly(delta, prec):
     D, l, h, R, C, res = cfg["D"], cfg["l"], cfg["half"], cfg["rows"], 333, cfg["res"]
     tau = label_tau(D)
     mp = Mapper(D, 0, l, sc.bounds, delta=delta)
+    mp.set_tuning("dec_method", 0)   # both variants of the GEMM decode
     mp.encode_bundle(*_cuda(xy, lab))
     outs = {}
     for agen in (0, 1):

@@ -99,8 +99,9 @@ def _check_windows(qg, Lg, row_off, tx, ty, l, mo, res, R, C, h, tau, centres, p
 # ------------------------------------------------------------------ C3
 
 def test_c3_full_size_fp16_bf16():
-    """C3 (2.04M points, D=4096, 1000x1000 grid, 5x5): full GPU decode in fp16 and bf16 operands;
-    memories vs the oracle's full encode, q on >= 250k window cells, labels on >= 12k centres."""
+    """C3 (2.04M points, D=4096, 1000x1000 grid, 5x5): full GPU decode by the tcgen05 GEMM in fp16
+    and bf16 operands and by the NUFFT (dec_method 1); memories vs the oracle's full encode, q on
+    >= 250k window cells, labels on >= 12k centres."""
     from paper_2408_09066_b200 import Mapper
     sc = Scenario("C3")
     cfg = sc.cfg
@@ -110,13 +111,18 @@ def test_c3_full_size_fp16_bf16():
     mp = Mapper(D, 0, l, sc.bounds)
     mp.encode_bundle(*_cuda(xy, lab))
     out = {}
-    for prec in (0, 1):
+    for key, (method, prec) in {"f16": (0, 0), "bf16": (0, 1), "nufft": (1, 0)}.items():
+        mp.set_tuning("dec_method", method)
+        mp.profile_enable(True)
         q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
         mp.decode(0.0, 0.0, res, R, C, 0, R, h, precision=prec, q_out=q)
         L = torch.empty((R, C), dtype=torch.uint8, device="cuda")
         mp.entropy(h, h, tau, -tau, 0, None, L)
         assert mp.sync() == 0
-        out[prec] = (q.cpu().numpy().astype(np.float64), L.cpu().numpy())
+        prof = mp.profile_read()
+        mp.profile_enable(False)
+        assert prof["nd_rowfft" if method else "decode_gemm"][1] == 1
+        out[key] = (q.cpu().numpy().astype(np.float64), L.cpu().numpy())
     mg, cg = mp.get_memory()
     mp.close()
     tx, ty = oracle.theta(0, D)
@@ -125,16 +131,20 @@ def test_c3_full_size_fp16_bf16():
     assert _mem_err(mg, mo) <= M_TOL
     centres = _centres(np.random.default_rng(3), xy, res, R, C)
     assert len(centres) >= 12_000
-    e16, a16, n16 = _check_windows(*out[0], 0, tx, ty, l, mo, res, R, C, h, tau, centres)
-    ebf, abf, _ = _check_windows(*out[1], 0, tx, ty, l, mo, res, R, C, h, tau, centres)
+    e16, a16, n16 = _check_windows(*out["f16"], 0, tx, ty, l, mo, res, R, C, h, tau, centres)
+    ebf, abf, _ = _check_windows(*out["bf16"], 0, tx, ty, l, mo, res, R, C, h, tau, centres)
+    enu, anu, _ = _check_windows(*out["nufft"], 0, tx, ty, l, mo, res, R, C, h, tau, centres)
     print(f"C3: fp16 q err {e16:.2e} labels {a16:.5f} ({n16} q cells, {len(centres)} centres); "
-          f"bf16 q err {ebf:.2e} labels {abf:.5f}")
+          f"bf16 q err {ebf:.2e} labels {abf:.5f}; NUFFT q err {enu:.2e} labels {anu:.5f}")
     assert n16 >= 250_000
     assert e16 <= Q_TOL[0], e16
     assert ebf <= Q_TOL[1], ebf
+    assert enu <= 5e-5, enu
     assert a16 >= LABEL_BAR, a16
+    assert anu >= LABEL_BAR, anu
     assert abf >= 0.995, abf          # bf16: reported separately (north_star); SURVEY A.3 predicts >= 0.9992
-    assert (out[0][1] == out[1][1]).mean() >= 0.999
+    assert (out["f16"][1] == out["bf16"][1]).mean() >= 0.999
+    assert (out["f16"][1] == out["nufft"][1]).mean() >= 0.999
 
 
 # ------------------------------------------------------------------ C4 streaming (bench schedule)
