@@ -29,16 +29,20 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
-SHORT = {"k_encode_pairs": "encode", "k_encode_bundle": "encode", "k_decode_gemm": "decode_gemm",
+SHORT = {"k_nu_": None, "k_nd_": None, "k_encode_pairs": "encode", "k_encode_bundle": "encode", "k_decode_gemm": "decode_gemm",
          "k_entropy": "entropy",
          "k_table<__half2, 1>": "table_A", "k_table<__nv_bfloat162, 1>": "table_A",
          "k_table<__half2, 0>": "table_B", "k_table<__nv_bfloat162, 0>": "table_B",
-         "k_reduce_partials": "reduce", "k_commit_norms": "norms", "k_commit": "commit"}
+         "k_reduce_partials": "reduce", "k_commit_norms": "norms", "k_commit": "commit",
+         "k_nu_spread_tiles": "nu_spread", "k_nu_rowfft": "nu_rowfft", "k_nu_colfft": "nu_colfft",
+         "k_nu_interp": "nu_interp", "k_nu_bin": "nu_bin", "k_nu_scan": "nu_scan", "k_nu_place": "nu_place",
+         "k_nd_spread": "nd_spread", "k_nd_strength": "nd_strength", "k_nd_colfft": "nd_colfft",
+         "k_nd_rowfft": "nd_rowfft"}
 
 
 def short(name):
     for k, v in SHORT.items():
-        if k in name:
+        if v is not None and k in name:
             return v
     return name[:60]
 
@@ -91,7 +95,16 @@ def main(tag):
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     out = os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md")
     open(out, "w").write("\n".join(lines) + "\n")
-    json.dump({"tag": tag, **traffic}, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    # merge: kernels not in this capture keep the figure (and the tag) of the capture they came from
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    old = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    tags = old.get("tags", {k: old.get("tag", "?") for k in old if k not in ("tag", "tags")})
+    merged = {k: v for k, v in old.items() if k not in ("tag", "tags") and not k.startswith(("<unnamed>", "void "))}
+    for k, v in traffic.items():
+        merged[k] = v
+        tags[k] = tag
+    tags = {k: t for k, t in tags.items() if k in merged}
+    json.dump({"tag": tag, "tags": tags, **merged}, open(tpath, "w"), indent=1)
     print(out)
 
 
