@@ -115,7 +115,8 @@ __device__ __forceinline__ void fft_last_r4(const float2 *a, const float2 *__res
 // Register-blocked Stockham FFT (the same transform, G_m = sum_j x_j e^{+2 pi i j m / N}): radix-16
 // passes with the 16 values of a butterfly in registers (16 = 4 x 4, the quarter turns exact), a
 // first pass of radix 2^(LOGN mod 4) when LOGN is not a multiple of 4; the first pass reads its
-// inputs through load(j) (global memory, zero padding inside load), the last pass hands its
+// inputs through load(j, slot) (global memory, zero padding inside load; slot = b R + r, the compile-time
+// index of the value within the thread's first-pass inputs, for callers that prefetch them into registers), the last pass hands its
 // outputs to store(i, m, G_m) from registers (i = the output's compile-time index within the thread's
 // last-pass outputs, b R + q, for per-thread tables the caller keeps in registers), and the passes between exchange through ONE shared
 // buffer of N + N/16 values (pad(i) = i + i/16 makes every pass's reads and writes conflict-free
@@ -294,7 +295,7 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
         if (NB % T == 0 || j < NB) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (r < NZ) x[b][r] = SRC == 0 ? load(j + r * NB) : buf[pad(j + r * NB)];
+                if (r < NZ) x[b][r] = SRC == 0 ? load(j + r * NB, b * R + r) : buf[pad(j + r * NB)];
             }
         }
     }

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(co
         float2 *out = Tt + (size_t)ux * ldt;
         __syncthreads();   // the previous column's transform consumed the buffer
         fftr::fft<LOGN, T, NZ, true>(
-            sm_fft, tw, [&](int i) { return i < Wy ? __ldg(in + i) : make_float2(0.f, 0.f); },
+            sm_fft, tw, [&](int i, int) { return i < Wy ? __ldg(in + i) : make_float2(0.f, 0.f); },
             [&](int q, int, float2 v) {
                 if (rq[q] >= 0) out[rq[q]] = cmulf(py[q], v);
             });
@@ -236,18 +236,16 @@ struct NdEpi {
 
 __device__ __forceinline__ float nd_hb_of_p(float p)
 {
-    // binary entropy in bits, 0 log 0 = 0, with MUFU log2: -p log2 p - (1 - p) log2(1 - p).  For
-    // p < 1/16, log(1 - p) = -(p + p^2/2 + ... + p^6/6) (truncation < 1e-8 relative): 1 - p in
-    // fp32 would lose log2(1/p) bits of p, the cancellation log1pf avoids in the GEMM epilogue.
-    float h = 0.f;
-    if (p > 0.f) h = -p * __log2f(p);
-    if (p < 0.0625f) {
-        const float s = p * (1.f + p * (0.5f + p * (0.33333333f + p * (0.25f + p * (0.2f + p * 0.16666667f)))));
-        h += (1.f - p) * s * 1.44269504088896341f;
-    } else if (p < 1.f) {
-        h -= (1.f - p) * __log2f(1.f - p);
-    }
-    return h;
+    // binary entropy in bits of p in [0, 1], 0 log 0 = 0, branch-free with MUFU log2:
+    // -p log2 p + (1 - p) L, L = -log2(1 - p).  For p < 1/32, L = (p + p^2/2 + p^3/3 + p^4/4) / ln 2
+    // (truncation p^5/5: < 6e-8 of H_b): 1 - p in fp32 would lose log2(1/p) bits of p, the
+    // cancellation log1pf avoids in the GEMM epilogue.  The clamps make 0 x log2(0) = 0 x finite.
+    const float lp = __log2f(fmaxf(p, 1e-37f));
+    const float om = 1.f - p;
+    const float ser = p * fmaf(p, fmaf(p, fmaf(p, 0.36067376f, 0.48089835f), 0.72134752f), 1.44269504f);
+    const float lg = -__log2f(fmaxf(om, 1e-37f));
+    const float L = p < 0.03125f ? ser : lg;
+    return fmaf(om, L, -p * lp);
 }
 
 __device__ __forceinline__ uint8_t nd_code8(float p)
@@ -256,26 +254,14 @@ __device__ __forceinline__ uint8_t nd_code8(float p)
     return (uint8_t)min(255, max(0, c));
 }
 
-__device__ __forceinline__ void nd_store(const NdEpi &e, int row, int col, float2 g, bool live0, bool live1)
-{
-    // an empty class decodes to exactly 0 (L8), not to the other class's transform rounding
-    const float qv[2] = {live0 ? g.x : 0.f, live1 ? g.y : 0.f};
-    const int br = row + e.q_off;
-#pragma unroll
-    for (int cls = 0; cls < 2; ++cls) {
-        const float pr = fminf(qv[cls] * qv[cls], 1.f);
-        const size_t o = ((size_t)cls * e.r_ext + row) * e.ldh + col;
-        if (e.code) e.code[o] = nd_code8(pr);
-        else e.hb[o] = nd_hb_of_p(pr);
-        if (e.q && br >= 0 && br < e.band_rows) e.q[((size_t)cls * e.band_rows + br) * e.cols + col] = qv[cls];
-    }
-}
-
 // transforms along x of the decoded rows, persistent over rows row = blockIdx.x, += gridDim.x; the
 // first pass reads the column-transformed Tt[ux][row] (strided: neighbouring rows, on other blocks,
-// share the sectors in L2); outputs j in [0, cols) (j' = j - jc), times Px[j] (each thread's
-// columns are fixed: their factors are loaded once), then the epilogue
-template <int LOGN, int T, int NZ>
+// share the sectors in L2); thread j < N / 16 holds the last pass's outputs m = j + q N / 16, of which
+// the centred ones (q < 4: j' = m, q >= 12: j' = m - N) are columns col0 + off_s, col0 = jc + j,
+// off_s = (s < 4 ? s : s - 8) N / 16, s = 0..7: each thread's columns are fixed (their factors Px are
+// loaded once, their validity is a bit mask) and every store address is one per-row pointer plus a
+// compile-time offset.  FAST: H_b only (no q output, no histogram codes) -- the streaming step.
+template <int LOGN, int T, int NZ, bool FAST>
 __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(const float2 *__restrict__ Tt, int ldt, int Wx,
                                                                            const float2 *__restrict__ tw,
                                                                            const float2 *__restrict__ Px, int cols, int jc,
@@ -283,23 +269,65 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(co
 {
     constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
-    const bool live0 = e.mscale[0] != 0.0, live1 = e.mscale[1] != 0.0;
+    // an empty class decodes to exactly 0 (L8), not to the other class's transform rounding: bit masks
+    const unsigned live0 = e.mscale[0] != 0.0 ? 0xffffffffu : 0u, live1 = e.mscale[1] != 0.0 ? 0xffffffffu : 0u;
     const int j = threadIdx.x;
-    float2 px[16];
-    int cq[16];
+    const int col0 = jc + j;
+    float2 px[8];
+    unsigned ok = 0;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const int m = j + q * NS;
-        const int col = jc + (m < N / 2 ? m : m - N);
-        cq[q] = (j < NS && (q < 4 || q >= 12) && col >= 0 && col < cols) ? col : -1;
-        px[q] = cq[q] >= 0 ? __ldg(Px + col) : make_float2(0.f, 0.f);
+    for (int s = 0; s < 8; ++s) {
+        const int col = col0 + (s < 4 ? s : s - 8) * NS;
+        const bool v = j < NS && col >= 0 && col < cols;
+        px[s] = v ? __ldg(Px + col) : make_float2(0.f, 0.f);
+        ok |= (unsigned)v << s;
+    }
+    const size_t cls_h = (size_t)e.r_ext * e.ldh, cls_q = (size_t)e.band_rows * e.cols;
+    // a pruned radix-16 first pass reads NZ <= 4 values per thread: the next row's are loaded
+    // before this row's passes (the strided loads' latency is hidden behind a whole transform)
+    constexpr bool PF = (LOGN & 3) == 0 && NZ <= 4;
+    auto ld = [&](int i, int row) { return i < Wx ? __ldg(Tt + (size_t)i * ldt + row) : make_float2(0.f, 0.f); };
+    float2 nxt[PF ? NZ : 1], cur[PF ? NZ : 1];
+    if (PF) {
+#pragma unroll
+        for (int r = 0; r < NZ; ++r) nxt[r] = ld(j + r * NS, blockIdx.x);
     }
     for (int row = blockIdx.x; row < e.r_ext; row += gridDim.x) {
+        if (PF) {
+            const int nrow = row + gridDim.x;
+#pragma unroll
+            for (int r = 0; r < NZ; ++r) {
+                cur[r] = nxt[r];
+                if (nrow < e.r_ext) nxt[r] = ld(j + r * NS, nrow);
+            }
+        }
+        // per-row pointers at this thread's column col0 (class 0; class 1 at + cls_*)
+        float *h0 = e.hb + (size_t)row * e.ldh + col0, *h1 = h0 + cls_h;
+        uint8_t *c0 = e.code + (size_t)row * e.ldh + col0, *c1 = c0 + cls_h;
+        const int br = row + e.q_off;
+        float *q0 = (!FAST && e.q && br >= 0 && br < e.band_rows) ? e.q + (size_t)br * e.cols + col0 : nullptr;
+        float *q1 = q0 + cls_q;
         __syncthreads();   // the previous row's transform consumed the buffer
         fftr::fft<LOGN, T, NZ, true>(
-            sm_fft, tw, [&](int i) { return i < Wx ? __ldg(Tt + (size_t)i * ldt + row) : make_float2(0.f, 0.f); },
-            [&](int q, int, float2 v) {
-                if (cq[q] >= 0) nd_store(e, row, cq[q], cmulf(px[q], v), live0, live1);
+            sm_fft, tw, [&](int i, int slot) { return PF ? cur[PF ? slot : 0] : ld(i, row); },
+            [&](int qi, int, float2 v) {
+                const int s = qi < 4 ? qi : qi - 8;              // qi in {0..3, 12..15} (ENDS)
+                const int off = (qi < 4 ? qi : qi - 16) * NS;    // compile time after unrolling
+                if (!(ok >> s & 1)) return;
+                const float2 g = cmulf(px[s], v);
+                const float qa = __uint_as_float(__float_as_uint(g.x) & live0), qb = __uint_as_float(__float_as_uint(g.y) & live1);
+                const float pa = fminf(qa * qa, 1.f), pb = fminf(qb * qb, 1.f);   // Born rule
+                if (FAST || !e.code) {
+                    h0[off] = nd_hb_of_p(pa);
+                    h1[off] = nd_hb_of_p(pb);
+                } else {
+                    c0[off] = nd_code8(pa);
+                    c1[off] = nd_code8(pb);
+                }
+                if (!FAST && q0) {
+                    q0[off] = qa;
+                    q1[off] = qb;
+                }
             });
     }
 }
@@ -512,13 +540,13 @@ int launch_colfft_nz(vsaogm_ctx *c, const NdPlan &P)
     return VSAOGM_OK;
 }
 
-template <int LOGN, int NZ>
+template <int LOGN, int NZ, bool FAST>
 int launch_rowfft_nz(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
 {
     constexpr int N = 1 << LOGN;
     constexpr int T = N / 16 < 32 ? 32 : N / 16;
     const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
-    auto kern = k_nd_rowfft<LOGN, T, NZ>;
+    auto kern = k_nd_rowfft<LOGN, T, NZ, FAST>;
     VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = persistent_grid(c, kern, T, smem, P.r_ext);
     kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw, P.d_Px,
@@ -539,17 +567,24 @@ int launch_colfft(vsaogm_ctx *c, const NdPlan &P)
     return launch_colfft_nz<LOGN, 16>(c, P);
 }
 
-template <int LOGN>
-int launch_rowfft(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
+template <int LOGN, bool FAST>
+int launch_rowfft_f(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
 {
     if constexpr ((LOGN & 3) == 0) {
         switch (nz_of(P.Wx, LOGN)) {
-        case 3: return launch_rowfft_nz<LOGN, 3>(c, P, e);
-        case 4: return launch_rowfft_nz<LOGN, 4>(c, P, e);
-        default: return launch_rowfft_nz<LOGN, 8>(c, P, e);
+        case 3: return launch_rowfft_nz<LOGN, 3, FAST>(c, P, e);
+        case 4: return launch_rowfft_nz<LOGN, 4, FAST>(c, P, e);
+        default: return launch_rowfft_nz<LOGN, 8, FAST>(c, P, e);
         }
     }
-    return launch_rowfft_nz<LOGN, 16>(c, P, e);
+    return launch_rowfft_nz<LOGN, 16, FAST>(c, P, e);
+}
+
+template <int LOGN>
+int launch_rowfft(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
+{
+    // the streaming step (H_b only) runs the lean kernel; q outputs / histogram codes the generic one
+    return (!e.q && !e.code) ? launch_rowfft_f<LOGN, true>(c, P, e) : launch_rowfft_f<LOGN, false>(c, P, e);
 }
 
 }  // namespace

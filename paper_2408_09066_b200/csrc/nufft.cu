@@ -285,18 +285,23 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(unsigned long long *__restrict_
     const int gy = blockIdx.x;
     const float py = psi_inv[gy], alpha = nu_alpha(bcnt);
     unsigned long long *row0 = grid + (size_t)gy * n1, *row1 = grid + ((size_t)n1 + gy) * n1;
-    float2 *r = stockham_zp<LOGN, T>(sm_fft, sm_fft + N, tw, [&](int j) {
-        if (j >= n1) return make_float2(0.f, 0.f);
-        const unsigned long long v0 = row0[j], v1 = row1[j];
-        if (v0) row0[j] = 0ull;
-        if (v1) row1[j] = 0ull;
-        const float s = psi_inv[j] * py;
-        return make_float2((float)((double)v0 * (1.0 / NU_FIX)) * s, (float)((double)v1 * (1.0 / NU_FIX)) * s * alpha);
-    });
     // only the frequencies the interpolation reads: |m| < K2 = N/4 + 8 (|t| <= pi/2 plus the
     // 6-point reach), stored compactly at m + K2
     constexpr int K2 = N / 4 + 8;
-    for (int cc = threadIdx.x; cc < 2 * K2; cc += T) f1t[(size_t)cc * n1 + gy] = r[(cc - K2) & (N - 1)];
+    fftr::fft<LOGN, T, 8>(
+        sm_fft, tw,
+        [&](int j, int) {
+            if (j >= n1) return make_float2(0.f, 0.f);
+            const unsigned long long v0 = row0[j], v1 = row1[j];
+            if (v0) row0[j] = 0ull;
+            if (v1) row1[j] = 0ull;
+            const float s = psi_inv[j] * py;
+            return make_float2((float)((double)v0 * (1.0 / NU_FIX)) * s, (float)((double)v1 * (1.0 / NU_FIX)) * s * alpha);
+        },
+        [&](int, int m, float2 v) {
+            if (m < K2) f1t[(size_t)(m + K2) * n1 + gy] = v;
+            else if (m >= N - K2) f1t[(size_t)(m - N + K2) * n1 + gy] = v;
+        });
 }
 
 // column pass: block = one (compact) x-frequency; transforms along y and writes the compact
@@ -310,10 +315,13 @@ __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t,
     constexpr int K2 = N / 4 + 8;
     const int cx = blockIdx.x;
     const float2 *in = f1t + (size_t)cx * n1;
-    float2 *r = stockham_zp<LOGN, T>(sm_fft, sm_fft + N, tw,
-                                     [&](int j) { return j < n1 ? in[j] : make_float2(0.f, 0.f); });
     float2 *out = G + (size_t)cx * 2 * K2;
-    for (int cc = threadIdx.x; cc < 2 * K2; cc += T) out[cc] = r[(cc - K2) & (N - 1)];
+    fftr::fft<LOGN, T, 8>(
+        sm_fft, tw, [&](int j, int) { return j < n1 ? __ldg(in + j) : make_float2(0.f, 0.f); },
+        [&](int, int m, float2 v) {
+            if (m < K2) out[m + K2] = v;
+            else if (m >= N - K2) out[m - N + K2] = v;
+        });
 }
 
 // ---- 3. interpolation + deconvolution ------------------------------------------------------
@@ -476,11 +484,12 @@ namespace {
 template <int LOGN>
 int launch_ffts(vsaogm_ctx *c, const int *bcnt)
 {
-    constexpr int T = 512;
-    const int N = 1 << LOGN;
-    // 2 N complex values (32 KB at N = 2048): fits beside a decode-GEMM CTA in the pipelined
-    // schedule; the per-stage twiddles are read from global memory (coalesced, L1-resident)
-    const size_t smem = (2 * (size_t)N) * sizeof(float2);
+    // register radix-16 passes (fft.cuh, fftr): one butterfly per thread and pass, one padded
+    // shared buffer of N + N/16 values (17 KB at N = 2048: fits beside a decode-GEMM CTA in the
+    // pipelined schedule)
+    constexpr int N = 1 << LOGN;
+    constexpr int T = N / 16 < 32 ? 32 : N / 16;
+    const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_rowfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_colfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_nu_rowfft<LOGN, T><<<c->nu_n1, T, smem, c->stream>>>((unsigned long long *)c->d_nu_grid, c->nu_n1, bcnt,
