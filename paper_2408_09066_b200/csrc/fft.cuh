@@ -278,8 +278,9 @@ __device__ __forceinline__ void twiddle(float2 *x, float2 w)
 // SRC 0: load(i); 1: shared buf.  DST 0: shared buf; 1: store(b R + q, m, y).  NZ (first pass, R = 16): the
 // inputs of groups r >= NZ are zero padding (not loaded).  ENDS (last pass, R = 16): only the
 // outputs q < 4 and q >= 12 (|m| < N / 4, the centred modes) are formed and stored.
-template <int LOGN, int R, int NS, int T, int SRC, int DST, int NZ, bool ENDS, class Load, class Store>
-__device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw, Load &load, Store &store)
+// DB: the pass reads bin and writes bout != bin (ping-pong buffers: no barrier between its reads and writes).
+template <int LOGN, int R, int NS, int T, int SRC, int DST, int NZ, bool ENDS, bool DB, class Load, class Store>
+__device__ __forceinline__ void pass(float2 *bin, float2 *bout, const float2 *__restrict__ tw, Load &load, Store &store)
 {
     constexpr int N = 1 << LOGN;
     constexpr int NB = N / R;                         // butterflies
@@ -295,11 +296,11 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
         if (NB % T == 0 || j < NB) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (r < NZ) x[b][r] = SRC == 0 ? load(j + r * NB, b * R + r) : buf[pad(j + r * NB)];
+                if (r < NZ) x[b][r] = SRC == 0 ? load(j + r * NB, b * R + r) : bin[pad(j + r * NB)];
             }
         }
     }
-    if (SRC == 1 && DST == 0) __syncthreads();   // every read of the buffer precedes the first write
+    if (SRC == 1 && DST == 0 && !DB) __syncthreads();   // every read of the buffer precedes the first write
 #pragma unroll
     for (int b = 0; b < PER; ++b) {
         const int j = threadIdx.x + b * T;
@@ -312,7 +313,7 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 if (ENDS && q >= 4 && q < 12) continue;
-                if (DST == 0) buf[pad(o + q * NS)] = x[b][q];
+                if (DST == 0) bout[pad(o + q * NS)] = x[b][q];
                 else store(b * R + q, o + q * NS, x[b][q]);
             }
         }
@@ -320,8 +321,8 @@ __device__ __forceinline__ void pass(float2 *buf, const float2 *__restrict__ tw,
     if (DST == 0) __syncthreads();
 }
 
-template <int LOGN, int P, int T, bool ENDS, class Load, class Store>
-__device__ __forceinline__ void passes16(float2 *buf, const float2 *__restrict__ tw, Load &load, Store &store)
+template <int LOGN, int P, int T, bool ENDS, bool DB, class Load, class Store>
+__device__ __forceinline__ void passes16(float2 *bin, float2 *bout, const float2 *__restrict__ tw, Load &load, Store &store)
 {
     // radix-16 pass P (NS = RF 16^P) and the ones after it
     constexpr int RF = 1 << (LOGN & 3);
@@ -329,26 +330,37 @@ __device__ __forceinline__ void passes16(float2 *buf, const float2 *__restrict__
     if constexpr (P < NP16) {
         constexpr int NS = RF * (1 << (4 * P));
         constexpr bool LASTP = P == NP16 - 1;
-        pass<LOGN, 16, NS, T, 1, LASTP ? 1 : 0, 16, LASTP && ENDS>(buf, tw, load, store);
-        passes16<LOGN, P + 1, T, ENDS>(buf, tw, load, store);
+        pass<LOGN, 16, NS, T, 1, LASTP ? 1 : 0, 16, LASTP && ENDS, DB>(bin, bout, tw, load, store);
+        passes16<LOGN, P + 1, T, ENDS, DB>(bout, bin, tw, load, store);
     }
 }
 
-// the whole transform; buf: shared memory of N + N/16 float2; the caller synchronises before
-// reusing buf for another transform.  NZ: only x_j, j < NZ N / 16, can be nonzero (a radix-16 first
+// the whole transform; buf: shared memory of N + N/16 float2 (DB: twice that -- the passes ping-pong
+// between the halves, one barrier per pass instead of two, and a caller that runs transform after
+// transform needs no barrier between them when there are exactly two exchanges (chained<LOGN>():
+// the last pass then reads the second half while the next first pass writes the first)); otherwise
+// the caller synchronises before reusing the buffer for another transform.  NZ: only x_j,
+// j < NZ N / 16, can be nonzero (a radix-16 first
 // pass skips the zero groups; NZ = 16: dense).  ENDS: only the outputs |m| < N / 4 are needed.
-template <int LOGN, int T, int NZ = 16, bool ENDS = false, class Load, class Store>
+template <int LOGN>
+__host__ __device__ constexpr bool chained()
+{
+    return (LOGN >> 2) + ((LOGN & 3) ? 1 : 0) == 3;   // three passes: two exchanges
+}
+
+template <int LOGN, int T, int NZ = 16, bool ENDS = false, bool DB = false, class Load, class Store>
 __device__ __forceinline__ void fft(float2 *buf, const float2 *__restrict__ tw, Load load, Store store)
 {
     static_assert(LOGN >= 5, "at least one radix-16 pass after the first");
     constexpr int RF = 1 << (LOGN & 3);
     constexpr int NP16 = LOGN >> 2;
+    float2 *b0 = buf, *b1 = DB ? buf + (1 << LOGN) + (1 << LOGN) / 16 : buf;
     if constexpr (RF > 1) {
-        pass<LOGN, RF, 1, T, 0, 0, RF, false>(buf, tw, load, store);
-        passes16<LOGN, 0, T, ENDS>(buf, tw, load, store);
+        pass<LOGN, RF, 1, T, 0, 0, RF, false, DB>(b0, b0, tw, load, store);
+        passes16<LOGN, 0, T, ENDS, DB>(b0, b1, tw, load, store);
     } else {
-        pass<LOGN, 16, 1, T, 0, (NP16 == 1) ? 1 : 0, NZ, ENDS && NP16 == 1>(buf, tw, load, store);
-        passes16<LOGN, 1, T, ENDS>(buf, tw, load, store);
+        pass<LOGN, 16, 1, T, 0, (NP16 == 1) ? 1 : 0, NZ, ENDS && NP16 == 1, DB>(b0, b0, tw, load, store);
+        passes16<LOGN, 1, T, ENDS, DB>(b0, b1, tw, load, store);
     }
 }
 

@@ -195,7 +195,7 @@ __device__ __forceinline__ float2 cmulf(float2 a, float2 b)
 // transforms along y of the band columns (fftr::fft: register radix-16 passes), persistent over
 // columns ux = blockIdx.x, += gridDim.x; output rows r in [0, r_ext) (r' = r - rc, the centred modes
 // |r'| < M / 4), times Py[r] (each thread's rows are fixed: their factors are loaded once)
-template <int LOGN, int T, int NZ>
+template <int LOGN, int T, int NZ, bool DB>
 __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(const float2 *__restrict__ Gt, int Wx, int Wy,
                                                                            const float2 *__restrict__ tw,
                                                                            const float2 *__restrict__ Py, int r_ext, int rc,
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(co
     for (int ux = blockIdx.x; ux < Wx; ux += gridDim.x) {
         const float2 *in = Gt + (size_t)ux * Wy;
         float2 *out = Tt + (size_t)ux * ldt;
-        __syncthreads();   // the previous column's transform consumed the buffer
-        fftr::fft<LOGN, T, NZ, true>(
+        if (!(DB && fftr::chained<LOGN>())) __syncthreads();   // the previous column's transform consumed the buffer
+        fftr::fft<LOGN, T, NZ, true, DB>(
             sm_fft, tw, [&](int i, int) { return i < Wy ? __ldg(in + i) : make_float2(0.f, 0.f); },
             [&](int q, int, float2 v) {
                 if (rq[q] >= 0) out[rq[q]] = cmulf(py[q], v);
@@ -261,7 +261,7 @@ __device__ __forceinline__ uint8_t nd_code8(float p)
 // off_s = (s < 4 ? s : s - 8) N / 16, s = 0..7: each thread's columns are fixed (their factors Px are
 // loaded once, their validity is a bit mask) and every store address is one per-row pointer plus a
 // compile-time offset.  FAST: H_b only (no q output, no histogram codes) -- the streaming step.
-template <int LOGN, int T, int NZ, bool FAST>
+template <int LOGN, int T, int NZ, bool FAST, bool DB>
 __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(const float2 *__restrict__ Tt, int ldt, int Wx,
                                                                            const float2 *__restrict__ tw,
                                                                            const float2 *__restrict__ Px, int cols, int jc,
@@ -307,8 +307,8 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(co
         const int br = row + e.q_off;
         float *q0 = (!FAST && e.q && br >= 0 && br < e.band_rows) ? e.q + (size_t)br * e.cols + col0 : nullptr;
         float *q1 = q0 + cls_q;
-        __syncthreads();   // the previous row's transform consumed the buffer
-        fftr::fft<LOGN, T, NZ, true>(
+        if (!(DB && fftr::chained<LOGN>())) __syncthreads();   // the previous row's transform consumed the buffer
+        fftr::fft<LOGN, T, NZ, true, DB>(
             sm_fft, tw, [&](int i, int slot) { return PF ? cur[PF ? slot : 0] : ld(i, row); },
             [&](int qi, int, float2 v) {
                 const int s = qi < 4 ? qi : qi - 8;              // qi in {0..3, 12..15} (ENDS)
@@ -531,8 +531,11 @@ int launch_colfft_nz(vsaogm_ctx *c, const NdPlan &P)
 {
     constexpr int N = 1 << LOGN;
     constexpr int T = N / 16 < 32 ? 32 : N / 16;
-    const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
-    auto kern = k_nd_colfft<LOGN, T, NZ>;
+    // ping-pong buffers (fft.cuh DB: one barrier per pass) measured slower -- 209 KB of shared memory
+    // per SM leaves no L1 for the twiddle and Tt loads (row pass 30.4 -> 37.4 us at C4): off
+    constexpr bool DB = false;
+    const size_t smem = (size_t)(N + N / 16) * sizeof(float2) * (DB ? 2 : 1);
+    auto kern = k_nd_colfft<LOGN, T, NZ, DB>;
     VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = persistent_grid(c, kern, T, smem, P.Wx);
     kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_G, P.Wx, P.Wy, (const float2 *)c->d_nd_tw, P.d_Py,
@@ -545,8 +548,9 @@ int launch_rowfft_nz(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
 {
     constexpr int N = 1 << LOGN;
     constexpr int T = N / 16 < 32 ? 32 : N / 16;
-    const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
-    auto kern = k_nd_rowfft<LOGN, T, NZ, FAST>;
+    constexpr bool DB = false;   // see launch_colfft_nz
+    const size_t smem = (size_t)(N + N / 16) * sizeof(float2) * (DB ? 2 : 1);
+    auto kern = k_nd_rowfft<LOGN, T, NZ, FAST, DB>;
     VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = persistent_grid(c, kern, T, smem, P.r_ext);
     kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw, P.d_Px,
