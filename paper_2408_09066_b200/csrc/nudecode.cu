@@ -44,7 +44,7 @@
 
 namespace {
 
-constexpr int ND_TS = 16;          // spread tile side (cells)
+constexpr int ND_TS = 32;          // spread tile side (cells): 2 x 2 cells per thread
 constexpr int ND_BS = 8;           // point bin side (cells)
 constexpr int ND_CH = 64;          // points staged per chunk in the spread kernel
 constexpr double ND_MSP = 5.0;     // Gaussian width parameter (accuracy ~1e-6)
@@ -64,6 +64,7 @@ struct NdPlan {
     float ax = 0, ay = 0;              // h^2 / (4 tau) per axis
     int *d_kid = nullptr;              // point ids (k, or D + k for -xi_k) in bin order [2 D]
     float2 *d_pos = nullptr;           // per slot: position relative to its bin's first cell (cells)
+    int *d_binx = nullptr;             // per slot: its bin's column
     int *d_bin_off = nullptr;          // [nbx nby + 1]
     float2 *d_Px = nullptr;            // output factors per column [cols]
     float2 *d_Py = nullptr;            // output factors per decoded row [r_ext]
@@ -101,57 +102,65 @@ __global__ void __launch_bounds__(256) k_nd_strength(const int *__restrict__ kid
 struct NdSpread {
     const float2 *st;        // strengths per slot
     const float2 *pos;       // position per slot relative to its bin's first cell (cells, fp32)
+    const int *binx;         // bin column per slot
     const int *bin_off;      // [nbx nby + 1]
     int Wx, Wy, nbx, nby;
     float ax, ay;            // h^2 / (4 tau)
     float2 *Gt;              // compact band grid, x-major: Gt[ux][uy]
 };
 
-// block = one 16 x 16 tile of the band grid; gathers the points binned (8 x 8 bins) within 8 cells of
-// it -- the 4 x 4 bins covering [16 b - 8, 16 b + 24) per axis, four contiguous slot ranges (one per
-// bin row), where a point farther than 8 cells has weight < e^-31 --, up to 128 per pass.  One
-// thread per staged point computes its position relative to the tile; then all threads compute the
-// 16 x-weights g_x and the 16 strength-scaled y-weights h_y = g_y st of every staged point, and
-// every thread (one cell) sums g_x[q][x] h_y[q][y] over the points in slot order (deterministic).
+// block = one 32 x 32 tile of the band grid, 2 x 2 cells per thread (x = tx, tx + 16; y = ty, ty + 16);
+// gathers the points binned (8 x 8 bins) within 8 cells of it -- the 6 x 6 bins covering
+// [32 b - 8, 32 b + 40) per axis, six contiguous slot ranges (one per bin row), where a point farther
+// than 8 cells has weight < e^-31 --, up to 64 per pass.  One thread per staged point computes its
+// position relative to the tile (bin column from the plan: no search); then all threads compute the
+// 32 x-weights g_x and the 32 strength-scaled y-weights h_y = g_y st of every staged point, and
+// every thread sums g_x[q][x] h_y[q][y] for its four cells over the points in slot order
+// (deterministic).  ~76 points per tile at C4: one wave of 484 blocks.
 __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ NdSpread p)
 {
-    constexpr int CH = 128;
+    constexpr int CH = ND_CH, NB = ND_TS / ND_BS + 2;   // staged points per pass; bin rows / columns gathered
     __shared__ float2 s_st[CH];
     __shared__ float2 s_u[CH];   // the point's position relative to this tile's first cell
-    __shared__ float s_gx[CH][ND_TS + 1];
+    __shared__ float s_gx[CH][ND_TS];
     __shared__ float2 s_hy[CH][ND_TS];
     const int bx = blockIdx.x, by = blockIdx.y, tid = threadIdx.x;
     const int cxl = tid >> 4, cyl = tid & 15;   // a warp = 2 band columns x 16 rows (contiguous stores)
-    const int xb0 = max(2 * bx - 1, 0), xb1 = min(2 * bx + 2, p.nbx - 1);
-    int beg[4], len[4], yb_of[4], nr = 0, total = 0;
-    for (int dy = -1; dy <= 2; ++dy) {
-        const int yb = 2 * by + dy;
-        if (yb < 0 || yb >= p.nby) continue;
-        beg[nr] = __ldg(p.bin_off + yb * p.nbx + xb0);
-        len[nr] = __ldg(p.bin_off + yb * p.nbx + xb1 + 1) - beg[nr];
-        yb_of[nr] = yb;
-        total += len[nr];
-        ++nr;
+    constexpr int BPT = ND_TS / ND_BS;          // bins per tile side
+    const int xb0 = max(BPT * bx - 1, 0), xb1 = min(BPT * bx + BPT, p.nbx - 1);
+    int beg[NB], len[NB], total = 0;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+        const int yb = BPT * by - 1 + r;
+        const bool in = yb >= 0 && yb < p.nby;
+        beg[r] = in ? __ldg(p.bin_off + yb * p.nbx + xb0) : 0;
+        len[r] = in ? __ldg(p.bin_off + yb * p.nbx + xb1 + 1) - beg[r] : 0;
+        total += len[r];
     }
-    float accr = 0.f, acci = 0.f, accr2 = 0.f, acci2 = 0.f;
+    float2 acc[2][2] = {{make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}};
     for (int c0 = 0; c0 < total; c0 += CH) {
         const int nc = min(CH, total - c0);
         if (c0) __syncthreads();   // the previous pass is consumed
         if (tid < nc) {
-            int i = c0 + tid, r = 0;
-            while (i >= len[r]) { i -= len[r]; ++r; }
-            const int slot = beg[r] + i;
-            // the slot's bin column: the bins of this row range in order xb0 .. xb1
-            const int rowb = yb_of[r] * p.nbx;
-            int xbp = xb0;
-            while (xbp < xb1 && slot >= __ldg(p.bin_off + rowb + xbp + 1)) ++xbp;
+            int i = c0 + tid, slot = 0, yb = 0;
+            bool found = false;
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {   // the bin row of staged point i (registers only)
+                if (!found && i < len[r]) {
+                    slot = beg[r] + i;
+                    yb = BPT * by - 1 + r;
+                    found = true;
+                }
+                i -= len[r];
+            }
             const float2 ps = __ldg(p.pos + slot);
-            s_u[tid] = make_float2((float)(xbp * ND_BS - bx * ND_TS) + ps.x, (float)(yb_of[r] * ND_BS - by * ND_TS) + ps.y);
+            const int xbp = __ldg(p.binx + slot);
+            s_u[tid] = make_float2((float)(xbp * ND_BS - bx * ND_TS) + ps.x, (float)(yb * ND_BS - by * ND_TS) + ps.y);
             s_st[tid] = __ldg(p.st + slot);
         }
         __syncthreads();
         for (int e = tid; e < nc * 2 * ND_TS; e += 256) {
-            const int q = e >> 5, r = e & 31;
+            const int q = e / (2 * ND_TS), r = e % (2 * ND_TS);
             const float2 u = s_u[q];
             if (r < ND_TS) {
                 const float d = (float)r - u.x;
@@ -164,27 +173,27 @@ __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ Nd
             }
         }
         __syncthreads();
-        int q = 0;
 #pragma unroll 4
-        for (; q + 1 < nc; q += 2) {   // two independent accumulator pairs (summed in a fixed order)
-            const float g = s_gx[q][cxl], g2 = s_gx[q + 1][cxl];
-            const float2 hy = s_hy[q][cyl], hy2 = s_hy[q + 1][cyl];
-            accr = fmaf(g, hy.x, accr);
-            acci = fmaf(g, hy.y, acci);
-            accr2 = fmaf(g2, hy2.x, accr2);
-            acci2 = fmaf(g2, hy2.y, acci2);
-        }
-        if (q < nc) {
-            const float g = s_gx[q][cxl];
-            const float2 hy = s_hy[q][cyl];
-            accr = fmaf(g, hy.x, accr);
-            acci = fmaf(g, hy.y, acci);
+        for (int q = 0; q < nc; ++q) {   // four independent accumulator pairs, each summed in slot order
+            const float g0 = s_gx[q][cxl], g1 = s_gx[q][cxl + 16];
+            const float2 h0 = s_hy[q][cyl], h1 = s_hy[q][cyl + 16];
+            acc[0][0].x = fmaf(g0, h0.x, acc[0][0].x);
+            acc[0][0].y = fmaf(g0, h0.y, acc[0][0].y);
+            acc[0][1].x = fmaf(g0, h1.x, acc[0][1].x);
+            acc[0][1].y = fmaf(g0, h1.y, acc[0][1].y);
+            acc[1][0].x = fmaf(g1, h0.x, acc[1][0].x);
+            acc[1][0].y = fmaf(g1, h0.y, acc[1][0].y);
+            acc[1][1].x = fmaf(g1, h1.x, acc[1][1].x);
+            acc[1][1].y = fmaf(g1, h1.y, acc[1][1].y);
         }
     }
-    accr += accr2;
-    acci += acci2;
-    const int ux = bx * ND_TS + cxl, uy = by * ND_TS + cyl;
-    if (ux < p.Wx && uy < p.Wy) p.Gt[(size_t)ux * p.Wy + uy] = make_float2(accr, acci);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int ux = bx * ND_TS + cxl + 16 * a, uy = by * ND_TS + cyl + 16 * b;
+            if (ux < p.Wx && uy < p.Wy) p.Gt[(size_t)ux * p.Wy + uy] = acc[a][b];
+        }
 }
 
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b)
@@ -353,7 +362,7 @@ int ilog2_ceil(int64_t v)
 void free_plan(NdPlan *p)
 {
     if (!p) return;
-    void *ptrs[] = {p->d_kid, p->d_pos, p->d_bin_off, p->d_Px, p->d_Py};
+    void *ptrs[] = {p->d_kid, p->d_pos, p->d_binx, p->d_bin_off, p->d_Px, p->d_Py};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     delete p;
@@ -421,11 +430,13 @@ int nd_build(vsaogm_ctx *c, NdPlan &P)
     for (int b = 0; b < nb; ++b) cnt[b + 1] += cnt[b];
     std::vector<int> off(cnt.begin(), cnt.end()), kid(2 * (size_t)D);
     std::vector<float2> pos(2 * (size_t)D);
+    std::vector<int> binx(2 * (size_t)D);
     for (int pt = 0; pt < 2 * D; ++pt) {   // stable: ascending point id per bin
         const int s = off[bin[pt]]++;
         kid[s] = pt;
         const int bxp = bin[pt] % P.nbx, byp = bin[pt] / P.nbx;
         pos[s] = make_float2((float)(fxa[pt] - ND_BS * bxp), (float)(fya[pt] - ND_BS * byp));
+        binx[s] = bxp;
     }
     const double tx_ = nd_tau(P.cols, P.Mx), ty_ = nd_tau(P.r_ext, P.My);
     const double hx = 2.0 * kPi / P.Mx, hy = 2.0 * kPi / P.My;
@@ -447,12 +458,14 @@ int nd_build(vsaogm_ctx *c, NdPlan &P)
     }
     if (cudaMalloc(&P.d_kid, kid.size() * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&P.d_pos, pos.size() * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&P.d_binx, binx.size() * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&P.d_bin_off, cnt.size() * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&P.d_Px, px.size() * sizeof(float2)) != cudaSuccess ||
         cudaMalloc(&P.d_Py, py.size() * sizeof(float2)) != cudaSuccess)
         return VSAOGM_ENOMEM;
     VSA_CUDA_TRY(cudaMemcpy(P.d_kid, kid.data(), kid.size() * sizeof(int), cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(P.d_pos, pos.data(), pos.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    VSA_CUDA_TRY(cudaMemcpy(P.d_binx, binx.data(), binx.size() * sizeof(int), cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(P.d_bin_off, cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(P.d_Px, px.data(), px.size() * sizeof(float2), cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(P.d_Py, py.data(), py.size() * sizeof(float2), cudaMemcpyHostToDevice));
@@ -629,6 +642,7 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     NdSpread sp;
     sp.st = (const float2 *)c->d_nd_st;
     sp.pos = P->d_pos;
+    sp.binx = P->d_binx;
     sp.bin_off = P->d_bin_off;
     sp.Wx = P->Wx;
     sp.Wy = P->Wy;
