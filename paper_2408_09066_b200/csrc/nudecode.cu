@@ -46,7 +46,7 @@ namespace {
 
 constexpr int ND_TS = 32;          // spread tile side (cells): 2 x 2 cells per thread
 constexpr int ND_BS = 8;           // point bin side (cells)
-constexpr int ND_CH = 64;          // points staged per chunk in the spread kernel
+constexpr int ND_CH = 112;         // points staged per pass in the spread kernel (~76 per tile at C4: one pass)
 constexpr double ND_MSP = 5.0;     // Gaussian width parameter (accuracy ~1e-6)
 constexpr int ND_MARGIN = 6;       // band half-width beyond max |xi| / h (cells)
 constexpr int ND_LOGN_MAX = 13;    // shared-memory transforms up to 8192 points

@@ -49,9 +49,10 @@ constexpr double NU_FIX = 4294967296.0; // 2^32: fixed-point scale of the spread
 //     shared-memory atomics in integer fixed point (exact), then the window's nonzero cells into
 //     the class's dense 32.32 fixed-point grid with 64-bit integer atomics (exact: the result does
 //     not depend on the order).  The row FFT reads and re-zeroes the grid.
-constexpr int NU_TS = 16;                      // tile side (cells)
-constexpr int NU_WIN = NU_TS + NU_W - 1;       // 29: window side
-constexpr int NU_WST = 30;                     // window row stride (words): 7 rows apart = 18 banks
+constexpr int NU_TS = 32;                      // tile side (cells): ~180 points per unit at C4 (16: 38; the window's zeroing and flush are per unit)
+constexpr int NU_WIN = NU_TS + NU_W - 1;       // 45: window side
+constexpr int NU_WST = 48;                     // window row stride (words): the half-warps' rows, 7 apart, are 16 banks apart
+static_assert(NU_WST >= NU_WIN && (7 * NU_WST) % 32 >= 14 && (7 * NU_WST) % 32 <= 18, "half-warps on disjoint banks");
 constexpr int NU_WOFF = NU_MSP;                // window starts 6 cells before the tile
 
 __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n,
@@ -181,6 +182,13 @@ __global__ void __launch_bounds__(256) k_nu_place(const float2 *__restrict__ xy,
     sorted[bin_off[key.x] + key.y] = xy[i];
 }
 
+__device__ __forceinline__ float nu_ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restrict__ sorted, const int *__restrict__ bin_off,
                                                          const int *__restrict__ unit_bin,
                                                          const int *__restrict__ unit_first,
@@ -208,8 +216,9 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
     // Lane = support column dx (lanes 14, 15 of each half idle), half-warp = rows 7 half .. +6;
     // the row weights by the recurrence exp(-c (u+1)^2) = exp(-c u^2) r, r = exp(-c (2u + 1)),
     // r <- r exp(-2c) (Greengard & Lee's fast Gaussian gridding): 3 exponentials per lane and point.
-    const float c2 = (float)(h * h / (4.0 * tau));
-    const float e2 = __expf(-2.f * c2);
+    // in base 2: ex2.approx directly (arguments within [-30, 6]: no range guard needed)
+    const float c2 = (float)(h * h / (4.0 * tau) * 1.4426950408889634);
+    const float e2 = nu_ex2(-2.f * c2);
     const int dx = lane & 15, half = lane >> 4;
     const bool col_ok = dx < NU_W;
     const float2 *pts = sorted + first;
@@ -228,8 +237,8 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
             const float fx = __shfl_sync(0xffffffffu, mfx, jj), fy = __shfl_sync(0xffffffffu, mfy, jj);
             const int ix = cell & 0xffff, iy = cell >> 16;
             const float ux = (float)(dx - NU_MSP) - fx, uy = (float)(7 * half - NU_MSP) - fy;
-            const float wx = __expf(-c2 * ux * ux) * qscale;   // the x weight carries the scale
-            float wy = __expf(-c2 * uy * uy), r = __expf(-c2 * (2.f * uy + 1.f));
+            const float wx = nu_ex2(-c2 * ux * ux) * qscale;   // the x weight carries the scale
+            float wy = nu_ex2(-c2 * uy * uy), r = nu_ex2(-c2 * (2.f * uy + 1.f));
             unsigned int *wb = s_win + (iy - NU_MSP - gy0 + 7 * half) * NU_WST + (ix - NU_MSP - gx0 + dx);
             if (col_ok) {
 #pragma unroll
