@@ -175,7 +175,7 @@ def run_native(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2408_09066_b200 import BF16, F16, Mapper
+    from paper_2408_09066_b200 import BF16, F16, IO_SLOTS, Mapper
     from paper_2408_09066_b200.parallel import decoded_rows, fuse_and_commit, point_shard, row_band
     from synth.lidar import Scenario
 
@@ -341,7 +341,7 @@ def run_native(args):
     # host memory, bundles, decodes, and downloads the labels to pinned host memory; step k's
     # copies overlap the kernels of steps k-1 / k+1.  Wall clock over all K steps, including
     # the final wait; max over ranks.
-    labels_pipe = [torch.empty((band, C), dtype=torch.uint8).pin_memory() for _ in range(3)]
+    labels_pipe = [torch.empty((band, C), dtype=torch.uint8).pin_memory() for _ in range(IO_SLOTS)]
 
     def step_async(b, slot):
         xy, lab = pinned[b % nb]
@@ -352,25 +352,26 @@ def run_native(args):
         return mp.entropy_host_async(h, h, tau, -tau, 0, None, labels_pipe[slot])
 
     def run_e2e(first, count):
-        """`count` pipelined steps, two in flight (the library's three I/O slots); returns (total
+        """`count` pipelined steps, IO_SLOTS - 1 = three in flight (the library's four I/O slots: the 75 us
+        label download of step k - 2 then no longer delays the enqueue of step k + 1); returns (total
         wall ms, per-step wall ms between ticket waits)."""
         t0 = time.perf_counter()
         tickets, marks = [], []
         for k in range(count):
-            tickets.append(step_async(first + k, k % 3))
-            if k >= 2 and mp.wait(tickets[k - 2]) != 0:
+            tickets.append(step_async(first + k, k % IO_SLOTS))
+            if k >= IO_SLOTS - 1 and mp.wait(tickets[k - (IO_SLOTS - 1)]) != 0:
                 raise RuntimeError("deferred device error (e2e)")
             marks.append(time.perf_counter())
-        for t in tickets[-2:]:
+        for t in tickets[-(IO_SLOTS - 1):]:
             if mp.wait(t) != 0:
                 raise RuntimeError("deferred device error (e2e)")
         t1 = time.perf_counter()
         return (t1 - t0) * 1e3, [(b - a) * 1e3 for a, b in zip(marks, marks[1:])]
 
     with torch.cuda.stream(hi):                    # encode stream still set: the same pipeline
-        # untimed: lcm(3 slots, nb batches) steps, so every (slot, batch) pair is visited and
+        # untimed: lcm(IO_SLOTS, nb batches) steps, so every (slot, batch) pair is visited and
         # every slot is sized before the timed region (no reallocation inside it)
-        run_e2e(0, max(args.warmup, 3 * nb // math.gcd(3, nb)))
+        run_e2e(0, max(args.warmup, IO_SLOTS * nb // math.gcd(IO_SLOTS, nb)))
         barrier()
         e2e_total, e2e_steps = run_e2e(args.warmup, args.steps)
         mp.set_encode_stream(None)

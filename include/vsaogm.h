@@ -219,25 +219,29 @@ int vsaogm_entropy_host(vsaogm_ctx *ctx, const vsaogm_entropy_params *params, fl
  * Errors: EINVAL_ARG, ECUDA. */
 int vsaogm_set_encode_stream(vsaogm_ctx *ctx, void *stream);
 
+#define VSAOGM_IO_SLOTS 4
+
 /* Pipelined host I/O for streaming mapping (one batch per step, Alg. 1 then
  * Alg. 2): the host<->device copies of step k run on two
  * internal copy streams and overlap the kernels of steps k-1 and k+1.
  *
  * vsaogm_encode_bundle_host_async: as vsaogm_encode_bundle_host, but the
  * host->device copy of (xy_host float32 [n][2], labels_host uint8 [n]) goes to
- * one of three device staging slots on the upload stream, and the encode on the
- * context stream waits for it (with an encode stream set: the copy is queued on
- * the encode stream itself, ahead of the encode's wait for the previous
- * decode, and the download below follows the entropy on the context stream).  The host arrays must be page-locked for the
+ * one of VSAOGM_IO_SLOTS device staging slots on the upload stream, and the encode on the
+ * context stream (or the encode stream, when one is set) waits for it.  The host
+ * arrays must be page-locked for the
  * copy to be asynchronous, and must stay unmodified until the ticket of the
  * vsaogm_entropy_host_async that follows this call has been waited for.
  *
- * vsaogm_entropy_host_async: as vsaogm_entropy_host, into one of three device
- * output slots, then a device->host copy on the download stream; returns at
- * once with *ticket.  s_host / labels_host (page-locked for overlap) are written
- * when vsaogm_wait(ctx, *ticket) returns.  There are three staging and three
- * output slots; a slot is reused three calls later (the device orders the
- * reuse after its previous download), so up to two steps may be in flight.
+ * vsaogm_entropy_host_async: as vsaogm_entropy_host, into one of VSAOGM_IO_SLOTS
+ * device output slots, then a device->host copy on the download stream (it
+ * overlaps the next step's kernels); returns at once with *ticket.  s_host /
+ * labels_host (page-locked for overlap) are written when vsaogm_wait(ctx, *ticket)
+ * returns.  There are VSAOGM_IO_SLOTS (4) staging and output slots; a slot is reused that
+ * many calls later (the device orders the reuse after its previous download), so
+ * up to VSAOGM_IO_SLOTS - 1 steps may be in flight: the caller waits for ticket
+ * k - 3 after queuing step k (at C4 the 75 us label download of a step is half a step long: with
+ * fewer steps in flight the host queues the next encode too late to overlap the running decode).
  *
  * vsaogm_wait: block until step `ticket` has been downloaded; returns a deferred
  * device error like vsaogm_sync (the error bits are sticky until vsaogm_sync and are

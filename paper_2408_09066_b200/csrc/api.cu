@@ -407,19 +407,15 @@ int vsaogm_encode_bundle_host_async(vsaogm_ctx *c, const float *xy, const uint8_
     if ((rc = grow_slot((void **)&c->d_in_xy[s], &c->in_xy_cap[s], n * sizeof(float2), c->ev_used[s], used))) return rc;
     if ((rc = grow_slot((void **)&c->d_in_lab[s], &c->in_lab_cap[s], (size_t)n, c->ev_used[s], used))) return rc;
     cudaStream_t es = c->enc_stream ? c->enc_stream : c->stream;
-    if (c->enc_stream) {
-        // encode-stream pipeline: upload on the encode stream itself, queued before the encode's
-        // wait for the previous decode, so it runs while that decode's commit / table build do
-        // (the slot's previous reader is earlier on the same stream; no cross-stream event)
-        VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_xy[s], xy, n * sizeof(float2), cudaMemcpyHostToDevice, es));
-        VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_lab[s], lab, n, cudaMemcpyHostToDevice, es));
-    } else {
-        if (used) VSA_CUDA_TRY(cudaStreamWaitEvent(c->up, c->ev_used[s], 0));
-        VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_xy[s], xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->up));
-        VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_lab[s], lab, n, cudaMemcpyHostToDevice, c->up));
-        VSA_CUDA_TRY(cudaEventRecord(c->ev_up[s], c->up));
-        VSA_CUDA_TRY(cudaStreamWaitEvent(es, c->ev_up[s], 0));
-    }
+    // upload on the upload stream, after the slot's previous encode; the encode (on the encode
+    // stream when one is set) waits for it.  Not on the encode stream itself: between two encodes
+    // that stream is on the step's critical path (encode -> norms -> strengths -> next encode), and
+    // the 36 us copy of a C4 batch would sit in it
+    if (used) VSA_CUDA_TRY(cudaStreamWaitEvent(c->up, c->ev_used[s], 0));
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_xy[s], xy, n * sizeof(float2), cudaMemcpyHostToDevice, c->up));
+    VSA_CUDA_TRY(cudaMemcpyAsync(c->d_in_lab[s], lab, n, cudaMemcpyHostToDevice, c->up));
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_up[s], c->up));
+    VSA_CUDA_TRY(cudaStreamWaitEvent(es, c->ev_up[s], 0));
     if ((rc = vsaogm_encode_bundle(c, (const float *)c->d_in_xy[s], c->d_in_lab[s], n))) return rc;
     VSA_CUDA_TRY(cudaEventRecord(c->ev_used[s], es));
     c->in_seq++;
@@ -680,16 +676,14 @@ int vsaogm_entropy_host_async(vsaogm_ctx *c, const vsaogm_entropy_params *p, flo
         return rc;
     if (lab_host && (rc = grow_slot((void **)&c->d_out_lab[s], &c->out_lab_cap[s], cells, c->ev_down[s], used)))
         return rc;
-    // encode-stream pipeline: the download follows the entropy on the context stream (the next
-    // encode runs on the encode stream, so nothing waits behind it); otherwise on the download
-    // stream so that it overlaps the next step's kernels
-    cudaStream_t ds = c->enc_stream ? c->stream : c->down;
-    if (used && !c->enc_stream) VSA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_down[s], 0));
+    // the download runs on the download stream so that it overlaps the next step's kernels (at C4
+    // the 4 MB of labels take ~75 us over PCIe, half a step: on the context stream they would
+    // delay the next decode by that much)
+    cudaStream_t ds = c->down;
+    if (used) VSA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_down[s], 0));
     if ((rc = vsa_launch_entropy(c, p, S_host ? c->d_out_S[s] : nullptr, lab_host ? c->d_out_lab[s] : nullptr))) return rc;
-    if (!c->enc_stream) {
-        VSA_CUDA_TRY(cudaEventRecord(c->ev_out[s], c->stream));
-        VSA_CUDA_TRY(cudaStreamWaitEvent(c->down, c->ev_out[s], 0));
-    }
+    VSA_CUDA_TRY(cudaEventRecord(c->ev_out[s], c->stream));
+    VSA_CUDA_TRY(cudaStreamWaitEvent(c->down, c->ev_out[s], 0));
     if (S_host) VSA_CUDA_TRY(cudaMemcpyAsync(S_host, c->d_out_S[s], 3 * cells * sizeof(float), cudaMemcpyDeviceToHost, ds));
     if (lab_host) VSA_CUDA_TRY(cudaMemcpyAsync(lab_host, c->d_out_lab[s], cells, cudaMemcpyDeviceToHost, ds));
     // deferred error bits as of this step (sticky until vsaogm_sync clears them)

@@ -45,9 +45,9 @@ void vsa_report_cuda_error(cudaError_t e, const char *expr, const char *file, in
 
 #define VSA_MAX_GROUPS (VSAOGM_MAX_DELTA * VSAOGM_MAX_DELTA)
 
-// staging / output slots of the pipelined host I/O (vsaogm_*_host_async): three of each; a slot
+// staging / output slots of the pipelined host I/O (vsaogm_*_host_async): VSAOGM_IO_SLOTS of each; a slot
 // is reused VSA_IO_SLOTS calls later, so the host may keep VSA_IO_SLOTS - 1 steps in flight
-#define VSA_IO_SLOTS 3
+#define VSA_IO_SLOTS VSAOGM_IO_SLOTS
 #define VSA_ND_PLANS 4   // cached NUFFT-decode plans (decode geometries)
 
 // Decode GEMM problem groups (one per quadrant with decoded cells; delta = 1: one group).
@@ -175,7 +175,7 @@ struct vsaogm_ctx {
     float *d_S = nullptr; size_t S_cap = 0;        // host-entropy scratch
     uint8_t *d_lab = nullptr; size_t lab_cap = 0;
 
-    // pipelined host I/O (vsaogm_*_host_async): three staging / output slots each, copy streams
+    // pipelined host I/O (vsaogm_*_host_async): VSA_IO_SLOTS staging / output slots each, copy streams
     cudaStream_t up = nullptr, down = nullptr;     // upload (H2D) / download (D2H) streams
     float2 *d_in_xy[VSA_IO_SLOTS] = {}; size_t in_xy_cap[VSA_IO_SLOTS] = {};
     uint8_t *d_in_lab[VSA_IO_SLOTS] = {}; size_t in_lab_cap[VSA_IO_SLOTS] = {};

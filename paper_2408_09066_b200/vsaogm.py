@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libvsaogm.so")
 
 OK, EINVAL_DIM, EINVAL_ARG, EEMPTY, ELABEL, ENONFINITE, ENOMEM, ECUDA, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8
 F16, BF16 = 0, 1
+IO_SLOTS = 4   # VSAOGM_IO_SLOTS: up to IO_SLOTS - 1 pipelined host steps in flight
 KERNELS = ("encode", "reduce", "commit", "norms", "table_B", "table_A", "decode_gemm", "entropy", "nd_spread", "nd_colfft", "nd_rowfft")
 
 # every symbol include/vsaogm.h declares
