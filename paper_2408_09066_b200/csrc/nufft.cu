@@ -101,6 +101,13 @@ __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, c
     if (threadIdx.x >= 2 && threadIdx.x < 4 && s_cnt[threadIdx.x]) atomicAdd(&bcnt[threadIdx.x - 2], s_cnt[threadIdx.x]);
 }
 
+__global__ void __launch_bounds__(256) k_nu_zero(int *__restrict__ a, int na, int *__restrict__ b, int nb)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) a[i] = 0;
+    if (i < nb) b[i] = 0;
+}
+
 // exclusive prefix of the bin counts and of the bins' work units (NU_UNIT points each): unit u
 // covers points [unit_first[u], +NU_UNIT) of bin unit_bin[u]; *n_units = the total
 constexpr int NU_UNIT = 256;
@@ -542,8 +549,10 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     int *bin_cnt = c->d_nu_bins, *bcnt = c->d_nu_bins + nbins, *bin_off = bcnt + 2, *unit_off = bin_off + nbins + 1;
     int *n_units = unit_off + nbins + 1;
     int *unit_bin = c->d_nu_units, *unit_first = c->d_nu_units + (c->nu_pts_cap / NU_UNIT + nbins);
-    VSA_CUDA_TRY(cudaMemsetAsync(c->d_nu_out, 0, chunks * sizeof(int), c->stream));
-    VSA_CUDA_TRY(cudaMemsetAsync(bin_cnt, 0, (nbins + 2) * sizeof(int), c->stream));
+    // one small kernel instead of two memsets (a memset may be queued on a copy engine behind a
+    // pipelined host upload: the encode's start would wait for the whole batch copy)
+    const int nz = std::max(chunks, nbins + 2);
+    k_nu_zero<<<(nz + 255) / 256, 256, 0, c->stream>>>(c->d_nu_out, chunks, bin_cnt, nbins + 2);
     const unsigned pblocks = (unsigned)((n + 255) / 256);
     const double inv_h = 1.0 / c->nu_h;
     k_nu_bin<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, lab, n, c->cx, c->cy, c->nu_lo, inv_h, c->nu_n1, ntx,
@@ -572,6 +581,6 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
                                                                       c->nu_tau, c->nu_tau2, (const float2 *)c->d_nu_ph,
                                                                       bcnt, c->d_pending);
     VSA_CUDA_TRY(cudaGetLastError());
-    c->launches += 7;
+    c->launches += 8;
     return VSAOGM_OK;
 }
