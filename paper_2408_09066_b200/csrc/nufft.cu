@@ -346,22 +346,26 @@ __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t,
 // centred at n1/2), B_c separated from Z^(m), Z^(-m) (above); lanes take the points in a fixed
 // order and the warp sums them in a fixed tree (deterministic); then pending_c += h^2 g_c / Phi(s)
 // for each class with grid points in this batch (an empty class stays exactly zero).
+struct NuKpar {          // per dimension k (fixed per context: theta and the grid geometry), host-built
+    int m0x, m0y;        // nearest transform grid point to t_k = s_k h
+    float ftx, fty;      // offset from it in grid units, in [-1/2, 1/2]
+    double scale;        // h^2 hs^2 / Phi(s_k)
+};
+
 __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G, int logn, int n1, int D, int Dp,
-                                                   const double *__restrict__ tx_turns, const double *__restrict__ ty_turns,
-                                                   double h, double tau, double tau2, const float2 *__restrict__ ph,
-                                                   const int *__restrict__ bcnt, double *__restrict__ pending)
+                                                   const NuKpar *__restrict__ kpar, double tau2,
+                                                   const float2 *__restrict__ ph, const int *__restrict__ bcnt,
+                                                   double *__restrict__ pending)
 {
     constexpr int NP = 2 * NU_MSP2 + 1;   // 13
     const int lane = threadIdx.x & 31;
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (k >= D) return;   // warp-uniform
     const int N = 1 << logn;
-    const double hs = 2.0 * 3.14159265358979323846 / N;
-    const double sx = 2.0 * 3.14159265358979323846 * tx_turns[k], sy = 2.0 * 3.14159265358979323846 * ty_turns[k];
-    const double tx = sx * h, ty = sy * h;   // fp64 frequencies w = theta / l
-    const int m0x = (int)rint(tx / hs), m0y = (int)rint(ty / hs);
-    const float ftx = (float)(tx / hs - m0x), fty = (float)(ty / hs - m0y);   // in [-1/2, 1/2]
-    const float hsf = (float)hs;
+    const NuKpar kp = kpar[k];
+    const int m0x = kp.m0x, m0y = kp.m0y;
+    const float ftx = kp.ftx, fty = kp.fty;
+    const float hsf = (float)(2.0 * 3.14159265358979323846 / N);
     const float inv4t2 = (float)(1.0 / (4.0 * tau2));
     const float inv2a = 0.5f / nu_alpha(bcnt);
     const int K2 = N / 4 + 8;                // compact frequency range (k_nu_colfft); |m| <= N/4 + 7
@@ -393,8 +397,7 @@ __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G,
         a1i += __shfl_xor_sync(0xffffffffu, a1i, o);
     }
     if (lane == 0) {
-        const double s2 = sx * sx + sy * sy;
-        const double scale = h * h * hs * hs / (4.0 * 3.14159265358979323846 * tau * exp(-s2 * tau));
+        const double scale = kp.scale;
         if (bcnt[0] > 0) {
             double *pd = pending + 2 * (size_t)k;
             pd[0] += scale * a0r;
@@ -464,6 +467,22 @@ int vsa_nufft_plan(vsaogm_ctx *c)
         const double lc = l - n1 / 2;
         psi[l] = (float)(1.0 / (sqrt(4.0 * 3.14159265358979323846 * c->nu_tau2) * exp(-lc * lc * c->nu_tau2)));
     }
+    // per-k interpolation parameters (fp64 frequencies w = theta / l from the turn rates of vsaogm_create)
+    std::vector<NuKpar> kpar(c->D);
+    {
+        const double hs = 2.0 * 3.14159265358979323846 / N;
+        for (int k = 0; k < c->D; ++k) {
+            const double sx = 2.0 * 3.14159265358979323846 * (c->thx[k] / (2.0 * 3.14159265358979323846 * c->l));
+            const double sy = 2.0 * 3.14159265358979323846 * (c->thy[k] / (2.0 * 3.14159265358979323846 * c->l));
+            const double tx = sx * h, ty = sy * h;
+            kpar[k].m0x = (int)rint(tx / hs);
+            kpar[k].m0y = (int)rint(ty / hs);
+            kpar[k].ftx = (float)(tx / hs - kpar[k].m0x);
+            kpar[k].fty = (float)(ty / hs - kpar[k].m0y);
+            const double s2 = sx * sx + sy * sy;
+            kpar[k].scale = h * h * hs * hs / (4.0 * 3.14159265358979323846 * c->nu_tau * exp(-s2 * c->nu_tau));
+        }
+    }
     std::vector<float2> tw(N), ph(N);
     for (int p = 1; p < N; p <<= 1)
         for (int k = 0; k < p; ++k) {
@@ -487,8 +506,10 @@ int vsa_nufft_plan(vsaogm_ctx *c)
     VSA_CUDA_TRY(cudaMemset(c->d_nu_grid, 0, grid_bytes));
     if (cudaMalloc(&c->d_nu_f1, f1_bytes) != cudaSuccess ||
         cudaMalloc(&c->d_nu_G, g_bytes) != cudaSuccess || cudaMalloc(&c->d_nu_psi, n1 * 4) != cudaSuccess ||
-        cudaMalloc(&c->d_nu_tw, N * 8) != cudaSuccess || cudaMalloc(&c->d_nu_ph, N * 8) != cudaSuccess)
+        cudaMalloc(&c->d_nu_tw, N * 8) != cudaSuccess || cudaMalloc(&c->d_nu_ph, N * 8) != cudaSuccess ||
+        cudaMalloc(&c->d_nu_kpar, kpar.size() * sizeof(NuKpar)) != cudaSuccess)
         return VSAOGM_ENOMEM;
+    VSA_CUDA_TRY(cudaMemcpy(c->d_nu_kpar, kpar.data(), kpar.size() * sizeof(NuKpar), cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(c->d_nu_psi, psi.data(), n1 * 4, cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(c->d_nu_tw, tw.data(), N * 8, cudaMemcpyHostToDevice));
     VSA_CUDA_TRY(cudaMemcpy(c->d_nu_ph, ph.data(), N * 8, cudaMemcpyHostToDevice));
@@ -577,9 +598,8 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     if (rc) return rc;
     VSA_CUDA_TRY(cudaGetLastError());
     k_nu_interp<<<(c->D + 7) / 8, 256, 0, c->stream>>>((const float2 *)c->d_nu_G, c->nu_logn, c->nu_n1,
-                                                                      c->D, c->Dp, c->d_tx_turns, c->d_ty_turns, c->nu_h,
-                                                                      c->nu_tau, c->nu_tau2, (const float2 *)c->d_nu_ph,
-                                                                      bcnt, c->d_pending);
+                                                                      c->D, c->Dp, (const NuKpar *)c->d_nu_kpar, c->nu_tau2,
+                                                                      (const float2 *)c->d_nu_ph, bcnt, c->d_pending);
     VSA_CUDA_TRY(cudaGetLastError());
     c->launches += 8;
     return VSAOGM_OK;
