@@ -111,6 +111,7 @@ struct vsaogm_ctx {
     void *d_nu_key = nullptr, *d_nu_sorted = nullptr; size_t nu_pts_cap = 0;   // per-point (bin, slot); binned points
     float *d_nu_psi = nullptr;                                         // 1 / psi^(l - n1/2)
     void *d_nu_tw = nullptr, *d_nu_ph = nullptr;                       // twiddles, centring phases
+    int pdl = 1;                                                       // programmatic dependent launch of the step's kernels (tuning)
     void *d_nu_kpar = nullptr;                                         // per-k interpolation parameters (NuKpar [D])
     int *d_nu_out = nullptr; size_t nu_out_cap = 0;                    // outliers per chunk  // 1 (default): one class per block (k_encode_pairs1, 64 registers, 4 per SM)
     int enc_x2_npoly = 4;   // polynomial dimensions of 8 in the second warp role
@@ -387,6 +388,46 @@ __device__ __forceinline__ void sincos_fma(float phi, float *s_out, float *c_out
 // angle, accumulation and polynomial arithmetic frees issue for more phasors
 // (DESIGN.md section 6).  A scalar operand broadcast as pk2(f, f) compiles to
 // the R.F32 / immediate broadcast form of the packed instruction.
+// ---- programmatic dependent launch (PDL) -------------------------------------------------------
+// The streaming step is a chain of ~20 short dependent kernels; an ordinary launch starts a kernel
+// only after its predecessor has drained (~2 us of launch latency per link on the step's critical
+// path).  vsa_launch_pdl launches with programmatic stream serialization: the kernel's blocks are
+// scheduled as soon as every block of the predecessor has passed vsa_pdl() (which all of our
+// kernels do first), and wait there -- griddepcontrol.wait returns when the predecessor grid has
+// completed and its writes are visible -- so the launch latency and the block scheduling overlap
+// the predecessor's execution.  Every kernel launched this way calls vsa_pdl() before it touches
+// global memory; launched ordinarily the two instructions are no-ops.
+__device__ __forceinline__ void vsa_pdl()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t vsa_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// launch on the context's current stream: PDL unless the tuning knob `pdl` is 0
+template <typename... KArgs, typename... Args>
+inline cudaError_t vsa_launch(const vsaogm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args &&...args)
+{
+    if (c->pdl) return vsa_launch_pdl(kern, grid, block, smem, c->stream, static_cast<Args &&>(args)...);
+    kern<<<grid, block, smem, c->stream>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+}
+
 typedef unsigned long long f32x2;
 
 __device__ __forceinline__ f32x2 pk2(float a, float b)

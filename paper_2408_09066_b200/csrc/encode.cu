@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_encode_pairs1(
     const float *__restrict__ wx, const float *__restrict__ wy, double cx, double cy, int Dp,
     float2 *__restrict__ part, long long *__restrict__ part_cnt, int *__restrict__ err, NuOutl nu = NuOutl{})
 {
+    vsa_pdl();
     if (OUTL && nu.out_cnt[blockIdx.y] == 0) return;   // block-uniform
     constexpr int KT = 8;
     constexpr int NW = THREADS / 32;
@@ -741,6 +742,7 @@ __global__ void __launch_bounds__(NORM_THREADS) k_commit_norms(double *__restric
                                                                unsigned int *__restrict__ ticket,
                                                                double *__restrict__ norm2)
 {
+    vsa_pdl();
     __shared__ double s[NORM_THREADS];
     __shared__ bool s_last;
     const int c = blockIdx.x, b = blockIdx.y, nb = gridDim.y;
@@ -817,9 +819,9 @@ int vsa_launch_nufft_outliers(vsaogm_ctx *c, const float *xy, const uint8_t *lab
 {
     NuOutl nu{c->nu_lo, 1.0 / c->nu_h, c->nu_n1, c->d_nu_out, c->d_pending, c->D};
     const int kblocks = (c->Dp + 2047) / 2048;
-    k_encode_pairs1<256, 0, 4, 4, true><<<dim3(kblocks, chunks, 2), 256, 0, c->stream>>>(
-        (const float2 *)xy, lab, n, chunk_pts, c->d_wx, c->d_wy, c->cx, c->cy, c->Dp, nullptr, nullptr, c->d_err, nu);
-    VSA_CUDA_TRY(cudaGetLastError());
+    VSA_CUDA_TRY(vsa_launch(c, k_encode_pairs1<256, 0, 4, 4, true>, dim3(kblocks, chunks, 2), dim3(256), 0, (const float2 *)xy, lab, n,
+                            chunk_pts, (const float *)c->d_wx, (const float *)c->d_wy, c->cx, c->cy, c->Dp, (float2 *)nullptr,
+                            (long long *)nullptr, c->d_err, nu));
     c->launches++;
     return VSAOGM_OK;
 }
@@ -1043,9 +1045,8 @@ int vsa_launch_norms(vsaogm_ctx *c, int do_commit)
         double *pcnt = c->d_pcounts;
         // nb fixed per Dp (so the norm's summation order is too); tickets after the partials
         const int nb = std::max(1, std::min(NORM_BLOCKS, (c->Dp + 2 * NORM_THREADS - 1) / (2 * NORM_THREADS)));
-        k_commit_norms<<<dim3(c->nslots, nb), NORM_THREADS, 0, c->stream>>>(
-            m, pend, cnt, pcnt, do_commit, c->Dp, c->D, np, reinterpret_cast<unsigned int *>(np + (size_t)c->nslots * NORM_BLOCKS),
-            n2);
+        VSA_CUDA_TRY(vsa_launch(c, k_commit_norms, dim3(c->nslots, nb), dim3(NORM_THREADS), 0, m, pend, cnt, pcnt, do_commit, c->Dp,
+                                c->D, np, reinterpret_cast<unsigned int *>(np + (size_t)c->nslots * NORM_BLOCKS), n2));
 
     }
     VSA_CUDA_TRY(cudaGetLastError());

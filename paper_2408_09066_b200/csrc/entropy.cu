@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(ST_WARPS * 32, StCfg<H>::BLOCKS_PER_SM)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncwarp();
+    vsa_pdl();   // the barrier set-up above overlaps the decode's tail; H_b is read only from here on
     const int items = a.strips * a.chunks;
     uint32_t blk = 0;   // row blocks this warp has consumed: every slot is used once per block
     const float *lane_base = ring_smem + 4 + 4 * lane;        // this lane's 4 columns
@@ -429,7 +430,7 @@ int launch_stream(vsaogm_ctx *c, const CUtensorMap &tm, StreamArgs sa, int band,
     const int blocks = c->num_sms * Cfg::BLOCKS_PER_SM;
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_entropy_stream<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BLOCK_SMEM));
     vsa_prof_begin(c, VSAOGM_K_ENTROPY, ev);
-    k_entropy_stream<H><<<blocks, ST_WARPS * 32, Cfg::BLOCK_SMEM, c->stream>>>(tm, sa);
+    VSA_CUDA_TRY(vsa_launch(c, k_entropy_stream<H>, dim3(blocks), dim3(ST_WARPS * 32), (size_t)Cfg::BLOCK_SMEM, tm, sa));
     return VSAOGM_OK;
 }
 

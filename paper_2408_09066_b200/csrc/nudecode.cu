@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) k_nd_strength(const int *__restrict__ kid
                                                      const double *__restrict__ ty_t, double U0, double V0,
                                                      float2 *__restrict__ st)
 {
+    vsa_pdl();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= npts) return;
     const int pt = kid[s];
@@ -119,6 +120,7 @@ struct NdSpread {
 // (deterministic).  ~76 points per tile at C4: one wave of 484 blocks.
 __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ NdSpread p)
 {
+    vsa_pdl();
     constexpr int CH = ND_CH, NB = ND_TS / ND_BS + 2;   // staged points per pass; bin rows / columns gathered
     __shared__ float2 s_st[CH];
     __shared__ float2 s_u[CH];   // the point's position relative to this tile's first cell
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(co
                                                                            const float2 *__restrict__ Py, int r_ext, int rc,
                                                                            int ldt, float2 *__restrict__ Tt)
 {
+    vsa_pdl();
     constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
     const int j = threadIdx.x;
@@ -276,6 +279,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(co
                                                                            const float2 *__restrict__ Px, int cols, int jc,
                                                                            const NdEpi e)
 {
+    vsa_pdl();
     constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
     // an empty class decodes to exactly 0 (L8), not to the other class's transform rounding: bit masks
@@ -551,8 +555,8 @@ int launch_colfft_nz(vsaogm_ctx *c, const NdPlan &P)
     auto kern = k_nd_colfft<LOGN, T, NZ, DB>;
     VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = persistent_grid(c, kern, T, smem, P.Wx);
-    kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_G, P.Wx, P.Wy, (const float2 *)c->d_nd_tw, P.d_Py,
-                                       P.r_ext, P.rc, P.ldt, (float2 *)c->d_nd_T);
+    VSA_CUDA_TRY(vsa_launch(c, kern, dim3(grid), dim3(T), smem, (const float2 *)c->d_nd_G, P.Wx, P.Wy, (const float2 *)c->d_nd_tw,
+                            (const float2 *)P.d_Py, P.r_ext, P.rc, P.ldt, (float2 *)c->d_nd_T));
     return VSAOGM_OK;
 }
 
@@ -566,8 +570,8 @@ int launch_rowfft_nz(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
     auto kern = k_nd_rowfft<LOGN, T, NZ, FAST, DB>;
     VSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = persistent_grid(c, kern, T, smem, P.r_ext);
-    kern<<<grid, T, smem, c->stream>>>((const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw, P.d_Px,
-                                       P.cols, P.jc, e);
+    VSA_CUDA_TRY(vsa_launch(c, kern, dim3(grid), dim3(T), smem, (const float2 *)c->d_nd_T, P.ldt, P.Wx, (const float2 *)c->d_nd_tw,
+                            (const float2 *)P.d_Px, P.cols, P.jc, e));
     return VSAOGM_OK;
 }
 
@@ -634,9 +638,9 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     cudaEvent_t ev;
     vsa_prof_begin(c, VSAOGM_K_ND_SPREAD, &ev);
     const int npts = 2 * c->D;
-    k_nd_strength<<<(npts + 255) / 256, 256, 0, c->stream>>>(P->d_kid, npts, c->D, c->Dp, (const double2 *)c->d_m,
-                                                            c->d_norm2 + c->nslots, 1.0 / c->D, c->d_tx_turns,
-                                                            c->d_ty_turns, P->U0, P->V0, (float2 *)c->d_nd_st);
+    VSA_CUDA_TRY(vsa_launch(c, k_nd_strength, dim3((npts + 255) / 256), dim3(256), 0, (const int *)P->d_kid, npts, c->D, c->Dp,
+                            (const double2 *)c->d_m, (const double *)(c->d_norm2 + c->nslots), 1.0 / c->D,
+                            (const double *)c->d_tx_turns, (const double *)c->d_ty_turns, P->U0, P->V0, (float2 *)c->d_nd_st));
     // the memories are consumed: the next encode (encode stream) may start
     if (mark_main && (rc = vsa_mark_main(c))) return rc;
     NdSpread sp;
@@ -651,8 +655,7 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     sp.ax = P->ax;
     sp.ay = P->ay;
     sp.Gt = (float2 *)c->d_nd_G;
-    k_nd_spread<<<dim3(P->ntx, P->nty), 256, 0, c->stream>>>(sp);
-    VSA_CUDA_TRY(cudaGetLastError());
+    VSA_CUDA_TRY(vsa_launch(c, k_nd_spread, dim3(P->ntx, P->nty), dim3(256), 0, sp));
     vsa_prof_end(c, VSAOGM_K_ND_SPREAD, ev);
     vsa_prof_begin(c, VSAOGM_K_ND_COLFFT, &ev);
     switch (P->logy) {

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, c
                                                 int *__restrict__ out_cnt, double *__restrict__ pcount,
                                                 int *__restrict__ bcnt, int *__restrict__ err)
 {
+    vsa_pdl();
     __shared__ int s_cnt[4];   // class counts: all valid points, grid points
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cn
                                                   int *__restrict__ unit_off, int *__restrict__ unit_bin,
                                                   int *__restrict__ unit_first, int *__restrict__ n_units)
 {
+    vsa_pdl();
     // chunks of 1024 bins, one per thread (coalesced); up to CH chunks' counts loaded at once;
     // each chunk scanned by warp shuffles (two barriers) on top of the running carry
     constexpr int CH = 8;
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cn
 __global__ void __launch_bounds__(256) k_nu_place(const float2 *__restrict__ xy, int64_t n, const int2 *__restrict__ pkey,
                                                   const int *__restrict__ bin_off, float2 *__restrict__ sorted)
 {
+    vsa_pdl();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int2 key = pkey[i];
@@ -203,6 +206,7 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
                                                          double cy, double lo, double h, double inv_h, double tau,
                                                          unsigned long long *__restrict__ grid)
 {
+    vsa_pdl();
     __shared__ unsigned int s_win[NU_WIN * NU_WST];   // the block's window (row stride NU_WST)
     const int unit = blockIdx.x;
     if (unit >= *n_units) return;                     // block-uniform (the grid is an upper bound)
@@ -296,6 +300,7 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(unsigned long long *__restrict_
                                                  const int *__restrict__ bcnt, const float *__restrict__ psi_inv,
                                                  const float2 *__restrict__ tw, float2 *__restrict__ f1t)
 {
+    vsa_pdl();
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
     const int gy = blockIdx.x;
@@ -326,6 +331,7 @@ template <int LOGN, int T>
 __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t, int n1, const float2 *__restrict__ tw,
                                                  float2 *__restrict__ G)
 {
+    vsa_pdl();
     constexpr int N = 1 << LOGN;
     extern __shared__ float2 sm_fft[];
     constexpr int K2 = N / 4 + 8;
@@ -357,6 +363,7 @@ __global__ void __launch_bounds__(256) k_nu_interp(const float2 *__restrict__ G,
                                                    const float2 *__restrict__ ph, const int *__restrict__ bcnt,
                                                    double *__restrict__ pending)
 {
+    vsa_pdl();
     constexpr int NP = 2 * NU_MSP2 + 1;   // 13
     const int lane = threadIdx.x & 31;
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -529,11 +536,10 @@ int launch_ffts(vsaogm_ctx *c, const int *bcnt)
     const size_t smem = (size_t)(N + N / 16) * sizeof(float2);
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_rowfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     VSA_CUDA_TRY(cudaFuncSetAttribute(k_nu_colfft<LOGN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_nu_rowfft<LOGN, T><<<c->nu_n1, T, smem, c->stream>>>((unsigned long long *)c->d_nu_grid, c->nu_n1, bcnt,
-                                                           c->d_nu_psi, (const float2 *)c->d_nu_tw,
-                                                           (float2 *)c->d_nu_f1);
-    k_nu_colfft<LOGN, T><<<2 * (N / 4 + 8), T, smem, c->stream>>>((const float2 *)c->d_nu_f1, c->nu_n1,
-                                                              (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_G);
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_rowfft<LOGN, T>, dim3(c->nu_n1), dim3(T), smem, (unsigned long long *)c->d_nu_grid, c->nu_n1,
+                            bcnt, (const float *)c->d_nu_psi, (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_f1));
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_colfft<LOGN, T>, dim3(2 * (N / 4 + 8)), dim3(T), smem, (const float2 *)c->d_nu_f1, c->nu_n1,
+                            (const float2 *)c->d_nu_tw, (float2 *)c->d_nu_G));
     return VSAOGM_OK;
 }
 }  // namespace
@@ -576,15 +582,15 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     k_nu_zero<<<(nz + 255) / 256, 256, 0, c->stream>>>(c->d_nu_out, chunks, bin_cnt, nbins + 2);
     const unsigned pblocks = (unsigned)((n + 255) / 256);
     const double inv_h = 1.0 / c->nu_h;
-    k_nu_bin<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, lab, n, c->cx, c->cy, c->nu_lo, inv_h, c->nu_n1, ntx,
-                                             bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out, c->d_pcounts,
-                                             bcnt, c->d_err);
-    k_nu_scan<<<1, 1024, 0, c->stream>>>(bin_cnt, nbins, bin_off, unit_off, unit_bin, unit_first, n_units);
-    k_nu_place<<<pblocks, 256, 0, c->stream>>>((const float2 *)xy, n, (const int2 *)c->d_nu_key, bin_off,
-                                               (float2 *)c->d_nu_sorted);
-    k_nu_spread_tiles<<<(unsigned)max_units, 256, 0, c->stream>>>(
-        (const float2 *)c->d_nu_sorted, bin_off, unit_bin, unit_first, n_units, ntx, c->nu_n1, c->cx, c->cy, c->nu_lo, c->nu_h,
-        inv_h, c->nu_tau, (unsigned long long *)c->d_nu_grid);
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_bin, dim3(pblocks), dim3(256), 0, (const float2 *)xy, lab, n, c->cx, c->cy, c->nu_lo, inv_h,
+                            c->nu_n1, ntx, bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out, c->d_pcounts, bcnt, c->d_err));
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_scan, dim3(1), dim3(1024), 0, (const int *)bin_cnt, nbins, bin_off, unit_off, unit_bin,
+                            unit_first, n_units));
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_place, dim3(pblocks), dim3(256), 0, (const float2 *)xy, n, (const int2 *)c->d_nu_key,
+                            (const int *)bin_off, (float2 *)c->d_nu_sorted));
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_spread_tiles, dim3((unsigned)max_units), dim3(256), 0, (const float2 *)c->d_nu_sorted,
+                            (const int *)bin_off, (const int *)unit_bin, (const int *)unit_first, (const int *)n_units, ntx,
+                            c->nu_n1, c->cx, c->cy, c->nu_lo, c->nu_h, inv_h, c->nu_tau, (unsigned long long *)c->d_nu_grid));
     VSA_CUDA_TRY(cudaGetLastError());
     switch (c->nu_logn) {
     case 8: rc = launch_ffts<8>(c, bcnt); break;
@@ -597,9 +603,9 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     }
     if (rc) return rc;
     VSA_CUDA_TRY(cudaGetLastError());
-    k_nu_interp<<<(c->D + 7) / 8, 256, 0, c->stream>>>((const float2 *)c->d_nu_G, c->nu_logn, c->nu_n1,
-                                                                      c->D, c->Dp, (const NuKpar *)c->d_nu_kpar, c->nu_tau2,
-                                                                      (const float2 *)c->d_nu_ph, bcnt, c->d_pending);
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_interp, dim3((c->D + 7) / 8), dim3(256), 0, (const float2 *)c->d_nu_G, c->nu_logn, c->nu_n1,
+                            c->D, c->Dp, (const NuKpar *)c->d_nu_kpar, c->nu_tau2, (const float2 *)c->d_nu_ph, (const int *)bcnt,
+                            c->d_pending));
     VSA_CUDA_TRY(cudaGetLastError());
     c->launches += 8;
     return VSAOGM_OK;
