@@ -397,10 +397,12 @@ __device__ __forceinline__ void sincos_fma(float phi, float *s_out, float *c_out
 // completed and its writes are visible -- so the launch latency and the block scheduling overlap
 // the predecessor's execution.  Every kernel launched this way calls vsa_pdl() before it touches
 // global memory; launched ordinarily the two instructions are no-ops.
+__device__ __forceinline__ void vsa_pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void vsa_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void vsa_pdl()
 {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    vsa_pdl_launch();
+    vsa_pdl_wait();
 }
 
 template <typename... KArgs, typename... Args>

@@ -120,7 +120,7 @@ struct NdSpread {
 // (deterministic).  ~76 points per tile at C4: one wave of 484 blocks.
 __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ NdSpread p)
 {
-    vsa_pdl();
+    vsa_pdl_launch();
     constexpr int CH = ND_CH, NB = ND_TS / ND_BS + 2;   // staged points per pass; bin rows / columns gathered
     __shared__ float2 s_st[CH];
     __shared__ float2 s_u[CH];   // the point's position relative to this tile's first cell
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ Nd
         len[r] = in ? __ldg(p.bin_off + yb * p.nbx + xb1 + 1) - beg[r] : 0;
         total += len[r];
     }
+    vsa_pdl_wait();   // the plan's bin offsets above are not the predecessor's output (the strengths are)
     float2 acc[2][2] = {{make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}};
     for (int c0 = 0; c0 < total; c0 += CH) {
         const int nc = min(CH, total - c0);
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(co
                                                                            const float2 *__restrict__ Py, int r_ext, int rc,
                                                                            int ldt, float2 *__restrict__ Tt)
 {
-    vsa_pdl();
+    vsa_pdl_launch();
     constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
     const int j = threadIdx.x;
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(co
         rq[q] = (j < NS && (q < 4 || q >= 12) && r >= 0 && r < r_ext) ? r : -1;
         py[q] = rq[q] >= 0 ? __ldg(Py + r) : make_float2(0.f, 0.f);
     }
+    vsa_pdl_wait();   // the plan's factors above are not the predecessor's output
     for (int ux = blockIdx.x; ux < Wx; ux += gridDim.x) {
         const float2 *in = Gt + (size_t)ux * Wy;
         float2 *out = Tt + (size_t)ux * ldt;
@@ -279,11 +281,9 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(co
                                                                            const float2 *__restrict__ Px, int cols, int jc,
                                                                            const NdEpi e)
 {
-    vsa_pdl();
+    vsa_pdl_launch();
     constexpr int N = 1 << LOGN, NS = N / 16;
     extern __shared__ float2 sm_fft[];
-    // an empty class decodes to exactly 0 (L8), not to the other class's transform rounding: bit masks
-    const unsigned live0 = e.mscale[0] != 0.0 ? 0xffffffffu : 0u, live1 = e.mscale[1] != 0.0 ? 0xffffffffu : 0u;
     const int j = threadIdx.x;
     const int col0 = jc + j;
     float2 px[8];
@@ -295,6 +295,9 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(co
         px[s] = v ? __ldg(Px + col) : make_float2(0.f, 0.f);
         ok |= (unsigned)v << s;
     }
+    vsa_pdl_wait();   // the plan's factors above are not the predecessor's output
+    // an empty class decodes to exactly 0 (L8), not to the other class's transform rounding: bit masks
+    const unsigned live0 = e.mscale[0] != 0.0 ? 0xffffffffu : 0u, live1 = e.mscale[1] != 0.0 ? 0xffffffffu : 0u;
     const size_t cls_h = (size_t)e.r_ext * e.ldh, cls_q = (size_t)e.band_rows * e.cols;
     // a pruned radix-16 first pass reads NZ <= 4 values per thread: the next row's are loaded
     // before this row's passes (the strided loads' latency is hidden behind a whole transform)
