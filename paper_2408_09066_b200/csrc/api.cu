@@ -611,6 +611,7 @@ static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *g
         {"table_rows", &c->table_rows, 1, 256},
         {"dec_method", &c->dec_method, -1, 1},
         {"pdl", &c->pdl, 0, 1},
+        {"nd_bps", &c->nd_bps, 0, 8},
     };
     for (const Knob &k : knobs)
         if (strcmp(k.name, key) == 0) {

@@ -111,6 +111,7 @@ struct vsaogm_ctx {
     void *d_nu_key = nullptr, *d_nu_sorted = nullptr; size_t nu_pts_cap = 0;   // per-point (bin, slot); binned points
     float *d_nu_psi = nullptr;                                         // 1 / psi^(l - n1/2)
     void *d_nu_tw = nullptr, *d_nu_ph = nullptr;                       // twiddles, centring phases
+    int nd_bps = 0;                                                    // NUFFT decode FFTs: resident blocks per SM cap (0 = occupancy limit; tuning)
     int pdl = 1;                                                       // programmatic dependent launch of the step's kernels (tuning)
     void *d_nu_kpar = nullptr;                                         // per-k interpolation parameters (NuKpar [D])
     int *d_nu_out = nullptr; size_t nu_out_cap = 0;                    // outliers per chunk  // 1 (default): one class per block (k_encode_pairs1, 64 registers, 4 per SM)

@@ -543,6 +543,7 @@ int persistent_grid(vsaogm_ctx *c, K kernel, int T, size_t smem, int work)
 {
     int per_sm = 0;
     VSA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, T, smem));
+    if (c->nd_bps > 0) per_sm = std::min(per_sm, c->nd_bps);
     return std::max(1, std::min(work, c->num_sms * std::max(1, per_sm)));
 }
 
