@@ -456,7 +456,7 @@ def test_multi_rank_emulated_on_one_gpu():
 
 def test_pipelined_host_steps_match_synchronous():
     """vsaogm_encode_bundle_host_async / vsaogm_entropy_host_async / vsaogm_wait: a pipelined run
-    of several streaming steps (copies on the upload / download streams, three slots each)
+    of several streaming steps (copies on the upload / download streams, four slots each)
     returns, per step, the same labels and S as the synchronous host path."""
     import math
     from paper_2408_09066_b200 import Mapper

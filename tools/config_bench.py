@@ -25,7 +25,7 @@ def tau_of(D):
     return -p * math.log2(p) - (1 - p) * math.log2(1 - p)
 
 
-def bench_config(name, reps, pk, points=None, band=None, delta=1):
+def bench_config(name, reps, pk, points=None, band=None, delta=1, dec_method=-1):
     sc = Scenario(name)
     cfg = sc.cfg
     xy, lab = points if points is not None else sc.all_points()
@@ -33,6 +33,7 @@ def bench_config(name, reps, pk, points=None, band=None, delta=1):
     r0, r1 = band if band else (0, R)
     tau = tau_of(D)
     mp = Mapper(D, 0, l, sc.bounds, delta=delta)
+    mp.set_tuning("dec_method", dec_method)
     xg, lg = torch.from_numpy(xy).cuda(), torch.from_numpy(lab).cuda()
     L = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -61,17 +62,21 @@ def bench_config(name, reps, pk, points=None, band=None, delta=1):
     ra, rb = decoded_rows(R, r0, r1, h)
     flops = 2.0 * 2 * (rb - ra) * C * 2 * Dp
     enc_ms = per["encode"] + per["reduce"]
-    dec_ms = per["norms"] + per["table_A"] + per["decode_gemm"]
+    nd_ms = per.get("nd_spread", 0.0) + per.get("nd_colfft", 0.0) + per.get("nd_rowfft", 0.0)
+    dec_ms = per["norms"] + per["table_A"] + per["decode_gemm"] + nd_ms
+    gemm_tf = flops / (per["decode_gemm"] * 1e-3) / 1e12 if per["decode_gemm"] > 0 else None
     sfu_peak = 148 * 8 * pk["sm_max_mhz"] * 1e6   # one point at a time: 2 MUFU per phasor
     out = {
         "config": name, "delta": delta, "points": n, "D": D, "grid": f"{R}x{C}", "band_rows": [r0, r1],
+        "decode_method": "nufft" if nd_ms > 0 else "gemm",
         "kernel_ms": {k: round(v, 5) for k, v in per.items()},
         "points_bundled_per_s": n / (enc_ms * 1e-3),
         "encode_frac_mufu_roofline": n * D / (per["encode"] * 1e-3) / sfu_peak,
         "cells_decoded_per_s": (r1 - r0) * C / (dec_ms * 1e-3),
-        "gemm_tflops": flops / (per["decode_gemm"] * 1e-3) / 1e12,
-        "gemm_frac_sustained": flops / (per["decode_gemm"] * 1e-3) / 1e12 / pk["bf16_tflops_sustained"],
-        "gemm_frac_burst": flops / (per["decode_gemm"] * 1e-3) / 1e12 / pk["bf16_tflops"],
+        "gemm_tflops": gemm_tf,
+        "gemm_frac_sustained": gemm_tf / pk["bf16_tflops_sustained"] if gemm_tf else None,
+        "gemm_frac_burst": gemm_tf / pk["bf16_tflops"] if gemm_tf else None,
+        "dense_equivalent_tflops": flops / (dec_ms * 1e-3) / 1e12,
         "entropy_GBps": (r1 - r0) * C * 9 / (per["entropy"] * 1e-3) / 1e9,
         "step_ms": sum(per.values()),
     }
@@ -85,7 +90,9 @@ def main(tag):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"sm_max_mhz": 1965.0, "bf16_tflops_sustained": 1400.0,
                                                         "bf16_tflops": 1600.0}
     res = [bench_config("C1", 50, pk), bench_config("C2", 20, pk), bench_config("C3", 5, pk),
-           bench_config("C4", 10, pk, points=Scenario("C4").batch(0))]
+           bench_config("C3", 5, pk, dec_method=0), bench_config("C2", 20, pk, dec_method=1),
+           bench_config("C4", 10, pk, points=Scenario("C4").batch(0)),
+           bench_config("C4", 10, pk, points=Scenario("C4").batch(0), dec_method=0)]
     sc5 = Scenario("C5")
     res.append(bench_config("C5", 2, pk, points=sc5.all_points(), band=row_band(4000, 0, 8)))
     # quadrant memories (NEXT #1): the C4 step with delta = 2 and 4
