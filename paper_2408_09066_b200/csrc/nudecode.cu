@@ -620,12 +620,14 @@ bool vsa_nudecode_applies(vsaogm_ctx *c, double x0, double y0, double res, int32
     NdPlan G;
     if (!nd_geometry(c, x0, y0, res, cols, r_lo, r_ext, G)) return false;
     if (c->dec_method == 1) return true;
-    // auto: modelled times.  GEMM: 8 R C D flops at ~1.1 PF/s plus the
-    // tables; NUFFT: transform work (point-stages, 0.32 ps each: 132 M in 41 us at C4), the gather
-    // (1.1 ns per point: 18 us for 2 D = 16384), four launches.
-    const double t_gemm = 8.0 * r_ext * (double)cols * c->D / 1.1e15 + 2.0 * (r_ext + 0.5 * cols) * (double)c->Dp * 2.0 / 4e12 + 8e-6;
+    // auto: modelled times, fitted to profiles/r5z_configs.json.  GEMM: 8 R C D
+    // flops at ~1.1 PF/s plus the tables plus ~35 us of fixed cost (table A build + a one-wave GEMM:
+    // 45 us at C2, 78 at C3, 249 at C4); NUFFT: transform work (point-stages, 0.32 ps each: 132 M in
+    // 41 us at C4), the gather (1.1 ns per point: 15-18 us for 2 D = 16384), ~22 us for the four
+    // launches and the short kernels' latency (32 us at C2, 40 at C3, 68 at C4).
+    const double t_gemm = 8.0 * r_ext * (double)cols * c->D / 1.1e15 + 2.0 * (r_ext + 0.5 * cols) * (double)c->Dp * 2.0 / 4e12 + 35e-6;
     const double work = (double)G.Wx * G.My * G.logy + (double)r_ext * G.Mx * G.logx;
-    const double t_nufft = work * 0.32e-12 + 2.0 * c->D * 1.1e-9 + 10e-6;
+    const double t_nufft = work * 0.32e-12 + 2.0 * c->D * 1.1e-9 + 22e-6;
     return t_nufft < t_gemm;
 }
 
