@@ -5,8 +5,10 @@ A step is one pass of the whole hot path over one
 batch of the streaming config C4 (BASELINE.json configs[3], the config the
 metric "... at D=8192" is quoted on): bundle one 100-scan batch (~204k
 labelled points) into the persistent D=8192 memories, [all-reduce + commit
-across ranks], decode the 2000 x 2000 grid (0.05 m, 100 m x 100 m) on the
-tensor cores, and compute the 5x5 local-entropy map and labels.
+across ranks], decode the 2000 x 2000 grid (0.05 m, 100 m x 100 m) -- by the
+library's auto choice, the type-1 NUFFT decode at C4; the tcgen05 tensor-core
+GEMM decode of the same step is measured in the `gemm` / `bf16` sub-lines --
+and compute the 5x5 local-entropy map and labels.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
 
