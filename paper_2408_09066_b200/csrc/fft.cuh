@@ -132,8 +132,30 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b)
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// complex add / subtract as ONE packed fp32x2 instruction (FADD2: both lanes round to nearest, so the
+// results are those of two scalar adds; the kernels are issue-bound, and the butterflies' adds are a
+// third of their instructions: 128 FADD -> 32 FADD + 48 FADD2 per radix-16 butterfly, no moves -- a
+// float2 already lives in an aligned register pair)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b)
+{
+    unsigned long long pa, pb, pr;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(pb) : "f"(b.x), "f"(b.y));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(pr) : "l"(pa), "l"(pb));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(pr));
+    return r;
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b)
+{
+    unsigned long long pa, pb, pr;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(pb) : "f"(b.x), "f"(b.y));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(pr) : "l"(pa), "l"(pb));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(pr));
+    return r;
+}
 
 // x e^{2 pi i m / 16}, the quarter turns exact
 __device__ __forceinline__ float2 rot16(float2 x, int m)
