@@ -606,7 +606,7 @@ static int tuning_knob(vsaogm_ctx *c, const char *key, int64_t value, int64_t *g
         {"gemm_l2_hints", &c->gemm_l2_hints, 0, 2},
         {"gemm_agen", &c->gemm_agen, 0, 1},
         {"pipe_early", &c->pipe_early, 0, 1},
-        {"entropy_kernel", &c->entropy_kernel, 0, 1},
+        {"entropy_kernel", &c->entropy_kernel, 0, 2},
         {"entropy_rw", &c->entropy_rw, 0, 1 << 20},
         {"table_rows", &c->table_rows, 1, 256},
         {"dec_method", &c->dec_method, -1, 1},

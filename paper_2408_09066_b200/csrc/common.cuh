@@ -126,7 +126,7 @@ struct vsaogm_ctx {
     int gemm_agen = 0;      // 1: A phasor tiles generated in the GEMM (no table A)
     int gemm_l2_hints = 0;  // TMA L2 eviction hints in the decode GEMM: 0 none (default: no measured gain), 1 A first + B last, 2 B last
     int pipe_early = 0;     // 1: release the next encode before table A (measured slower)
-    int entropy_kernel = 0; // 0 auto (streamed box kernel where it applies); 1 generic kernel
+    int entropy_kernel = 0; // 0 auto (column-walk box kernel where it applies); 1 generic kernel; 2 TMA-streamed box kernel
     int entropy_rw = 0;     // 0 auto, else output rows per streamed work item (test hook)
     int table_rows = 32;    // table rows per thread of k_table (setup amortised over them)
     // decode method: -1 auto (the type-1 NUFFT of nudecode.cu where it applies and its modelled

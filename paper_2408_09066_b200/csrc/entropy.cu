@@ -418,6 +418,150 @@ __global__ void __launch_bounds__(HT) k_entropy_hist(const uint8_t *__restrict__
     }
 }
 
+// Box window, equal radii H <= 4, labels only -- the same contract as k_entropy_stream, without
+// shared memory, TMA or barriers: a thread owns 4 adjacent columns of one chunk of `rw` output rows
+// and walks down the rw + 2H input rows.  Per row it loads its float4 and the HL = 2 (H <= 2) or 4
+// halo columns on each side of both classes straight from global memory (the H_b map was written by
+// the decode just before and is L2-resident; the halos are its neighbours' float4s: L1 hits),
+// forms d = h_occ - h_emp per column, the four horizontal (2H+1)-sums of d (the first in order,
+// the next three sliding) and the running vertical sum V += s_new - s_old over the last 2H+1 rows
+// (a register ring, rows unrolled by 2H+1 so that the ring slot is compile-time and the loads of
+// 2H+1 rows are in flight together): S = V / count for the row 2H above, then the label.  Rows and
+// columns outside the grid contribute 0 and the count is the clipped one (L13).
+template <int H>
+__global__ void __launch_bounds__(128) k_entropy_cols(const float *__restrict__ hb, int ldh, int r_ext, int R, int C, int r_lo,
+                                                      int r0, int band_rows, int rw, float rho_occ, float rho_emp,
+                                                      uint8_t *__restrict__ lab)
+{
+    vsa_pdl();
+    constexpr int W = 2 * H + 1;
+    constexpr int HL = H <= 2 ? 2 : 4;             // halo columns loaded per side
+    const int c0 = (blockIdx.x * 128 + threadIdx.x) * 4;
+    if (c0 >= C) return;
+    const int oA = blockIdx.y * rw, oB = min(band_rows, oA + rw);   // band-relative output rows
+    const int rA = r0 + oA;                                         // full-grid row of output oA
+    const int nrows = (oB - oA) + 2 * H;                            // input rows rA - H .. rA - H + nrows - 1
+    float ncf[4], inv_in[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        ncf[j] = (float)(min(c0 + j + H, C - 1) - max(c0 + j - H, 0) + 1);
+        inv_in[j] = 1.0f / ((float)W * ncf[j]);
+    }
+    const bool fast = c0 - HL >= 0 && c0 + 4 + HL <= C;             // every loaded column is inside the grid
+    const bool full4 = c0 + 3 < C && (C & 3) == 0;
+    const float *p0 = hb + c0, *p1 = hb + (size_t)r_ext * ldh + c0;
+    float ring[W][4];
+#pragma unroll
+    for (int u = 0; u < W; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ring[u][j] = 0.f;
+    float V[4] = {0.f, 0.f, 0.f, 0.f};
+    constexpr int NV = 4 + 2 * HL;                                  // columns loaded per row and class
+    constexpr int G = H <= 2 ? W : 4;                               // rows whose loads are in flight together
+    for (int ib = 0; ib < nrows; ib += W) {
+#pragma unroll
+        for (int ug = 0; ug < W; ug += G) {
+            // phase 1: every load of the group's rows, unconditionally (rows outside the grid or the
+            // chunk read a clamped row and are masked below), so that they are all in flight at once
+            float x1[G][NV], x0[G][NV];
+            bool rv[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int u = ug + g;
+                if (u >= W) continue;                               // compile time
+                const int i = ib + u;
+                const int gr = rA - H + i, dr = gr - r_lo;
+                rv[g] = i < nrows && gr >= 0 && gr < R && dr >= 0 && dr < r_ext;
+                const size_t off = (size_t)min(max(dr, 0), r_ext - 1) * ldh;
+                if (fast) {
+                    const float4 a1 = __ldg(reinterpret_cast<const float4 *>(p1 + off));
+                    const float4 a0 = __ldg(reinterpret_cast<const float4 *>(p0 + off));
+                    x1[g][HL] = a1.x; x1[g][HL + 1] = a1.y; x1[g][HL + 2] = a1.z; x1[g][HL + 3] = a1.w;
+                    x0[g][HL] = a0.x; x0[g][HL + 1] = a0.y; x0[g][HL + 2] = a0.z; x0[g][HL + 3] = a0.w;
+                    if (HL == 2) {
+                        const float2 l1 = __ldg(reinterpret_cast<const float2 *>(p1 + off - 2));
+                        const float2 l0 = __ldg(reinterpret_cast<const float2 *>(p0 + off - 2));
+                        const float2 r1 = __ldg(reinterpret_cast<const float2 *>(p1 + off + 4));
+                        const float2 r0v = __ldg(reinterpret_cast<const float2 *>(p0 + off + 4));
+                        x1[g][0] = l1.x; x1[g][1] = l1.y; x1[g][HL + 4] = r1.x; x1[g][HL + 5] = r1.y;
+                        x0[g][0] = l0.x; x0[g][1] = l0.y; x0[g][HL + 4] = r0v.x; x0[g][HL + 5] = r0v.y;
+                    } else {
+                        const float4 l1 = __ldg(reinterpret_cast<const float4 *>(p1 + off - 4));
+                        const float4 l0 = __ldg(reinterpret_cast<const float4 *>(p0 + off - 4));
+                        const float4 r1 = __ldg(reinterpret_cast<const float4 *>(p1 + off + 4));
+                        const float4 r0v = __ldg(reinterpret_cast<const float4 *>(p0 + off + 4));
+                        x1[g][0] = l1.x; x1[g][1] = l1.y; x1[g][2] = l1.z; x1[g][3] = l1.w;
+                        x0[g][0] = l0.x; x0[g][1] = l0.y; x0[g][2] = l0.z; x0[g][3] = l0.w;
+                        x1[g][8] = r1.x; x1[g][9] = r1.y; x1[g][10] = r1.z; x1[g][11] = r1.w;
+                        x0[g][8] = r0v.x; x0[g][9] = r0v.y; x0[g][10] = r0v.z; x0[g][11] = r0v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < NV; ++e) {
+                        const int col = c0 + e - HL;
+                        const bool in = col >= 0 && col < C;
+                        x1[g][e] = in ? __ldg(p1 + off + e - HL) : 0.f;
+                        x0[g][e] = in ? __ldg(p0 + off + e - HL) : 0.f;
+                    }
+                }
+            }
+            // phase 2: class difference, horizontal sums, running vertical sum, labels
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int u = ug + g;
+                if (u >= W) continue;                               // compile time
+                const int i = ib + u;
+                float d[NV];                                        // d[HL + j] = column c0 + j
+#pragma unroll
+                for (int e = 0; e < NV; ++e) d[e] = rv[g] ? x1[g][e] - x0[g][e] : 0.f;
+                float hs[4];
+                float h0 = d[HL - H];
+#pragma unroll
+                for (int dv = -H + 1; dv <= H; ++dv) h0 += d[HL + dv];
+                hs[0] = h0;
+#pragma unroll
+                for (int j = 1; j < 4; ++j) hs[j] = (hs[j - 1] - d[HL + j - 1 - H]) + d[HL + j + H];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    V[j] += hs[j];
+                    V[j] -= ring[u][j];                             // row i - W (0 for the first W rows)
+                    ring[u][j] = hs[j];
+                }
+                const int o = oA + i - 2 * H;                       // band-relative output row
+                if (i >= 2 * H && o < oB) {                         // warp-uniform
+                    const int row = r0 + o;
+                    float g4[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) g4[j] = V[j] * inv_in[j];
+                    if (row < H || row >= R - H) {                  // clipped rows (grid top / bottom)
+                        const float cntr = (float)(min(row + H, R - 1) - max(row - H, 0) + 1);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) g4[j] = V[j] * (1.0f / (cntr * ncf[j]));
+                    }
+                    const uint32_t l4 = label_of(g4[0], rho_occ, rho_emp) | label_of(g4[1], rho_occ, rho_emp) << 8 |
+                                        label_of(g4[2], rho_occ, rho_emp) << 16 | label_of(g4[3], rho_occ, rho_emp) << 24;
+                    uint8_t *lrow = lab + (size_t)o * C + c0;
+                    if (full4) *reinterpret_cast<uint32_t *>(lrow) = l4;
+                    else
+                        for (int j = 0; j < 4 && c0 + j < C; ++j) lrow[j] = (uint8_t)(l4 >> (8 * j));
+                }
+            }
+        }
+    }
+}
+
+template <int H>
+int launch_cols(vsaogm_ctx *c, const vsaogm_entropy_params *p, int band, int ldh, uint8_t *lab, cudaEvent_t *ev)
+{
+    // chunks of rw output rows: 20 by default (C4: 4 x 100 blocks of 128 threads, one wave of 3 blocks per SM)
+    const int rw = c->entropy_rw > 0 ? c->entropy_rw : 20;
+    dim3 grid((c->g_cols + 511) / 512, (band + rw - 1) / rw);
+    vsa_prof_begin(c, VSAOGM_K_ENTROPY, ev);
+    VSA_CUDA_TRY(vsa_launch(c, k_entropy_cols<H>, grid, dim3(128), 0, (const float *)c->d_hb, ldh, c->g_rext, c->g_rows, c->g_cols,
+                            c->g_rlo, c->g_r0, band, rw, p->rho_occ, p->rho_emp, lab));
+    return VSAOGM_OK;
+}
+
 template <int H>
 int launch_stream(vsaogm_ctx *c, const CUtensorMap &tm, StreamArgs sa, int band, cudaEvent_t *ev)
 {
@@ -461,7 +605,16 @@ int vsa_launch_entropy(vsaogm_ctx *c, const vsaogm_entropy_params *p, float *S, 
     cudaEvent_t ev;
     const bool stream_k =
         p->half_occ == p->half_emp && !p->disk && H <= 4 && lab && !S && c->entropy_kernel != 1;
-    if (stream_k) {
+    if (stream_k && c->entropy_kernel != 2) {   // default: the column-walk kernel; 2: the TMA-streamed one
+        int rc = VSAOGM_OK;
+        switch (H) {
+        case 1: rc = launch_cols<1>(c, p, band, ldh, lab, &ev); break;
+        case 2: rc = launch_cols<2>(c, p, band, ldh, lab, &ev); break;
+        case 3: rc = launch_cols<3>(c, p, band, ldh, lab, &ev); break;
+        default: rc = launch_cols<4>(c, p, band, ldh, lab, &ev); break;
+        }
+        if (rc) return rc;
+    } else if (stream_k) {
         // tensor map over the decoded H_b rows: dims {cols, r_ext, 2 classes}; out-of-bounds
         // boxes are zero-filled (the window clipping)
         auto fn = vsa_tmap_encode_fn();

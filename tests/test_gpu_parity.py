@@ -332,8 +332,9 @@ def test_entropy_equal_radii_fast_path(disk, h):
 @pytest.mark.parametrize("h", [1, 2, 3, 4])
 @pytest.mark.parametrize("R,C,rw", [(75, 203, 0), (75, 203, 3), (300, 1000, 0), (300, 1000, 5), (64, 2000, 7)])
 def test_entropy_stream_kernel(h, R, C, rw):
-    """k_entropy_stream (TMA-streamed warps, box windows h <= 4, labels only; running vertical
-    sums of the class difference) against the generic staged kernel and the oracle: on ragged
+    """k_entropy_cols (the default: a thread walks 4 columns down a chunk of rows) and k_entropy_stream
+    (TMA-streamed warps) -- box windows h <= 4, labels only, running vertical sums of the class
+    difference -- against the generic staged kernel and the oracle: on ragged
     grids (203 and 1000 columns: partial strips, C not a multiple of 8), on bands with halo
     rows, and with short work items (rw) so that warps stream several items through their
     stage rings and the work queue wraps; S from the generic kernel is within 2e-5 of the
@@ -346,24 +347,26 @@ def test_entropy_stream_kernel(h, R, C, rw):
     mp.encode_bundle(*_cuda(xy, lab))
     q = torch.empty((2, R, C), dtype=torch.float32, device="cuda")
     mp.set_tuning("entropy_rw", rw)
-    outs = []
-    for kernel in (0, 1):
+    outs = {}
+    for kernel in (0, 2, 1):   # both labels-only box kernels (0 column walk, 2 TMA-streamed), then the generic one
         mp.set_tuning("entropy_kernel", kernel)
+        outs[kernel] = []
         for (r0, r1) in ((0, R), (21, 58), (R - 17, R)):
             mp.decode(0, 0, res, R, C, r0, r1, h, q_out=q if (r0, r1) == (0, R) else None)
             L = torch.empty((r1 - r0, C), dtype=torch.uint8, device="cuda")
             mp.entropy(h, h, 0.001, -0.001, 0, None, L)
-            outs.append(L.cpu())
+            outs[kernel].append(L.cpu())
     S = torch.empty((3, R, C), dtype=torch.float32, device="cuda")
     mp.decode(0, 0, res, R, C, 0, R, h)
     mp.entropy(h, h, 0.001, -0.001, 0, S, None)          # S maps: the generic kernel
     assert mp.sync() == 0
-    for a, b in zip(outs[:3], outs[3:]):
-        assert (a == b).float().mean().item() >= 0.9999
     So, Lo = oracle.entropy_grid(q.cpu().numpy().astype(np.float64), h, h, 0, 0.001, -0.001)
     assert np.abs(S.cpu().numpy() - So).max() <= 2e-5
-    assert (outs[0].numpy() == Lo).mean() >= 0.9999
-    assert torch.equal(outs[1], outs[0][21:58]) and torch.equal(outs[2], outs[0][R - 17:])
+    for fast in (0, 2):
+        for a, b in zip(outs[fast], outs[1]):
+            assert (a == b).float().mean().item() >= 0.9999
+        assert (outs[fast][0].numpy() == Lo).mean() >= 0.9999
+        assert torch.equal(outs[fast][1], outs[fast][0][21:58]) and torch.equal(outs[fast][2], outs[fast][0][R - 17:])
     mp.close()
 
 
