@@ -162,6 +162,17 @@ def workload_config(sc, n_pts_mean, world):
     }
 
 
+def load_ncu_stats():
+    """Per-kernel figures of the committed ncu capture (tools/ncu_summary.py): context for the rooflines."""
+    path = os.path.join(ROOT, "profiles", "ncu_kernel_stats.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path))
+        except Exception:
+            return {}
+    return {}
+
+
 def load_ncu_traffic():
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
@@ -404,6 +415,7 @@ def run_native(args):
     enc_rate = phasors / (enc_ms * 1e-3)
     clocks = clk.summary()
     traffic = load_ncu_traffic()
+    ncu_stats = load_ncu_stats()
 
     def alu_line(rate):
         return {"kernel": "k_encode_pairs", "bound": "alu", "achieved": round(rate / 1e9, 2),
@@ -443,7 +455,8 @@ def run_native(args):
         fl = n_tr * 5.0 * (1 << logn) * logn
         return {"kernel": kernel, "bound": "alu", "achieved": round(fl / (ms * 1e-3) / 1e12, 3),
                 "peak": round(fp32_peak / 1e12, 2), "unit": "TFLOP/s", "frac": round(fl / (ms * 1e-3) / fp32_peak, 4),
-                "traffic": traffic.get(name), "ms": round(ms, 5), "transforms": int(n_tr), "n": 1 << logn,
+                "traffic": traffic.get(name), "ncu": ncu_stats.get(name), "ms": round(ms, 5), "transforms": int(n_tr),
+                "n": 1 << logn,
                 "peak_basis": "FP32 FMA peak: 148 SM x 128 lanes x 2 flop x max SM clock (guide unit counts); "
                               "work = 5 N log2 N per transform (conventional FFT flop count)"}
     nd_lines = {"nd_rowfft": fft_line("k_nd_rowfft (x transforms of the decoded rows + Born rule / H_b epilogue)",

@@ -61,6 +61,7 @@ def main(tag):
     lines = [f"# ncu summary `{tag}` (`--set full --clock-control none`, one capture per kernel; cold-cache, serialised)",
              "", "| kernel | " + " | ".join(m[1] for m in METRICS) + " |", "|---" * (len(METRICS) + 1) + "|"]
     traffic = {}
+    stats = {}
     for r in data:
         name = short(r[col["Kernel Name"]])
         vals = []
@@ -71,6 +72,19 @@ def main(tag):
         rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
         wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
         traffic.setdefault(name, rd + wr)
+
+        def num(metric):
+            i = col.get(metric)
+            try:
+                return float(r[i].replace(",", "")) if i is not None else None
+            except ValueError:
+                return None
+        stats.setdefault(name, {"tag": tag, "duration_us": num("gpu__time_duration.sum"),
+                                "issue_active_pct": num("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+                                "warp_instructions": num("smsp__inst_executed.sum"),
+                                "fma_pipe_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                                "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                                "registers": num("launch__registers_per_thread")})
     launches = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(launches):
         txt = open(launches).read()
@@ -105,6 +119,10 @@ def main(tag):
         tags[k] = tag
     tags = {k: t for k, t in tags.items() if k in merged}
     json.dump({"tag": tag, "tags": tags, **merged}, open(tpath, "w"), indent=1)
+    spath = os.path.join(ROOT, "profiles", "ncu_kernel_stats.json")
+    old_stats = json.load(open(spath)) if os.path.exists(spath) else {}
+    old_stats.update(stats)
+    json.dump(old_stats, open(spath, "w"), indent=1)
     print(out)
 
 
