@@ -303,7 +303,7 @@ def test_c5_band_and_full_grid():
 
 # ------------------------------------------------------------------ two ranks through the library
 
-def _rank_worker(rank, world, port, out):
+def _rank_worker(rank, world, port, out, force_nufft=0):
     import os
 
     import torch.distributed as dist
@@ -320,6 +320,9 @@ def _rank_worker(rank, world, port, out):
     tau = label_tau(D)
     lo, hi = point_shard(len(lab), rank, world)
     mp = Mapper(D, 0, l, sc.bounds)
+    if force_nufft:                                   # the NUFFT encode writes the pending buffer too
+        mp.set_tuning("enc_method", 1)
+        mp.set_tuning("dec_method", 1)
     chunks = np.array_split(np.arange(lo, hi), 3)
     for k, ch in enumerate(chunks):                   # three streamed batches per rank
         mp.encode_bundle(*_cuda(xy[ch], lab[ch]))
@@ -336,8 +339,10 @@ def _rank_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_two_ranks_through_the_library():
-    """Two processes (world 2, gloo; both on GPU 0 -- their kernels never wait on each other):
+@pytest.mark.parametrize("force_nufft", [0, 1])
+def test_two_ranks_through_the_library(force_nufft):
+    """Two processes (world 2, gloo; both on GPU 0 -- their kernels never wait on each other;
+    force_nufft = 1: the NUFFT encode and decode on every rank instead of the auto choice):
     each bundles its point shard of C2 in three batches into its own context, all-reduces the
     library's packed pending buffer (memories + counts) and commits after every batch, then
     decodes its row band with halo rows.  Every rank's memories equal the oracle's one-shot
@@ -353,7 +358,7 @@ def test_two_ranks_through_the_library():
     ctx = tmp.get_context("spawn")
     manager = ctx.Manager()
     out = manager.dict()
-    tmp.start_processes(_rank_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+    tmp.start_processes(_rank_worker, args=(world, port, out, force_nufft), nprocs=world, join=True, start_method="spawn")
     sc = Scenario("C2")
     cfg = sc.cfg
     xy, lab = sc.all_points()
@@ -371,6 +376,6 @@ def test_two_ranks_through_the_library():
     L = np.concatenate([out[r][3] for r in range(world)], axis=0)
     err = max(np.abs(q[k] - qo[k]).max() / np.abs(qo[k]).max() for k in (0, 1))
     agree = float((L == Lo).mean())
-    print(f"2 ranks: q err {err:.2e}, labels {agree:.5f}")
+    print(f"2 ranks (force_nufft={force_nufft}): q err {err:.2e}, labels {agree:.5f}")
     assert err <= Q_TOL[0], err
     assert agree >= LABEL_BAR, agree
