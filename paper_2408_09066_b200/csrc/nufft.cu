@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
     // in base 2: ex2.approx directly (arguments within [-30, 6]: no range guard needed)
     const float c2 = (float)(h * h / (4.0 * tau) * 1.4426950408889634);
     const float e2 = nu_ex2(-2.f * c2);
+    const f32x2 e13 = pk2(e2, e2 * e2 * e2), e44 = bc2((e2 * e2) * (e2 * e2));
     const int dx = lane & 15, half = lane >> 4;
     const bool col_ok = dx < NU_W;
     const float2 *pts = sorted + first;
@@ -252,15 +253,24 @@ __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restric
             float wy = nu_ex2(-c2 * uy * uy), r = nu_ex2(-c2 * (2.f * uy + 1.f));
             unsigned int *wb = s_win + (iy - NU_MSP - gy0 + 7 * half) * NU_WST + (ix - NU_MSP - gx0 + dx);
             if (col_ok) {
+                // the 7 rows two at a time in packed fp32x2 (the kernel is issue-bound): P = (wy_k, wy_k+1)
+                // advances two rows by rho = (r_k r_k+1, r_k+1 r_k+2) = r_k^2 (e2, e2^3), rho <- rho e2^4.
+                // Rounding to the nearest integer by the 1.5 * 2^23 bias (wx wy <= 2^20 < 2^22): ALU ops
+                // instead of a conversion on the XU pipe; shared-memory integer atomics: exact
+                const f32x2 wxb = bc2(wx), bias = bc2(12582912.f);
+                f32x2 P = pk2(wy, wy * r);
+                f32x2 rho = mul2(bc2(r * r), e13);
+                float v0, v1;
 #pragma unroll
-                for (int k = 0; k < 7; ++k) {
-                    // round to the nearest integer by the 1.5 * 2^23 bias (wx wy <= 2^20 < 2^22):
-                    // ALU ops instead of a conversion on the XU pipe
-                    const unsigned int q = __float_as_uint(fmaf(wx, wy, 12582912.f)) - 0x4B400000u;
-                    atomicAdd(wb + k * NU_WST, q);   // shared-memory integer atomics: exact
-                    wy *= r;
-                    r *= e2;
+                for (int k = 0; k < 6; k += 2) {
+                    upk2(fma2(wxb, P, bias), v0, v1);
+                    atomicAdd(wb + k * NU_WST, __float_as_uint(v0) - 0x4B400000u);
+                    atomicAdd(wb + (k + 1) * NU_WST, __float_as_uint(v1) - 0x4B400000u);
+                    P = mul2(P, rho);
+                    if (k < 4) rho = mul2(rho, e44);
                 }
+                upk2(P, v0, v1);                     // row 6
+                atomicAdd(wb + 6 * NU_WST, __float_as_uint(fmaf(wx, v0, 12582912.f)) - 0x4B400000u);
             }
         }
     }
