@@ -304,7 +304,9 @@ __device__ __forceinline__ float nu_alpha(const int *__restrict__ bcnt)
 // row pass: block = one grid row gy.  Reads the row of both classes' fixed-point grids (and
 // zeroes what it read: the grid is clean for the next encode), pre-corrects (psi_inv[gx]
 // psi_inv[gy]), packs Z = b_0 + i alpha b_1, zero-pads to N, transforms along x, and writes the
-// column-major intermediate F1T[mx][gy] (compact mx, gy < n1).
+// row-major intermediate F1[gy][mx] (compact mx; coalesced stores -- the column pass reads it
+// strided, all of a thread's loads in flight together: measured 12.7 + 7.5 us with the transposed
+// layout, 9.2 + 10.4 us with this one).
 template <int LOGN, int T>
 __global__ void __launch_bounds__(T) k_nu_rowfft(unsigned long long *__restrict__ grid, int n1,
                                                  const int *__restrict__ bcnt, const float *__restrict__ psi_inv,
@@ -322,17 +324,22 @@ __global__ void __launch_bounds__(T) k_nu_rowfft(unsigned long long *__restrict_
     fftr::fft<LOGN, T, 8>(
         sm_fft, tw,
         [&](int j, int) {
+            // loads only (no store between them: the first pass's loads are all in flight together;
+            // the row is re-zeroed below)
             if (j >= n1) return make_float2(0.f, 0.f);
-            const unsigned long long v0 = row0[j], v1 = row1[j];
-            if (v0) row0[j] = 0ull;
-            if (v1) row1[j] = 0ull;
-            const float s = psi_inv[j] * py;
+            const unsigned long long v0 = __ldcg(row0 + j), v1 = __ldcg(row1 + j);
+            const float s = __ldg(psi_inv + j) * py;
             return make_float2((float)((double)v0 * (1.0 / NU_FIX)) * s, (float)((double)v1 * (1.0 / NU_FIX)) * s * alpha);
         },
         [&](int, int m, float2 v) {
-            if (m < K2) f1t[(size_t)(m + K2) * n1 + gy] = v;
-            else if (m >= N - K2) f1t[(size_t)(m - N + K2) * n1 + gy] = v;
+            if (m < K2) f1t[(size_t)gy * (2 * K2) + (m + K2)] = v;
+            else if (m >= N - K2) f1t[(size_t)gy * (2 * K2) + (m - N + K2)] = v;
         });
+    // the grid is clean for the next encode (every thread's loads of the row completed in the first pass)
+    for (int j = threadIdx.x; j < n1; j += T) {
+        row0[j] = 0ull;
+        row1[j] = 0ull;
+    }
 }
 
 // column pass: block = one (compact) x-frequency; transforms along y and writes the compact
@@ -346,10 +353,10 @@ __global__ void __launch_bounds__(T) k_nu_colfft(const float2 *__restrict__ f1t,
     extern __shared__ float2 sm_fft[];
     constexpr int K2 = N / 4 + 8;
     const int cx = blockIdx.x;
-    const float2 *in = f1t + (size_t)cx * n1;
+    const float2 *in = f1t + cx;   // row-major F1[gy][cx]: this column's values are 2 K2 apart
     float2 *out = G + (size_t)cx * 2 * K2;
     fftr::fft<LOGN, T, 8>(
-        sm_fft, tw, [&](int j, int) { return j < n1 ? __ldg(in + j) : make_float2(0.f, 0.f); },
+        sm_fft, tw, [&](int j, int) { return j < n1 ? __ldg(in + (size_t)j * (2 * K2)) : make_float2(0.f, 0.f); },
         [&](int, int m, float2 v) {
             if (m < K2) out[m + K2] = v;
             else if (m >= N - K2) out[m - N + K2] = v;
