@@ -319,6 +319,7 @@ __device__ __forceinline__ void pass(float2 *bin, float2 *bout, const float2 *__
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (r < NZ) x[b][r] = SRC == 0 ? load(j + r * NB, b * R + r) : bin[pad(j + r * NB)];
+                else x[b][r] = make_float2(0.f, 0.f);   // zero padding (never read by the pruned butterfly)
             }
         }
     }
@@ -367,17 +368,25 @@ __device__ __forceinline__ void passes16(float2 *bin, float2 *bout, const float2
 template <int LOGN>
 __host__ __device__ constexpr bool chained()
 {
-    return (LOGN >> 2) + ((LOGN & 3) ? 1 : 0) == 3;   // three passes: two exchanges
+    return (LOGN >> 2) + ((LOGN & 3) ? 1 : 0) == 3;   // three passes: two exchanges (without the ZP skip)
 }
 
-template <int LOGN, int T, int NZ = 16, bool ENDS = false, bool DB = false, class Load, class Store>
+// ZP: the caller's input is zero-padded, x_j = 0 for j >= N / 2.  For odd-by-one sizes (LOGN = 4 p + 1) the
+// radix-2 first pass would then only duplicate its inputs, buf[i] = x_{i >> 1}: it is skipped, and the
+// first radix-16 pass (sub-transform length 2) reads load(i >> 1) itself, with NZ counting ITS nonzero
+// input groups (x_{(j + r N/16) >> 1}: r < ceil(2 W / (N / 16)) for W nonzero values).
+template <int LOGN, int T, int NZ = 16, bool ENDS = false, bool DB = false, bool ZP = false, class Load, class Store>
 __device__ __forceinline__ void fft(float2 *buf, const float2 *__restrict__ tw, Load load, Store store)
 {
     static_assert(LOGN >= 5, "at least one radix-16 pass after the first");
     constexpr int RF = 1 << (LOGN & 3);
     constexpr int NP16 = LOGN >> 2;
     float2 *b0 = buf, *b1 = DB ? buf + (1 << LOGN) + (1 << LOGN) / 16 : buf;
-    if constexpr (RF > 1) {
+    if constexpr (RF == 2 && ZP && NP16 >= 2) {
+        auto load2 = [&](int i, int slot) { return load(i >> 1, slot); };
+        pass<LOGN, 16, 2, T, 0, 0, NZ, false, DB>(b0, b0, tw, load2, store);
+        passes16<LOGN, 1, T, ENDS, DB>(b0, b1, tw, load2, store);
+    } else if constexpr (RF > 1) {
         pass<LOGN, RF, 1, T, 0, 0, RF, false, DB>(b0, b0, tw, load, store);
         passes16<LOGN, 0, T, ENDS, DB>(b0, b1, tw, load, store);
     } else {

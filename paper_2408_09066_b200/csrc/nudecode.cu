@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_colfft(co
         const float2 *in = Gt + (size_t)ux * Wy;
         float2 *out = Tt + (size_t)ux * ldt;
         if (!(DB && fftr::chained<LOGN>())) __syncthreads();   // the previous column's transform consumed the buffer
-        fftr::fft<LOGN, T, NZ, true, DB>(
+        fftr::fft<LOGN, T, NZ, true, DB, true>(
             sm_fft, tw, [&](int i, int) { return i < Wy ? __ldg(in + i) : make_float2(0.f, 0.f); },
             [&](int q, int, float2 v) {
                 if (rq[q] >= 0) out[rq[q]] = cmulf(py[q], v);
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(T, (768 / T < 1 ? 1 : 768 / T)) k_nd_rowfft(co
         float *q0 = (!FAST && e.q && br >= 0 && br < e.band_rows) ? e.q + (size_t)br * e.cols + col0 : nullptr;
         float *q1 = q0 + cls_q;
         if (!(DB && fftr::chained<LOGN>())) __syncthreads();   // the previous row's transform consumed the buffer
-        fftr::fft<LOGN, T, NZ, true, DB>(
+        fftr::fft<LOGN, T, NZ, true, DB, true>(
             sm_fft, tw, [&](int i, int slot) { return PF ? cur[PF ? slot : 0] : ld(i, row); },
             [&](int qi, int, float2 v) {
                 const int s = qi < 4 ? qi : qi - 8;              // qi in {0..3, 12..15} (ENDS)
@@ -533,9 +533,12 @@ int nd_plan(vsaogm_ctx *c, double x0, double y0, double res, int cols, int r_lo,
 // to an instantiated count (transforms whose first pass is radix 16: LOGN = 8, 12)
 int nz_of(int W, int logn)
 {
-    if ((logn & 3) != 0) return 16;
-    const int g = (W + (1 << logn) / 16 - 1) / ((1 << logn) / 16);
-    return g <= 3 ? 3 : g <= 4 ? 4 : 8;
+    if ((logn & 3) > 1) return 16;
+    // sizes 16^p: groups of N / 16 inputs; sizes 2 x 16^p: the skipped radix-2 pass doubles every input
+    // (fft.cuh, ZP), so a group holds N / 32 distinct ones
+    const int per = (logn & 3) == 0 ? (1 << logn) / 16 : (1 << logn) / 32;
+    const int g = (W + per - 1) / per;
+    return g <= 3 ? 3 : g <= 4 ? 4 : g <= 8 ? 8 : 16;
 }
 
 template <typename K>
@@ -582,11 +585,12 @@ int launch_rowfft_nz(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
 template <int LOGN>
 int launch_colfft(vsaogm_ctx *c, const NdPlan &P)
 {
-    if constexpr ((LOGN & 3) == 0) {
+    if constexpr ((LOGN & 3) <= 1) {
         switch (nz_of(P.Wy, LOGN)) {
         case 3: return launch_colfft_nz<LOGN, 3>(c, P);
         case 4: return launch_colfft_nz<LOGN, 4>(c, P);
-        default: return launch_colfft_nz<LOGN, 8>(c, P);
+        case 8: return launch_colfft_nz<LOGN, 8>(c, P);
+        default: break;
         }
     }
     return launch_colfft_nz<LOGN, 16>(c, P);
@@ -595,11 +599,12 @@ int launch_colfft(vsaogm_ctx *c, const NdPlan &P)
 template <int LOGN, bool FAST>
 int launch_rowfft_f(vsaogm_ctx *c, const NdPlan &P, const NdEpi &e)
 {
-    if constexpr ((LOGN & 3) == 0) {
+    if constexpr ((LOGN & 3) <= 1) {
         switch (nz_of(P.Wx, LOGN)) {
         case 3: return launch_rowfft_nz<LOGN, 3, FAST>(c, P, e);
         case 4: return launch_rowfft_nz<LOGN, 4, FAST>(c, P, e);
-        default: return launch_rowfft_nz<LOGN, 8, FAST>(c, P, e);
+        case 8: return launch_rowfft_nz<LOGN, 8, FAST>(c, P, e);
+        default: break;
         }
     }
     return launch_rowfft_nz<LOGN, 16, FAST>(c, P, e);
