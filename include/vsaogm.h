@@ -184,10 +184,14 @@ int vsaogm_set_estimator(vsaogm_ctx *ctx, int32_t estimator);
  * "enc_runs_waves" (encode variants), "gemm_variant" (-1 auto, 0
  * CTA pair, 1 single CTA, 2 two CTA pairs per cluster with B multicast), "gemm_bn" (0 auto, else the tile width), "gemm_splits" (0 auto,
  * else the split-K factor), "gemm_l2_hints" (0 none, the default; 1 A evict-first + B evict-last; 2 B evict-last), "pipe_early" (0/1), "entropy_kernel"
- * (0 auto, 1 the generic staged kernel), "entropy_rw" (0 auto, else output rows per
- * work item of the streamed entropy kernel), "table_rows" (1..256, default 32: phasor-table
- * rows per thread of the table kernels), "dec_method" (-1 auto, the default; 0 the tcgen05 GEMM;
- * 1 the NUFFT where it applies, else the GEMM).  Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
+ * (0 auto: the column-walk box kernel for labels-only equal-radius box windows h <= 4, else the
+ * generic staged kernel; 1 the generic kernel; 2 the TMA-streamed box kernel), "entropy_rw" (0 auto,
+ * else output rows per thread chunk / work item of the box kernels), "table_rows" (1..256, default 32:
+ * phasor-table rows per thread of the table kernels), "dec_method" (-1 auto, the default; 0 the
+ * tcgen05 GEMM; 1 the NUFFT where it applies, else the GEMM), "pdl" (1, the default: the step's
+ * kernels are chained by programmatic dependent launches; 0 ordinary launches), "nd_bps" (0, the
+ * default: the NUFFT decode's FFT kernels fill the SMs; else a cap on their resident blocks per SM).
+ * Errors: EINVAL_ARG (unknown key or value out of range; nothing changes). */
 int vsaogm_set_tuning(vsaogm_ctx *ctx, const char *key, int64_t value);
 
 /* Read a tuning knob of this context into *value (the same keys).  Errors: EINVAL_ARG. */
