@@ -29,8 +29,8 @@
 // Accuracy: ~1e-6 of the peak |q| (Gaussian gridding with msp = 5, fp32 transforms), against the
 // fp16-operand GEMM's ~1e-4..1e-3.
 //
-// Kernels (one decode): k_nd_spread (block = 16 x 16 tile of the band grid; gathers the points of
-// the 3 x 3 neighbouring bins in a fixed host-sorted order: deterministic, no atomics),
+// Kernels (one decode): k_nd_spread (block = 32 x 32 tile of the band grid; gathers the points of
+// the 6 x 6 neighbouring bins in a fixed host-sorted order: deterministic, no atomics),
 // k_nd_colfft (persistent over band columns), k_nd_rowfft (persistent over decoded rows).  The binning
 // of the 2 D points depends only on theta and the grid geometry: it is built on the host once per
 // geometry (a plan) and cached.
@@ -44,7 +44,8 @@
 
 namespace {
 
-constexpr int ND_TS = 32;          // spread tile side (cells): 2 x 2 cells per thread
+constexpr int ND_TS = 32;          // spread tile side (cells): 2 x 2 cells per thread, 256 threads per tile (16: 10.5 us alone
+                                   // instead of 14.7, but 1936 small blocks on the high-priority stream: pipelined step 0.131 -> 0.136 ms)
 constexpr int ND_BS = 8;           // point bin side (cells)
 constexpr int ND_CH = 112;         // points staged per pass in the spread kernel (~76 per tile at C4: one pass)
 constexpr double ND_MSP = 5.0;     // Gaussian width parameter (accuracy ~1e-6)
@@ -118,16 +119,18 @@ struct NdSpread {
 // 32 x-weights g_x and the 32 strength-scaled y-weights h_y = g_y st of every staged point, and
 // every thread sums g_x[q][x] h_y[q][y] for its four cells over the points in slot order
 // (deterministic).  ~76 points per tile at C4: one wave of 484 blocks.
-__global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ NdSpread p)
+constexpr int ND_NT = ND_TS * ND_TS / 4;   // threads per tile: 2 x 2 cells each
+__global__ void __launch_bounds__(ND_NT, 1024 / ND_NT) k_nd_spread(const __grid_constant__ NdSpread p)
 {
     vsa_pdl_launch();
     constexpr int CH = ND_CH, NB = ND_TS / ND_BS + 2;   // staged points per pass; bin rows / columns gathered
+    constexpr int HT = ND_TS / 2;                       // a thread's cells: x = cxl, cxl + HT; y = cyl, cyl + HT
     __shared__ float2 s_st[CH];
     __shared__ float2 s_u[CH];   // the point's position relative to this tile's first cell
     __shared__ float s_gx[CH][ND_TS];
     __shared__ float2 s_hy[CH][ND_TS];
     const int bx = blockIdx.x, by = blockIdx.y, tid = threadIdx.x;
-    const int cxl = tid >> 4, cyl = tid & 15;   // a warp = 2 band columns x 16 rows (contiguous stores)
+    const int cxl = tid / HT, cyl = tid % HT;   // consecutive threads = consecutive rows (contiguous stores)
     constexpr int BPT = ND_TS / ND_BS;          // bins per tile side
     const int xb0 = max(BPT * bx - 1, 0), xb1 = min(BPT * bx + BPT, p.nbx - 1);
     int beg[NB], len[NB], total = 0;
@@ -144,8 +147,8 @@ __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ Nd
     for (int c0 = 0; c0 < total; c0 += CH) {
         const int nc = min(CH, total - c0);
         if (c0) __syncthreads();   // the previous pass is consumed
-        if (tid < nc) {
-            int i = c0 + tid, slot = 0, yb = 0;
+        for (int t = tid; t < nc; t += ND_NT) {
+            int i = c0 + t, slot = 0, yb = 0;
             bool found = false;
 #pragma unroll
             for (int r = 0; r < NB; ++r) {   // the bin row of staged point i (registers only)
@@ -158,11 +161,11 @@ __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ Nd
             }
             const float2 ps = __ldg(p.pos + slot);
             const int xbp = __ldg(p.binx + slot);
-            s_u[tid] = make_float2((float)(xbp * ND_BS - bx * ND_TS) + ps.x, (float)(yb * ND_BS - by * ND_TS) + ps.y);
-            s_st[tid] = __ldg(p.st + slot);
+            s_u[t] = make_float2((float)(xbp * ND_BS - bx * ND_TS) + ps.x, (float)(yb * ND_BS - by * ND_TS) + ps.y);
+            s_st[t] = __ldg(p.st + slot);
         }
         __syncthreads();
-        for (int e = tid; e < nc * 2 * ND_TS; e += 256) {
+        for (int e = tid; e < nc * 2 * ND_TS; e += ND_NT) {
             const int q = e / (2 * ND_TS), r = e % (2 * ND_TS);
             const float2 u = s_u[q];
             if (r < ND_TS) {
@@ -178,8 +181,8 @@ __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ Nd
         __syncthreads();
 #pragma unroll 4
         for (int q = 0; q < nc; ++q) {   // four independent accumulator pairs, each summed in slot order
-            const float g0 = s_gx[q][cxl], g1 = s_gx[q][cxl + 16];
-            const float2 h0 = s_hy[q][cyl], h1 = s_hy[q][cyl + 16];
+            const float g0 = s_gx[q][cxl], g1 = s_gx[q][cxl + HT];
+            const float2 h0 = s_hy[q][cyl], h1 = s_hy[q][cyl + HT];
             acc[0][0].x = fmaf(g0, h0.x, acc[0][0].x);
             acc[0][0].y = fmaf(g0, h0.y, acc[0][0].y);
             acc[0][1].x = fmaf(g0, h1.x, acc[0][1].x);
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(256, 4) k_nd_spread(const __grid_constant__ Nd
     for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-            const int ux = bx * ND_TS + cxl + 16 * a, uy = by * ND_TS + cyl + 16 * b;
+            const int ux = bx * ND_TS + cxl + HT * a, uy = by * ND_TS + cyl + HT * b;
             if (ux < p.Wx && uy < p.Wy) p.Gt[(size_t)ux * p.Wy + uy] = acc[a][b];
         }
 }
@@ -666,7 +669,7 @@ int vsa_launch_decode_nufft(vsaogm_ctx *c, double x0, double y0, double res, int
     sp.ax = P->ax;
     sp.ay = P->ay;
     sp.Gt = (float2 *)c->d_nd_G;
-    VSA_CUDA_TRY(vsa_launch(c, k_nd_spread, dim3(P->ntx, P->nty), dim3(256), 0, sp));
+    VSA_CUDA_TRY(vsa_launch(c, k_nd_spread, dim3(P->ntx, P->nty), dim3(ND_NT), 0, sp));
     vsa_prof_end(c, VSAOGM_K_ND_SPREAD, ev);
     vsa_prof_begin(c, VSAOGM_K_ND_COLFFT, &ev);
     switch (P->logy) {
