@@ -55,6 +55,9 @@ constexpr int NU_WST = 48;                     // window row stride (words): the
 static_assert(NU_WST >= NU_WIN && (7 * NU_WST) % 32 >= 14 && (7 * NU_WST) % 32 <= 18, "half-warps on disjoint banks");
 constexpr int NU_WOFF = NU_MSP;                // window starts 6 cells before the tile
 
+// NU_PT points per thread in k_nu_bin / k_nu_place (their loads in flight together): 4 for large batches
+// (C5's 10M points: 93 + 52 -> 64 + 40 us), 1 for small ones (C4's 204k: more blocks than SMs)
+template <int NU_PT>
 __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, const uint8_t *__restrict__ lab, int64_t n,
                                                 double cx, double cy, double lo, double inv_h, int n1, int ntx,
                                                 int *__restrict__ bin_cnt, int2 *__restrict__ pkey, int64_t chunk_pts,
@@ -65,38 +68,57 @@ __global__ void __launch_bounds__(256) k_nu_bin(const float2 *__restrict__ xy, c
     __shared__ int s_cnt[4];   // class counts: all valid points, grid points
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t base_i = (int64_t)blockIdx.x * (256 * NU_PT) + threadIdx.x;
+    float2 v[NU_PT];
+    int L[NU_PT];
+#pragma unroll
+    for (int p = 0; p < NU_PT; ++p) {   // coalesced: point base + 256 p + thread
+        const int64_t i = base_i + 256 * p;
+        v[p] = i < n ? xy[i] : make_float2(0.f, 0.f);
+        L[p] = i < n ? (int)lab[i] : -1;
+    }
     int my_err = 0;
-    int2 key = make_int2(-1, 0);
-    if (i < n) {
-        const float2 v = xy[i];
-        const int L = lab[i];
-        if (L > 1) my_err |= VSA_ERRBIT_LABEL;
-        else if (!(isfinite(v.x) && isfinite(v.y))) my_err |= VSA_ERRBIT_NONFINITE;
-        else {
-            atomicAdd(&s_cnt[L], 1);
-            const int ix = (int)floor(((double)v.x - cx - lo) * inv_h), iy = (int)floor(((double)v.y - cy - lo) * inv_h);
-            if (ix - NU_MSP < 0 || iy - NU_MSP < 0 || ix + NU_MSP + 1 >= n1 || iy + NU_MSP + 1 >= n1)
-                atomicAdd(&out_cnt[i / chunk_pts], 1);       // outlier: direct fallback
+    int cnt[4] = {0, 0, 0, 0};   // this thread's class counts: valid points, grid points
+#pragma unroll
+    for (int p = 0; p < NU_PT; ++p) {
+        const int64_t i = base_i + 256 * p;
+        int2 key = make_int2(-1, 0);
+        if (L[p] >= 0) {
+            if (L[p] > 1) my_err |= VSA_ERRBIT_LABEL;
+            else if (!(isfinite(v[p].x) && isfinite(v[p].y))) my_err |= VSA_ERRBIT_NONFINITE;
             else {
-                key.x = (L * ntx + iy / NU_TS) * ntx + ix / NU_TS;
-                atomicAdd(&s_cnt[2 + L], 1);
+                cnt[0] += L[p] == 0;
+                cnt[1] += L[p] == 1;
+                const int ix = (int)floor(((double)v[p].x - cx - lo) * inv_h), iy = (int)floor(((double)v[p].y - cy - lo) * inv_h);
+                if (ix - NU_MSP < 0 || iy - NU_MSP < 0 || ix + NU_MSP + 1 >= n1 || iy + NU_MSP + 1 >= n1)
+                    atomicAdd(&out_cnt[i / chunk_pts], 1);       // outlier: direct fallback
+                else {
+                    key.x = (L[p] * ntx + iy / NU_TS) * ntx + ix / NU_TS;
+                    cnt[2] += L[p] == 0;
+                    cnt[3] += L[p] == 1;
+                }
             }
         }
+        // warp-aggregated slot allocation: one atomic per distinct bin in the warp (neighbouring
+        // points of a scan share bins; a hot bin would otherwise serialise thousands of atomics)
+        const unsigned peers = __match_any_sync(0xffffffffu, key.x);
+        if (key.x >= 0) {
+            const int leader = __ffs(peers) - 1;
+            const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+            int base = 0;
+            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&bin_cnt[key.x], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            key.y = base + rank;
+        }
+        if (i < n) pkey[i] = key;
     }
-    // warp-aggregated slot allocation: one atomic per distinct bin in the warp (neighbouring
-    // points of a scan share bins; a hot bin would otherwise serialise thousands of atomics)
-    const unsigned peers = __match_any_sync(0xffffffffu, key.x);
-    if (key.x >= 0) {
-        const int leader = __ffs(peers) - 1;
-        const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
-        int base = 0;
-        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&bin_cnt[key.x], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        key.y = base + rank;
-    }
-    if (i < n) pkey[i] = key;
     if (my_err) atomicOr(err, my_err);
+    // class counts: warp sums (integer: exact), one shared atomic per warp and counter
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int w = __reduce_add_sync(0xffffffffu, cnt[k]);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_cnt[k], w);
+    }
     __syncthreads();
     if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&pcount[threadIdx.x], (double)s_cnt[threadIdx.x]);
     if (threadIdx.x >= 2 && threadIdx.x < 4 && s_cnt[threadIdx.x]) atomicAdd(&bcnt[threadIdx.x - 2], s_cnt[threadIdx.x]);
@@ -180,16 +202,27 @@ __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cn
     }
 }
 
+template <int NU_PT>
 __global__ void __launch_bounds__(256) k_nu_place(const float2 *__restrict__ xy, int64_t n, const int2 *__restrict__ pkey,
                                                   const int *__restrict__ bin_off, float2 *__restrict__ sorted)
 {
     vsa_pdl();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int2 key = pkey[i];
-    if (key.x < 0) return;
+    const int64_t base_i = (int64_t)blockIdx.x * (256 * NU_PT) + threadIdx.x;
+    int2 key[NU_PT];
+    float2 v[NU_PT];
+    int off[NU_PT];
+#pragma unroll
+    for (int p = 0; p < NU_PT; ++p) {
+        const int64_t i = base_i + 256 * p;
+        key[p] = i < n ? pkey[i] : make_int2(-1, 0);
+        v[p] = i < n ? xy[i] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int p = 0; p < NU_PT; ++p) off[p] = key[p].x >= 0 ? bin_off[key[p].x] : 0;
     // the raw coordinates: k_nu_spread_tiles recomputes the cell with k_nu_bin's fp64 expression
-    sorted[bin_off[key.x] + key.y] = xy[i];
+#pragma unroll
+    for (int p = 0; p < NU_PT; ++p)
+        if (key[p].x >= 0) sorted[off[p] + key[p].y] = v[p];
 }
 
 __device__ __forceinline__ float nu_ex2(float x)
@@ -597,14 +630,16 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     // pipelined host upload: the encode's start would wait for the whole batch copy)
     const int nz = std::max(chunks, nbins + 2);
     k_nu_zero<<<(nz + 255) / 256, 256, 0, c->stream>>>(c->d_nu_out, chunks, bin_cnt, nbins + 2);
-    const unsigned pblocks = (unsigned)((n + 255) / 256);
+    const int pt = n >= (int64_t)1 << 21 ? 4 : 1;   // points per thread of the bin / place kernels
+    const unsigned pblocks = (unsigned)((n + 256 * pt - 1) / (256 * pt));
     const double inv_h = 1.0 / c->nu_h;
-    VSA_CUDA_TRY(vsa_launch(c, k_nu_bin, dim3(pblocks), dim3(256), 0, (const float2 *)xy, lab, n, c->cx, c->cy, c->nu_lo, inv_h,
-                            c->nu_n1, ntx, bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out, c->d_pcounts, bcnt, c->d_err));
+    VSA_CUDA_TRY(vsa_launch(c, pt == 4 ? k_nu_bin<4> : k_nu_bin<1>, dim3(pblocks), dim3(256), 0, (const float2 *)xy, lab, n, c->cx,
+                            c->cy, c->nu_lo, inv_h, c->nu_n1, ntx, bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out,
+                            c->d_pcounts, bcnt, c->d_err));
     VSA_CUDA_TRY(vsa_launch(c, k_nu_scan, dim3(1), dim3(1024), 0, (const int *)bin_cnt, nbins, bin_off, unit_off, unit_bin,
                             unit_first, n_units));
-    VSA_CUDA_TRY(vsa_launch(c, k_nu_place, dim3(pblocks), dim3(256), 0, (const float2 *)xy, n, (const int2 *)c->d_nu_key,
-                            (const int *)bin_off, (float2 *)c->d_nu_sorted));
+    VSA_CUDA_TRY(vsa_launch(c, pt == 4 ? k_nu_place<4> : k_nu_place<1>, dim3(pblocks), dim3(256), 0, (const float2 *)xy, n,
+                            (const int2 *)c->d_nu_key, (const int *)bin_off, (float2 *)c->d_nu_sorted));
     VSA_CUDA_TRY(vsa_launch(c, k_nu_spread_tiles, dim3((unsigned)max_units), dim3(256), 0, (const float2 *)c->d_nu_sorted,
                             (const int *)bin_off, (const int *)unit_bin, (const int *)unit_first, (const int *)n_units, ntx,
                             c->nu_n1, c->cx, c->cy, c->nu_lo, c->nu_h, inv_h, c->nu_tau, (unsigned long long *)c->d_nu_grid));
