@@ -132,11 +132,11 @@ __global__ void __launch_bounds__(256) k_nu_zero(int *__restrict__ a, int na, in
 }
 
 // exclusive prefix of the bin counts and of the bins' work units (NU_UNIT points each): unit u
-// covers points [unit_first[u], +NU_UNIT) of bin unit_bin[u]; *n_units = the total
+// is NU_UNIT points of the bin b with unit_off[b] <= u < unit_off[b + 1] (k_nu_spread_tiles finds b);
+// *n_units = the total
 constexpr int NU_UNIT = 256;
 __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cnt, int nbins, int *__restrict__ bin_off,
-                                                  int *__restrict__ unit_off, int *__restrict__ unit_bin,
-                                                  int *__restrict__ unit_first, int *__restrict__ n_units)
+                                                  int *__restrict__ unit_off, int *__restrict__ n_units)
 {
     vsa_pdl();
     // chunks of 1024 bins, one per thread (coalesced); up to CH chunks' counts loaded at once;
@@ -186,10 +186,6 @@ __global__ void __launch_bounds__(1024) k_nu_scan(const int *__restrict__ bin_cn
             if (b < nbins) {
                 bin_off[b] = run;
                 unit_off[b] = urun;
-                for (int u = 0; u < nu; ++u) {
-                    unit_bin[urun + u] = b;
-                    unit_first[urun + u] = run + u * NU_UNIT;
-                }
             }
             carry += __shfl_sync(0xffffffffu, wi, 31);
             ucarry += __shfl_sync(0xffffffffu, uwi, 31);
@@ -233,18 +229,30 @@ __device__ __forceinline__ float nu_ex2(float x)
 }
 
 __global__ void __launch_bounds__(256) k_nu_spread_tiles(const float2 *__restrict__ sorted, const int *__restrict__ bin_off,
-                                                         const int *__restrict__ unit_bin,
-                                                         const int *__restrict__ unit_first,
+                                                         const int *__restrict__ unit_off,
                                                          const int *__restrict__ n_units, int ntx, int n1, double cx,
                                                          double cy, double lo, double h, double inv_h, double tau,
                                                          unsigned long long *__restrict__ grid)
 {
     vsa_pdl();
     __shared__ unsigned int s_win[NU_WIN * NU_WST];   // the block's window (row stride NU_WST)
+    __shared__ int s_bin;
     const int unit = blockIdx.x;
     if (unit >= *n_units) return;                     // block-uniform (the grid is an upper bound)
-    const int bin = unit_bin[unit];                   // (class, tile_y, tile_x)
-    const int first = unit_first[unit];
+    // the unit's bin: the b with unit_off[b] <= unit < unit_off[b + 1] (two parallel steps: the thread
+    // whose segment of the prefix array brackets the unit scans it -- no per-unit lists to build)
+    {
+        const int nbins = 2 * ntx * ntx, step = (nbins + 255) / 256;
+        const int b0 = threadIdx.x * step, b1 = min(b0 + step, nbins);
+        if (b0 < nbins && unit_off[b0] <= unit && unit < unit_off[b1]) {
+            int b = b0;
+            while (unit_off[b + 1] <= unit) ++b;      // < step iterations
+            s_bin = b;
+        }
+    }
+    __syncthreads();
+    const int bin = s_bin;                            // (class, tile_y, tile_x)
+    const int first = bin_off[bin] + (unit - unit_off[bin]) * NU_UNIT;
     const int cnt = min(NU_UNIT, bin_off[bin + 1] - first);
     // fixed point 2^20 per unit weight: a cell sums at most NU_UNIT weights <= 1 (< 2^28, no 32-bit
     // overflow); written as 32.32 fixed point (an exact shift)
@@ -625,7 +633,6 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     // offsets [nbins + 1], unit count
     int *bin_cnt = c->d_nu_bins, *bcnt = c->d_nu_bins + nbins, *bin_off = bcnt + 2, *unit_off = bin_off + nbins + 1;
     int *n_units = unit_off + nbins + 1;
-    int *unit_bin = c->d_nu_units, *unit_first = c->d_nu_units + (c->nu_pts_cap / NU_UNIT + nbins);
     // one small kernel instead of two memsets (a memset may be queued on a copy engine behind a
     // pipelined host upload: the encode's start would wait for the whole batch copy)
     const int nz = std::max(chunks, nbins + 2);
@@ -636,12 +643,11 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     VSA_CUDA_TRY(vsa_launch(c, pt == 4 ? k_nu_bin<4> : k_nu_bin<1>, dim3(pblocks), dim3(256), 0, (const float2 *)xy, lab, n, c->cx,
                             c->cy, c->nu_lo, inv_h, c->nu_n1, ntx, bin_cnt, (int2 *)c->d_nu_key, chunk_pts, c->d_nu_out,
                             c->d_pcounts, bcnt, c->d_err));
-    VSA_CUDA_TRY(vsa_launch(c, k_nu_scan, dim3(1), dim3(1024), 0, (const int *)bin_cnt, nbins, bin_off, unit_off, unit_bin,
-                            unit_first, n_units));
+    VSA_CUDA_TRY(vsa_launch(c, k_nu_scan, dim3(1), dim3(1024), 0, (const int *)bin_cnt, nbins, bin_off, unit_off, n_units));
     VSA_CUDA_TRY(vsa_launch(c, pt == 4 ? k_nu_place<4> : k_nu_place<1>, dim3(pblocks), dim3(256), 0, (const float2 *)xy, n,
                             (const int2 *)c->d_nu_key, (const int *)bin_off, (float2 *)c->d_nu_sorted));
     VSA_CUDA_TRY(vsa_launch(c, k_nu_spread_tiles, dim3((unsigned)max_units), dim3(256), 0, (const float2 *)c->d_nu_sorted,
-                            (const int *)bin_off, (const int *)unit_bin, (const int *)unit_first, (const int *)n_units, ntx,
+                            (const int *)bin_off, (const int *)unit_off, (const int *)n_units, ntx,
                             c->nu_n1, c->cx, c->cy, c->nu_lo, c->nu_h, inv_h, c->nu_tau, (unsigned long long *)c->d_nu_grid));
     VSA_CUDA_TRY(cudaGetLastError());
     switch (c->nu_logn) {
