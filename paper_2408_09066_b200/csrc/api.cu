@@ -225,7 +225,7 @@ void vsaogm_destroy(vsaogm_ctx *c)
                     c->d_B, c->d_hb, c->d_ws, c->d_S, c->d_lab, c->d_qc, c->d_slot, c->d_bhist,
                     c->d_sortmeta, c->d_sorted, c->d_runs, c->d_code, c->d_nu_grid, c->d_nu_f1, c->d_nu_G,
                     c->d_nu_psi, c->d_nu_tw, c->d_nu_ph, c->d_nu_kpar, c->d_nu_out, c->d_nu_bins,
-                    c->d_nu_key, c->d_nu_sorted, c->d_nu_units};
+                    c->d_nu_key, c->d_nu_sorted};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     vsa_nudecode_free(c);

@@ -107,7 +107,6 @@ struct vsaogm_ctx {
     int nu_n1 = 0, nu_logn = 0, nu_ntx = 0;
     void *d_nu_grid = nullptr, *d_nu_f1 = nullptr, *d_nu_G = nullptr;   // u64 32.32 grids [2][n1][n1], packed f32x2 [n1][2 K2], [2 K2][2 K2]
     int *d_nu_bins = nullptr;   // bin counts [nb], offsets [nb + 1], unit offsets [nb + 1], unit count [1]
-    int *d_nu_units = nullptr;  // unit -> bin, unit -> first point
     void *d_nu_key = nullptr, *d_nu_sorted = nullptr; size_t nu_pts_cap = 0;   // per-point (bin, slot); binned points
     float *d_nu_psi = nullptr;                                         // 1 / psi^(l - n1/2)
     void *d_nu_tw = nullptr, *d_nu_ph = nullptr;                       // twiddles, centring phases

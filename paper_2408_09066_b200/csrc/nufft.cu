@@ -617,15 +617,11 @@ int vsa_launch_encode_nufft(vsaogm_ctx *c, const float *xy, const uint8_t *lab, 
     if ((size_t)n > c->nu_pts_cap) {
         if (c->d_nu_key) cudaFree(c->d_nu_key);
         if (c->d_nu_sorted) cudaFree(c->d_nu_sorted);
-        if (c->d_nu_units) cudaFree(c->d_nu_units);
         c->d_nu_key = c->d_nu_sorted = nullptr;
-        c->d_nu_units = nullptr;
         c->nu_pts_cap = 0;
         const size_t cap = (size_t)n + (size_t)n / 4;   // headroom: batch sizes vary
-        const size_t ucap = cap / NU_UNIT + nbins;
         if (cudaMalloc(&c->d_nu_key, cap * sizeof(int2)) != cudaSuccess ||
-            cudaMalloc(&c->d_nu_sorted, cap * sizeof(float2)) != cudaSuccess ||
-            cudaMalloc(&c->d_nu_units, 2 * ucap * sizeof(int)) != cudaSuccess)
+            cudaMalloc(&c->d_nu_sorted, cap * sizeof(float2)) != cudaSuccess)
             return VSAOGM_ENOMEM;
         c->nu_pts_cap = cap;
     }
