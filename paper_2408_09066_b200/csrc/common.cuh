@@ -381,23 +381,21 @@ __device__ __forceinline__ void sincos_fma(float phi, float *s_out, float *c_out
     *c_out = __int_as_float(__float_as_int(c) ^ sign);
 }
 
-// ---- packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2, sm_100a) ----------------
-// Two fp32 lanes in one 64-bit register pair; each lane rounds exactly as the
-// scalar fmaf / __fmul_rn / __fadd_rn would.  One issue slot per two lanes: the
-// encode is bound by the MUFU pipe and the issue slots together, so packing the
-// angle, accumulation and polynomial arithmetic frees issue for more phasors
-// (DESIGN.md section 6).  A scalar operand broadcast as pk2(f, f) compiles to
-// the R.F32 / immediate broadcast form of the packed instruction.
 // ---- programmatic dependent launch (PDL) -------------------------------------------------------
-// The streaming step is a chain of ~20 short dependent kernels; an ordinary launch starts a kernel
+// The streaming step is a chain of 15 short dependent kernels; an ordinary launch starts a kernel
 // only after its predecessor has drained (~2 us of launch latency per link on the step's critical
 // path).  vsa_launch_pdl launches with programmatic stream serialization: the kernel's blocks are
-// scheduled as soon as every block of the predecessor has passed vsa_pdl() (which all of our
-// kernels do first), and wait there -- griddepcontrol.wait returns when the predecessor grid has
-// completed and its writes are visible -- so the launch latency and the block scheduling overlap
-// the predecessor's execution.  Every kernel launched this way calls vsa_pdl() before it touches
-// global memory; launched ordinarily the two instructions are no-ops.
-__device__ __forceinline__ void vsa_pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// scheduled as the predecessor's blocks exit, and wait at vsa_pdl_wait() -- griddepcontrol.wait
+// returns when the predecessor grid has completed and its writes are visible -- so the launch
+// latency, the block scheduling and the plan-constant prologues overlap the predecessor's tail.
+// Every kernel launched this way calls vsa_pdl() / vsa_pdl_wait() before it touches global memory
+// written by its predecessor; launched ordinarily the instruction is a no-op.
+// The trigger is the implicit one, at each block's exit: an explicit griddepcontrol.launch_dependents at
+// the start of every kernel (the first version) made the dependent grid's blocks resident -- holding
+// registers, shared memory and thread slots while they wait -- for the whole run of their predecessor,
+// which starved the other stream's kernels in the pipelined schedule (C4 step 0.129 -> 0.113 ms, end
+// to end 0.136 -> 0.126 ms without it; the serial step is unchanged).
+__device__ __forceinline__ void vsa_pdl_launch() {}
 __device__ __forceinline__ void vsa_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void vsa_pdl()
 {
@@ -430,6 +428,13 @@ inline cudaError_t vsa_launch(const vsaogm_ctx *c, void (*kern)(KArgs...), dim3 
     return cudaGetLastError();
 }
 
+// ---- packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2, sm_100a) ----------------
+// Two fp32 lanes in one 64-bit register pair; each lane rounds exactly as the
+// scalar fmaf / __fmul_rn / __fadd_rn would.  One issue slot per two lanes: the
+// encode is bound by the MUFU pipe and the issue slots together, so packing the
+// angle, accumulation and polynomial arithmetic frees issue for more phasors
+// (DESIGN.md section 6).  A scalar operand broadcast as pk2(f, f) compiles to
+// the R.F32 / immediate broadcast form of the packed instruction.
 typedef unsigned long long f32x2;
 
 __device__ __forceinline__ f32x2 pk2(float a, float b)
