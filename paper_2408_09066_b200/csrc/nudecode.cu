@@ -29,8 +29,8 @@
 // Accuracy: ~1e-6 of the peak |q| (Gaussian gridding with msp = 5, fp32 transforms), against the
 // fp16-operand GEMM's ~1e-4..1e-3.
 //
-// Kernels (one decode): k_nd_spread (block = 32 x 32 tile of the band grid; gathers the points of
-// the 6 x 6 neighbouring bins in a fixed host-sorted order: deterministic, no atomics),
+// Kernels (one decode): k_nd_spread (block = 16 x 16 tile of the band grid; gathers the points of
+// the 4 x 4 neighbouring bins in a fixed host-sorted order: deterministic, no atomics),
 // k_nd_colfft (persistent over band columns), k_nd_rowfft (persistent over decoded rows).  The binning
 // of the 2 D points depends only on theta and the grid geometry: it is built on the host once per
 // geometry (a plan) and cached.
@@ -44,10 +44,10 @@
 
 namespace {
 
-constexpr int ND_TS = 32;          // spread tile side (cells): 2 x 2 cells per thread, 256 threads per tile (16: 10.5 us alone
-                                   // instead of 14.7, but 1936 small blocks on the high-priority stream: pipelined step 0.131 -> 0.136 ms)
+constexpr int ND_TS = 16;          // spread tile side (cells): 2 x 2 cells per thread, 64 threads per tile (10.5 us at C4; 32-cell
+                                   // tiles: 14.7 us -- a point is evaluated on (side + 16)^2 cells)
 constexpr int ND_BS = 8;           // point bin side (cells)
-constexpr int ND_CH = 112;         // points staged per pass in the spread kernel (~76 per tile at C4: one pass)
+constexpr int ND_CH = 64;          // points staged per pass in the spread kernel (~34 per tile at C4: one pass)
 constexpr double ND_MSP = 5.0;     // Gaussian width parameter (accuracy ~1e-6)
 constexpr int ND_MARGIN = 6;       // band half-width beyond max |xi| / h (cells)
 constexpr int ND_LOGN_MAX = 13;    // shared-memory transforms up to 8192 points
@@ -111,14 +111,14 @@ struct NdSpread {
     float2 *Gt;              // compact band grid, x-major: Gt[ux][uy]
 };
 
-// block = one 32 x 32 tile of the band grid, 2 x 2 cells per thread (x = tx, tx + 16; y = ty, ty + 16);
-// gathers the points binned (8 x 8 bins) within 8 cells of it -- the 6 x 6 bins covering
-// [32 b - 8, 32 b + 40) per axis, six contiguous slot ranges (one per bin row), where a point farther
-// than 8 cells has weight < e^-31 --, up to 64 per pass.  One thread per staged point computes its
-// position relative to the tile (bin column from the plan: no search); then all threads compute the
-// 32 x-weights g_x and the 32 strength-scaled y-weights h_y = g_y st of every staged point, and
-// every thread sums g_x[q][x] h_y[q][y] for its four cells over the points in slot order
-// (deterministic).  ~76 points per tile at C4: one wave of 484 blocks.
+// block = one ND_TS x ND_TS tile of the band grid (16 x 16), 2 x 2 cells per thread (x = tx, tx + ND_TS/2;
+// y = ty, ty + ND_TS/2); gathers the points binned (8 x 8 bins) within 8 cells of it -- the bins covering
+// [ND_TS b - 8, ND_TS b + ND_TS + 8) per axis (4 x 4 of them), one contiguous slot range per bin row, where
+// a point farther than 8 cells has weight < e^-31 --, up to ND_CH per pass.  One thread per staged point
+// computes its position relative to the tile (bin column from the plan: no search); then all threads
+// compute the ND_TS x-weights g_x and the ND_TS strength-scaled y-weights h_y = g_y st of every staged
+// point, and every thread sums g_x[q][x] h_y[q][y] for its four cells over the points in slot order
+// (deterministic).  ~34 points per tile at C4, 1936 blocks of 64 threads.
 constexpr int ND_NT = ND_TS * ND_TS / 4;   // threads per tile: 2 x 2 cells each
 __global__ void __launch_bounds__(ND_NT, 1024 / ND_NT) k_nd_spread(const __grid_constant__ NdSpread p)
 {
